@@ -1,0 +1,363 @@
+// C ABI (include/meshgrad_b200.h): state management and orchestration.
+#include <cstring>
+#include <string>
+
+#include "mg_internal.cuh"
+
+using namespace mg;
+
+struct mg_mesh {
+  Mesh m;
+};
+struct mg_problem {
+  Problem p;
+  mg_mesh* mesh;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MG_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::exception& e) {
+    return fail(MG_ERR_CUDA, e.what());
+  }
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int natural_op(int type) {
+  switch (type) {
+    case MG_TERM_INERTIA: return MG_OP_V;
+    case MG_TERM_SPRING: return MG_OP_EV;
+    case MG_TERM_GRAVITY: return MG_OP_V;
+    case MG_TERM_EDGE_LENGTH: return MG_OP_EV;
+    case MG_TERM_SYM_DIRICHLET: return MG_OP_FV;
+    case MG_TERM_SPHERE: return MG_OP_FV;
+    default: return -1;
+  }
+}
+int natural_P(int op) { return op == MG_OP_FV ? 3 : op == MG_OP_EV ? 2 : 1; }
+int attrs_needed(int type) {
+  switch (type) {
+    case MG_TERM_INERTIA: return 2;
+    case MG_TERM_SPRING: return 1;
+    case MG_TERM_GRAVITY: return 1;
+    case MG_TERM_EDGE_LENGTH: return 0;
+    case MG_TERM_SYM_DIRICHLET: return 2;
+    case MG_TERM_SPHERE: return 3;
+    default: return 0;
+  }
+}
+const char* op_name(int op) {
+  switch (op) {
+    case MG_OP_FV: return "FV";
+    case MG_OP_EV: return "EV";
+    case MG_OP_VV: return "VV";
+    default: return "V";
+  }
+}
+
+void ensure_ready(Problem& p, cudaStream_t s) {
+  if (p.terms.empty()) throw Error(MG_ERR_VALUE, "no energy terms registered");
+  if (!p.pattern_ready) build_pattern(p, s);
+  if (p.deterministic && !p.layout_ready && patch_supported(p)) build_patch_layout(p, s);
+}
+
+void ensure_partials(Problem& p, int64_t need) {
+  if (need > p.partial_cap) {
+    p.partials.alloc(need);
+    p.partial_cap = need;
+  }
+}
+
+int64_t partials_needed(const Problem& p) {
+  int64_t need = 1;
+  for (auto& t : p.terms) need += elem_partials_needed(t);
+  if (p.mesh->patches.num > need) need = p.mesh->patches.num;
+  return need + 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mg_last_error(void) { return g_err.c_str(); }
+int mg_abi_version(void) { return MG_ABI_VERSION; }
+
+int mg_mesh_create(const int64_t* faces_d, int64_t num_faces, const int64_t* edges_d,
+                   int64_t num_edges, int64_t num_vertices, const double* positions_d,
+                   int patch_vertices, void* stream, mg_mesh** out) {
+  if (!out) return fail(MG_ERR_VALUE, "out is NULL");
+  if (num_vertices < 0 || num_faces < 0 || num_edges < 0) return fail(MG_ERR_VALUE, "negative size");
+  auto* h = new mg_mesh();
+  int rc = guard([&] {
+    h->m.V = num_vertices;
+    h->m.F = num_faces;
+    h->m.patch_vertices = patch_vertices > 0 ? patch_vertices : 128;
+    mesh_build(h->m, faces_d, edges_d, num_edges, positions_d, S(stream));
+  });
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return MG_OK;
+}
+
+int mg_mesh_counts(const mg_mesh* mesh, int64_t* V, int64_t* E, int64_t* F, int64_t* P) {
+  if (!mesh) return fail(MG_ERR_VALUE, "mesh is NULL");
+  if (V) *V = mesh->m.V;
+  if (E) *E = mesh->m.E;
+  if (F) *F = mesh->m.F;
+  if (P) *P = mesh->m.patches.num;
+  return MG_OK;
+}
+
+namespace {
+__global__ void k_widen_pairs(const int32_t* in, int64_t n, int64_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+}  // namespace
+
+int mg_mesh_copy_edges(const mg_mesh* mesh, int64_t* edges_d, void* stream) {
+  if (!mesh) return fail(MG_ERR_VALUE, "mesh is NULL");
+  return guard([&] {
+    int64_t n = 2 * mesh->m.E;
+    if (n) k_widen_pairs<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(mesh->m.edges.p, n, edges_d);
+    MG_LAUNCH_CHECK();
+  });
+}
+
+int mg_mesh_copy_vertex_patches(const mg_mesh* mesh, int32_t* patch_d, void* stream) {
+  if (!mesh) return fail(MG_ERR_VALUE, "mesh is NULL");
+  if (!mesh->m.patches.num) return fail(MG_ERR_STATE, "patches are built with the first deterministic problem");
+  return guard([&] {
+    MG_CUDA(cudaMemcpyAsync(patch_d, mesh->m.patches.patch_of_vertex.p, sizeof(int32_t) * mesh->m.V,
+                            cudaMemcpyDeviceToDevice, S(stream)));
+  });
+}
+
+int mg_mesh_destroy(mg_mesh* mesh) {
+  delete mesh;
+  return MG_OK;
+}
+
+int mg_problem_create(mg_mesh* mesh, int var_dim, int with_hessian, const uint8_t* fixed_mask_d,
+                      int deterministic, mg_problem** out) {
+  if (!mesh || !out) return fail(MG_ERR_VALUE, "mesh/out is NULL");
+  if (var_dim < 1) return fail(MG_ERR_VALUE, "var_dim must be at least 1");
+  auto* h = new mg_problem();
+  int rc = guard([&] {
+    h->mesh = mesh;
+    Problem& p = h->p;
+    p.mesh = &mesh->m;
+    p.n = var_dim;
+    p.with_hessian = with_hessian != 0;
+    p.deterministic = deterministic != 0;
+    const int64_t V = mesh->m.V;
+    p.fixed.alloc(V > 0 ? V : 1);
+    if (fixed_mask_d && V) {
+      MG_CUDA(cudaMemcpy(p.fixed.p, fixed_mask_d, V, cudaMemcpyDeviceToDevice));
+      std::vector<uint8_t> hm(V);
+      MG_CUDA(cudaMemcpy(hm.data(), fixed_mask_d, V, cudaMemcpyDeviceToHost));
+      for (auto b : hm) p.any_fixed |= (b != 0);
+    } else if (V) {
+      MG_CUDA(cudaMemset(p.fixed.p, 0, V));
+    }
+  });
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return MG_OK;
+}
+
+int mg_problem_add_term(mg_problem* prob, int term_type, int op, const double* params, int num_params,
+                        const double* const* attrs_d, int num_attrs, int* term_id) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  const int nat = natural_op(term_type);
+  if (nat < 0) return fail(MG_ERR_VALUE, "unknown builtin term type " + std::to_string(term_type));
+  if (op != MG_OP_FV && op != MG_OP_EV && op != MG_OP_VV && op != MG_OP_V)
+    return fail(MG_ERR_VALUE, "op does not resolve to vertex variables; terms support FV, EV, VV, V");
+  if (op != nat)
+    return fail(MG_ERR_VALUE, std::string("builtin term iterates over op ") + op_name(nat) + ", not " + op_name(op));
+  if (num_params < 0 || num_params > 6) return fail(MG_ERR_VALUE, "at most 6 scalar params");
+  if (num_attrs != attrs_needed(term_type))
+    return fail(MG_ERR_VALUE, "term needs " + std::to_string(attrs_needed(term_type)) + " attribute arrays");
+  if (term_type == MG_TERM_GRAVITY && num_params != 1 + prob->p.n)
+    return fail(MG_ERR_VALUE, "gravity needs params [h2, g_0..g_{n-1}]");
+  if ((term_type == MG_TERM_SYM_DIRICHLET || term_type == MG_TERM_SPHERE) && prob->p.n != 2)
+    return fail(MG_ERR_VALUE, "term requires var_dim == 2");
+  if ((term_type != MG_TERM_SYM_DIRICHLET && term_type != MG_TERM_SPHERE) && (prob->p.n < 2 || prob->p.n > 3))
+    return fail(MG_ERR_UNSUPPORTED, "builtin vertex/edge terms support var_dim 2 or 3");
+  Term t;
+  std::memset(&t.dev, 0, sizeof(t.dev));
+  t.dev.type = term_type;
+  t.dev.op = op;
+  t.dev.P = natural_P(op);
+  for (int i = 0; i < num_params; ++i) t.dev.c[i] = params[i];
+  for (int i = 0; i < num_attrs; ++i) t.dev.a[i] = attrs_d[i];
+  t.M = op_count(prob->p.mesh[0], op);
+  prob->p.terms.push_back(std::move(t));
+  prob->p.pattern_ready = false;
+  prob->p.layout_ready = false;
+  if (term_id) *term_id = (int)prob->p.terms.size() - 1;
+  return MG_OK;
+}
+
+int mg_problem_set_attr(mg_problem* prob, int term_id, int slot, const double* attr_d) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  if (term_id < 0 || term_id >= (int)prob->p.terms.size()) return fail(MG_ERR_VALUE, "bad term id");
+  if (slot < 0 || slot >= 4) return fail(MG_ERR_VALUE, "bad attribute slot");
+  prob->p.terms[term_id].dev.a[slot] = attr_d;
+  return MG_OK;
+}
+
+int mg_precompute_sparsity(mg_problem* prob, int64_t* nnzb, void* stream) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  return guard([&] {
+    Problem& p = prob->p;
+    if (p.terms.empty()) throw Error(MG_ERR_VALUE, "no energy terms registered");
+    build_pattern(p, S(stream));
+    if (p.deterministic && patch_supported(p)) build_patch_layout(p, S(stream));
+    if (nnzb) *nnzb = p.nnzb;
+  });
+}
+
+int mg_copy_pattern(const mg_problem* prob, int64_t* row_offsets_d, int64_t* col_indices_d, void* stream) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  if (!prob->p.pattern_ready) return fail(MG_ERR_STATE, "sparsity pattern not computed");
+  return guard([&] {
+    const Problem& p = prob->p;
+    MG_CUDA(cudaMemcpyAsync(row_offsets_d, p.row_offsets.p, sizeof(int64_t) * (p.mesh->V + 1),
+                            cudaMemcpyDeviceToDevice, S(stream)));
+    if (p.nnzb)
+      MG_CUDA(cudaMemcpyAsync(col_indices_d, p.col_indices.p, sizeof(int64_t) * p.nnzb,
+                              cudaMemcpyDeviceToDevice, S(stream)));
+  });
+}
+
+int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, double* energy_d,
+            double* grad_d, double* hess_d, void* stream) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  Problem& p = prob->p;
+  if (use_psd && !p.with_hessian) return fail(MG_ERR_VALUE, "psd_floor requires a Hessian-mode problem");
+  if (use_psd && !(psd_floor > 0)) return fail(MG_ERR_VALUE, "floor must be positive");
+  if (!x_d || !energy_d || !grad_d) return fail(MG_ERR_VALUE, "x/energy/grad must be non-NULL");
+  if (p.with_hessian && !hess_d && p.nnzb) return fail(MG_ERR_VALUE, "hess must be non-NULL in Hessian mode");
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    ensure_ready(p, s);
+    ensure_partials(p, partials_needed(p));
+    LaunchCtx c{x_d, nullptr, p.any_fixed ? p.fixed.p : nullptr, grad_d, hess_d, nullptr,
+                p.partials.p, use_psd != 0, psd_floor, s};
+    const Mode mode = p.with_hessian ? MODE_HESS : MODE_GRAD;
+    int launches = 0;
+    int64_t np = 0;
+    if (p.deterministic && p.layout_ready) {
+      np = launch_patch(p, mode, c, 0);
+      launches += 1;
+    } else {
+      MG_CUDA(cudaMemsetAsync(grad_d, 0, sizeof(double) * p.n * p.mesh->V, s));
+      if (p.with_hessian && p.nnzb)
+        MG_CUDA(cudaMemsetAsync(hess_d, 0, sizeof(double) * p.n * p.n * p.nnzb, s));
+      for (auto& t : p.terms) {
+        np += launch_elem(p, t, mode, c, np);
+        ++launches;
+      }
+    }
+    reduce_partials(p.partials.p, np, energy_d, s);
+    p.last_launches = launches + 1;
+  });
+}
+
+int mg_energy(mg_problem* prob, const double* x_d, double* energy_d, void* stream) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  Problem& p = prob->p;
+  if (!x_d || !energy_d) return fail(MG_ERR_VALUE, "x/energy must be non-NULL");
+  if (p.terms.empty()) return fail(MG_ERR_VALUE, "no energy terms registered");
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    ensure_partials(p, partials_needed(p));
+    LaunchCtx c{x_d, nullptr, nullptr, nullptr, nullptr, nullptr, p.partials.p, false, 0.0, s};
+    int64_t np = 0;
+    int launches = 0;
+    for (auto& t : p.terms) {
+      np += launch_elem(p, t, MODE_ENERGY, c, np);
+      ++launches;
+    }
+    reduce_partials(p.partials.p, np, energy_d, s);
+    p.last_launches = launches + 1;
+  });
+}
+
+int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, double psd_floor,
+           double* y_d, void* stream) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  Problem& p = prob->p;
+  if (use_psd && !(psd_floor > 0)) return fail(MG_ERR_VALUE, "floor must be positive");
+  if (!x_d || !v_d || !y_d) return fail(MG_ERR_VALUE, "x/v/y must be non-NULL");
+  if (p.terms.empty()) return fail(MG_ERR_VALUE, "no energy terms registered");
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    if (p.deterministic) ensure_ready(p, s);
+    ensure_partials(p, partials_needed(p));
+    LaunchCtx c{x_d, v_d, p.any_fixed ? p.fixed.p : nullptr, nullptr, nullptr, y_d,
+                p.partials.p, use_psd != 0, psd_floor, s};
+    int launches = 0;
+    if (p.deterministic && p.layout_ready) {
+      launch_patch(p, MODE_HVP, c, 0);
+      launches = 1;
+    } else {
+      MG_CUDA(cudaMemsetAsync(y_d, 0, sizeof(double) * p.n * p.mesh->V, s));
+      for (auto& t : p.terms) {
+        launch_elem(p, t, MODE_HVP, c, 0);
+        ++launches;
+      }
+    }
+    p.last_launches = launches;
+  });
+}
+
+int mg_bsr_matvec(const mg_problem* prob, const double* hess_d, const double* v_d, double* y_d, void* stream) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  if (!prob->p.pattern_ready) return fail(MG_ERR_STATE, "sparsity pattern not computed");
+  return guard([&] { launch_bsr_matvec(prob->p, hess_d, v_d, y_d, S(stream)); });
+}
+
+int mg_problem_destroy(mg_problem* prob) {
+  delete prob;
+  return MG_OK;
+}
+
+int mg_last_launch_count(const mg_problem* prob, int* launches) {
+  if (!prob || !launches) return fail(MG_ERR_VALUE, "NULL argument");
+  *launches = prob->p.last_launches;
+  return MG_OK;
+}
+
+int mg_problem_patch_stats(const mg_problem* prob, int64_t* stats4) {
+  if (!prob || !stats4) return fail(MG_ERR_VALUE, "NULL argument");
+  const Problem& p = prob->p;
+  stats4[0] = p.mesh->patches.num;
+  stats4[1] = p.mesh->V;
+  stats4[2] = p.mesh->patches.ribbon_total;
+  stats4[3] = p.recomputed_elements;
+  return MG_OK;
+}
+
+}  // extern "C"

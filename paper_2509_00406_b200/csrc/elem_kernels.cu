@@ -1,0 +1,306 @@
+// Element-parallel kernels: one thread per term element, dual numbers in
+// registers, outputs scattered with fp64 atomics into caller-zeroed buffers.
+// This is the reference's "atomic" accumulation mode (problem.py:16-21,
+// 486-499): merge order is whatever the hardware gives, results agree with
+// the deterministic path to rounding. The energy is reduced through fixed-
+// order per-block partials so it is reproducible in every mode.
+//
+// Per-element pipeline (problem.py:526-544): lift (seeds) -> term_eval ->
+// _extract (symmetrise, optional PSD clamp) -> scatter.
+#include "mg_internal.cuh"
+#include "psd.cuh"
+
+namespace mg {
+
+namespace {
+
+constexpr int TPB = 128;
+
+struct ElemArgs {
+  const double* x;
+  const double* w;
+  const uint8_t* fixed;
+  const int32_t* sel;
+  const int32_t* bids;
+  double* grad;
+  double* hess;
+  double* y;
+  double* partials;
+  double floor;
+  int64_t M;
+};
+
+// Fixed-order block sum (warp shuffle tree, then warp 0 over the warp sums).
+__device__ double block_sum(double v) {
+  __shared__ double ws[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) ws[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    r = lane < nw ? ws[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+template <int P, int N, int K, class H>
+__device__ __forceinline__ void scatter_hess(const ElemArgs& a, int64_t e, const double* h) {
+  const int32_t* b = a.bids + e * P * P;
+#pragma unroll
+  for (int q1 = 0; q1 < P; ++q1)
+#pragma unroll
+    for (int q2 = 0; q2 < P; ++q2) {
+      const int32_t bid = b[q1 * P + q2];
+      if (bid >= 0) {
+        double* dst = a.hess + (int64_t)bid * N * N;
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int c = 0; c < N; ++c) atomicAdd(dst + r * N + c, h[tri(q1 * N + r, q2 * N + c)]);
+      }
+    }
+}
+
+template <int TT, int N, int MODE, bool PSD>
+__global__ void __launch_bounds__(TPB) k_elem(TermDev t, ElemArgs a) {
+  constexpr int P = TermInfo<TT>::P;
+  constexpr int K = P * N;
+  const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  double ev = 0.0;
+  if (e < a.M) {
+    int vid[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) vid[q] = a.sel ? a.sel[e * P + q] : (int)e;
+    bool fr[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) fr[q] = !a.fixed || !a.fixed[vid[q]];
+
+    if constexpr (MODE == MODE_ENERGY) {
+      Vec<Dv<K>, N> X[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < N; ++c) X[q][c].v = a.x[(int64_t)vid[q] * N + c];
+      ev = term_eval<TT, N>(t, e, vid, X).v;
+    } else if constexpr (MODE == MODE_GRAD) {
+      Vec<Dg<K>, N> X[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          X[q][c].v = a.x[(int64_t)vid[q] * N + c];
+#pragma unroll
+          for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
+        }
+      auto r = term_eval<TT, N>(t, e, vid, X);
+      ev = r.v;
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+        if (fr[q])
+#pragma unroll
+          for (int c = 0; c < N; ++c) atomicAdd(a.grad + (int64_t)vid[q] * N + c, r.g[q * N + c]);
+    } else if constexpr (MODE == MODE_HESS || (MODE == MODE_HVP && PSD)) {
+      Vec<Dh<K, true>, N> X[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          X[q][c].v = a.x[(int64_t)vid[q] * N + c];
+#pragma unroll
+          for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
+        }
+      auto r = term_eval<TT, N>(t, e, vid, X);
+      using R = decltype(r);
+      ev = r.v;
+      if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+          if (fr[q])
+#pragma unroll
+            for (int c = 0; c < N; ++c) atomicAdd(a.grad + (int64_t)vid[q] * N + c, r.g[q * N + c]);
+      }
+      // _extract (problem.py:454-476): structural zero -> no Hessian unless
+      // a PSD floor is requested (then project(0) = floor*I).
+      if constexpr (!R::kZero || PSD) {
+        double h[TriN<K>::value];
+        if constexpr (R::kZero) {
+#pragma unroll
+          for (int i = 0; i < TriN<K>::value; ++i) h[i] = 0.0;
+        } else {
+#pragma unroll
+          for (int i = 0; i < TriN<K>::value; ++i) h[i] = r.h[i];
+        }
+        if constexpr (PSD) {
+          // pinned variables are seeded passively by the reference: zero
+          // their rows/cols before the clamp so the free block projects alone
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            if (!fr[q])
+#pragma unroll
+              for (int c = 0; c < N; ++c)
+#pragma unroll
+                for (int j = 0; j < K; ++j) h[tri(q * N + c, j)] = 0.0;
+          extract_psd<P, N>(h, a.floor);
+        } else {
+#pragma unroll
+          for (int i = 0; i < TriN<K>::value; ++i) h[i] = 0.5 * (h[i] + h[i]);
+        }
+        if constexpr (MODE == MODE_HESS) {
+          scatter_hess<P, N, K, R>(a, e, h);
+        } else {
+          double vl[K];
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int c = 0; c < N; ++c) vl[q * N + c] = fr[q] ? a.w[(int64_t)vid[q] * N + c] : 0.0;
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            if (fr[q])
+#pragma unroll
+              for (int c = 0; c < N; ++c) {
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < K; ++j) acc += h[tri(q * N + c, j)] * vl[j];
+                atomicAdd(a.y + (int64_t)vid[q] * N + c, acc);
+              }
+        }
+      }
+    } else {  // MODE_HVP, no PSD: forward-over-forward dual, H never formed
+      Vec<Df<K, true>, N> X[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          X[q][c].v = a.x[(int64_t)vid[q] * N + c];
+          X[q][c].vd = fr[q] ? a.w[(int64_t)vid[q] * N + c] : 0.0;
+#pragma unroll
+          for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
+        }
+      auto r = term_eval<TT, N>(t, e, vid, X);
+      using R = decltype(r);
+      if constexpr (!R::kZero) {
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+          if (fr[q])
+#pragma unroll
+            for (int c = 0; c < N; ++c) atomicAdd(a.y + (int64_t)vid[q] * N + c, r.gd[q * N + c]);
+      }
+    }
+  }
+  if constexpr (MODE != MODE_HVP) {
+    const double s = block_sum(ev);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
+  }
+}
+
+template <int TT, int N>
+void launch_tn(const Term& t, Mode mode, bool psd, const ElemArgs& a, cudaStream_t s) {
+  const unsigned grid = (unsigned)((a.M + TPB - 1) / TPB);
+  switch (mode) {
+    case MODE_ENERGY: k_elem<TT, N, MODE_ENERGY, false><<<grid, TPB, 0, s>>>(t.dev, a); break;
+    case MODE_GRAD: k_elem<TT, N, MODE_GRAD, false><<<grid, TPB, 0, s>>>(t.dev, a); break;
+    case MODE_HESS:
+      if (psd) k_elem<TT, N, MODE_HESS, true><<<grid, TPB, 0, s>>>(t.dev, a);
+      else k_elem<TT, N, MODE_HESS, false><<<grid, TPB, 0, s>>>(t.dev, a);
+      break;
+    case MODE_HVP:
+      if (psd) k_elem<TT, N, MODE_HVP, true><<<grid, TPB, 0, s>>>(t.dev, a);
+      else k_elem<TT, N, MODE_HVP, false><<<grid, TPB, 0, s>>>(t.dev, a);
+      break;
+  }
+  MG_LAUNCH_CHECK();
+}
+
+template <int TT>
+void launch_t(int n, const Term& t, Mode mode, bool psd, const ElemArgs& a, cudaStream_t s) {
+  if constexpr (TT == MG_TERM_SYM_DIRICHLET || TT == MG_TERM_SPHERE) {
+    if (n != 2) throw Error(MG_ERR_VALUE, "term requires var_dim == 2");
+    launch_tn<TT, 2>(t, mode, psd, a, s);
+  } else {
+    if (n == 3) launch_tn<TT, 3>(t, mode, psd, a, s);
+    else if (n == 2) launch_tn<TT, 2>(t, mode, psd, a, s);
+    else throw Error(MG_ERR_UNSUPPORTED, "builtin vertex/edge terms support var_dim 2 or 3");
+  }
+}
+
+__global__ void k_reduce(const double* partials, int64_t n, double* out) {
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+template <int N>
+__global__ void k_bsr_matvec(const int64_t* ro, const int32_t* col, const double* H, const double* v,
+                             double* y, int64_t V) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  double acc[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) acc[r] = 0.0;
+  for (int64_t k = ro[i]; k < ro[i + 1]; ++k) {
+    const double* b = H + k * N * N;
+    const double* vv = v + (int64_t)col[k] * N;
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) acc[r] += b[r * N + c] * vv[c];
+  }
+#pragma unroll
+  for (int r = 0; r < N; ++r) y[i * N + r] = acc[r];
+}
+
+}  // namespace
+
+int64_t elem_partials_needed(const Term& t) { return (t.M + TPB - 1) / TPB; }
+
+int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c,
+                    int64_t partial_offset) {
+  if (t.M == 0) return 0;
+  ElemArgs a;
+  a.x = c.x;
+  a.w = c.w;
+  a.fixed = p.any_fixed ? p.fixed.p : nullptr;
+  a.sel = op_sel(*p.mesh, t.dev.op);
+  a.bids = t.bids.p;
+  a.grad = c.grad;
+  a.hess = c.hess;
+  a.y = c.y;
+  a.partials = c.partials + partial_offset;
+  a.floor = c.floor;
+  a.M = t.M;
+  switch (t.dev.type) {
+    case MG_TERM_INERTIA: launch_t<MG_TERM_INERTIA>(p.n, t, mode, c.psd, a, c.stream); break;
+    case MG_TERM_SPRING: launch_t<MG_TERM_SPRING>(p.n, t, mode, c.psd, a, c.stream); break;
+    case MG_TERM_GRAVITY: launch_t<MG_TERM_GRAVITY>(p.n, t, mode, c.psd, a, c.stream); break;
+    case MG_TERM_EDGE_LENGTH: launch_t<MG_TERM_EDGE_LENGTH>(p.n, t, mode, c.psd, a, c.stream); break;
+    case MG_TERM_SYM_DIRICHLET: launch_t<MG_TERM_SYM_DIRICHLET>(p.n, t, mode, c.psd, a, c.stream); break;
+    case MG_TERM_SPHERE: launch_t<MG_TERM_SPHERE>(p.n, t, mode, c.psd, a, c.stream); break;
+    default: throw Error(MG_ERR_VALUE, "unknown term type");
+  }
+  return mode == MODE_HVP ? 0 : elem_partials_needed(t);
+}
+
+void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s) {
+  k_reduce<<<1, 1024, 0, s>>>(partials, n, out);
+  MG_LAUNCH_CHECK();
+}
+
+void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s) {
+  const int64_t V = p.mesh->V;
+  const unsigned grid = (unsigned)((V + 255) / 256);
+  switch (p.n) {
+    case 1: k_bsr_matvec<1><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V); break;
+    case 2: k_bsr_matvec<2><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V); break;
+    case 3: k_bsr_matvec<3><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V); break;
+    default: throw Error(MG_ERR_UNSUPPORTED, "bsr matvec supports block dims 1..3");
+  }
+  MG_LAUNCH_CHECK();
+}
+
+}  // namespace mg

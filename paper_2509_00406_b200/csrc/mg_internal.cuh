@@ -1,0 +1,168 @@
+// Library-internal state shared by the setup, kernel and ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/meshgrad_b200.h"
+#include "terms.cuh"
+
+namespace mg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define MG_CUDA(expr)                                                                       \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      throw ::mg::Error(MG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define MG_LAUNCH_CHECK() MG_CUDA(cudaGetLastError())
+
+// Owned device buffer (library-owned state only; caller buffers are raw pointers).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept { reset(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; return *this; }
+  ~DBuf() { reset(); }
+  void alloc(int64_t count) {
+    reset();
+    if (count > 0) MG_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    n = count;
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Stream-ordered temporary (setup paths).
+struct Tmp {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit Tmp(cudaStream_t st, size_t bytes) : s(st) {
+    if (bytes) MG_CUDA(cudaMallocAsync(&p, bytes, s));
+  }
+  ~Tmp() { if (p) cudaFreeAsync(p, s); }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Vertex patches (RXMesh-style, re-designed for row-owner assembly):
+//   owned rows: a contiguous run of the Morton-ordered vertex list;
+//   ribbon: vertices referenced by elements incident to owned rows but owned
+//   by another patch. Elements incident to owned rows are listed per patch
+//   (ribbon elements therefore appear in two or three patches: the owner
+//   computes, nobody communicates).
+struct PatchSet {
+  int64_t num = 0;
+  int vmax = 0;                 // owned rows per patch (upper bound)
+  DBuf<int32_t> order;          // (V) vertex ids, patch-major
+  DBuf<int32_t> patch_of_vertex;
+  DBuf<int32_t> vtx_offsets;    // (num+1) owned+ribbon vertex list offsets
+  DBuf<int32_t> vtx;            // patch vertex lists (owned first, then ribbon)
+  DBuf<int32_t> owned_count;    // (num)
+  int64_t ribbon_total = 0;
+};
+
+struct Mesh {
+  int64_t V = 0, E = 0, F = 0;
+  DBuf<int32_t> faces;   // (F,3)
+  DBuf<int32_t> edges;   // (E,2) canonical, sorted
+  DBuf<double> pos;      // (V,3) or empty
+  PatchSet patches;
+  int patch_vertices = 128;
+};
+
+struct Term {
+  TermDev dev;
+  int64_t M = 0;               // elements
+  DBuf<int32_t> bids;          // (M,P,P) Hessian block ids, -1 = pinned pair
+  // patch layout (deterministic path)
+  DBuf<int32_t> pe_offsets;    // (num_patches+1)
+  DBuf<int32_t> pe_elem;       // element id
+  DBuf<uint32_t> pe_local;     // packed local vertex ids (10 bits each)
+  DBuf<uint32_t> pe_pos;       // packed row positions (see patch kernels)
+  DBuf<uint8_t> pe_color;
+  int num_colors = 0;
+};
+
+struct Problem {
+  Mesh* mesh = nullptr;
+  int n = 3;
+  bool with_hessian = true;
+  bool deterministic = true;
+  DBuf<uint8_t> fixed;         // (V)
+  bool any_fixed = false;
+  std::vector<Term> terms;
+  bool pattern_ready = false;
+  bool layout_ready = false;
+  int64_t nnzb = 0;
+  DBuf<int64_t> row_offsets;   // (V+1)
+  DBuf<int64_t> col_indices;   // (nnzb)
+  DBuf<int32_t> col32;         // (nnzb)
+  DBuf<double> partials;       // energy partials
+  int64_t partial_cap = 0;
+  int last_launches = 0;
+  // patch-owner assembly state
+  DBuf<int32_t> prow_offsets;  // (num_patches+1) owned-row block offsets within patch smem
+  int max_patch_blocks = 0;
+  int64_t recomputed_elements = 0;
+};
+
+// element vertex ids of an op (nullptr for V: the element is the vertex)
+inline const int32_t* op_sel(const Mesh& m, int op) {
+  if (op == MG_OP_FV) return m.faces.p;
+  if (op == MG_OP_EV) return m.edges.p;
+  return nullptr;
+}
+inline int64_t op_count(const Mesh& m, int op) {
+  if (op == MG_OP_FV) return m.F;
+  if (op == MG_OP_EV) return m.E;
+  return m.V;
+}
+
+// setup.cu
+void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t num_edges_in,
+                const double* pos_d, cudaStream_t s);
+void build_pattern(Problem& p, cudaStream_t s);
+void build_patch_layout(Problem& p, cudaStream_t s);
+
+// elem_kernels.cu (element-parallel, atomic accumulation)
+enum Mode { MODE_ENERGY = 0, MODE_GRAD = 1, MODE_HESS = 2, MODE_HVP = 3 };
+struct LaunchCtx {
+  const double* x;
+  const double* w;     // hvp direction
+  const uint8_t* fixed;
+  double* grad;
+  double* hess;
+  double* y;
+  double* partials;    // energy partials
+  bool psd;
+  double floor;
+  cudaStream_t stream;
+};
+// Launch one term element-parallel; returns number of energy partials written.
+int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c,
+                    int64_t partial_offset);
+int64_t elem_partials_needed(const Term& t);
+// patch_kernels.cu (deterministic row-owner assembly)
+int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
+bool patch_supported(const Problem& p);
+// fixed-order reduction of energy partials -> out[0]
+void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s);
+void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s);
+
+}  // namespace mg

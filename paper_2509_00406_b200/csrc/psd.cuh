@@ -1,0 +1,152 @@
+// Per-element eigenvalue clamp, in registers.
+//
+// Reference: project_psd (meshgrad/active.py:490-504): w, Q = eigh(H);
+// w = max(w, floor); out = Q diag(w) Q^T; out = 0.5 (out + out^T).
+// `_extract` (problem.py:454-476) symmetrises first and only projects lanes
+// whose Hessian is entirely finite.
+//
+// The spectral projector is unique even when eigenvectors are not, so any
+// accurate symmetric eigensolver reproduces the reference to rounding
+// (cyclic Jacobi matched eigh to <= 1e-14 relative).
+//
+// Two paths:
+//  * cyclic Jacobi on the packed K x K matrix (generic, K <= 12);
+//  * a two-point shortcut: when H == [[A,-A],[-A,A]] bitwise (every
+//    translation-invariant edge term: springs, edge lengths), the spectrum is
+//    {2 eig(A)} U {0,0,0}, so P(H) = 1/2 [[P2, -P2],[-P2, P2]] + f/2 [[I, I],[I, I]]
+//    with P2 = Q max(2 Lambda, f) Q^T from an n x n Jacobi. Exact same
+//    projector, a fraction of the flops. The test is a runtime bitwise check,
+//    so any other Hessian silently takes the generic path.
+#pragma once
+#include "dual.cuh"
+
+namespace mg {
+
+// In-place: A (packed K x K, symmetric) -> Q max(Lambda, floor) Q^T.
+template <int K>
+MG_DI void jacobi_project(double* A, double floor) {
+  constexpr int T = TriN<K>::value;
+  double Q[K][K];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) Q[i][j] = (i == j) ? 1.0 : 0.0;
+
+  double fro2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) fro2 += (i == j ? 1.0 : 2.0) * A[tri(i, j)] * A[tri(i, j)];
+  const double tol2 = fro2 * 1e-34;  // off-diagonal mass ~1e-17 relative
+
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    double off = 0.0;
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < i; ++j) off += A[tri(i, j)] * A[tri(i, j)];
+    if (!(off > tol2)) break;
+#pragma unroll
+    for (int p = 0; p < K - 1; ++p) {
+#pragma unroll
+      for (int q = p + 1; q < K; ++q) {
+        const double apq = A[tri(q, p)];
+        if (apq != 0.0) {
+          const double app = A[tri(p, p)], aqq = A[tri(q, q)];
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + ::sqrt(theta * theta + 1.0));
+          const double c = 1.0 / ::sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (k != p && k != q) {
+              const double akp = A[tri(k, p)], akq = A[tri(k, q)];
+              A[tri(k, p)] = c * akp - s * akq;
+              A[tri(k, q)] = s * akp + c * akq;
+            }
+          }
+          A[tri(p, p)] = app - t * apq;
+          A[tri(q, q)] = aqq + t * apq;
+          A[tri(q, p)] = 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double qkp = Q[k][p], qkq = Q[k][q];
+            Q[k][p] = c * qkp - s * qkq;
+            Q[k][q] = s * qkp + c * qkq;
+          }
+        }
+      }
+    }
+  }
+  double w[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double l = A[tri(j, j)];
+    w[j] = l > floor ? l : floor;  // np.maximum (NaN-free here: lanes are finite)
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc += Q[i][j] * w[j] * Q[k][j];
+      A[tri(i, k)] = acc;
+    }
+  (void)T;
+}
+
+template <int K>
+MG_DI bool all_finite(const double* A) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < TriN<K>::value; ++i) ok &= isfinite(A[i]);
+  return ok;
+}
+
+// `_extract` epilogue for a packed Hessian: symmetrise (identity on packed
+// storage except for overflow, mirrored anyway) then clamp finite lanes.
+// N: per-vertex block dim; P: vertices per element (K = P*N).
+template <int P, int N>
+MG_DI void extract_psd(double* H, double floor) {
+  constexpr int K = P * N;
+#pragma unroll
+  for (int i = 0; i < TriN<K>::value; ++i) H[i] = 0.5 * (H[i] + H[i]);
+  if (!all_finite<K>(H)) return;
+  if constexpr (P == 2) {
+    // bitwise two-point structure test
+    bool two = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        two &= H[tri(N + i, N + j)] == H[tri(i, j)];
+        two &= H[tri(N + i, j)] == -H[tri(i, j)];
+        if (i != j) two &= H[tri(N + j, i)] == -H[tri(i, j)];
+      }
+    if (two) {
+      double A2[TriN<N>::value];
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) A2[tri(i, j)] = 2.0 * H[tri(i, j)];
+      jacobi_project<N>(A2, floor);
+      const double hf = 0.5 * floor;
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double p = 0.5 * A2[tri(i, j)];
+          const double d = (i == j) ? hf : 0.0;
+          if (j <= i) {
+            H[tri(i, j)] = p + d;
+            H[tri(N + i, N + j)] = p + d;
+          }
+          H[tri(N + i, j)] = -p + d;
+        }
+      return;
+    }
+  }
+  jacobi_project<K>(H, floor);
+}
+
+}  // namespace mg

@@ -1,0 +1,135 @@
+"""CUDA engine vs the reference's golden vectors and the pinned oracle.
+
+Bar (BASELINE north_star): Hessian pattern bit-exact; energy, gradient,
+Hessian values and HVP within 1e-10 relative (max|diff| / max|ref|, NaN
+masks equal) in fp64.
+"""
+
+import numpy as np
+import pytest
+
+from engine_util import engine_mesh, engine_problem
+from golden_util import FLOOR, cases, load, oracle_problem, rel, rel_scalar, states
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+MODES = ["deterministic", "atomic"]
+CASES = [c for c in cases() if c != "cloth16_asis"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_edges_bit_exact(name):
+    d = load(name)
+    assert np.array_equal(engine_mesh(d).to_device().edges, d["edges"])
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", CASES)
+def test_matches_reference(name, mode):
+    d = load(name)
+    p = engine_problem(d, mode)
+    if "row_offsets" in d and p.with_hessian:
+        h = p.precompute_sparsity()
+        assert np.array_equal(h.row_offsets, d["row_offsets"])
+        assert np.array_equal(h.col_indices, d["col_indices"])
+    for s in states(d):
+        x = d[f"s{s}_x"]
+        p.x = x
+        e = p.eval_terms()
+        assert rel_scalar(e, d[f"s{s}_energy"]) <= TOL, (e, d[f"s{s}_energy"])
+        assert rel(p.grad, d[f"s{s}_grad"]) <= TOL
+        if f"s{s}_hess" in d:
+            assert rel(p.hess.values, d[f"s{s}_hess"]) <= TOL
+        if f"s{s}_psd_hess" in d:
+            e = p.eval_terms(psd_floor=FLOOR)
+            assert rel_scalar(e, d[f"s{s}_psd_energy"]) <= TOL
+            assert rel(p.grad, d[f"s{s}_psd_grad"]) <= TOL
+            assert rel(p.hess.values, d[f"s{s}_psd_hess"]) <= TOL
+        assert rel_scalar(p.eval_energy_only(x), d[f"s{s}_energy_only"]) <= TOL
+        k = 0
+        while f"s{s}_v{k}" in d:
+            v = d[f"s{s}_v{k}"]
+            ref = d[f"s{s}_hvp{k}"]
+            got = p.hvp(x, v)
+            if np.isfinite(ref).all():
+                assert rel(got, ref) <= TOL
+            else:  # non-finite states: NaN surfaces (masks may differ for HVP)
+                assert not np.isfinite(got).all()
+            if f"s{s}_hvp_psd{k}" in d:
+                ref = d[f"s{s}_hvp_psd{k}"]
+                got = p.hvp(x, v, psd_floor=FLOOR)
+                if np.isfinite(ref).all():
+                    assert rel(got, ref) <= TOL
+            k += 1
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_cloth_asis_trajectory(mode):
+    """Every Newton iterate of the unmodified 2-step ClothSim (config 1 as-is)."""
+    import torch
+
+    d = load("cloth16_asis")
+    target = torch.from_numpy(d["s0_target"].copy()).cuda()
+    d["a_target"] = d["s0_target"]
+    p = engine_problem(d, mode)
+    p.set_term_attr(0, "target", target)
+    for s in range(int(d["iterates"])):
+        target.copy_(torch.from_numpy(d[f"s{s}_target"]))
+        p.x = d[f"s{s}_x"]
+        floor = float(d[f"s{s}_floor"])
+        e = p.eval_terms(psd_floor=None if np.isnan(floor) else floor)
+        assert rel_scalar(e, d[f"s{s}_energy"]) <= TOL
+        assert rel(p.grad, d[f"s{s}_grad"]) <= TOL
+        assert rel(p.hess.values, d[f"s{s}_hess"]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cloth64", "dirichlet_ico2", "sphere_ico2", "smooth_ico2"])
+def test_deterministic_is_bitwise_reproducible(name):
+    d = load(name)
+    p = engine_problem(d, "deterministic")
+    p.x = d["s0_x"]
+    e1 = p.eval_terms(psd_floor=FLOOR)
+    g1, h1 = p.grad, p.hess.values
+    y1 = p.hvp(d["s0_x"], d["s0_v0"])
+    for _ in range(3):
+        assert p.eval_terms(psd_floor=FLOOR) == e1
+        assert np.array_equal(p.grad, g1)
+        assert np.array_equal(p.hess.values, h1)
+        assert np.array_equal(p.hvp(d["s0_x"], d["s0_v0"]), y1)
+
+
+@pytest.mark.parametrize("name", ["cloth64", "dirichlet_ico2", "sphere_ico2"])
+def test_hvp_equals_assembled_matvec(name):
+    """Two independent kernels: matrix-free HVP vs SpMV on the assembled H."""
+    d = load(name)
+    p = engine_problem(d)
+    x, v = d["s0_x"], d["s0_v0"]
+    p.x = x
+    p.eval_terms()
+    hv = p.hess.matvec(v)
+    free = np.repeat(~p.fixed_mask, p.n)
+    assert rel(p.hvp(x, np.where(free, v, 0.0))[free], hv[free]) <= TOL
+
+
+def test_error_behaviour():
+    import paper_2509_00406_b200 as mg
+
+    d = load("spring_single")
+    p = engine_problem(d)
+    p.x = d["s0_x"]
+    with pytest.raises(ValueError, match="floor must be positive"):
+        p.eval_terms(psd_floor=0.0)
+    with pytest.raises(ValueError, match="shape"):
+        p.eval_energy_only(np.zeros(5))
+    with pytest.raises(ValueError, match="iterates over"):
+        p.add_term(mg.Element.VERTEX, mg.Op.FV, mg.EdgeLength())
+    q = mg.Problem(engine_mesh(d), 3, with_hessian=False)
+    q.add_term(mg.Element.EDGE, mg.Op.EV, mg.EdgeLength())
+    with pytest.raises(ValueError, match="Hessian-mode"):
+        q.eval_terms(psd_floor=1e-9)
+    r = mg.Problem(engine_mesh(d), 3)
+    with pytest.raises(ValueError, match="no energy terms"):
+        r.precompute_sparsity()
+    with pytest.raises(mg.MeshError, match="repeated"):
+        mg.Mesh(np.eye(3), [[0, 0, 1]])
