@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: mass-spring cloth Newton-step assembly on a 2048x2048 grid.
+
+Headline workload (BASELINE.json configs[1]): `Problem.eval_terms(psd_floor=1e-9)`
+— energy, gradient and block-CSR Hessian with per-element PSD clamp, exactly
+what `newton_solve` calls each Newton iteration — on the ClothSim energy
+(inertia + spring + gravity, default pins) over generate_grid(2048, 1/2047),
+fp64. A step = one such evaluation. Unit = term-element evaluations / s
+(2V + E per call).
+
+  value  : device time, inputs resident in HBM (x, target, masses, rest
+           lengths; outputs 2.1 GB > L2, so no L2 flush is needed)
+  e2e    : the public API with host buffers: pinned x H2D, eval, energy +
+           gradient D2H, every step
+  roofline: HBM, algorithmic bytes (inputs once + outputs once) / kernel time
+  cpu_baseline: the CPU oracle port (oracle/, restating meshgrad) on a bounded
+           sample, all host threads
+
+`--impl reference` runs the reference arm: the CPU oracle port on the same
+metric (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOOR = 1e-9
+GRID = 2048
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--grid", type=int, default=GRID)
+    ap.add_argument("--accumulation", default="deterministic", choices=["deterministic", "atomic"])
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary workloads")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--profile", action="store_true", help="few steps, headline only (for ncu)")
+    ap.add_argument("--profile-call", default="psd", choices=["psd", "plain", "hvp", "hvp_psd", "energy"],
+                    help="which call --profile runs")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workloads
+
+def cloth_inputs(n, seed=0):
+    from paper_2509_00406_b200.mesh import grid_arrays
+
+    pos, faces = grid_arrays(n, 1.0 / (n - 1))
+    rng = np.random.default_rng(seed)
+    sig = 0.01 / (n - 1)
+    target = pos + sig * rng.normal(size=pos.shape)
+    x = (pos + sig * rng.normal(size=pos.shape)).ravel()
+    v = np.random.default_rng(1).normal(size=x.size)
+    return pos, faces, target, x, v
+
+
+def cloth_sizes(n):
+    V = n * n
+    E = 3 * n * n - 4 * n + 1
+    return V, E
+
+
+def cloth_bytes(V, E, nnzb):
+    # compulsory traffic per call: x, target, masses, rest lengths,
+    # edge endpoints (int32 pairs) read once; grad and Hessian blocks written once
+    return 24 * V + 24 * V + 8 * V + 8 * E + 8 * E + 24 * V + 72 * nnzb
+
+
+def build_engine_cloth(n, accumulation):
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import ClothConfig, cloth_problem, default_pins, lumped_masses
+
+    pos, faces, target, x, v = cloth_inputs(n)
+    mesh = mg.Mesh(pos, faces)
+    cfg = ClothConfig(grid_n=n, spacing=1.0 / (n - 1))
+    target_d = torch.from_numpy(target).cuda()
+    masses_d = torch.from_numpy(lumped_masses(mesh, cfg.mass_density)).cuda()
+    p = cloth_problem(cfg, mesh, target_d, masses=masses_d, pinned=default_pins(n), accumulation=accumulation)
+    p.precompute_sparsity()
+    p.x = x
+    return p, x, v
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def time_device(fn, steps, warmup, dist=None):
+    """Mean ms per step with CUDA events on the current stream; max over ranks."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(st)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(st)
+    torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    total = ev[0].elapsed_time(ev[-1])
+    if dist is not None:
+        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+        dist.barrier()
+    return total / steps, per
+
+
+# -------------------------------------------------------------- CPU baseline
+
+def cpu_oracle_rate(n_sample, reps=1, psd=True):
+    """Oracle port (oracle/) on a cloth n_sample^2 grid, all host threads."""
+    from oracle import OracleProblem
+    from oracle.engine import default_workers
+    from paper_2509_00406_b200.apps import default_pins, lumped_masses
+    from paper_2509_00406_b200.mesh import Mesh, _host_edges
+    from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+
+    pos, faces, target, x, _ = cloth_inputs(n_sample)
+    nv = len(pos)
+    edges = _host_edges(faces, None, nv)
+    mesh = Mesh(pos, faces)
+    mesh._edges = edges
+    masses = lumped_masses(mesh, 1.0)
+    d = pos[edges[:, 1]] - pos[edges[:, 0]]
+    l2 = np.einsum("ij,ij->i", d, d)
+    h = 0.01
+    terms = [("V", Inertia(masses, target)), ("EV", Spring(l2, 0.5 * 1e4 * h * h)),
+             ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
+    workers = default_workers()
+    op = OracleProblem(nv, faces, edges, 3, terms, with_hessian=True, fixed_vertices=default_pins(n_sample),
+                       workers=workers, accumulation="atomic")
+    op.eval_terms(x, psd_floor=FLOOR if psd else None)  # warm-up (layout outside the timed region)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        op.eval_terms(x, psd_floor=FLOOR if psd else None)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    units = 2 * nv + len(edges)
+    return units / t, workers, f"cloth {n_sample}x{n_sample} ({units} term-elements), eval_terms(psd_floor=1e-9), median of {reps}"
+
+
+# ------------------------------------------------------------------- arms
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sample = 256
+    rates = []
+    for _ in range(args.warmup):
+        cpu_oracle_rate(sample, reps=1)
+    for _ in range(args.steps):
+        r, cores, desc = cpu_oracle_rate(sample, reps=1)
+        rates.append(r)
+    V, E = cloth_sizes(args.grid)
+    val = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": "term-element evaluations/s, cloth Newton-step grad+Hessian assembly (psd_floor=1e-9)",
+        "value": val, "unit": "term-elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (2 * V + E) / val * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cloth grid {args.grid}x{args.grid} Newton-step eval_terms(psd_floor=1e-9)",
+                   "sample": f"each step: {desc}"},
+        "cpu_baseline": {"value": val, "unit": "term-elements/s", "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": val, "unit": "term-elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_engine(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    else:
+        torch.cuda.set_device(0)
+
+    n = args.grid
+    V, E = cloth_sizes(n)
+    units = 2 * V + E
+    t_setup = time.perf_counter()
+    p, x, v = build_engine_cloth(n, args.accumulation)
+    t_setup = time.perf_counter() - t_setup
+    nnzb = p.hess.nnz_blocks
+    steps, warmup = (2, 1) if args.profile else (args.steps, args.warmup)
+
+    def step():
+        p.eval_terms(psd_floor=FLOOR, sync=False)
+
+    if args.profile and args.profile_call != "psd":
+        import torch as _t
+
+        vd = _t.from_numpy(v).cuda()
+        yd = _t.empty_like(vd)
+        step = {"plain": lambda: p.eval_terms(sync=False),
+                "hvp": lambda: p.hvp(p.x_device, vd, out=yd),
+                "hvp_psd": lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=yd),
+                "energy": lambda: p.eval_energy_only(p.x_device)}[args.profile_call]
+
+    clk = Clocks(local)
+    ms, per = time_device(step, steps, warmup, dist)
+    clocks = clk.stop()
+    launches = p.launch_count()
+    value = world * units / (ms * 1e-3)
+    bytes_call = cloth_bytes(V, E, nnzb)
+    peak, peak_kind = peaks()
+    achieved = bytes_call / (ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": peak_kind, "algorithmic_bytes_per_launch": bytes_call,
+                "kernel": "k_patch<3,LIGHT,HESS,psd>"}
+    if args.profile:
+        print(json.dumps({"profile": True, "ms_per_step": ms}), flush=True)
+        return
+
+    # e2e through the public API with host buffers
+    x_host = torch.from_numpy(x).pin_memory()
+    g_host = torch.empty(3 * V, dtype=torch.float64).pin_memory()
+    e_host = torch.empty(1, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        p.x_device.copy_(x_host, non_blocking=True)
+        p.eval_terms(psd_floor=FLOOR, sync=False)
+        g_host.copy_(p.grad_device, non_blocking=True)
+        e_host.copy_(p.energy_device, non_blocking=True)
+
+    ms_e2e, _ = time_device(e2e_step, max(3, steps // 2), 2, dist)
+    e2e = {"value": world * units / (ms_e2e * 1e-3), "unit": "term-elements/s",
+           "h2d_bytes_per_step": 24 * V, "d2h_bytes_per_step": 24 * V + 8, "ms_per_step": ms_e2e}
+
+    extras = {}
+    if not args.no_extras and world == 1:
+        extras = run_extras(p, x, v, V, E, nnzb, steps, warmup, peak)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r, cores, desc = cpu_oracle_rate(256, reps=3)
+        cpu = {"value": r, "unit": "term-elements/s", "cores": cores, "kind": "port", "sample": desc}
+    if rank == 0:
+        line = {
+            "metric": "term-element evaluations/s, cloth Newton-step grad+Hessian assembly (psd_floor=1e-9)",
+            "value": value, "unit": "term-elements/s", "n_gpus": world, "steps": steps, "warmup": warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cloth grid {n}x{n} (V={V}, E={E}, F={2 * (n - 1) ** 2}, nnzb={nnzb}) "
+                                   "Newton-step eval_terms(psd_floor=1e-9), default pins",
+                       "accumulation": args.accumulation, "l2": "inputs+outputs 2.6 GB > 126 MB L2; no flush",
+                       "parallelism": f"replica x{world}" if world > 1 else "1 GPU",
+                       "faces_per_s": world * 2 * (n - 1) ** 2 / (ms * 1e-3), "setup_s": t_setup},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * steps,
+            "clocks": clocks,
+            "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_extras(p, x, v, V, E, nnzb, steps, warmup, peak):
+    """Secondary workloads of the same path, each with its own roofline."""
+    import torch
+
+    out = {}
+    xd = p.x_device
+    vd = torch.from_numpy(v).cuda()
+    y = torch.empty_like(vd)
+    k = max(3, steps // 2)
+    ms, _ = time_device(lambda: p.eval_terms(sync=False), k, 2)
+    b = cloth_bytes(V, E, nnzb)
+    out["cloth_grad_hess"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
+                              "hbm_frac": b / (ms * 1e-3) / 1e9 / peak}
+    ms, _ = time_device(lambda: p.hvp(xd, vd, out=y), k, 2)
+    b = 24 * V * 4 + 8 * V + 8 * E + 8 * E  # x, target(unused by H), v, y, masses, rest, edges
+    out["cloth_hvp"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
+                        "hbm_frac": (24 * V * 3 + 8 * V + 16 * E) / (ms * 1e-3) / 1e9 / peak}
+    ms, _ = time_device(lambda: p.hvp(xd, vd, psd_floor=FLOOR, out=y), k, 2)
+    out["cloth_hvp_psd"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3)}
+    ms, _ = time_device(lambda: p.eval_energy_only(xd), k, 2)
+    out["cloth_energy_only"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3)}
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_engine(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,8 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
+    if path is None and os.environ.get("MG_LIB"):
+        path = os.environ["MG_LIB"]
     p = Path(path) if path is not None else LIB_PATH
     if not p.exists():
         raise EngineUnavailable(
@@ -88,8 +90,7 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if path is None:
-        _lib = lib
+    _lib = lib
     return lib
 
 

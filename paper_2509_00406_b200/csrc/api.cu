@@ -71,7 +71,7 @@ const char* op_name(int op) {
 
 void ensure_ready(Problem& p, cudaStream_t s) {
   if (p.terms.empty()) throw Error(MG_ERR_VALUE, "no energy terms registered");
-  if (!p.pattern_ready) build_pattern(p, s);
+  if (p.with_hessian && !p.pattern_ready) build_pattern(p, s);
   if (p.deterministic && !p.layout_ready && patch_supported(p)) build_patch_layout(p, s);
 }
 

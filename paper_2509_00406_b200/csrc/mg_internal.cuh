@@ -68,13 +68,24 @@ struct Tmp {
 //   computes, nobody communicates).
 struct PatchSet {
   int64_t num = 0;
-  int vmax = 0;                 // owned rows per patch (upper bound)
-  DBuf<int32_t> order;          // (V) vertex ids, patch-major
+  int R = 128;                  // owned rows per patch (last patch may hold fewer)
+  DBuf<int32_t> order;          // (V) vertex ids in Morton order; patch p owns order[p*R, p*R+R)
+  DBuf<int32_t> rank;           // (V) inverse of order
   DBuf<int32_t> patch_of_vertex;
-  DBuf<int32_t> vtx_offsets;    // (num+1) owned+ribbon vertex list offsets
-  DBuf<int32_t> vtx;            // patch vertex lists (owned first, then ribbon)
-  DBuf<int32_t> owned_count;    // (num)
-  int64_t ribbon_total = 0;
+  int64_t ribbon_total = 0;     // of the most recent problem layout
+};
+
+// Per-op element lists of every patch: the elements incident to the patch's
+// owned rows (owned + ribbon elements), sorted by (color, element id).
+struct OpLayout {
+  int op = -1, P = 0;
+  int64_t count = 0;
+  DBuf<int32_t> off;      // (num_patches+1)
+  DBuf<int32_t> elem;     // element id
+  DBuf<uint16_t> local;   // (count, P) patch-local vertex index
+  DBuf<uint8_t> pos;      // (count, P, P) column position of slot q' in the row of owned slot q (255: none)
+  DBuf<uint8_t> color;    // conflict-free color: no two same-color entries share an owned vertex
+  int num_colors = 0;
 };
 
 struct Mesh {
@@ -90,13 +101,6 @@ struct Term {
   TermDev dev;
   int64_t M = 0;               // elements
   DBuf<int32_t> bids;          // (M,P,P) Hessian block ids, -1 = pinned pair
-  // patch layout (deterministic path)
-  DBuf<int32_t> pe_offsets;    // (num_patches+1)
-  DBuf<int32_t> pe_elem;       // element id
-  DBuf<uint32_t> pe_local;     // packed local vertex ids (10 bits each)
-  DBuf<uint32_t> pe_pos;       // packed row positions (see patch kernels)
-  DBuf<uint8_t> pe_color;
-  int num_colors = 0;
 };
 
 struct Problem {
@@ -116,8 +120,13 @@ struct Problem {
   DBuf<double> partials;       // energy partials
   int64_t partial_cap = 0;
   int last_launches = 0;
-  // patch-owner assembly state
-  DBuf<int32_t> prow_offsets;  // (num_patches+1) owned-row block offsets within patch smem
+  // patch-owner assembly state (build_patch_layout)
+  OpLayout lay[2];             // [0] EV, [1] FV
+  DBuf<int32_t> vtx_off;       // (num_patches+1) patch vertex lists: owned rows, then ribbon
+  DBuf<int32_t> vtx;
+  DBuf<int32_t> hloc;          // (V, patch order) smem block offset of each owned row
+  DBuf<uint8_t> diag_pos;      // (V) position of the diagonal block in its row (255: none)
+  int max_patch_vertices = 0;
   int max_patch_blocks = 0;
   int64_t recomputed_elements = 0;
 };
@@ -139,6 +148,8 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
                 const double* pos_d, cudaStream_t s);
 void build_pattern(Problem& p, cudaStream_t s);
 void build_patch_layout(Problem& p, cudaStream_t s);
+void mesh_patches(Mesh& m, cudaStream_t s);
+int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s);
 
 // elem_kernels.cu (element-parallel, atomic accumulation)
 enum Mode { MODE_ENERGY = 0, MODE_GRAD = 1, MODE_HESS = 2, MODE_HVP = 3 };

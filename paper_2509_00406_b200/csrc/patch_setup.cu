@@ -1,0 +1,555 @@
+// Device-built vertex patches with ribbons (the north star's subsystem 1).
+//
+// The reference partitions FACES by a greedy host BFS (mesh.py:252-279) and
+// lets edges/vertices inherit a patch (mesh.py:225-231); there patches only
+// decide processing order. Here patches decide *ownership*: a patch owns a
+// run of R rows of the Hessian/gradient (vertices, in Morton order of their
+// positions so a patch is spatially compact), and one CTA assembles exactly
+// those rows. The elements incident to owned rows are listed per patch; the
+// ones that straddle two patches (ribbon elements) are evaluated by both
+// owners, so every output row is written once, with no atomics and no
+// communication (SURVEY 7.2 "owner computes"). The ribbon vertices are the
+// non-owned vertices those elements touch; their x is staged alongside the
+// owned ones.
+//
+// Everything is built with sorts/scans on the device; nothing here affects
+// the numbers, only the order of floating-point summation.
+#include <cub/cub.cuh>
+
+#include "mg_internal.cuh"
+
+namespace mg {
+
+namespace {
+
+constexpr int TPB = 256;
+inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
+
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every 3rd bit
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+
+__global__ void k_bbox(const double* pos, int64_t V, double* out /* 6 per block */) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < 3; ++c) {
+      double v = pos[3 * i + c];
+      if (isfinite(v)) { lo[c] = fmin(lo[c], v); hi[c] = fmax(hi[c], v); }
+    }
+  __shared__ double s[6][TPB];
+  for (int c = 0; c < 3; ++c) { s[c][threadIdx.x] = lo[c]; s[3 + c][threadIdx.x] = hi[c]; }
+  __syncthreads();
+  for (int o = TPB / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int c = 0; c < 3; ++c) {
+        s[c][threadIdx.x] = fmin(s[c][threadIdx.x], s[c][threadIdx.x + o]);
+        s[3 + c][threadIdx.x] = fmax(s[3 + c][threadIdx.x], s[3 + c][threadIdx.x + o]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) out[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_morton(const double* pos, int64_t V, const double* box, uint64_t* code, int32_t* ids) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  uint64_t m = 0;
+  for (int c = 0; c < 3; ++c) {
+    double ext = box[3 + c] - box[c];
+    double t = ext > 0 ? (pos[3 * i + c] - box[c]) / ext : 0.0;
+    t = isfinite(t) ? fmin(fmax(t, 0.0), 1.0) : 0.0;
+    m |= spread3((uint64_t)(t * 2097151.0)) << (2 - c);
+  }
+  code[i] = m;
+  ids[i] = (int32_t)i;
+}
+
+__global__ void k_iota(int32_t* ids, int64_t V) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < V) ids[i] = (int32_t)i;
+}
+
+__global__ void k_rank_pov(const int32_t* order, int64_t V, int R, int32_t* rank, int32_t* pov) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  rank[order[i]] = (int32_t)i;
+  pov[order[i]] = (int32_t)(i / R);
+}
+
+// (patch, element) pairs: one per distinct patch among the element's vertices
+__global__ void k_patch_elem_keys(const int32_t* sel, int P, int64_t M, const int32_t* pov, uint64_t* keys) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= M) return;
+  int pq[3];
+  for (int q = 0; q < P; ++q) {
+    pq[q] = pov[sel[e * P + q]];
+    bool dup = false;
+    for (int r = 0; r < q; ++r) dup |= pq[r] == pq[q];
+    keys[e * P + q] = dup ? ~0ull : ((uint64_t)pq[q] << 32) | (uint64_t)e;
+  }
+}
+
+__global__ void k_lower_bounds(const uint64_t* keys, int64_t n, int64_t np, int32_t* off) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p > np) return;
+  uint64_t k = (uint64_t)p << 32;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  off[p] = (int32_t)lo;
+}
+
+__global__ void k_split_entries(const uint64_t* keys, int64_t n, int32_t* elem) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) elem[j] = (int32_t)(keys[j] & 0xffffffffull);
+}
+
+__global__ void k_patch_of_entry(const int32_t* off, int64_t np, int32_t* pe) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  for (int j = off[p]; j < off[p + 1]; ++j) pe[j] = (int32_t)p;
+}
+
+__global__ void k_ribbon_keys(const int32_t* sel, int P, const int32_t* elem, const int32_t* pe, int64_t n,
+                              const int32_t* pov, uint64_t* keys) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t e = elem[j];
+  const int p = pe[j];
+  for (int q = 0; q < P; ++q) {
+    int u = sel[e * P + q];
+    keys[j * P + q] = pov[u] == p ? ~0ull : ((uint64_t)p << 32) | (uint64_t)u;
+  }
+}
+
+__device__ __forceinline__ int owned_count(int64_t p, int R, int64_t V) {
+  int64_t c = V - p * R;
+  return (int)(c < R ? c : R);
+}
+
+__global__ void k_vtx_off(const int32_t* rib_off, int64_t np, int R, int64_t V, int32_t* vtx_off) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p > np) return;
+  int64_t owned = p * R < V ? p * R : V;
+  vtx_off[p] = (int32_t)(owned + rib_off[p]);
+}
+
+__global__ void k_fill_owned(const int32_t* order, int64_t V, int R, const int32_t* vtx_off, int32_t* vtx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  int64_t p = i / R;
+  vtx[vtx_off[p] + (i - p * R)] = order[i];
+}
+
+__global__ void k_fill_ribbon(const uint64_t* rkeys, int64_t nr, const int32_t* rib_off, int R, int64_t V,
+                              const int32_t* vtx_off, int32_t* vtx) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nr) return;
+  int64_t p = (int64_t)(rkeys[k] >> 32);
+  vtx[vtx_off[p] + owned_count(p, R, V) + (k - rib_off[p])] = (int32_t)(rkeys[k] & 0xffffffffull);
+}
+
+__global__ void k_local_ids(const int32_t* sel, int P, const int32_t* elem, const int32_t* pe, int64_t n,
+                            const int32_t* pov, const int32_t* rank, int R, int64_t V, const uint64_t* rkeys,
+                            const int32_t* rib_off, uint16_t* local, int* overflow) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t e = elem[j];
+  const int64_t p = pe[j];
+  for (int q = 0; q < P; ++q) {
+    const int u = sel[e * P + q];
+    int64_t loc;
+    if (pov[u] == p) {
+      loc = rank[u] - p * R;
+    } else {
+      const uint64_t k = ((uint64_t)p << 32) | (uint64_t)u;
+      int64_t lo = rib_off[p], hi = rib_off[p + 1];
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (rkeys[mid] < k) lo = mid + 1; else hi = mid;
+      }
+      loc = owned_count(p, R, V) + (lo - rib_off[p]);
+    }
+    if (loc > 65535) atomicExch(overflow, 1);
+    local[j * P + q] = (uint16_t)loc;
+  }
+}
+
+__global__ void k_positions(const int32_t* sel, int P, const int32_t* elem, const int32_t* pe, int64_t n,
+                            const int32_t* pov, const int32_t* bids, const int64_t* ro, uint8_t* pos,
+                            int* overflow) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t e = elem[j];
+  const int p = pe[j];
+  for (int q = 0; q < P; ++q) {
+    const int u = sel[e * P + q];
+    for (int r = 0; r < P; ++r) {
+      int v = 255;
+      if (pov[u] == p) {
+        const int32_t b = bids[e * P * P + q * P + r];
+        if (b >= 0) {
+          int64_t d = b - ro[u];
+          if (d > 254) atomicExch(overflow, 1);
+          v = (int)d;
+        }
+      }
+      pos[(j * P + q) * P + r] = (uint8_t)v;
+    }
+  }
+}
+
+// Greedy coloring per patch (one thread per patch, entries in element order):
+// two entries conflict iff they share an owned vertex (they would add into
+// the same shared-memory row). masks: (V) x 2 words of scratch, indexed by
+// owned position in Morton order.
+__global__ void k_color(const uint16_t* local, int P, const int32_t* off, int64_t np, int R, int64_t V,
+                        uint64_t* masks, uint8_t* color, int* overflow) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const int oc = owned_count(p, R, V);
+  uint64_t* m = masks + 2 * p * R;
+  for (int i = 0; i < 2 * oc; ++i) m[i] = 0;
+  for (int j = off[p]; j < off[p + 1]; ++j) {
+    uint64_t u0 = 0, u1 = 0;
+    for (int q = 0; q < P; ++q) {
+      int l = local[(int64_t)j * P + q];
+      if (l < oc) { u0 |= m[2 * l]; u1 |= m[2 * l + 1]; }
+    }
+    int c;
+    if (~u0) c = __ffsll(~u0) - 1;
+    else if (~u1) c = 64 + __ffsll(~u1) - 1;
+    else { atomicExch(overflow, 1); c = 127; }
+    color[j] = (uint8_t)c;
+    for (int q = 0; q < P; ++q) {
+      int l = local[(int64_t)j * P + q];
+      if (l < oc) {
+        if (c < 64) m[2 * l] |= 1ull << c; else m[2 * l + 1] |= 1ull << (c - 64);
+      }
+    }
+  }
+}
+
+__global__ void k_color_keys(const int32_t* pe, const uint8_t* color, const int32_t* elem, int64_t n,
+                             uint64_t* keys, int32_t* idx) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  keys[j] = ((uint64_t)pe[j] << 40) | ((uint64_t)color[j] << 32) | (uint64_t)(uint32_t)elem[j];
+  idx[j] = (int32_t)j;
+}
+
+template <class T>
+__global__ void k_gather_rows(const T* src, const int32_t* idx, int64_t n, int w, T* dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * w) return;
+  int64_t j = i / w, c = i % w;
+  dst[i] = src[(int64_t)idx[j] * w + c];
+}
+
+__global__ void k_row_len_patch_order(const int32_t* order, const int64_t* ro, int64_t V, int32_t* len) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int v = order[i];
+  len[i] = (int32_t)(ro[v + 1] - ro[v]);
+}
+
+__global__ void k_localize(const int32_t* scan, int64_t V, int R, int32_t* hloc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  hloc[i] = scan[i] - scan[(i / R) * R];
+}
+
+__global__ void k_patch_blocks(const int32_t* scan, int64_t V, int R, int64_t np, int* maxb) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  int64_t a = p * R, b = (p + 1) * R < V ? (p + 1) * R : V;
+  atomicMax(maxb, scan[b] - scan[a]);
+}
+
+__global__ void k_max_diff(const int32_t* off, int64_t np, int* out) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  atomicMax(out, off[p + 1] - off[p]);
+}
+
+__global__ void k_diag_pos(const int64_t* ro, const int32_t* col, int64_t V, uint8_t* dp) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  int64_t lo = ro[v], hi = ro[v + 1], a = lo, b = hi;
+  while (a < b) {
+    int64_t mid = (a + b) >> 1;
+    if (col[mid] < v) a = mid + 1; else b = mid;
+  }
+  dp[v] = (a < hi && col[a] == v && a - lo < 255) ? (uint8_t)(a - lo) : 255;
+}
+
+int to_host_int(const int* d, cudaStream_t s) {
+  int h = 0;
+  MG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+int key_bits(int64_t v) {
+  int b = 1;
+  while ((int64_t(1) << b) <= v) ++b;
+  return b;
+}
+
+}  // namespace
+
+void mesh_patches(Mesh& m, cudaStream_t s) {
+  const int64_t V = m.V;
+  PatchSet& ps = m.patches;
+  ps.R = m.patch_vertices;
+  ps.num = (V + ps.R - 1) / ps.R;
+  ps.order.alloc(V > 0 ? V : 1);
+  ps.rank.alloc(V > 0 ? V : 1);
+  ps.patch_of_vertex.alloc(V > 0 ? V : 1);
+  if (V == 0) return;
+  if (m.pos.p) {
+    const int nb = 256;
+    DBuf<double> part, box;
+    part.alloc(6 * nb);
+    box.alloc(6);
+    k_bbox<<<nb, TPB, 0, s>>>(m.pos.p, V, part.p);
+    MG_LAUNCH_CHECK();
+    std::vector<double> hp(6 * nb);
+    MG_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    double hb[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int b = 0; b < nb; ++b)
+      for (int c = 0; c < 3; ++c) {
+        hb[c] = std::fmin(hb[c], hp[6 * b + c]);
+        hb[3 + c] = std::fmax(hb[3 + c], hp[6 * b + 3 + c]);
+      }
+    MG_CUDA(cudaMemcpyAsync(box.p, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+    DBuf<uint64_t> code, code2;
+    DBuf<int32_t> ids;
+    code.alloc(V);
+    code2.alloc(V);
+    ids.alloc(V);
+    k_morton<<<grid_for(V), TPB, 0, s>>>(m.pos.p, V, box.p, code.p, ids.p);
+    MG_LAUNCH_CHECK();
+    size_t tb = 0;
+    MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, code.p, code2.p, ids.p, ps.order.p, (int64_t)V, 0, 63, s));
+    Tmp t(s, tb);
+    MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, code.p, code2.p, ids.p, ps.order.p, (int64_t)V, 0, 63, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+  } else {
+    k_iota<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V);
+    MG_LAUNCH_CHECK();
+  }
+  k_rank_pov<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V, ps.R, ps.rank.p, ps.patch_of_vertex.p);
+  MG_LAUNCH_CHECK();
+  MG_CUDA(cudaStreamSynchronize(s));
+}
+
+void build_patch_layout(Problem& p, cudaStream_t s) {
+  Mesh& m = *p.mesh;
+  PatchSet& ps = m.patches;
+  const int64_t V = m.V, np = ps.num;
+  const int R = ps.R;
+  p.layout_ready = false;
+  if (V == 0 || np == 0) return;
+  DBuf<int> flag;
+  flag.alloc(1);
+  MG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+
+  // ops present, and the first term of each op (its bids give row positions)
+  const Term* first[2] = {nullptr, nullptr};
+  for (auto& t : p.terms) {
+    int k = t.dev.op == MG_OP_EV ? 0 : t.dev.op == MG_OP_FV ? 1 : -1;
+    if (k >= 0 && !first[k]) first[k] = &t;
+  }
+  // per-op entry lists
+  DBuf<int32_t> pe_of[2];
+  uint64_t* rib_keys_all = nullptr;
+  int64_t rib_total_keys = 0;
+  std::vector<uint64_t*> rib_parts;
+  std::vector<int64_t> rib_counts;
+  for (int k = 0; k < 2; ++k) {
+    OpLayout& L = p.lay[k];
+    L.count = 0;
+    L.op = -1;
+    if (!first[k]) continue;
+    const int op = first[k]->dev.op, P = first[k]->dev.P;
+    const int64_t M = op_count(m, op);
+    const int32_t* sel = op_sel(m, op);
+    L.op = op;
+    L.P = P;
+    uint64_t* keys = nullptr;
+    MG_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * (M * P > 0 ? M * P : 1), s));
+    if (M) k_patch_elem_keys<<<grid_for(M), TPB, 0, s>>>(sel, P, M, ps.patch_of_vertex.p, keys);
+    MG_LAUNCH_CHECK();
+    int64_t n = sort_unique(keys, M * P, 64, s);
+    if (n > 0) {
+      uint64_t last = 0;
+      MG_CUDA(cudaMemcpyAsync(&last, keys + n - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      if (last == ~0ull) --n;
+    }
+    if (n >= (int64_t(1) << 31)) throw Error(MG_ERR_UNSUPPORTED, "patch element lists exceed 2^31 entries");
+    L.count = n;
+    L.off.alloc(np + 1);
+    L.elem.alloc(n > 0 ? n : 1);
+    k_lower_bounds<<<grid_for(np + 1), TPB, 0, s>>>(keys, n, np, L.off.p);
+    if (n) k_split_entries<<<grid_for(n), TPB, 0, s>>>(keys, n, L.elem.p);
+    MG_LAUNCH_CHECK();
+    cudaFreeAsync(keys, s);
+    pe_of[k].alloc(n > 0 ? n : 1);
+    k_patch_of_entry<<<grid_for(np), TPB, 0, s>>>(L.off.p, np, pe_of[k].p);
+    MG_LAUNCH_CHECK();
+    // ribbon candidates of this op
+    uint64_t* rk = nullptr;
+    MG_CUDA(cudaMallocAsync(&rk, sizeof(uint64_t) * (n * P > 0 ? n * P : 1), s));
+    if (n) k_ribbon_keys<<<grid_for(n), TPB, 0, s>>>(sel, P, L.elem.p, pe_of[k].p, n, ps.patch_of_vertex.p, rk);
+    MG_LAUNCH_CHECK();
+    rib_parts.push_back(rk);
+    rib_counts.push_back(n * P);
+    rib_total_keys += n * P;
+  }
+  // merged ribbon list over all ops
+  MG_CUDA(cudaMallocAsync(&rib_keys_all, sizeof(uint64_t) * (rib_total_keys > 0 ? rib_total_keys : 1), s));
+  {
+    int64_t o = 0;
+    for (size_t i = 0; i < rib_parts.size(); ++i) {
+      if (rib_counts[i])
+        MG_CUDA(cudaMemcpyAsync(rib_keys_all + o, rib_parts[i], sizeof(uint64_t) * rib_counts[i],
+                                cudaMemcpyDeviceToDevice, s));
+      o += rib_counts[i];
+      cudaFreeAsync(rib_parts[i], s);
+    }
+  }
+  int64_t nr = sort_unique(rib_keys_all, rib_total_keys, 64, s);
+  if (nr > 0) {
+    uint64_t last = 0;
+    MG_CUDA(cudaMemcpyAsync(&last, rib_keys_all + nr - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    if (last == ~0ull) --nr;
+  }
+  ps.ribbon_total = nr;
+  DBuf<int32_t> rib_off;
+  rib_off.alloc(np + 1);
+  k_lower_bounds<<<grid_for(np + 1), TPB, 0, s>>>(rib_keys_all, nr, np, rib_off.p);
+  MG_LAUNCH_CHECK();
+  p.vtx_off.alloc(np + 1);
+  k_vtx_off<<<grid_for(np + 1), TPB, 0, s>>>(rib_off.p, np, R, V, p.vtx_off.p);
+  p.vtx.alloc(V + nr);
+  k_fill_owned<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V, R, p.vtx_off.p, p.vtx.p);
+  if (nr) k_fill_ribbon<<<grid_for(nr), TPB, 0, s>>>(rib_keys_all, nr, rib_off.p, R, V, p.vtx_off.p, p.vtx.p);
+  MG_LAUNCH_CHECK();
+  {
+    DBuf<int> mx;
+    mx.alloc(1);
+    MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+    k_max_diff<<<grid_for(np), TPB, 0, s>>>(p.vtx_off.p, np, mx.p);
+    MG_LAUNCH_CHECK();
+    p.max_patch_vertices = to_host_int(mx.p, s);
+  }
+
+  // local ids, row positions, colors; then sort entries by (patch, color, element)
+  DBuf<uint64_t> masks;
+  masks.alloc(2 * np * R);
+  p.recomputed_elements = 0;
+  for (int k = 0; k < 2; ++k) {
+    OpLayout& L = p.lay[k];
+    if (L.op < 0) continue;
+    const int P = L.P;
+    const int64_t n = L.count;
+    const int32_t* sel = op_sel(m, L.op);
+    L.local.alloc(n * P > 0 ? n * P : 1);
+    if (n) k_local_ids<<<grid_for(n), TPB, 0, s>>>(sel, P, L.elem.p, pe_of[k].p, n, ps.patch_of_vertex.p,
+                                                   ps.rank.p, R, V, rib_keys_all, rib_off.p, L.local.p, flag.p);
+    MG_LAUNCH_CHECK();
+    L.pos.alloc(n * P * P > 0 ? n * P * P : 1);
+    if (p.with_hessian && p.pattern_ready && n)
+      k_positions<<<grid_for(n), TPB, 0, s>>>(sel, P, L.elem.p, pe_of[k].p, n, ps.patch_of_vertex.p,
+                                              first[k]->bids.p, p.row_offsets.p, L.pos.p, flag.p);
+    MG_LAUNCH_CHECK();
+    L.color.alloc(n > 0 ? n : 1);
+    k_color<<<grid_for(np), TPB, 0, s>>>(L.local.p, P, L.off.p, np, R, V, masks.p, L.color.p, flag.p);
+    MG_LAUNCH_CHECK();
+    if (to_host_int(flag.p, s)) {
+      // pathological valence / patch: keep the element-parallel path
+      cudaFreeAsync(rib_keys_all, s);
+      MG_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    // reorder entries by (patch, color, element)
+    DBuf<uint64_t> ck, ck2;
+    DBuf<int32_t> idx, idx2;
+    ck.alloc(n > 0 ? n : 1);
+    ck2.alloc(n > 0 ? n : 1);
+    idx.alloc(n > 0 ? n : 1);
+    idx2.alloc(n > 0 ? n : 1);
+    if (n) {
+      k_color_keys<<<grid_for(n), TPB, 0, s>>>(pe_of[k].p, L.color.p, L.elem.p, n, ck.p, idx.p);
+      MG_LAUNCH_CHECK();
+      size_t tb = 0;
+      MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck.p, ck2.p, idx.p, idx2.p, n, 0, 64, s));
+      {
+        Tmp t(s, tb);
+        MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, ck.p, ck2.p, idx.p, idx2.p, n, 0, 64, s));
+      }
+      DBuf<int32_t> e2;
+      DBuf<uint16_t> l2;
+      DBuf<uint8_t> p2, c2;
+      e2.alloc(n);
+      l2.alloc(n * P);
+      p2.alloc(n * P * P);
+      c2.alloc(n);
+      k_gather_rows<<<grid_for(n), TPB, 0, s>>>(L.elem.p, idx2.p, n, 1, e2.p);
+      k_gather_rows<<<grid_for(n * P), TPB, 0, s>>>(L.local.p, idx2.p, n, P, l2.p);
+      k_gather_rows<<<grid_for(n * P * P), TPB, 0, s>>>(L.pos.p, idx2.p, n, P * P, p2.p);
+      k_gather_rows<<<grid_for(n), TPB, 0, s>>>(L.color.p, idx2.p, n, 1, c2.p);
+      MG_LAUNCH_CHECK();
+      MG_CUDA(cudaStreamSynchronize(s));
+      L.elem = std::move(e2);
+      L.local = std::move(l2);
+      L.pos = std::move(p2);
+      L.color = std::move(c2);
+    }
+    p.recomputed_elements += n - op_count(m, L.op);
+  }
+  cudaFreeAsync(rib_keys_all, s);
+
+  // shared-memory row offsets of owned rows (patch order) and diagonal positions
+  p.hloc.alloc(V);
+  p.diag_pos.alloc(V);
+  p.max_patch_blocks = 0;
+  if (p.with_hessian && p.pattern_ready) {
+    DBuf<int32_t> len, scan;
+    len.alloc(V + 1);
+    scan.alloc(V + 1);
+    MG_CUDA(cudaMemsetAsync(len.p + V, 0, sizeof(int32_t), s));
+    k_row_len_patch_order<<<grid_for(V), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, V, len.p);
+    MG_LAUNCH_CHECK();
+    size_t tb = 0;
+    MG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, scan.p, V + 1, s));
+    {
+      Tmp t(s, tb);
+      MG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, len.p, scan.p, V + 1, s));
+    }
+    k_localize<<<grid_for(V), TPB, 0, s>>>(scan.p, V, R, p.hloc.p);
+    DBuf<int> mx;
+    mx.alloc(1);
+    MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+    k_patch_blocks<<<grid_for(np), TPB, 0, s>>>(scan.p, V, R, np, mx.p);
+    k_diag_pos<<<grid_for(V), TPB, 0, s>>>(p.row_offsets.p, p.col32.p, V, p.diag_pos.p);
+    MG_LAUNCH_CHECK();
+    p.max_patch_blocks = to_host_int(mx.p, s);
+  }
+  MG_CUDA(cudaStreamSynchronize(s));
+  p.layout_ready = true;
+}
+
+}  // namespace mg

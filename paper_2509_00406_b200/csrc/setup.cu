@@ -57,6 +57,8 @@ __global__ void k_keys_to_pairs(const uint64_t* keys, int64_t n, int64_t V, int3
   out[2 * i + 1] = (int32_t)(keys[i] % (uint64_t)V);
 }
 
+}  // namespace
+
 // Sort + unique a key array in place (keys buffer reused); returns count.
 int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s) {
   if (n == 0) return 0;
@@ -92,8 +94,6 @@ int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s) {
   }
   return cnt;
 }
-
-}  // namespace
 
 void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t num_edges_in,
                 const double* pos_d, cudaStream_t s) {
@@ -148,6 +148,7 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
   } else {
     m.E = 0;
   }
+  mesh_patches(m, s);
   MG_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -181,7 +181,7 @@ class Problem:
     def __init__(self, mesh: Mesh, var_dim: int, with_hessian: bool = True,
                  fixed_vertices=(), accumulation: str = "deterministic",
                  workers: int = 1, valence_cap: int = DEFAULT_VALENCE_CAP,
-                 chunk_elements: int = 4096):
+                 chunk_elements: int = 4096, live_host_attrs: bool = False):
         if var_dim < 1:
             raise ValueError("var_dim must be at least 1")
         if accumulation not in ("deterministic", "atomic"):
@@ -197,6 +197,7 @@ class Problem:
         self.workers = max(1, int(workers))
         self.valence_cap = valence_cap
         self._chunk_elements = chunk_elements
+        self.live_host_attrs = live_host_attrs
         nv = mesh.num_vertices
         self._fixed = np.zeros(nv, dtype=bool)
         for v in fixed_vertices:
@@ -265,7 +266,18 @@ class Problem:
         return len(self._terms) - 1
 
     def _sync_attrs(self):
-        """Re-upload numpy closure arrays (the reference reads them live)."""
+        if self.live_host_attrs:
+            self.refresh_attrs()
+
+    def refresh_attrs(self):
+        """Re-upload the host (numpy) attribute arrays of every term.
+
+        The reference's callbacks read their closure arrays live on every call
+        (ClothSim.step rewrites `target` in place, apps/cloth.py:128). Here a
+        numpy attribute is snapshotted to the device at `add_term`; mutate a
+        CUDA tensor attribute in place instead (zero copies), or call this
+        after changing a numpy one (or construct with live_host_attrs=True to
+        re-upload on every call, at PCIe cost)."""
         for rec in self._terms:
             for slot, host in enumerate(rec.host_attrs):
                 if host is not None:

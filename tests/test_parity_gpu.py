@@ -9,7 +9,18 @@ import numpy as np
 import pytest
 
 from engine_util import engine_mesh, engine_problem
-from golden_util import FLOOR, cases, load, oracle_problem, rel, rel_scalar, states
+from golden_util import FLOOR, build_terms, cases, load, oracle_problem, rel, rel_scalar, states
+
+
+def per_term_grads(d, x):
+    from oracle import OracleProblem
+
+    out = []
+    for op, term in build_terms(d):
+        op1 = OracleProblem(len(d["positions"]), d["faces"], d["edges"], int(d["n"]), [(op, term)],
+                            with_hessian=False, fixed_vertices=d["fixed"].tolist())
+        out.append(op1.eval_terms(x)[1])
+    return out
 
 pytestmark = pytest.mark.gpu
 
@@ -80,7 +91,13 @@ def test_cloth_asis_trajectory(mode):
         floor = float(d[f"s{s}_floor"])
         e = p.eval_terms(psd_floor=None if np.isnan(floor) else floor)
         assert rel_scalar(e, d[f"s{s}_energy"]) <= TOL
-        assert rel(p.grad, d[f"s{s}_grad"]) <= TOL
+        # Newton iterates converge to equilibrium (|grad| -> 1e-7) where the
+        # gradient is a cancellation of O(1e-2) per-term contributions: scale
+        # by the largest single-term gradient.
+        d["a_target"] = d[f"s{s}_target"]
+        scale = max(np.max(np.abs(g)) for g in per_term_grads(d, d[f"s{s}_x"]))
+        got, ref = p.grad, d[f"s{s}_grad"]
+        assert np.max(np.abs(got - ref)) <= TOL * max(scale, np.max(np.abs(ref)))
         assert rel(p.hess.values, d[f"s{s}_hess"]) <= TOL
 
 
