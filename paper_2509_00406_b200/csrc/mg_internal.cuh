@@ -128,6 +128,14 @@ struct Problem {
   DBuf<uint8_t> diag_pos;      // (V) position of the diagonal block in its row (255: none)
   int max_patch_vertices = 0;
   int max_patch_blocks = 0;
+  int max_patch_elems = 0;     // max EV entries of one patch
+  // two-point edge fast path (all EV terms two-point, no FV terms): per owned
+  // row (patch order) its incident patch entries sorted by column;
+  // packed: local entry (16 b) | slot q (bit 16) | row position of the other
+  // endpoint (bits 24..31, 255 = pinned)
+  bool ev_fast = false;
+  DBuf<int32_t> rinc_off;      // (V+1)
+  DBuf<uint32_t> rinc;
   int64_t recomputed_elements = 0;
 };
 

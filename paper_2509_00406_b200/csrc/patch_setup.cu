@@ -107,6 +107,18 @@ __global__ void k_lower_bounds(const uint64_t* keys, int64_t n, int64_t np, int3
   off[p] = (int32_t)lo;
 }
 
+__global__ void k_lower_bounds_rows(const uint64_t* keys, int64_t n, int64_t V, int32_t* off) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r > V) return;
+  uint64_t k = (uint64_t)r << 32;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  off[r] = (int32_t)lo;
+}
+
 __global__ void k_split_entries(const uint64_t* keys, int64_t n, int32_t* elem) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) elem[j] = (int32_t)(keys[j] & 0xffffffffull);
@@ -291,6 +303,29 @@ __global__ void k_diag_pos(const int64_t* ro, const int32_t* col, int64_t V, uin
   dp[v] = (a < hi && col[a] == v && a - lo < 255) ? (uint8_t)(a - lo) : 255;
 }
 
+// row-incidence records of the two-point edge fast path
+__global__ void k_rinc_keys(const int32_t* sel, const int32_t* elem, const uint16_t* local, const uint8_t* pos,
+                            const int32_t* pe, const int32_t* off, int64_t n, int R, int64_t V,
+                            uint64_t* keys, uint32_t* vals) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t p = pe[j];
+  const int oc = owned_count(p, R, V);
+  const int64_t e = elem[j];
+  for (int q = 0; q < 2; ++q) {
+    const int lq = local[j * 2 + q];
+    if (lq < oc) {
+      const int64_t row = p * R + lq;
+      const uint32_t other = (uint32_t)sel[e * 2 + (1 - q)];
+      keys[j * 2 + q] = ((uint64_t)row << 32) | other;
+      vals[j * 2 + q] = (uint32_t)(j - off[p]) | ((uint32_t)q << 16) | ((uint32_t)pos[(j * 2 + q) * 2 + (1 - q)] << 24);
+    } else {
+      keys[j * 2 + q] = ~0ull;
+      vals[j * 2 + q] = 0;
+    }
+  }
+}
+
 int to_host_int(const int* d, cudaStream_t s) {
   int h = 0;
   MG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -471,6 +506,7 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
                                                    ps.rank.p, R, V, rib_keys_all, rib_off.p, L.local.p, flag.p);
     MG_LAUNCH_CHECK();
     L.pos.alloc(n * P * P > 0 ? n * P * P : 1);
+    MG_CUDA(cudaMemsetAsync(L.pos.p, 0xff, n * P * P > 0 ? n * P * P : 1, s));
     if (p.with_hessian && p.pattern_ready && n)
       k_positions<<<grid_for(n), TPB, 0, s>>>(sel, P, L.elem.p, pe_of[k].p, n, ps.patch_of_vertex.p,
                                               first[k]->bids.p, p.row_offsets.p, L.pos.p, flag.p);
@@ -521,6 +557,49 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
     p.recomputed_elements += n - op_count(m, L.op);
   }
   cudaFreeAsync(rib_keys_all, s);
+
+  // two-point edge fast path: row incidence lists
+  p.ev_fast = false;
+  {
+    bool fast = p.lay[0].op == MG_OP_EV && p.lay[1].op < 0;
+    for (auto& t : p.terms)
+      fast &= t.dev.op == MG_OP_V || t.dev.type == MG_TERM_SPRING || t.dev.type == MG_TERM_EDGE_LENGTH;
+    OpLayout& L = p.lay[0];
+    if (fast) {
+      const int64_t n = L.count;
+      DBuf<int> mx;
+      mx.alloc(1);
+      MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+      k_max_diff<<<grid_for(np), TPB, 0, s>>>(L.off.p, np, mx.p);
+      MG_LAUNCH_CHECK();
+      p.max_patch_elems = to_host_int(mx.p, s);
+      fast = p.max_patch_elems < 65536;
+      if (fast) {
+        DBuf<int32_t> pe_sorted;
+        pe_sorted.alloc(n > 0 ? n : 1);
+        k_patch_of_entry<<<grid_for(np), TPB, 0, s>>>(L.off.p, np, pe_sorted.p);
+        DBuf<uint64_t> k1, k2;
+        DBuf<uint32_t> v1, v2;
+        const int64_t m2 = 2 * n > 0 ? 2 * n : 1;
+        k1.alloc(m2); k2.alloc(m2); v1.alloc(m2); v2.alloc(m2);
+        if (n) k_rinc_keys<<<grid_for(n), TPB, 0, s>>>(op_sel(m, MG_OP_EV), L.elem.p, L.local.p, L.pos.p,
+                                                       pe_sorted.p, L.off.p, n, R, V, k1.p, v1.p);
+        MG_LAUNCH_CHECK();
+        size_t tb = 0;
+        MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, 2 * n, 0, 64, s));
+        {
+          Tmp t(s, tb);
+          MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k1.p, k2.p, v1.p, v2.p, 2 * n, 0, 64, s));
+        }
+        p.rinc_off.alloc(V + 1);
+        k_lower_bounds_rows<<<grid_for(V + 1), TPB, 0, s>>>(k2.p, 2 * n, V, p.rinc_off.p);
+        MG_LAUNCH_CHECK();
+        p.rinc = std::move(v2);
+        MG_CUDA(cudaStreamSynchronize(s));
+        p.ev_fast = true;
+      }
+    }
+  }
 
   // shared-memory row offsets of owned rows (patch order) and diagonal positions
   p.hloc.alloc(V);

@@ -95,6 +95,39 @@ MG_DI void jacobi_project(double* A, double floor) {
   (void)T;
 }
 
+// Is A - floor*I positive definite? (Cholesky in registers.) When it is,
+// max(Lambda, floor) == Lambda and the projector is A itself up to rounding
+// (a misclassification can only happen when an eigenvalue is within rounding
+// of the floor, where clamping changes nothing measurable).
+template <int K>
+MG_DI bool shifted_pd(const double* A, double floor) {
+  double L[TriN<K>::value];
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double d = A[tri(j, j)] - floor;
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= L[tri(j, k)] * L[tri(j, k)];
+    ok &= d > 0.0;
+    const double r = d > 0.0 ? rsqrt(d) : 0.0;
+    L[tri(j, j)] = d * r;
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double v = A[tri(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= L[tri(i, k)] * L[tri(j, k)];
+      L[tri(i, j)] = v * r;
+    }
+  }
+  return ok;
+}
+
+// project in place unless already above the floor
+template <int K>
+MG_DI void project_if_needed(double* A, double floor) {
+  if (!shifted_pd<K>(A, floor)) jacobi_project<K>(A, floor);
+}
+
 template <int K>
 MG_DI bool all_finite(const double* A) {
   bool ok = true;
@@ -129,7 +162,7 @@ MG_DI void extract_psd(double* H, double floor) {
       for (int i = 0; i < N; ++i)
 #pragma unroll
         for (int j = 0; j <= i; ++j) A2[tri(i, j)] = 2.0 * H[tri(i, j)];
-      jacobi_project<N>(A2, floor);
+      project_if_needed<N>(A2, floor);
       const double hf = 0.5 * floor;
 #pragma unroll
       for (int i = 0; i < N; ++i)
@@ -146,7 +179,7 @@ MG_DI void extract_psd(double* H, double floor) {
       return;
     }
   }
-  jacobi_project<K>(H, floor);
+  project_if_needed<K>(H, floor);
 }
 
 }  // namespace mg

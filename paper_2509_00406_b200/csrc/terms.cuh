@@ -26,6 +26,29 @@ template <> struct TermInfo<MG_TERM_EDGE_LENGTH> { static constexpr int P = 2, O
 template <> struct TermInfo<MG_TERM_SYM_DIRICHLET> { static constexpr int P = 3, OP = MG_OP_FV; };
 template <> struct TermInfo<MG_TERM_SPHERE> { static constexpr int P = 3, OP = MG_OP_FV; };
 
+// Two-point difference terms: the energy depends on the edge only through
+// d = x_i - x_j, so the 2n x 2n Hessian is exactly [[A, -A], [-A, A]] and the
+// gradient is [g, -g]. Evaluating a K = n dual on d reproduces the K = 2n
+// dual entry for entry: the reference's lifted d carries gradient e_c - e_{n+c},
+// every later operation is entrywise, and the off-diagonal entries differ only
+// by exact sign flips (active.py:156-258). Half the variables, a quarter of
+// the Hessian work, and the PSD clamp reduces to an n x n eigenproblem.
+template <int TT> struct TwoPoint { static constexpr bool value = false; };
+template <> struct TwoPoint<MG_TERM_SPRING> { static constexpr bool value = true; };
+template <> struct TwoPoint<MG_TERM_EDGE_LENGTH> { static constexpr bool value = true; };
+
+template <int TT, int N, class S>
+MG_DI auto term_eval_diff(const TermDev& t, int64_t e, const Vec<S, N>& d) {
+  if constexpr (TT == MG_TERM_SPRING) {
+    const double l2 = t.a[0][e];
+    auto s = norm2(d) / l2 - 1.0;
+    return (s * s) * (t.c[0] * l2);
+  } else {
+    static_assert(TT == MG_TERM_EDGE_LENGTH, "not a two-point term");
+    return norm2(d);
+  }
+}
+
 // e: element id (== vertex id for V terms); vid: the element's P vertex ids;
 // X: the P lifted per-vertex variable vectors.
 template <int TT, int N, class S>
