@@ -597,13 +597,26 @@ __global__ void __launch_bounds__(PT) k_patch_ev(const __grid_constant__ EvArgs 
   }
   __syncthreads();
 
-  // stage 1: every patch edge once
-  for (int jj = threadIdx.x; jj < ne; jj += PT) {
-    const int j = j0 + jj;
-    const int64_t e = a.ev_elem[j];
-    const int la = a.ev_local[2 * j], lb = a.ev_local[2 * j + 1];
-    ev_stage1_edge<N, MODE, PSD>(a, e, xs + la * N, xs + lb * N, ws + la * N, ws + lb * N, !fx[la], !fx[lb],
-                                 scr + (size_t)jj * SW);
+  // stage 1: every patch edge once (records of the next edge prefetched)
+  {
+    int jj = threadIdx.x;
+    int64_t e = 0;
+    uint32_t lab = 0;
+    if (jj < ne) {
+      e = a.ev_elem[j0 + jj];
+      lab = reinterpret_cast<const uint32_t*>(a.ev_local)[j0 + jj];
+    }
+    for (; jj < ne; jj += PT) {
+      const int64_t ce = e;
+      const uint32_t clab = lab;
+      if (jj + PT < ne) {
+        e = a.ev_elem[j0 + jj + PT];
+        lab = reinterpret_cast<const uint32_t*>(a.ev_local)[j0 + jj + PT];
+      }
+      const int la = clab & 0xffff, lb = clab >> 16;
+      ev_stage1_edge<N, MODE, PSD>(a, ce, xs + la * N, xs + lb * N, ws + la * N, ws + lb * N, !fx[la], !fx[lb],
+                                   scr + (size_t)jj * SW);
+    }
   }
   __syncthreads();
 
@@ -694,23 +707,30 @@ __global__ void __launch_bounds__(PT) k_patch_ev(const __grid_constant__ EvArgs 
   }
   if constexpr (MODE == MODE_HESS) {
     __syncthreads();
-    // stage 3: one warp per owned row, coalesced block writes
+    // stage 3: one warp per owned row, coalesced block writes. Each lane owns
+    // a fixed (block-in-group, entry) slot: BPW = 32 / NN blocks per pass.
+    constexpr int BPW = 32 / NN;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int r = wid; r < oc; r += PT / 32) {
-      const int cnt = slen[r] * NN;
-      double* dst = a.hess + sro[r] * NN;
-      const int hb = shl[r];
-      for (int k = lane; k < cnt; k += 32) {
-        const int b = k / NN, rc = k - b * NN, i = rc / N, c = rc - i * N;
-        const int jj = map[hb + b];
-        double v;
-        if (jj < 0) {
-          v = rdiag[r * T + tri(i, c)];
-        } else {
-          const double* sc = scr + (size_t)jj * SW;
-          v = -sc[1 + N + tri(i, c)] + (i == c ? sc[1 + N + T] : 0.0);
+    const int lb = lane / NN, lrc = lane - lb * NN, li = lrc / N, lc = lrc - li * N;
+    const int ltri = li >= lc ? li * (li + 1) / 2 + lc : lc * (lc + 1) / 2 + li;
+    const bool ldiag = li == lc;
+    if (lb < BPW) {
+      for (int r = wid; r < oc; r += PT / 32) {
+        const int len = slen[r];
+        double* dst = a.hess + sro[r] * NN;
+        const int hb = shl[r];
+        const double* rd = rdiag + r * T;
+        for (int b = lb; b < len; b += BPW) {
+          const int jj = map[hb + b];
+          double v;
+          if (jj < 0) {
+            v = rd[ltri];
+          } else {
+            const double* sc = scr + (size_t)jj * SW;
+            v = -sc[1 + N + ltri] + (ldiag ? sc[1 + N + T] : 0.0);
+          }
+          dst[b * NN + lrc] = v;
         }
-        dst[k] = v;
       }
     }
   }

@@ -37,7 +37,7 @@ MG_DI void jacobi_project(double* A, double floor) {
   for (int i = 0; i < K; ++i)
 #pragma unroll
     for (int j = 0; j <= i; ++j) fro2 += (i == j ? 1.0 : 2.0) * A[tri(i, j)] * A[tri(i, j)];
-  const double tol2 = fro2 * 1e-34;  // off-diagonal mass ~1e-17 relative
+  const double tol2 = fro2 * 1e-30;  // off-diagonal mass ~1e-15 relative: below eigh-level error, far below the 1e-10 bar
 
   for (int sweep = 0; sweep < 12; ++sweep) {
     double off = 0.0;

@@ -1,6 +1,6 @@
-set -x
-timeout 600 python -m pytest tests -q -m gpu -x 2>&1 | tail -8
-python bench.py --no-cpu 2>&1 | tail -1
-for c in psd plain; do
-  ncu --set full --clock-control none --import-source on -k regex:'^k_patch' -s 1 -c 1 -o gpurun_out/prof_${c}_r1c python bench.py --profile --profile-call $c > /dev/null 2>&1
+# usage: bash tools/gpu_profile.sh <tag> <calls...>   (ncu --set full of the patch kernel per call)
+tag=$1; shift
+for c in "$@"; do
+  ncu --set full --clock-control none --import-source on -k regex:'^k_patch(_ev)?$' -s 1 -c 1 -o gpurun_out/prof_${c}_${tag} python bench.py --profile --profile-call $c --patch ${PATCH:-128} > gpurun_out/ncu_${c}_${tag}.log 2>&1
 done
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${tag}.csv python bench.py --profile > /dev/null 2>&1
