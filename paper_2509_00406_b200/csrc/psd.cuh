@@ -9,7 +9,9 @@
 // accurate symmetric eigensolver reproduces the reference to rounding
 // (cyclic Jacobi matched eigh to <= 1e-14 relative).
 //
-// Two paths:
+// Paths:
+//  * a Cholesky test of A - floor*I: already above the floor -> unchanged;
+//  * 2x2 / 3x3: non-iterative deflation solver (psd_small.h);
 //  * cyclic Jacobi on the packed K x K matrix (generic, K <= 12);
 //  * a two-point shortcut: when H == [[A,-A],[-A,A]] bitwise (every
 //    translation-invariant edge term: springs, edge lengths), the spectrum is
@@ -19,6 +21,7 @@
 //    so any other Hessian silently takes the generic path.
 #pragma once
 #include "dual.cuh"
+#include "psd_small.h"
 
 namespace mg {
 
@@ -122,10 +125,14 @@ MG_DI bool shifted_pd(const double* A, double floor) {
   return ok;
 }
 
-// project in place unless already above the floor
+// project in place unless already above the floor; 2x2 / 3x3 blocks (vertex
+// terms, two-point edge terms) use the non-iterative solver of psd_small.h
 template <int K>
 MG_DI void project_if_needed(double* A, double floor) {
-  if (!shifted_pd<K>(A, floor)) jacobi_project<K>(A, floor);
+  if (shifted_pd<K>(A, floor)) return;
+  if constexpr (K == 2) psd_small::project2(A, floor);
+  else if constexpr (K == 3) psd_small::project3(A, floor);
+  else jacobi_project<K>(A, floor);
 }
 
 template <int K>
