@@ -101,6 +101,15 @@ MG_API int mg_mesh_counts(const mg_mesh* mesh, int64_t* num_vertices, int64_t* n
 MG_API int mg_mesh_copy_edges(const mg_mesh* mesh, int64_t* edges_d, void* stream);
 /* Patch id of every vertex (int32, device) — diagnostics / multi-GPU partitioning. */
 MG_API int mg_mesh_copy_vertex_patches(const mg_mesh* mesh, int32_t* patch_d, void* stream);
+/* Multi-GPU shard (no reference counterpart: the reference is single-process).
+ * Restrict the rows this mesh assembles to the vertices flagged in owned_d
+ * ((V,) uint8 device, 1 = owned; NULL = all). The other vertices are ribbon
+ * (halo) vertices: their x is read, their gradient / Hessian / HVP rows are
+ * left to the device that owns them (pattern rows empty, outputs untouched),
+ * and an element's energy counts only where its first vertex is owned, so the
+ * per-shard energies sum to the global energy. Call before creating problems
+ * on the mesh. Synchronizes `stream`. */
+MG_API int mg_mesh_set_owned(mg_mesh* mesh, const uint8_t* owned_d, void* stream);
 MG_API int mg_mesh_destroy(mg_mesh* mesh);
 
 /* Problem state. Replaces Problem.__init__ (problem.py:259-297).

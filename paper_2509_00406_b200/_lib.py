@@ -42,6 +42,7 @@ SIGNATURES = [
     ("mg_mesh_counts", _INT, [_P, _I64P, _I64P, _I64P, _I64P]),
     ("mg_mesh_copy_edges", _INT, [_P, _P, _P]),
     ("mg_mesh_copy_vertex_patches", _INT, [_P, _P, _P]),
+    ("mg_mesh_set_owned", _INT, [_P, _P, _P]),
     ("mg_mesh_destroy", _INT, [_P]),
     ("mg_problem_create", _INT, [_P, _INT, _INT, _P, _INT, ctypes.POINTER(_P)]),
     ("mg_problem_add_term", _INT, [_P, _INT, _INT, ctypes.POINTER(_DBL), _INT, ctypes.POINTER(_P), _INT,

@@ -150,6 +150,11 @@ int mg_mesh_copy_vertex_patches(const mg_mesh* mesh, int32_t* patch_d, void* str
   });
 }
 
+int mg_mesh_set_owned(mg_mesh* mesh, const uint8_t* owned_d, void* stream) {
+  if (!mesh) return fail(MG_ERR_VALUE, "mesh is NULL");
+  return guard([&] { mesh_set_owned(mesh->m, owned_d, S(stream)); });
+}
+
 int mg_mesh_destroy(mg_mesh* mesh) {
   delete mesh;
   return MG_OK;

@@ -20,6 +20,7 @@ struct ElemArgs {
   const double* x;
   const double* w;
   const uint8_t* fixed;
+  const uint8_t* owned;  // shard: energy of an element counts where its slot-0 vertex is owned
   const int32_t* sel;
   const int32_t* bids;
   double* grad;
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(TPB) k_elem(TermDev t, ElemArgs a) {
     }
   }
   if constexpr (MODE != MODE_HVP) {
+    if (a.owned && e < a.M && !a.owned[a.sel ? a.sel[e * P] : e]) ev = 0.0;
     const double s = block_sum(ev);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
   }
@@ -266,6 +268,7 @@ int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx&
   a.x = c.x;
   a.w = c.w;
   a.fixed = p.any_fixed ? p.fixed.p : nullptr;
+  a.owned = p.mesh->owned.p;
   a.sel = op_sel(*p.mesh, t.dev.op);
   a.bids = t.bids.p;
   a.grad = c.grad;

@@ -90,6 +90,12 @@ struct OpLayout {
 
 struct Mesh {
   int64_t V = 0, E = 0, F = 0;
+  // rows this device assembles: all V vertices, or an owned subset when the
+  // mesh is one shard of a multi-GPU partition (mg_mesh_set_owned). Patches
+  // cover owned vertices only; the others are ribbon (halo) vertices whose x
+  // is read but whose rows belong to another device.
+  int64_t Vr = 0;
+  DBuf<uint8_t> owned;   // (V) 1 = owned, or empty = all owned
   DBuf<int32_t> faces;   // (F,3)
   DBuf<int32_t> edges;   // (E,2) canonical, sorted
   DBuf<double> pos;      // (V,3) or empty
@@ -157,6 +163,7 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
 void build_pattern(Problem& p, cudaStream_t s);
 void build_patch_layout(Problem& p, cudaStream_t s);
 void mesh_patches(Mesh& m, cudaStream_t s);
+void mesh_set_owned(Mesh& m, const uint8_t* owned_d, cudaStream_t s);
 int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s);
 
 // elem_kernels.cu (element-parallel, atomic accumulation)

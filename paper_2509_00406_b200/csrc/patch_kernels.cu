@@ -824,7 +824,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
     EvArgs a;
     a.R = m.patches.R;
     a.nterms = (int)p.terms.size();
-    a.V = m.V;
+    a.V = m.Vr;
     a.vtx_off = p.vtx_off.p;
     a.vtx = p.vtx.p;
     a.ev_off = p.lay[0].off.p;
@@ -852,7 +852,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   PatchArgs a;
   a.R = m.patches.R;
   a.nterms = (int)p.terms.size();
-  a.V = m.V;
+  a.V = m.Vr;
   a.vtx_off = p.vtx_off.p;
   a.vtx = p.vtx.p;
   a.hloc = p.hloc.p;

@@ -56,7 +56,8 @@ __global__ void k_bbox(const double* pos, int64_t V, double* out /* 6 per block 
   if (threadIdx.x < 6) out[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
 }
 
-__global__ void k_morton(const double* pos, int64_t V, const double* box, uint64_t* code, int32_t* ids) {
+__global__ void k_morton(const double* pos, int64_t V, const double* box, const uint8_t* owned, uint64_t* code,
+                         int32_t* ids) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= V) return;
   uint64_t m = 0;
@@ -66,7 +67,15 @@ __global__ void k_morton(const double* pos, int64_t V, const double* box, uint64
     t = isfinite(t) ? fmin(fmax(t, 0.0), 1.0) : 0.0;
     m |= spread3((uint64_t)(t * 2097151.0)) << (2 - c);
   }
-  code[i] = m;
+  code[i] = (owned && !owned[i]) ? ~0ull : m;  // non-owned (halo) vertices sort last
+  ids[i] = (int32_t)i;
+}
+
+// no positions: owned vertices first, in id order (stable sort on this key)
+__global__ void k_owned_key(const uint8_t* owned, int64_t V, uint64_t* code, int32_t* ids) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  code[i] = owned[i] ? 0ull : 1ull;
   ids[i] = (int32_t)i;
 }
 
@@ -75,11 +84,19 @@ __global__ void k_iota(int32_t* ids, int64_t V) {
   if (i < V) ids[i] = (int32_t)i;
 }
 
-__global__ void k_rank_pov(const int32_t* order, int64_t V, int R, int32_t* rank, int32_t* pov) {
+__global__ void k_count_owned(const uint8_t* owned, int64_t V, int* cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int c = (i < V && owned[i]) ? 1 : 0;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// rank in patch order; patch of every owned vertex (-1: halo vertex, no row here)
+__global__ void k_rank_pov(const int32_t* order, int64_t V, int64_t Vr, int R, int32_t* rank, int32_t* pov) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= V) return;
   rank[order[i]] = (int32_t)i;
-  pov[order[i]] = (int32_t)(i / R);
+  pov[order[i]] = i < Vr ? (int32_t)(i / R) : -1;
 }
 
 // (patch, element) pairs: one per distinct patch among the element's vertices
@@ -89,7 +106,7 @@ __global__ void k_patch_elem_keys(const int32_t* sel, int P, int64_t M, const in
   int pq[3];
   for (int q = 0; q < P; ++q) {
     pq[q] = pov[sel[e * P + q]];
-    bool dup = false;
+    bool dup = pq[q] < 0;  // halo vertex: its rows live on another device
     for (int r = 0; r < q; ++r) dup |= pq[r] == pq[q];
     keys[e * P + q] = dup ? ~0ull : ((uint64_t)pq[q] << 32) | (uint64_t)e;
   }
@@ -344,46 +361,62 @@ int key_bits(int64_t v) {
 void mesh_patches(Mesh& m, cudaStream_t s) {
   const int64_t V = m.V;
   PatchSet& ps = m.patches;
+  const uint8_t* owned = m.owned.p;
   ps.R = m.patch_vertices;
-  ps.num = (V + ps.R - 1) / ps.R;
+  if (owned) {
+    DBuf<int> cnt;
+    cnt.alloc(1);
+    MG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
+    k_count_owned<<<grid_for(V), TPB, 0, s>>>(owned, V, cnt.p);
+    MG_LAUNCH_CHECK();
+    m.Vr = to_host_int(cnt.p, s);
+  } else {
+    m.Vr = V;
+  }
+  ps.num = (m.Vr + ps.R - 1) / ps.R;
   ps.order.alloc(V > 0 ? V : 1);
   ps.rank.alloc(V > 0 ? V : 1);
   ps.patch_of_vertex.alloc(V > 0 ? V : 1);
   if (V == 0) return;
-  if (m.pos.p) {
-    const int nb = 256;
-    DBuf<double> part, box;
-    part.alloc(6 * nb);
-    box.alloc(6);
-    k_bbox<<<nb, TPB, 0, s>>>(m.pos.p, V, part.p);
-    MG_LAUNCH_CHECK();
-    std::vector<double> hp(6 * nb);
-    MG_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
-    double hb[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    for (int b = 0; b < nb; ++b)
-      for (int c = 0; c < 3; ++c) {
-        hb[c] = std::fmin(hb[c], hp[6 * b + c]);
-        hb[3 + c] = std::fmax(hb[3 + c], hp[6 * b + 3 + c]);
-      }
-    MG_CUDA(cudaMemcpyAsync(box.p, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+  if (m.pos.p || owned) {
     DBuf<uint64_t> code, code2;
     DBuf<int32_t> ids;
     code.alloc(V);
     code2.alloc(V);
     ids.alloc(V);
-    k_morton<<<grid_for(V), TPB, 0, s>>>(m.pos.p, V, box.p, code.p, ids.p);
+    if (m.pos.p) {
+      const int nb = 256;
+      DBuf<double> part, box;
+      part.alloc(6 * nb);
+      box.alloc(6);
+      k_bbox<<<nb, TPB, 0, s>>>(m.pos.p, V, part.p);
+      MG_LAUNCH_CHECK();
+      std::vector<double> hp(6 * nb);
+      MG_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      double hb[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      for (int b = 0; b < nb; ++b)
+        for (int c = 0; c < 3; ++c) {
+          hb[c] = std::fmin(hb[c], hp[6 * b + c]);
+          hb[3 + c] = std::fmax(hb[3 + c], hp[6 * b + 3 + c]);
+        }
+      MG_CUDA(cudaMemcpyAsync(box.p, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+      k_morton<<<grid_for(V), TPB, 0, s>>>(m.pos.p, V, box.p, owned, code.p, ids.p);
+      MG_CUDA(cudaStreamSynchronize(s));
+    } else {
+      k_owned_key<<<grid_for(V), TPB, 0, s>>>(owned, V, code.p, ids.p);
+    }
     MG_LAUNCH_CHECK();
     size_t tb = 0;
-    MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, code.p, code2.p, ids.p, ps.order.p, (int64_t)V, 0, 63, s));
+    MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, code.p, code2.p, ids.p, ps.order.p, (int64_t)V, 0, 64, s));
     Tmp t(s, tb);
-    MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, code.p, code2.p, ids.p, ps.order.p, (int64_t)V, 0, 63, s));
+    MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, code.p, code2.p, ids.p, ps.order.p, (int64_t)V, 0, 64, s));
     MG_CUDA(cudaStreamSynchronize(s));
   } else {
     k_iota<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V);
     MG_LAUNCH_CHECK();
   }
-  k_rank_pov<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V, ps.R, ps.rank.p, ps.patch_of_vertex.p);
+  k_rank_pov<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V, m.Vr, ps.R, ps.rank.p, ps.patch_of_vertex.p);
   MG_LAUNCH_CHECK();
   MG_CUDA(cudaStreamSynchronize(s));
 }
@@ -391,7 +424,7 @@ void mesh_patches(Mesh& m, cudaStream_t s) {
 void build_patch_layout(Problem& p, cudaStream_t s) {
   Mesh& m = *p.mesh;
   PatchSet& ps = m.patches;
-  const int64_t V = m.V, np = ps.num;
+  const int64_t V = m.V, Vr = m.Vr, np = ps.num;  // Vr: rows in patch order
   const int R = ps.R;
   p.layout_ready = false;
   if (V == 0 || np == 0) return;
@@ -477,10 +510,10 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
   k_lower_bounds<<<grid_for(np + 1), TPB, 0, s>>>(rib_keys_all, nr, np, rib_off.p);
   MG_LAUNCH_CHECK();
   p.vtx_off.alloc(np + 1);
-  k_vtx_off<<<grid_for(np + 1), TPB, 0, s>>>(rib_off.p, np, R, V, p.vtx_off.p);
-  p.vtx.alloc(V + nr);
-  k_fill_owned<<<grid_for(V), TPB, 0, s>>>(ps.order.p, V, R, p.vtx_off.p, p.vtx.p);
-  if (nr) k_fill_ribbon<<<grid_for(nr), TPB, 0, s>>>(rib_keys_all, nr, rib_off.p, R, V, p.vtx_off.p, p.vtx.p);
+  k_vtx_off<<<grid_for(np + 1), TPB, 0, s>>>(rib_off.p, np, R, Vr, p.vtx_off.p);
+  p.vtx.alloc(Vr + nr > 0 ? Vr + nr : 1);
+  if (Vr) k_fill_owned<<<grid_for(Vr), TPB, 0, s>>>(ps.order.p, Vr, R, p.vtx_off.p, p.vtx.p);
+  if (nr) k_fill_ribbon<<<grid_for(nr), TPB, 0, s>>>(rib_keys_all, nr, rib_off.p, R, Vr, p.vtx_off.p, p.vtx.p);
   MG_LAUNCH_CHECK();
   {
     DBuf<int> mx;
@@ -503,7 +536,7 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
     const int32_t* sel = op_sel(m, L.op);
     L.local.alloc(n * P > 0 ? n * P : 1);
     if (n) k_local_ids<<<grid_for(n), TPB, 0, s>>>(sel, P, L.elem.p, pe_of[k].p, n, ps.patch_of_vertex.p,
-                                                   ps.rank.p, R, V, rib_keys_all, rib_off.p, L.local.p, flag.p);
+                                                   ps.rank.p, R, Vr, rib_keys_all, rib_off.p, L.local.p, flag.p);
     MG_LAUNCH_CHECK();
     L.pos.alloc(n * P * P > 0 ? n * P * P : 1);
     MG_CUDA(cudaMemsetAsync(L.pos.p, 0xff, n * P * P > 0 ? n * P * P : 1, s));
@@ -512,7 +545,7 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
                                               first[k]->bids.p, p.row_offsets.p, L.pos.p, flag.p);
     MG_LAUNCH_CHECK();
     L.color.alloc(n > 0 ? n : 1);
-    k_color<<<grid_for(np), TPB, 0, s>>>(L.local.p, P, L.off.p, np, R, V, masks.p, L.color.p, flag.p);
+    k_color<<<grid_for(np), TPB, 0, s>>>(L.local.p, P, L.off.p, np, R, Vr, masks.p, L.color.p, flag.p);
     MG_LAUNCH_CHECK();
     if (to_host_int(flag.p, s)) {
       // pathological valence / patch: keep the element-parallel path
@@ -583,7 +616,7 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
         const int64_t m2 = 2 * n > 0 ? 2 * n : 1;
         k1.alloc(m2); k2.alloc(m2); v1.alloc(m2); v2.alloc(m2);
         if (n) k_rinc_keys<<<grid_for(n), TPB, 0, s>>>(op_sel(m, MG_OP_EV), L.elem.p, L.local.p, L.pos.p,
-                                                       pe_sorted.p, L.off.p, n, R, V, k1.p, v1.p);
+                                                       pe_sorted.p, L.off.p, n, R, Vr, k1.p, v1.p);
         MG_LAUNCH_CHECK();
         size_t tb = 0;
         MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, 2 * n, 0, 64, s));
@@ -591,8 +624,8 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
           Tmp t(s, tb);
           MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k1.p, k2.p, v1.p, v2.p, 2 * n, 0, 64, s));
         }
-        p.rinc_off.alloc(V + 1);
-        k_lower_bounds_rows<<<grid_for(V + 1), TPB, 0, s>>>(k2.p, 2 * n, V, p.rinc_off.p);
+        p.rinc_off.alloc(Vr + 1);
+        k_lower_bounds_rows<<<grid_for(Vr + 1), TPB, 0, s>>>(k2.p, 2 * n, Vr, p.rinc_off.p);
         MG_LAUNCH_CHECK();
         p.rinc = std::move(v2);
         MG_CUDA(cudaStreamSynchronize(s));
@@ -602,27 +635,27 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
   }
 
   // shared-memory row offsets of owned rows (patch order) and diagonal positions
-  p.hloc.alloc(V);
+  p.hloc.alloc(Vr > 0 ? Vr : 1);
   p.diag_pos.alloc(V);
   p.max_patch_blocks = 0;
   if (p.with_hessian && p.pattern_ready) {
     DBuf<int32_t> len, scan;
-    len.alloc(V + 1);
-    scan.alloc(V + 1);
-    MG_CUDA(cudaMemsetAsync(len.p + V, 0, sizeof(int32_t), s));
-    k_row_len_patch_order<<<grid_for(V), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, V, len.p);
+    len.alloc(Vr + 1);
+    scan.alloc(Vr + 1);
+    MG_CUDA(cudaMemsetAsync(len.p + Vr, 0, sizeof(int32_t), s));
+    if (Vr) k_row_len_patch_order<<<grid_for(Vr), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, Vr, len.p);
     MG_LAUNCH_CHECK();
     size_t tb = 0;
-    MG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, scan.p, V + 1, s));
+    MG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, scan.p, Vr + 1, s));
     {
       Tmp t(s, tb);
-      MG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, len.p, scan.p, V + 1, s));
+      MG_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, len.p, scan.p, Vr + 1, s));
     }
-    k_localize<<<grid_for(V), TPB, 0, s>>>(scan.p, V, R, p.hloc.p);
+    if (Vr) k_localize<<<grid_for(Vr), TPB, 0, s>>>(scan.p, Vr, R, p.hloc.p);
     DBuf<int> mx;
     mx.alloc(1);
     MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
-    k_patch_blocks<<<grid_for(np), TPB, 0, s>>>(scan.p, V, R, np, mx.p);
+    k_patch_blocks<<<grid_for(np), TPB, 0, s>>>(scan.p, Vr, R, np, mx.p);
     k_diag_pos<<<grid_for(V), TPB, 0, s>>>(p.row_offsets.p, p.col32.p, V, p.diag_pos.p);
     MG_LAUNCH_CHECK();
     p.max_patch_blocks = to_host_int(mx.p, s);

@@ -148,6 +148,18 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
   } else {
     m.E = 0;
   }
+  m.Vr = V;
+  mesh_patches(m, s);
+  MG_CUDA(cudaStreamSynchronize(s));
+}
+
+void mesh_set_owned(Mesh& m, const uint8_t* owned_d, cudaStream_t s) {
+  if (!owned_d) {
+    m.owned.reset();
+  } else {
+    m.owned.alloc(m.V > 0 ? m.V : 1);
+    if (m.V) MG_CUDA(cudaMemcpyAsync(m.owned.p, owned_d, m.V, cudaMemcpyDeviceToDevice, s));
+  }
   mesh_patches(m, s);
   MG_CUDA(cudaStreamSynchronize(s));
 }
@@ -157,7 +169,7 @@ namespace {
 // All ordered vertex pairs (incl. (i,i)) of every element whose both ends are
 // free, as a*V+b keys (problem.py:391-396); pinned pairs become ~0 and sort last.
 __global__ void k_pair_keys(const int32_t* sel, int P, int64_t M, int64_t V, const uint8_t* fixed,
-                            uint64_t* keys) {
+                            const uint8_t* owned, uint64_t* keys) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t pp = (int64_t)P * P;
   if (i >= M * pp) return;
@@ -166,6 +178,7 @@ __global__ void k_pair_keys(const int32_t* sel, int P, int64_t M, int64_t V, con
   int64_t a = sel ? sel[e * P + q1] : e;
   int64_t b = sel ? sel[e * P + q2] : e;
   bool ok = !fixed || (!fixed[a] && !fixed[b]);
+  ok &= !owned || owned[a];  // shard: only owned rows are assembled here
   keys[i] = ok ? (uint64_t)(a * V + b) : ~0ull;
 }
 
@@ -182,7 +195,7 @@ __global__ void k_rows_cols(const uint64_t* keys, int64_t nnzb, int64_t V, int32
 // Per-element block ids by binary search in the sorted unique key list
 // (the reference's searchsorted, problem.py:407-414); -1 marks pinned pairs.
 __global__ void k_bids(const int32_t* sel, int P, int64_t M, int64_t V, const uint8_t* fixed,
-                       const uint64_t* keys, int64_t nnzb, int32_t* bids) {
+                       const uint8_t* owned, const uint64_t* keys, int64_t nnzb, int32_t* bids) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t pp = (int64_t)P * P;
   if (i >= M * pp) return;
@@ -190,7 +203,7 @@ __global__ void k_bids(const int32_t* sel, int P, int64_t M, int64_t V, const ui
   int r = (int)(i % pp), q1 = r / P, q2 = r % P;
   int64_t a = sel ? sel[e * P + q1] : e;
   int64_t b = sel ? sel[e * P + q2] : e;
-  if (fixed && (fixed[a] || fixed[b])) { bids[i] = -1; return; }
+  if ((fixed && (fixed[a] || fixed[b])) || (owned && !owned[a])) { bids[i] = -1; return; }
   uint64_t k = (uint64_t)(a * V + b);
   int64_t lo = 0, hi = nnzb;
   while (lo < hi) {
@@ -220,7 +233,7 @@ void build_pattern(Problem& p, cudaStream_t s) {
     for (auto& t : p.terms) {
       int64_t cnt = t.M * t.dev.P * t.dev.P;
       if (cnt) k_pair_keys<<<grid_for(cnt), TPB, 0, s>>>(op_sel(m, t.dev.op), t.dev.P, t.M, V,
-                                                          p.any_fixed ? p.fixed.p : nullptr, keys + off);
+                                                          p.any_fixed ? p.fixed.p : nullptr, m.owned.p, keys + off);
       MG_LAUNCH_CHECK();
       off += cnt;
     }
@@ -258,7 +271,7 @@ void build_pattern(Problem& p, cudaStream_t s) {
     int64_t cnt = t.M * t.dev.P * t.dev.P;
     t.bids.alloc(cnt > 0 ? cnt : 1);
     if (cnt) k_bids<<<grid_for(cnt), TPB, 0, s>>>(op_sel(m, t.dev.op), t.dev.P, t.M, V,
-                                                   p.any_fixed ? p.fixed.p : nullptr, keys, nnzb, t.bids.p);
+                                                   p.any_fixed ? p.fixed.p : nullptr, m.owned.p, keys, nnzb, t.bids.p);
     MG_LAUNCH_CHECK();
   }
   MG_CUDA(cudaStreamSynchronize(s));
