@@ -86,6 +86,7 @@ int64_t partials_needed(const Problem& p) {
   int64_t need = 1;
   for (auto& t : p.terms) need += elem_partials_needed(t);
   if (p.mesh->patches.num > need) need = p.mesh->patches.num;
+  if ((p.mesh->Vr + 31) / 32 > need) need = (p.mesh->Vr + 31) / 32;  // edge row kernel: one partial per warp
   return need + 1;
 }
 
@@ -275,7 +276,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
     int64_t np = 0;
     if (p.deterministic && p.layout_ready) {
       np = launch_patch(p, mode, c, 0);
-      launches += 1;
+      launches += p.ev_fast ? 2 : 1;
     } else {
       MG_CUDA(cudaMemsetAsync(grad_d, 0, sizeof(double) * p.n * p.mesh->V, s));
       if (p.with_hessian && p.nnzb)
@@ -285,7 +286,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
         ++launches;
       }
     }
-    reduce_partials(p.partials.p, np, energy_d, s);
+    reduce_partials(p.partials.p, np, energy_d, s, p.ev_fast && p.deterministic && p.layout_ready ? p.redo.p : nullptr);
     p.last_launches = launches + 1;
   });
 }
@@ -327,6 +328,10 @@ int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, 
     if (p.deterministic && p.layout_ready) {
       launch_patch(p, MODE_HVP, c, 0);
       launches = 1;
+      if (p.ev_fast) {
+        MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
+        launches = 2;
+      }
     } else {
       MG_CUDA(cudaMemsetAsync(y_d, 0, sizeof(double) * p.n * p.mesh->V, s));
       for (auto& t : p.terms) {

@@ -1,0 +1,556 @@
+// Edge row kernel: the patch-owner assembly specialised to problems whose
+// terms are V terms and radial EV terms E = phi(|x_i - x_j|^2) (cloth
+// springs, smoothing).
+//
+// One thread per owned row; rows in patch (Morton) order, EV_ROW_BLOCK rows
+// per CTA, so a CTA's rows and their neighbours are spatially compact and the
+// neighbours' x hit L1/L2. A thread
+//   * evaluates its V terms,
+//   * walks its incident edges in column order (records built at setup) and
+//     evaluates each from a one-variable dual on r = |d|^2 (Radial in
+//     terms.cuh) with the closed-form PSD clamp; non-finite lanes take the
+//     exact K = n dual so NaN / Inf land where the reference puts them,
+//   * accumulates gradient / HVP row and diagonal block in registers in that
+//     fixed order (bitwise reproducible), writes each off-diagonal block of its
+//     row into a shared-memory row buffer in output layout as it goes,
+//   * and streams the finished row to HBM with one bulk (TMA) copy.
+// No barriers, no atomics, no memset: every output byte is written once; an
+// edge is evaluated by each of its two owner rows (recompute instead of
+// communicate). The energy counts every element once (edges at their first
+// vertex) through fixed-order per-warp partials.
+#include "elem_eval.cuh"
+#include "mg_internal.cuh"
+#include "psd.cuh"
+
+namespace mg {
+
+namespace {
+
+constexpr int PT = EV_ROW_BLOCK;  // rows (threads) per CTA
+constexpr int MAXT = 8;
+
+struct EvArgs {
+  int nterms;
+  int64_t V;  // owned rows (patch order)
+  const int32_t* order;      // (V) vertex of each row
+  const uint8_t* pfix;       // (V) pinned flag of each row
+  const int32_t* rinc_off;   // (V+1)
+  const uint64_t* rrec;      // lo: edge | slot << 31, hi: other | pinned(other) << 31
+  const int64_t* prow_ro;
+  const int32_t* prow_len;
+  const uint8_t* prow_dp;
+  const int32_t* hoff;
+  const double* x;
+  const double* w;
+  double* grad;
+  double* hess;
+  double* y;
+  double* partials;
+  int* redo;  // raised by the radial kernel on a non-finite lane
+  double floor;
+  TermDev terms[MAXT];
+};
+
+// per-edge record (doubles) and per-row V-term accumulator widths
+template <int N, int MODE, bool PSD>
+struct EvRec {
+  static constexpr int T = TriN<N>::value;
+  // HESS: [g (N), A + dl I (T)];  GRAD: [g];  HVP: [y_a] or, with PSD, [y_a, y_b]
+  static constexpr int SW = MODE == MODE_HESS ? N + T : (MODE == MODE_HVP && PSD) ? 2 * N : N;
+  static constexpr int VW = MODE == MODE_HESS ? N + T : N;
+};
+
+MG_DI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// dst[0..n) = src[0..n) (doubles), src in shared memory with the same 16-byte
+// phase as dst: 8-byte head / tail stores plus one bulk (TMA) copy of the
+// aligned middle. The caller waits for the bulk group before leaving.
+MG_DI void row_store_bulk(double* dst, const double* src, int n) {
+  int k0 = 0;
+  if (reinterpret_cast<uintptr_t>(dst) & 15) {
+    if (n > 0) dst[0] = src[0];
+    k0 = 1;
+  }
+  int m = n - k0;
+  if (m <= 0) return;
+  if (m & 1) {
+    dst[n - 1] = src[n - 1];
+    --m;
+  }
+  if (m > 0) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src + k0);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(dst + k0), "r"(sa), "r"((uint32_t)m * 8u) : "memory");
+  }
+}
+
+template <class Q>
+MG_DI double hess00(const Q& q) {
+  if constexpr (Q::kZero) return 0.0;
+  else return q.h[0];
+}
+
+// Closed-form clamp of a radial block c_i I + c_d d d^T (r = |d|^2): the
+// transverse eigenvalue is c_i, the axial one c_i + c_d r. Already above the
+// floor -> unchanged (the reference's eigh recomposition equals the input to
+// rounding); otherwise Q max(L, f) Q^T = m_t I + (m_d - m_t) d d^T / r.
+MG_DI void radial_clamp(double& ci, double& cd, double r, double f) {
+  const double lt = ci, ld = ci + cd * r;
+  if (lt > f && ld > f) return;
+  const double mt = lt > f ? lt : f, md = ld > f ? ld : f;
+  ci = mt;
+  cd = r > 0.0 ? (md - mt) / r : 0.0;
+}
+
+// Radial evaluation of one patch edge (sum over the EV terms). Returns false
+// when any intermediate is non-finite (the caller then takes edge_dual).
+//   val: energy;  rec: record (EvRec);  dl: floor shift of the off-diagonal
+//   blocks (HESS): block(a,b) = -(A) + dl I = -rec_A + 2 dl I.
+template <int N, int MODE, bool PSD>
+MG_DI bool edge_radial(const EvArgs& a, int64_t e, const double* xa, const double* xb, const double* wa,
+                       const double* wb, bool fa, bool fb, double& val, double* rec, double& dl) {
+  using L = EvRec<N, MODE, PSD>;
+  double d[N];
+  double rr = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    d[c] = xa[c] - xb[c];
+    rr = d[c] * d[c] + rr;
+  }
+  double gam = 0.0;  // sum of 2 phi'
+  double ci_s = 0.0, cd_s = 0.0;
+  double yacc[2 * N];
+#pragma unroll
+  for (int i = 0; i < 2 * N; ++i) yacc[i] = 0.0;
+  bool ok = true;
+  val = 0.0;
+  dl = 0.0;
+  for (int ti = 0; ti < a.nterms; ++ti) {
+    const TermDev& t = a.terms[ti];
+    if (t.op != MG_OP_EV) continue;
+    if constexpr (MODE == MODE_GRAD) {
+      Dg<1> r;
+      r.v = rr;
+      r.g[0] = 1.0;
+      auto q = t.type == MG_TERM_SPRING ? term_eval_radial<MG_TERM_SPRING>(t, e, r)
+                                        : term_eval_radial<MG_TERM_EDGE_LENGTH>(t, e, r);
+      ok &= isfinite(q.v) && isfinite(q.g[0]);
+      val += q.v;
+      gam += 2.0 * q.g[0];
+    } else {
+      Dh<1, true> r;
+      r.v = rr;
+      r.g[0] = 1.0;
+      double pv, p1, p2;
+      if (t.type == MG_TERM_SPRING) {
+        auto q = term_eval_radial<MG_TERM_SPRING>(t, e, r);
+        pv = q.v; p1 = q.g[0]; p2 = hess00(q);
+      } else {
+        auto q = term_eval_radial<MG_TERM_EDGE_LENGTH>(t, e, r);
+        pv = q.v; p1 = q.g[0]; p2 = hess00(q);
+      }
+      ok &= isfinite(pv) && isfinite(p1) && isfinite(p2);
+      val += pv;
+      gam += 2.0 * p1;
+      double ci = 2.0 * p1, cd = 4.0 * p2, sh = 0.0;
+      if constexpr (PSD) {
+        if (fa && fb) {  // spectrum of [[A,-A],[-A,A]] = 2 eig(A) U {0}: clamp 2A, halve, shift floor/2
+          ci *= 2.0; cd *= 2.0;
+          radial_clamp(ci, cd, rr, a.floor);
+          ci *= 0.5; cd *= 0.5;
+          sh = 0.5 * a.floor;
+        } else if (fa || fb) {
+          radial_clamp(ci, cd, rr, a.floor);
+        }
+      }
+      if constexpr (MODE == MODE_HESS) {
+        ci_s += ci;
+        cd_s += cd;
+        dl += sh;
+      } else {  // HVP: y_a = M (wa - wb) + sh (wa + wb), y_b = -M (wa - wb) + sh (wa + wb)
+        double wd[N], ws[N], dw = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const double ua = fa ? wa[c] : 0.0, ub = fb ? wb[c] : 0.0;
+          wd[c] = ua - ub;
+          ws[c] = ua + ub;
+          dw += d[c] * wd[c];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double m = ci * wd[i] + cd * d[i] * dw;
+          yacc[i] += m + sh * ws[i];
+          yacc[N + i] += -m + sh * ws[i];
+        }
+      }
+    }
+  }
+  if (!ok) return false;
+  if constexpr (MODE == MODE_GRAD || MODE == MODE_HESS) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) rec[i] = gam * d[i];
+  }
+  if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) rec[N + tri(i, j)] = cd_s * d[i] * d[j] + (i == j ? ci_s + dl : 0.0);
+  }
+  if constexpr (MODE == MODE_HVP) {
+#pragma unroll
+    for (int i = 0; i < L::SW; ++i) rec[i] = yacc[i];
+  }
+  return true;
+}
+
+// Exact path: K = n dual on d = x_a - x_b (bitwise equal to the reference's
+// K = 2n dual, TwoPoint in terms.cuh), packed n x n blocks, generic clamp.
+
+template <int N, int MODE, bool PSD>
+MG_DI void edge_dual(const EvArgs& a, int64_t e, const double* xa, const double* xb, const double* wa,
+                     const double* wb, bool fa, bool fb, double& val, double* rec, double& dl) {
+  constexpr int T = TriN<N>::value;
+  using L = EvRec<N, MODE, PSD>;
+  double acc[L::SW];
+#pragma unroll
+  for (int i = 0; i < L::SW; ++i) acc[i] = 0.0;
+  val = 0.0;
+  dl = 0.0;
+  for (int ti = 0; ti < a.nterms; ++ti) {
+    const TermDev& t = a.terms[ti];
+    if (t.op != MG_OP_EV) continue;
+    const int tt = t.type;
+    if constexpr (MODE == MODE_GRAD) {
+      Vec<Dg<N>, N> d;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        d[c].v = xa[c] - xb[c];
+#pragma unroll
+        for (int i = 0; i < N; ++i) d[c].g[i] = (i == c) ? 1.0 : 0.0;
+      }
+      auto r = tt == MG_TERM_SPRING ? term_eval_diff<MG_TERM_SPRING, N>(t, e, d)
+                                    : term_eval_diff<MG_TERM_EDGE_LENGTH, N>(t, e, d);
+      val += r.v;
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] += r.g[i];
+    } else {
+      Vec<Dh<N, true>, N> d;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        d[c].v = xa[c] - xb[c];
+#pragma unroll
+        for (int i = 0; i < N; ++i) d[c].g[i] = (i == c) ? 1.0 : 0.0;
+      }
+      auto r = tt == MG_TERM_SPRING ? term_eval_diff<MG_TERM_SPRING, N>(t, e, d)
+                                    : term_eval_diff<MG_TERM_EDGE_LENGTH, N>(t, e, d);
+      double h[T];
+#pragma unroll
+      for (int i = 0; i < T; ++i) h[i] = 0.5 * (r.h[i] + r.h[i]);
+      double sh = 0.0;
+      if constexpr (PSD) {
+        if (all_finite<N>(h)) {
+          if (fa && fb) {
+#pragma unroll
+            for (int i = 0; i < T; ++i) h[i] = 2.0 * h[i];
+            project_if_needed<N>(h, a.floor);
+#pragma unroll
+            for (int i = 0; i < T; ++i) h[i] = 0.5 * h[i];
+            sh = 0.5 * a.floor;
+          } else if (fa || fb) {
+            project_if_needed<N>(h, a.floor);
+          }
+        }
+      }
+      val += r.v;
+      if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] += r.g[i];
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) acc[N + tri(i, j)] += h[tri(i, j)] + (i == j ? sh : 0.0);
+        dl += sh;
+      } else {
+        double wd[N], ws[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const double ua = fa ? wa[c] : 0.0, ub = fb ? wb[c] : 0.0;
+          wd[c] = ua - ub;
+          ws[c] = ua + ub;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double m = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) m += h[tri(i, j)] * wd[j];
+          acc[i] += m + sh * ws[i];
+          if constexpr (L::SW == 2 * N) acc[N + i] += -m + sh * ws[i];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < L::SW; ++i) rec[i] = acc[i];
+}
+
+// HVP without PSD: forward-over-forward dual on d (exact path)
+template <int N>
+MG_DI void edge_dual_fof(const EvArgs& a, int64_t e, const double* xa, const double* xb, const double* wa,
+                         const double* wb, bool fa, bool fb, double* rec) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) rec[i] = 0.0;
+  for (int ti = 0; ti < a.nterms; ++ti) {
+    const TermDev& t = a.terms[ti];
+    if (t.op != MG_OP_EV) continue;
+    Vec<Df<N, true>, N> d;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      d[c].v = xa[c] - xb[c];
+      d[c].vd = (fa ? wa[c] : 0.0) - (fb ? wb[c] : 0.0);
+#pragma unroll
+      for (int i = 0; i < N; ++i) d[c].g[i] = (i == c) ? 1.0 : 0.0;
+    }
+    auto r = t.type == MG_TERM_SPRING ? term_eval_diff<MG_TERM_SPRING, N>(t, e, d)
+                                      : term_eval_diff<MG_TERM_EDGE_LENGTH, N>(t, e, d);
+#pragma unroll
+    for (int i = 0; i < N; ++i) rec[i] += r.gd[i];
+  }
+}
+
+// EXACT = false: radial evaluation only; a non-finite lane raises *a.redo.
+// EXACT = true : launched after it; returns at once unless *a.redo is set,
+//                then recomputes every row with the exact K = n dual path.
+template <int N, int MODE, bool PSD, bool EXACT>
+__global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a) {
+  using L = EvRec<N, MODE, PSD>;
+  constexpr int T = L::T, SW = L::SW, NN = N * N;
+  extern __shared__ __align__(16) double hbuf[];  // this CTA's rows in output layout
+  if constexpr (EXACT) {
+    if (*(volatile const int*)a.redo == 0) return;
+  }
+  const int64_t nblk = (a.V + PT - 1) / PT;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  const int64_t row = blk * PT + threadIdx.x;
+  double eacc = 0.0;
+  bool finite = true;
+  if (row < a.V) {
+    const int g = a.order[row];
+    const bool fr = !a.pfix[row];
+    const int k0 = a.rinc_off[row], k1 = a.rinc_off[row + 1];
+    int64_t ro = 0;
+    int len = 0, dp = 255, ho = 0;
+    if constexpr (MODE == MODE_HESS) {
+      ro = a.prow_ro[row];
+      len = a.prow_len[row];
+      dp = a.prow_dp[row];
+      ho = a.hoff[row];
+    }
+    double xs[N], wsv[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      xs[c] = a.x[(int64_t)g * N + c];
+      if constexpr (MODE == MODE_HVP) wsv[c] = a.w[(int64_t)g * N + c];
+      else wsv[c] = 0.0;
+    }
+    double vec[N], dg[T];
+#pragma unroll
+    for (int i = 0; i < N; ++i) vec[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < T; ++i) dg[i] = 0.0;
+    // V terms
+    {
+      const double* xr[1] = {xs};
+      const double* wr[1] = {wsv};
+      for (int ti = 0; ti < a.nterms; ++ti) {
+        const TermDev& t = a.terms[ti];
+        if (t.op != MG_OP_V) continue;
+        if (t.type == MG_TERM_INERTIA) {
+          ElemOut<MG_TERM_INERTIA, N, MODE, PSD> o;
+          eval_element<MG_TERM_INERTIA, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
+          eacc += o.val;
+#pragma unroll
+          for (int k = 0; k < N; ++k) vec[k] += o.g[k];
+          if constexpr (MODE == MODE_HESS) {
+            if (o.has_h)
+#pragma unroll
+              for (int k = 0; k < T; ++k) dg[k] += o.h[k];
+          }
+        } else if (t.type == MG_TERM_GRAVITY) {
+          ElemOut<MG_TERM_GRAVITY, N, MODE, PSD> o;
+          eval_element<MG_TERM_GRAVITY, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
+          eacc += o.val;
+#pragma unroll
+          for (int k = 0; k < N; ++k) vec[k] += o.g[k];
+          if constexpr (MODE == MODE_HESS) {
+            if (o.has_h)
+#pragma unroll
+              for (int k = 0; k < T; ++k) dg[k] += o.h[k];
+          }
+        }
+      }
+    }
+    // incident edges in column order; the diagonal block's position is where
+    // the column passes g (free neighbours only own a block)
+    double* hrow = hbuf + ho;
+    int pos = 0;
+    uint64_t nrc = k0 < k1 ? a.rrec[k0] : 0;
+    for (int k = k0; k < k1; ++k) {
+      const uint64_t rc = nrc;
+      if (k + 1 < k1) nrc = a.rrec[k + 1];
+      const uint32_t lo = (uint32_t)rc, hi = (uint32_t)(rc >> 32);
+      const int64_t e = lo & 0x7fffffffu;
+      const int q = (int)(lo >> 31);
+      const int o = (int)(hi & 0x7fffffffu);
+      const bool fo = !(hi >> 31);
+      double xo[N], wo[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        xo[c] = a.x[(int64_t)o * N + c];
+        if constexpr (MODE == MODE_HVP) wo[c] = a.w[(int64_t)o * N + c];
+        else wo[c] = 0.0;
+      }
+      // canonical orientation: slot 0 is the edge's first vertex (values
+      // selected, not pointers, so everything stays in registers)
+      double xa[N], xb[N], wa[N], wb[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        xa[c] = q == 0 ? xs[c] : xo[c];
+        xb[c] = q == 0 ? xo[c] : xs[c];
+        wa[c] = q == 0 ? wsv[c] : wo[c];
+        wb[c] = q == 0 ? wo[c] : wsv[c];
+      }
+      const bool fa = q == 0 ? fr : fo, fb = q == 0 ? fo : fr;
+      double rec[SW], val, dl;
+      if constexpr (EXACT) {
+        if constexpr (MODE == MODE_HVP && !PSD) edge_dual_fof<N>(a, e, xa, xb, wa, wb, fa, fb, rec);
+        else edge_dual<N, MODE, PSD>(a, e, xa, xb, wa, wb, fa, fb, val, rec, dl);
+      } else {
+        finite &= edge_radial<N, MODE, PSD>(a, e, xa, xb, wa, wb, fa, fb, val, rec, dl);
+      }
+      if constexpr (MODE != MODE_HVP) {
+        if (q == 0) eacc += val;  // an edge's energy counts at its first vertex
+      }
+      if constexpr (MODE == MODE_HVP && PSD) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += rec[q * N + i];
+      } else {
+        const double sg = q == 0 ? 1.0 : -1.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += sg * rec[i];
+      }
+      if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+        for (int i = 0; i < T; ++i) dg[i] += rec[N + i];
+        if (fr && fo) {
+          if (dp != 255 && pos == dp) ++pos;  // leave the diagonal's slot
+          double* dst = hrow + pos * NN;
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int c = 0; c < N; ++c) dst[i * N + c] = -rec[N + tri(i, c)] + (i == c ? 2.0 * dl : 0.0);
+          ++pos;
+        }
+      }
+    }
+    double* vout = MODE == MODE_HVP ? a.y : a.grad;
+#pragma unroll
+    for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+    if constexpr (MODE == MODE_HESS) {
+      if (fr && dp != 255) {
+        double* dst = hrow + dp * NN;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
+      }
+      if (len > 0) {
+        fence_proxy_async_smem();
+        row_store_bulk(a.hess + ro * NN, hrow, len * NN);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    }
+  }
+  if constexpr (!EXACT) {
+    if (!finite) *a.redo = 1;
+  }
+  if constexpr (MODE != MODE_HVP) {
+    // fixed-order warp partial (no block barrier)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
+    if ((threadIdx.x & 31) == 0) a.partials[(blk * PT + threadIdx.x) >> 5] = eacc;
+  }
+  }  // row blocks
+}
+
+template <int N, int MODE, bool PSD>
+void launch_rows(const EvArgs& a, int hd_max, cudaStream_t st) {
+  const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
+  if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
+  const int64_t nb = (a.V + PT - 1) / PT;
+  if (!nb) return;
+  auto fast = k_rows_ev<N, MODE, PSD, false>;
+  auto exact = k_rows_ev<N, MODE, PSD, true>;
+  if (sm) {
+    MG_CUDA(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    MG_CUDA(cudaFuncSetAttribute(exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  }
+  fast<<<(unsigned)nb, PT, sm, st>>>(a);
+  MG_LAUNCH_CHECK();
+  // exact re-run only when a lane was non-finite (reads the flag and exits otherwise)
+  int dev = 0, sms = 148;
+  MG_CUDA(cudaGetDevice(&dev));
+  MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t ge = nb < (int64_t)sms * 4 ? nb : (int64_t)sms * 4;
+  exact<<<(unsigned)ge, PT, sm, st>>>(a);
+  MG_LAUNCH_CHECK();
+}
+
+template <int N>
+void launch_rows_mode(const EvArgs& a, int hd, Mode mode, bool psd, cudaStream_t st) {
+  switch (mode) {
+    case MODE_GRAD: launch_rows<N, MODE_GRAD, false>(a, hd, st); break;
+    case MODE_HESS:
+      if (psd) launch_rows<N, MODE_HESS, true>(a, hd, st);
+      else launch_rows<N, MODE_HESS, false>(a, hd, st);
+      break;
+    case MODE_HVP:
+      if (psd) launch_rows<N, MODE_HVP, true>(a, hd, st);
+      else launch_rows<N, MODE_HVP, false>(a, hd, st);
+      break;
+    default: throw Error(MG_ERR_UNSUPPORTED, "edge row kernel assembles grad / Hessian / HVP only");
+  }
+}
+
+}  // namespace
+
+int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset) {
+  const Mesh& m = *p.mesh;
+  if (p.terms.size() > MAXT) throw Error(MG_ERR_UNSUPPORTED, "at most 8 terms per problem on the patch path");
+  EvArgs a;
+  a.nterms = (int)p.terms.size();
+  a.V = m.Vr;
+  a.order = m.patches.order.p;
+  a.pfix = p.pfix.p;
+  a.rinc_off = p.rinc_off.p;
+  a.rrec = p.rrec.p;
+  a.prow_ro = p.prow_ro.p;
+  a.prow_len = p.prow_len.p;
+  a.prow_dp = p.prow_dp.p;
+  a.hoff = p.hoff.p;
+  a.x = c.x;
+  a.w = c.w;
+  a.grad = c.grad;
+  a.hess = c.hess;
+  a.y = c.y;
+  a.partials = c.partials + partial_offset;
+  a.redo = p.redo.p;
+  a.floor = c.floor;
+  for (int i = 0; i < a.nterms; ++i) a.terms[i] = p.terms[i].dev;
+  const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
+  if (p.n == 3) launch_rows_mode<3>(a, hd, mode, c.psd, c.stream);
+  else launch_rows_mode<2>(a, hd, mode, c.psd, c.stream);
+  return mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
+}
+
+}  // namespace mg

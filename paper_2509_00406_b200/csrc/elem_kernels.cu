@@ -230,11 +230,14 @@ void launch_t(int n, const Term& t, Mode mode, bool psd, const ElemArgs& a, cuda
   }
 }
 
-__global__ void k_reduce(const double* partials, int64_t n, double* out) {
+__global__ void k_reduce(const double* partials, int64_t n, double* out, int* clear_flag) {
   double acc = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
   const double s = block_sum(acc);
-  if (threadIdx.x == 0) out[0] = s;
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    if (clear_flag) *clear_flag = 0;
+  }
 }
 
 template <int N>
@@ -289,8 +292,8 @@ int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx&
   return mode == MODE_HVP ? 0 : elem_partials_needed(t);
 }
 
-void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s) {
-  k_reduce<<<1, 1024, 0, s>>>(partials, n, out);
+void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag) {
+  k_reduce<<<1, 1024, 0, s>>>(partials, n, out, clear_flag);
   MG_LAUNCH_CHECK();
 }
 

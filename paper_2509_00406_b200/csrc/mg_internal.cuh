@@ -109,6 +109,8 @@ struct Term {
   DBuf<int32_t> bids;          // (M,P,P) Hessian block ids, -1 = pinned pair
 };
 
+constexpr int EV_ROW_BLOCK = 64;  // rows (threads) per CTA of the edge row kernel
+
 struct Problem {
   Mesh* mesh = nullptr;
   int n = 3;
@@ -135,13 +137,18 @@ struct Problem {
   int max_patch_vertices = 0;
   int max_patch_blocks = 0;
   int max_patch_elems = 0;     // max EV entries of one patch
-  // two-point edge fast path (all EV terms two-point, no FV terms): per owned
-  // row (patch order) its incident patch entries sorted by column;
-  // packed: local entry (16 b) | slot q (bit 16) | row position of the other
-  // endpoint (bits 24..31, 255 = pinned)
+  // edge row kernel (all EV terms radial, no FV terms): one thread per owned
+  // row, rows in patch order; per row its incident edges in column order
   bool ev_fast = false;
-  DBuf<int32_t> rinc_off;      // (V+1)
-  DBuf<uint32_t> rinc;
+  DBuf<int32_t> rinc_off;      // (Vr+1)
+  DBuf<uint64_t> rrec;         // (incidences) lo: edge | slot << 31, hi: other | pinned(other) << 31
+  DBuf<uint8_t> pfix;          // (Vr) pinned flag of each row
+  DBuf<int64_t> prow_ro;       // (Vr) row start
+  DBuf<int32_t> prow_len;      // (Vr) row length (blocks)
+  DBuf<uint8_t> prow_dp;       // (Vr) diagonal block position (255: none)
+  DBuf<int32_t> hoff;          // (Vr) row-buffer offset (doubles) in its CTA, 16-byte phase matched
+  int max_patch_hdoubles = 0;  // max row-buffer doubles of one CTA
+  DBuf<int> redo;              // (1) non-finite lane seen by the radial kernel; cleared by the energy reduction
   int64_t recomputed_elements = 0;
 };
 
@@ -162,6 +169,7 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
                 const double* pos_d, cudaStream_t s);
 void build_pattern(Problem& p, cudaStream_t s);
 void build_patch_layout(Problem& p, cudaStream_t s);
+void build_rows_ev(Problem& p, cudaStream_t s);
 void mesh_patches(Mesh& m, cudaStream_t s);
 void mesh_set_owned(Mesh& m, const uint8_t* owned_d, cudaStream_t s);
 int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s);
@@ -186,9 +194,11 @@ int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx&
 int64_t elem_partials_needed(const Term& t);
 // patch_kernels.cu (deterministic row-owner assembly)
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
+// edge_kernels.cu (two-point edge fast path of the patch-owner assembly)
+int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 bool patch_supported(const Problem& p);
 // fixed-order reduction of energy partials -> out[0]
-void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s);
+void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag = nullptr);
 void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s);
 
 }  // namespace mg

@@ -20,6 +20,7 @@
 // light problems (cloth) independent of heavy terms (sphere).
 #include "mg_internal.cuh"
 #include "psd.cuh"
+#include "elem_eval.cuh"
 
 namespace mg {
 
@@ -94,122 +95,6 @@ __device__ double block_sum(double v) {
   if (threadIdx.x == 0)
     for (int i = 0; i < PT / 32; ++i) r += ws[i];
   return r;
-}
-
-// Evaluate one element: dual result -> value + per-slot contributions.
-//   MODE_GRAD: g[K];  MODE_HESS: g[K] and packed h (valid flag);
-//   MODE_HVP: hv[K] (H v, PSD-clamped if requested).
-template <int TT, int N, int MODE, bool PSD>
-struct ElemOut {
-  static constexpr int P = TermInfo<TT>::P, K = P * N;
-  double val;
-  double g[K];
-  double h[(MODE == MODE_HESS) ? TriN<K>::value : 1];
-  bool has_h;
-};
-
-template <int TT, int N, int MODE, bool PSD>
-__device__ __forceinline__ void eval_element(const TermDev& t, int64_t e, const int* vid, const double* const* xr,
-                                             const double* const* wr, const bool* fr, double floor,
-                                             ElemOut<TT, N, MODE, PSD>& o) {
-  constexpr int P = TermInfo<TT>::P, K = P * N;
-  if constexpr (MODE == MODE_ENERGY) {
-    Vec<Dv<K>, N> X[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q)
-#pragma unroll
-      for (int c = 0; c < N; ++c) X[q][c].v = xr[q][c];
-    o.val = term_eval<TT, N>(t, e, vid, X).v;
-  } else if constexpr (MODE == MODE_GRAD) {
-    Vec<Dg<K>, N> X[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q)
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        X[q][c].v = xr[q][c];
-#pragma unroll
-        for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
-      }
-    auto r = term_eval<TT, N>(t, e, vid, X);
-    o.val = r.v;
-#pragma unroll
-    for (int i = 0; i < K; ++i) o.g[i] = r.g[i];
-  } else if constexpr (MODE == MODE_HESS || (MODE == MODE_HVP && PSD)) {
-    Vec<Dh<K, true>, N> X[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q)
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        X[q][c].v = xr[q][c];
-#pragma unroll
-        for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
-      }
-    auto r = term_eval<TT, N>(t, e, vid, X);
-    using R = decltype(r);
-    o.val = r.v;
-    if constexpr (MODE == MODE_HESS) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) o.g[i] = r.g[i];
-    }
-    o.has_h = !R::kZero || PSD;
-    double h[TriN<K>::value];
-    if constexpr (R::kZero) {
-#pragma unroll
-      for (int i = 0; i < TriN<K>::value; ++i) h[i] = 0.0;
-    } else {
-#pragma unroll
-      for (int i = 0; i < TriN<K>::value; ++i) h[i] = r.h[i];
-    }
-    if constexpr (PSD) {
-#pragma unroll
-      for (int q = 0; q < P; ++q)
-        if (!fr[q])
-#pragma unroll
-          for (int c = 0; c < N; ++c)
-#pragma unroll
-            for (int j = 0; j < K; ++j) h[tri(q * N + c, j)] = 0.0;
-      extract_psd<P, N>(h, floor);
-    } else {
-#pragma unroll
-      for (int i = 0; i < TriN<K>::value; ++i) h[i] = 0.5 * (h[i] + h[i]);
-    }
-    if constexpr (MODE == MODE_HESS) {
-#pragma unroll
-      for (int i = 0; i < TriN<K>::value; ++i) o.h[i] = h[i];
-    } else {
-      double vl[K];
-#pragma unroll
-      for (int q = 0; q < P; ++q)
-#pragma unroll
-        for (int c = 0; c < N; ++c) vl[q * N + c] = fr[q] ? wr[q][c] : 0.0;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc += h[tri(i, j)] * vl[j];
-        o.g[i] = o.has_h ? acc : 0.0;
-      }
-    }
-  } else {  // HVP without PSD: forward-over-forward
-    Vec<Df<K, true>, N> X[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q)
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        X[q][c].v = xr[q][c];
-        X[q][c].vd = fr[q] ? wr[q][c] : 0.0;
-#pragma unroll
-        for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
-      }
-    auto r = term_eval<TT, N>(t, e, vid, X);
-    using R = decltype(r);
-    o.val = r.v;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      if constexpr (R::kZero) o.g[i] = 0.0;
-      else o.g[i] = r.gd[i];
-    }
-  }
 }
 
 // V terms: one thread per owned row, no conflicts.
@@ -408,374 +293,6 @@ __global__ void __launch_bounds__(PT) k_patch(const __grid_constant__ PatchArgs 
 }
 
 
-// ---------------------------------------------------------------------------
-// Two-point edge fast path (every term is a V term or a two-point EV term:
-// cloth, smoothing). Per patch CTA:
-//   stage 1  every patch edge once: K = n dual on d = x_i - x_j (bitwise equal
-//            to the reference's K = 2n dual, see TwoPoint in terms.cuh); the
-//            result (value, g, A or its PSD clamp, floor shift) goes to a
-//            shared-memory scratch slot;
-//   stage 2  one thread per owned row: V terms + its incident edges in column
-//            order (fixed summation order -> bitwise reproducible), gradient /
-//            HVP row written, diagonal block kept in shared memory;
-//   stage 3  one warp per owned row writes the row's blocks with coalesced
-//            stores: off-diagonal block (i,j) = -M_e + delta_e I of the unique
-//            edge (i,j), diagonal = the stage-2 sum.
-// No color phases: three barriers per patch.
-struct EvArgs {
-  int R;
-  int nterms;
-  int64_t V;
-  const int32_t* vtx_off;
-  const int32_t* vtx;
-  const int32_t* ev_off;
-  const int32_t* ev_elem;
-  const uint16_t* ev_local;
-  const int32_t* rinc_off;
-  const uint32_t* rinc;
-  const int32_t* hloc;
-  const uint8_t* diag_pos;
-  const int64_t* row_offsets;
-  const uint8_t* fixed;
-  const double* x;
-  const double* w;
-  double* grad;
-  double* hess;
-  double* y;
-  double* partials;
-  double floor;
-  TermDev terms[MAXT];
-};
-
-template <int N, int MODE, bool PSD>
-struct EvLayout {
-  static constexpr int T = TriN<N>::value;
-  // scratch doubles per edge
-  static constexpr int SW = MODE == MODE_GRAD ? 1 + N : MODE == MODE_HESS ? 1 + N + T + 1 : (PSD ? 2 * N : N);
-};
-
-template <int N, int MODE, bool PSD>
-__device__ __forceinline__ void ev_stage1_edge(const EvArgs& a, int64_t e, const double* xa, const double* xb,
-                                               const double* wa, const double* wb, bool fa, bool fb, double* out) {
-  using L = EvLayout<N, MODE, PSD>;
-  constexpr int T = L::T;
-  double acc[L::SW];
-#pragma unroll
-  for (int i = 0; i < L::SW; ++i) acc[i] = 0.0;
-  for (int ti = 0; ti < a.nterms; ++ti) {
-    const TermDev& t = a.terms[ti];
-    if (t.op != MG_OP_EV) continue;
-    const int tt = t.type;
-    if constexpr (MODE == MODE_GRAD) {
-      Vec<Dg<N>, N> d;
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        d[c].v = xa[c] - xb[c];
-#pragma unroll
-        for (int i = 0; i < N; ++i) d[c].g[i] = (i == c) ? 1.0 : 0.0;
-      }
-      auto r = tt == MG_TERM_SPRING ? term_eval_diff<MG_TERM_SPRING, N>(t, e, d) : term_eval_diff<MG_TERM_EDGE_LENGTH, N>(t, e, d);
-      acc[0] += r.v;
-#pragma unroll
-      for (int i = 0; i < N; ++i) acc[1 + i] += r.g[i];
-    } else if constexpr (MODE == MODE_HESS || (MODE == MODE_HVP && PSD)) {
-      Vec<Dh<N, true>, N> d;
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        d[c].v = xa[c] - xb[c];
-#pragma unroll
-        for (int i = 0; i < N; ++i) d[c].g[i] = (i == c) ? 1.0 : 0.0;
-      }
-      auto r = tt == MG_TERM_SPRING ? term_eval_diff<MG_TERM_SPRING, N>(t, e, d) : term_eval_diff<MG_TERM_EDGE_LENGTH, N>(t, e, d);
-      double h[T];
-#pragma unroll
-      for (int i = 0; i < T; ++i) h[i] = 0.5 * (r.h[i] + r.h[i]);
-      double dl = 0.0;
-      if constexpr (PSD) {
-        if (all_finite<N>(h)) {
-          if (fa && fb) {
-#pragma unroll
-            for (int i = 0; i < T; ++i) h[i] = 2.0 * h[i];
-            project_if_needed<N>(h, a.floor);
-#pragma unroll
-            for (int i = 0; i < T; ++i) h[i] = 0.5 * h[i];
-            dl = 0.5 * a.floor;
-          } else if (fa || fb) {
-            project_if_needed<N>(h, a.floor);
-          }
-        }
-      }
-      if constexpr (MODE == MODE_HESS) {
-        acc[0] += r.v;
-#pragma unroll
-        for (int i = 0; i < N; ++i) acc[1 + i] += r.g[i];
-#pragma unroll
-        for (int i = 0; i < T; ++i) acc[1 + N + i] += h[i];
-        acc[1 + N + T] += dl;
-      } else {
-        // y_a = M (wa - wb) + dl (wa + wb), y_b = -M (wa - wb) + dl (wa + wb);
-        // one free endpoint: y_free = P(A) w_free
-        double wd[N], ws[N];
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-          const double ua = fa ? wa[c] : 0.0, ub = fb ? wb[c] : 0.0;
-          wd[c] = ua - ub;
-          ws[c] = ua + ub;
-        }
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          double m = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) m += h[tri(i, j)] * wd[j];
-          acc[i] += m + dl * ws[i];
-          acc[N + i] += -m + dl * ws[i];
-        }
-      }
-    } else {  // HVP, forward-over-forward on d with direction (wa - wb) (free-masked)
-      Vec<Df<N, true>, N> d;
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        d[c].v = xa[c] - xb[c];
-        d[c].vd = (fa ? wa[c] : 0.0) - (fb ? wb[c] : 0.0);
-#pragma unroll
-        for (int i = 0; i < N; ++i) d[c].g[i] = (i == c) ? 1.0 : 0.0;
-      }
-      auto r = tt == MG_TERM_SPRING ? term_eval_diff<MG_TERM_SPRING, N>(t, e, d) : term_eval_diff<MG_TERM_EDGE_LENGTH, N>(t, e, d);
-#pragma unroll
-      for (int i = 0; i < N; ++i) acc[i] += r.gd[i];
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < L::SW; ++i) out[i] = acc[i];
-}
-
-template <int N, int MODE, bool PSD>
-__global__ void __launch_bounds__(PT) k_patch_ev(const __grid_constant__ EvArgs a, int nvp_max, int ne_max,
-                                                  int blocks_max) {
-  using L = EvLayout<N, MODE, PSD>;
-  constexpr int T = L::T, SW = L::SW, NN = N * N;
-  extern __shared__ __align__(16) double smem[];
-  const int p = blockIdx.x;
-  const int R = a.R;
-  const int64_t own0 = (int64_t)p * R;
-  const int oc = (int)min((int64_t)R, a.V - own0);
-  const int v0 = a.vtx_off[p];
-  const int nvp = a.vtx_off[p + 1] - v0;
-  const int j0 = a.ev_off[p];
-  const int ne = a.ev_off[p + 1] - j0;
-
-  double* xs = smem;
-  double* ws = xs + (size_t)nvp_max * N;
-  double* scr = ws + (MODE == MODE_HVP ? (size_t)nvp_max * N : 0);
-  double* rdiag = scr + (size_t)ne_max * SW;
-  int64_t* sro = reinterpret_cast<int64_t*>(rdiag + (MODE == MODE_HESS ? (size_t)R * T : 0));
-  int* vid = reinterpret_cast<int*>(sro + (MODE == MODE_HESS ? R : 0));
-  int* shl = vid + nvp_max;
-  int* slen = shl + R;
-  int16_t* map = reinterpret_cast<int16_t*>(slen + R);
-  uint8_t* fx = reinterpret_cast<uint8_t*>(map + (MODE == MODE_HESS ? blocks_max : 0));
-
-  // stage 0: patch vertices
-  for (int i = threadIdx.x; i < nvp; i += PT) {
-    const int g = a.vtx[v0 + i];
-    vid[i] = g;
-    fx[i] = a.fixed ? a.fixed[g] : 0;
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      xs[i * N + c] = a.x[(int64_t)g * N + c];
-      if constexpr (MODE == MODE_HVP) ws[i * N + c] = a.w[(int64_t)g * N + c];
-    }
-  }
-  if constexpr (MODE == MODE_HESS) {
-    for (int r = threadIdx.x; r < oc; r += PT) {
-      const int g = a.vtx[v0 + r];
-      const int64_t ro = a.row_offsets[g];
-      sro[r] = ro;
-      slen[r] = (int)(a.row_offsets[g + 1] - ro);
-      shl[r] = a.hloc[own0 + r];
-    }
-  }
-  __syncthreads();
-
-  // stage 1: every patch edge once (records of the next edge prefetched)
-  {
-    int jj = threadIdx.x;
-    int64_t e = 0;
-    uint32_t lab = 0;
-    if (jj < ne) {
-      e = a.ev_elem[j0 + jj];
-      lab = reinterpret_cast<const uint32_t*>(a.ev_local)[j0 + jj];
-    }
-    for (; jj < ne; jj += PT) {
-      const int64_t ce = e;
-      const uint32_t clab = lab;
-      if (jj + PT < ne) {
-        e = a.ev_elem[j0 + jj + PT];
-        lab = reinterpret_cast<const uint32_t*>(a.ev_local)[j0 + jj + PT];
-      }
-      const int la = clab & 0xffff, lb = clab >> 16;
-      ev_stage1_edge<N, MODE, PSD>(a, ce, xs + la * N, xs + lb * N, ws + la * N, ws + lb * N, !fx[la], !fx[lb],
-                                   scr + (size_t)jj * SW);
-    }
-  }
-  __syncthreads();
-
-  // stage 2: one thread per owned row
-  double eacc = 0.0;
-  for (int r = threadIdx.x; r < oc; r += PT) {
-    const int g = vid[r];
-    const bool fr = !fx[r];
-    double vec[N];
-    double dg[T];
-#pragma unroll
-    for (int i = 0; i < N; ++i) vec[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < T; ++i) dg[i] = 0.0;
-    // V terms
-    for (int ti = 0; ti < a.nterms; ++ti) {
-      const TermDev& t = a.terms[ti];
-      if (t.op != MG_OP_V) continue;
-      const double* xr[1] = {xs + r * N};
-      const double* wr[1] = {ws + r * N};
-      const int vv = g;
-      if (t.type == MG_TERM_INERTIA) {
-        ElemOut<MG_TERM_INERTIA, N, MODE, PSD> o;
-        eval_element<MG_TERM_INERTIA, N, MODE, PSD>(t, g, &vv, xr, wr, &fr, a.floor, o);
-        eacc += o.val;
-#pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += o.g[i];
-        if constexpr (MODE == MODE_HESS) {
-          if (o.has_h)
-#pragma unroll
-            for (int i = 0; i < T; ++i) dg[i] += o.h[i];
-        }
-      } else if (t.type == MG_TERM_GRAVITY) {
-        ElemOut<MG_TERM_GRAVITY, N, MODE, PSD> o;
-        eval_element<MG_TERM_GRAVITY, N, MODE, PSD>(t, g, &vv, xr, wr, &fr, a.floor, o);
-        eacc += o.val;
-#pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += o.g[i];
-        if constexpr (MODE == MODE_HESS) {
-          if (o.has_h)
-#pragma unroll
-            for (int i = 0; i < T; ++i) dg[i] += o.h[i];
-        }
-      }
-    }
-    // incident edges, column order
-    const int k0 = a.rinc_off[own0 + r], k1 = a.rinc_off[own0 + r + 1];
-    for (int k = k0; k < k1; ++k) {
-      const uint32_t rec = a.rinc[k];
-      const int jj = rec & 0xffff;
-      const int q = (rec >> 16) & 1;
-      const double* sc = scr + (size_t)jj * SW;
-      if constexpr (MODE == MODE_GRAD || MODE == MODE_HESS) {
-        if (q == 0) eacc += sc[0];
-        const double sg = q == 0 ? 1.0 : -1.0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += sg * sc[1 + i];
-      }
-      if constexpr (MODE == MODE_HESS) {
-        const double dl = sc[1 + N + T];
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int c = 0; c <= i; ++c) dg[tri(i, c)] += sc[1 + N + tri(i, c)] + (i == c ? dl : 0.0);
-        const int pos = rec >> 24;
-        if (pos != 255) map[shl[r] + pos] = (int16_t)jj;
-      }
-      if constexpr (MODE == MODE_HVP) {
-        if constexpr (PSD) {
-#pragma unroll
-          for (int i = 0; i < N; ++i) vec[i] += sc[q * N + i];
-        } else {
-          const double sg = q == 0 ? 1.0 : -1.0;
-#pragma unroll
-          for (int i = 0; i < N; ++i) vec[i] += sg * sc[i];
-        }
-      }
-    }
-    double* vout = MODE == MODE_HVP ? a.y : a.grad;
-#pragma unroll
-    for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
-    if constexpr (MODE == MODE_HESS) {
-#pragma unroll
-      for (int i = 0; i < T; ++i) rdiag[r * T + i] = dg[i];
-      const int dp = a.diag_pos[g];
-      if (fr && dp != 255) map[shl[r] + dp] = -1;
-    }
-  }
-  if constexpr (MODE == MODE_HESS) {
-    __syncthreads();
-    // stage 3: one warp per owned row, coalesced block writes. Each lane owns
-    // a fixed (block-in-group, entry) slot: BPW = 32 / NN blocks per pass.
-    constexpr int BPW = 32 / NN;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int lb = lane / NN, lrc = lane - lb * NN, li = lrc / N, lc = lrc - li * N;
-    const int ltri = li >= lc ? li * (li + 1) / 2 + lc : lc * (lc + 1) / 2 + li;
-    const bool ldiag = li == lc;
-    if (lb < BPW) {
-      for (int r = wid; r < oc; r += PT / 32) {
-        const int len = slen[r];
-        double* dst = a.hess + sro[r] * NN;
-        const int hb = shl[r];
-        const double* rd = rdiag + r * T;
-        for (int b = lb; b < len; b += BPW) {
-          const int jj = map[hb + b];
-          double v;
-          if (jj < 0) {
-            v = rd[ltri];
-          } else {
-            const double* sc = scr + (size_t)jj * SW;
-            v = -sc[1 + N + ltri] + (ldiag ? sc[1 + N + T] : 0.0);
-          }
-          dst[b * NN + lrc] = v;
-        }
-      }
-    }
-  }
-  if constexpr (MODE != MODE_HVP) {
-    const double tot = block_sum(eacc);
-    if (threadIdx.x == 0) a.partials[p] = tot;
-  }
-}
-
-size_t ev_smem_bytes(int N, int mode, bool psd, int R, int nvp_max, int ne_max, int blocks_max) {
-  const int T = N * (N + 1) / 2;
-  const int SW = mode == MODE_GRAD ? 1 + N : mode == MODE_HESS ? 1 + N + T + 1 : (psd ? 2 * N : N);
-  size_t b = 8 * ((size_t)nvp_max * N + (mode == MODE_HVP ? (size_t)nvp_max * N : 0) + (size_t)ne_max * SW +
-                  (mode == MODE_HESS ? (size_t)R * T + R : 0));
-  b += 4 * ((size_t)nvp_max + 2 * R) + (mode == MODE_HESS ? 2 * (size_t)blocks_max : 0) + nvp_max + 16;
-  return b;
-}
-
-template <int N, int MODE, bool PSD>
-void launch_ev(const EvArgs& a, int64_t np, int nvp_max, int ne_max, int blocks_max, cudaStream_t st) {
-  auto kern = k_patch_ev<N, MODE, PSD>;
-  const size_t sm = ev_smem_bytes(N, MODE, PSD, a.R, nvp_max, ne_max, blocks_max);
-  if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "patch does not fit in shared memory");
-  MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  kern<<<(unsigned)np, PT, sm, st>>>(a, nvp_max, ne_max, blocks_max);
-  MG_LAUNCH_CHECK();
-}
-
-template <int N>
-void launch_ev_mode(const EvArgs& a, int64_t np, int nvp, int ne, int nb, Mode mode, bool psd, cudaStream_t st) {
-  switch (mode) {
-    case MODE_GRAD: launch_ev<N, MODE_GRAD, false>(a, np, nvp, ne, nb, st); break;
-    case MODE_HESS:
-      if (psd) launch_ev<N, MODE_HESS, true>(a, np, nvp, ne, nb, st);
-      else launch_ev<N, MODE_HESS, false>(a, np, nvp, ne, nb, st);
-      break;
-    case MODE_HVP:
-      if (psd) launch_ev<N, MODE_HVP, true>(a, np, nvp, ne, nb, st);
-      else launch_ev<N, MODE_HVP, false>(a, np, nvp, ne, nb, st);
-      break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "edge fast path assembles grad / Hessian / HVP only");
-  }
-}
-
-
 size_t smem_bytes(int N, int mode, int R, int nvp_max, int blocks_max) {
   size_t d = (size_t)nvp_max * N + (mode == MODE_HVP ? (size_t)nvp_max * N : 0) + (size_t)R * N +
              (mode == MODE_HESS ? (size_t)blocks_max * N * N : 0);
@@ -820,35 +337,7 @@ bool patch_supported(const Problem& p) {
 
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset) {
   const Mesh& m = *p.mesh;
-  if (p.ev_fast) {
-    EvArgs a;
-    a.R = m.patches.R;
-    a.nterms = (int)p.terms.size();
-    a.V = m.Vr;
-    a.vtx_off = p.vtx_off.p;
-    a.vtx = p.vtx.p;
-    a.ev_off = p.lay[0].off.p;
-    a.ev_elem = p.lay[0].elem.p;
-    a.ev_local = p.lay[0].local.p;
-    a.rinc_off = p.rinc_off.p;
-    a.rinc = p.rinc.p;
-    a.hloc = p.hloc.p;
-    a.diag_pos = p.diag_pos.p;
-    a.row_offsets = p.row_offsets.p;
-    a.fixed = p.any_fixed ? p.fixed.p : nullptr;
-    a.x = c.x;
-    a.w = c.w;
-    a.grad = c.grad;
-    a.hess = c.hess;
-    a.y = c.y;
-    a.partials = c.partials + partial_offset;
-    a.floor = c.floor;
-    for (int i = 0; i < a.nterms; ++i) a.terms[i] = p.terms[i].dev;
-    const int64_t np = m.patches.num;
-    if (p.n == 3) launch_ev_mode<3>(a, np, p.max_patch_vertices, p.max_patch_elems, p.max_patch_blocks, mode, c.psd, c.stream);
-    else launch_ev_mode<2>(a, np, p.max_patch_vertices, p.max_patch_elems, p.max_patch_blocks, mode, c.psd, c.stream);
-    return mode == MODE_HVP ? 0 : np;
-  }
+  if (p.ev_fast) return launch_patch_ev(p, mode, c, partial_offset);
   PatchArgs a;
   a.R = m.patches.R;
   a.nterms = (int)p.terms.size();

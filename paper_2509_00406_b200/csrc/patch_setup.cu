@@ -320,26 +320,62 @@ __global__ void k_diag_pos(const int64_t* ro, const int32_t* col, int64_t V, uin
   dp[v] = (a < hi && col[a] == v && a - lo < 255) ? (uint8_t)(a - lo) : 255;
 }
 
-// row-incidence records of the two-point edge fast path
-__global__ void k_rinc_keys(const int32_t* sel, const int32_t* elem, const uint16_t* local, const uint8_t* pos,
-                            const int32_t* pe, const int32_t* off, int64_t n, int R, int64_t V,
-                            uint64_t* keys, uint32_t* vals) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const int64_t p = pe[j];
-  const int oc = owned_count(p, R, V);
-  const int64_t e = elem[j];
-  for (int q = 0; q < 2; ++q) {
-    const int lq = local[j * 2 + q];
-    if (lq < oc) {
-      const int64_t row = p * R + lq;
-      const uint32_t other = (uint32_t)sel[e * 2 + (1 - q)];
-      keys[j * 2 + q] = ((uint64_t)row << 32) | other;
-      vals[j * 2 + q] = (uint32_t)(j - off[p]) | ((uint32_t)q << 16) | ((uint32_t)pos[(j * 2 + q) * 2 + (1 - q)] << 24);
-    } else {
-      keys[j * 2 + q] = ~0ull;
-      vals[j * 2 + q] = 0;
-    }
+// Shared-memory offset (in doubles) of every owned row's Hessian blocks in the
+// edge fast path's row buffer: rows stacked in patch order, with one pad
+// double where needed so each row has the same 16-byte phase in shared memory
+// as in the output (the row is then streamed out with one bulk copy).
+__global__ void k_row_smem_offsets(const int32_t* order, const int64_t* ro, int64_t Vr, int R, int64_t np, int NN,
+                                   int32_t* hoff, int* maxd) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const int64_t a = p * R, b = (p + 1) * R < Vr ? (p + 1) * R : Vr;
+  int64_t off = 0;
+  for (int64_t i = a; i < b; ++i) {
+    const int v = order[i];
+    const int64_t r0 = ro[v];
+    if ((off - r0 * NN) & 1) ++off;
+    hoff[i] = (int32_t)off;
+    off += (ro[v + 1] - r0) * NN;
+  }
+  atomicMax(maxd, (int)off);
+}
+
+__global__ void k_vertex_flags(const uint8_t* fixed, const int32_t* vtx, int64_t n, uint8_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fixed ? fixed[vtx[i]] : 0;
+}
+
+__global__ void k_patch_rows(const int32_t* order, const int64_t* ro, const uint8_t* dp, int64_t Vr,
+                             int64_t* pro, int32_t* plen, uint8_t* pdp) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Vr) return;
+  const int v = order[i];
+  pro[i] = ro[v];
+  plen[i] = (int32_t)(ro[v + 1] - ro[v]);
+  pdp[i] = dp[v];
+}
+
+
+// Row-incidence records of the edge row kernel: for every edge and each
+// endpoint that is an owned row, key = (row in patch order, other endpoint),
+// value = (edge | slot << 31, other | pinned(other) << 31). Sorted by key, a
+// row's records are its incident edges in column order.
+__global__ void k_row_inc(const int32_t* edges, int64_t E, const int32_t* rank, int64_t Vr, const uint8_t* fixed,
+                          uint64_t* keys, uint64_t* vals) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 2 * E) return;
+  const int64_t e = i >> 1;
+  const int q = (int)(i & 1);
+  const int v = edges[2 * e + q], o = edges[2 * e + 1 - q];
+  const int64_t row = rank[v];
+  if (row < Vr) {
+    keys[i] = ((uint64_t)row << 32) | (uint32_t)o;
+    const uint32_t hi = (uint32_t)o | ((fixed && fixed[o]) ? 0x80000000u : 0u);
+    const uint32_t lo = (uint32_t)e | ((uint32_t)q << 31);
+    vals[i] = ((uint64_t)hi << 32) | lo;
+  } else {
+    keys[i] = ~0ull;
+    vals[i] = 0;
   }
 }
 
@@ -421,6 +457,65 @@ void mesh_patches(Mesh& m, cudaStream_t s) {
   MG_CUDA(cudaStreamSynchronize(s));
 }
 
+// Layout of the edge row kernel (edge_kernels.cu): rows in patch (Morton)
+// order, per-row incidence records, static per-row streams and the shared-
+// memory row offsets of each ROW_BLOCK-row CTA.
+void build_rows_ev(Problem& p, cudaStream_t s) {
+  Mesh& m = *p.mesh;
+  PatchSet& ps = m.patches;
+  const int64_t V = m.V, Vr = m.Vr, E = m.E;
+  const int RB = EV_ROW_BLOCK;
+  const int64_t nb = (Vr + RB - 1) / RB;
+  DBuf<int> mx;
+  mx.alloc(1);
+  {
+    DBuf<uint64_t> k1, k2, v1, v2;
+    const int64_t n = 2 * E > 0 ? 2 * E : 1;
+    k1.alloc(n); k2.alloc(n); v1.alloc(n); v2.alloc(n);
+    if (E) k_row_inc<<<grid_for(2 * E), TPB, 0, s>>>(m.edges.p, E, ps.rank.p, Vr, p.any_fixed ? p.fixed.p : nullptr,
+                                                     k1.p, v1.p);
+    MG_LAUNCH_CHECK();
+    if (E) {
+      size_t tb = 0;
+      MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, 2 * E, 0, 64, s));
+      Tmp t(s, tb);
+      MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k1.p, k2.p, v1.p, v2.p, 2 * E, 0, 64, s));
+    }
+    p.rinc_off.alloc(Vr + 1);
+    k_lower_bounds_rows<<<grid_for(Vr + 1), TPB, 0, s>>>(k2.p, 2 * E, Vr, p.rinc_off.p);
+    MG_LAUNCH_CHECK();
+    MG_CUDA(cudaStreamSynchronize(s));
+    p.rrec = std::move(v2);
+  }
+  p.pfix.alloc(Vr > 0 ? Vr : 1);
+  if (Vr) k_vertex_flags<<<grid_for(Vr), TPB, 0, s>>>(p.any_fixed ? p.fixed.p : nullptr, ps.order.p, Vr, p.pfix.p);
+  MG_LAUNCH_CHECK();
+  p.max_patch_hdoubles = 0;
+  if (p.with_hessian && p.pattern_ready) {
+    p.diag_pos.alloc(V > 0 ? V : 1);
+    if (V) k_diag_pos<<<grid_for(V), TPB, 0, s>>>(p.row_offsets.p, p.col32.p, V, p.diag_pos.p);
+    p.prow_ro.alloc(Vr > 0 ? Vr : 1);
+    p.prow_len.alloc(Vr > 0 ? Vr : 1);
+    p.prow_dp.alloc(Vr > 0 ? Vr : 1);
+    if (Vr) k_patch_rows<<<grid_for(Vr), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, p.diag_pos.p, Vr, p.prow_ro.p,
+                                                     p.prow_len.p, p.prow_dp.p);
+    MG_LAUNCH_CHECK();
+    p.hoff.alloc(Vr > 0 ? Vr : 1);
+    MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+    if (nb) k_row_smem_offsets<<<grid_for(nb), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, Vr, RB, nb, p.n * p.n,
+                                                           p.hoff.p, mx.p);
+    MG_LAUNCH_CHECK();
+    p.max_patch_hdoubles = to_host_int(mx.p, s);
+  }
+  MG_CUDA(cudaStreamSynchronize(s));
+  p.redo.alloc(1);
+  MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  p.recomputed_elements = 0;
+  p.ev_fast = true;
+  p.layout_ready = true;
+}
+
 void build_patch_layout(Problem& p, cudaStream_t s) {
   Mesh& m = *p.mesh;
   PatchSet& ps = m.patches;
@@ -428,6 +523,18 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
   const int R = ps.R;
   p.layout_ready = false;
   if (V == 0 || np == 0) return;
+  p.ev_fast = false;
+  {
+    bool fast = false;
+    for (auto& t : p.terms) fast |= t.dev.op == MG_OP_EV;
+    for (auto& t : p.terms)
+      fast &= t.dev.op == MG_OP_V || t.dev.type == MG_TERM_SPRING || t.dev.type == MG_TERM_EDGE_LENGTH;
+    fast &= m.E < (int64_t(1) << 31);
+    if (fast) {
+      build_rows_ev(p, s);
+      return;
+    }
+  }
   DBuf<int> flag;
   flag.alloc(1);
   MG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
@@ -590,49 +697,6 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
     p.recomputed_elements += n - op_count(m, L.op);
   }
   cudaFreeAsync(rib_keys_all, s);
-
-  // two-point edge fast path: row incidence lists
-  p.ev_fast = false;
-  {
-    bool fast = p.lay[0].op == MG_OP_EV && p.lay[1].op < 0;
-    for (auto& t : p.terms)
-      fast &= t.dev.op == MG_OP_V || t.dev.type == MG_TERM_SPRING || t.dev.type == MG_TERM_EDGE_LENGTH;
-    OpLayout& L = p.lay[0];
-    if (fast) {
-      const int64_t n = L.count;
-      DBuf<int> mx;
-      mx.alloc(1);
-      MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
-      k_max_diff<<<grid_for(np), TPB, 0, s>>>(L.off.p, np, mx.p);
-      MG_LAUNCH_CHECK();
-      p.max_patch_elems = to_host_int(mx.p, s);
-      fast = p.max_patch_elems < 65536;
-      if (fast) {
-        DBuf<int32_t> pe_sorted;
-        pe_sorted.alloc(n > 0 ? n : 1);
-        k_patch_of_entry<<<grid_for(np), TPB, 0, s>>>(L.off.p, np, pe_sorted.p);
-        DBuf<uint64_t> k1, k2;
-        DBuf<uint32_t> v1, v2;
-        const int64_t m2 = 2 * n > 0 ? 2 * n : 1;
-        k1.alloc(m2); k2.alloc(m2); v1.alloc(m2); v2.alloc(m2);
-        if (n) k_rinc_keys<<<grid_for(n), TPB, 0, s>>>(op_sel(m, MG_OP_EV), L.elem.p, L.local.p, L.pos.p,
-                                                       pe_sorted.p, L.off.p, n, R, Vr, k1.p, v1.p);
-        MG_LAUNCH_CHECK();
-        size_t tb = 0;
-        MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, 2 * n, 0, 64, s));
-        {
-          Tmp t(s, tb);
-          MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k1.p, k2.p, v1.p, v2.p, 2 * n, 0, 64, s));
-        }
-        p.rinc_off.alloc(Vr + 1);
-        k_lower_bounds_rows<<<grid_for(Vr + 1), TPB, 0, s>>>(k2.p, 2 * n, Vr, p.rinc_off.p);
-        MG_LAUNCH_CHECK();
-        p.rinc = std::move(v2);
-        MG_CUDA(cudaStreamSynchronize(s));
-        p.ev_fast = true;
-      }
-    }
-  }
 
   // shared-memory row offsets of owned rows (patch order) and diagonal positions
   p.hloc.alloc(Vr > 0 ? Vr : 1);

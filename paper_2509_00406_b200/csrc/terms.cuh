@@ -37,6 +37,27 @@ template <int TT> struct TwoPoint { static constexpr bool value = false; };
 template <> struct TwoPoint<MG_TERM_SPRING> { static constexpr bool value = true; };
 template <> struct TwoPoint<MG_TERM_EDGE_LENGTH> { static constexpr bool value = true; };
 
+// Radial two-point terms: E = phi(r) with r = |x_i - x_j|^2. The n x n block
+// is then A = 2 phi'(r) I + 4 phi''(r) d d^T, so value, gradient and Hessian
+// follow from a one-variable second-order dual on r, and the block's spectrum
+// is known in closed form: 2 phi' (n-1 times, transverse) and
+// 2 phi' + 4 phi'' r (along d). Results agree with the full dual to rounding.
+template <int TT> struct Radial { static constexpr bool value = false; };
+template <> struct Radial<MG_TERM_SPRING> { static constexpr bool value = true; };
+template <> struct Radial<MG_TERM_EDGE_LENGTH> { static constexpr bool value = true; };
+
+template <int TT, class S>
+MG_DI auto term_eval_radial(const TermDev& t, int64_t e, const S& r) {
+  if constexpr (TT == MG_TERM_SPRING) {
+    const double l2 = t.a[0][e];
+    auto s = r / l2 - 1.0;
+    return (s * s) * (t.c[0] * l2);
+  } else {
+    static_assert(TT == MG_TERM_EDGE_LENGTH, "not a radial term");
+    return r;
+  }
+}
+
 template <int TT, int N, class S>
 MG_DI auto term_eval_diff(const TermDev& t, int64_t e, const Vec<S, N>& d) {
   if constexpr (TT == MG_TERM_SPRING) {
