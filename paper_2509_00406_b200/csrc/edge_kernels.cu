@@ -47,6 +47,9 @@ struct EvArgs {
   double* y;
   double* partials;
   int* redo;  // raised by the radial kernel on a non-finite lane
+  int nev, nvt;                 // compacted term lists (indices into terms)
+  int ev_idx[MAXT], vt_idx[MAXT];
+  const double* ev_a0;          // per-edge attribute of ev_idx[0] (prefetched), or null
   double floor;
   TermDev terms[MAXT];
 };
@@ -317,6 +320,238 @@ MG_DI void edge_dual_fof(const EvArgs& a, int64_t e, const double* xa, const dou
   }
 }
 
+// phi, phi', phi'' of EV term j at r (attribute value a0 preloaded)
+template <int MODE>
+MG_DI bool radial_term(const TermDev& t, double a0, double rr, double& pv, double& p1, double& p2) {
+  if constexpr (MODE == MODE_GRAD) {
+    Dg<1> r;
+    r.v = rr;
+    r.g[0] = 1.0;
+    if (t.type == MG_TERM_SPRING) {
+      auto q = radial_phi<MG_TERM_SPRING>(t, a0, r);
+      pv = q.v; p1 = q.g[0];
+    } else {
+      auto q = radial_phi<MG_TERM_EDGE_LENGTH>(t, a0, r);
+      pv = q.v; p1 = q.g[0];
+    }
+    p2 = 0.0;
+    return isfinite(pv) && isfinite(p1);
+  } else {
+    Dh<1, true> r;
+    r.v = rr;
+    r.g[0] = 1.0;
+    if (t.type == MG_TERM_SPRING) {
+      auto q = radial_phi<MG_TERM_SPRING>(t, a0, r);
+      pv = q.v; p1 = q.g[0]; p2 = hess00(q);
+    } else {
+      auto q = radial_phi<MG_TERM_EDGE_LENGTH>(t, a0, r);
+      pv = q.v; p1 = q.g[0]; p2 = hess00(q);
+    }
+    return isfinite(pv) && isfinite(p1) && isfinite(p2);
+  }
+}
+
+// Radial fast kernel: one thread per owned row, d = x_row - x_other (radial
+// terms are even in d, so no orientation bookkeeping), records and neighbour
+// data software-pipelined one incidence ahead.
+template <int N, int MODE, bool PSD>
+__global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs a) {
+  constexpr int T = TriN<N>::value, NN = N * N;
+  extern __shared__ __align__(16) double hbuf[];
+  const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
+  double eacc = 0.0;
+  bool finite = true;
+  if (row < a.V) {
+    // level 1: static per-row streams
+    const int g = a.order[row];
+    const bool fr = !a.pfix[row];
+    const int k0 = a.rinc_off[row], k1 = a.rinc_off[row + 1];
+    int64_t ro = 0;
+    int len = 0, dp = 255, ho = 0;
+    if constexpr (MODE == MODE_HESS) {
+      ro = a.prow_ro[row];
+      len = a.prow_len[row];
+      dp = a.prow_dp[row];
+      ho = a.hoff[row];
+    }
+    // level 2: own data and the first records
+    uint64_t rc_n = k0 < k1 ? a.rrec[k0] : 0;
+    uint64_t rc_nn = k0 + 1 < k1 ? a.rrec[k0 + 1] : 0;
+    double xs[N], us[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      xs[c] = a.x[(int64_t)g * N + c];
+      if constexpr (MODE == MODE_HVP) us[c] = fr ? a.w[(int64_t)g * N + c] : 0.0;
+      else us[c] = 0.0;
+    }
+    double vec[N], dg[T];
+#pragma unroll
+    for (int i = 0; i < N; ++i) vec[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < T; ++i) dg[i] = 0.0;
+    {  // V terms
+      double wv[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) wv[c] = us[c];
+      const double* xr[1] = {xs};
+      const double* wr[1] = {wv};
+      for (int j = 0; j < a.nvt; ++j) {
+        const TermDev& t = a.terms[a.vt_idx[j]];
+        if (t.type == MG_TERM_INERTIA) {
+          ElemOut<MG_TERM_INERTIA, N, MODE, PSD> o;
+          eval_element<MG_TERM_INERTIA, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
+          eacc += o.val;
+#pragma unroll
+          for (int k = 0; k < N; ++k) vec[k] += o.g[k];
+          if constexpr (MODE == MODE_HESS) {
+            if (o.has_h)
+#pragma unroll
+              for (int k = 0; k < T; ++k) dg[k] += o.h[k];
+          }
+        } else {
+          ElemOut<MG_TERM_GRAVITY, N, MODE, PSD> o;
+          eval_element<MG_TERM_GRAVITY, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
+          eacc += o.val;
+#pragma unroll
+          for (int k = 0; k < N; ++k) vec[k] += o.g[k];
+          if constexpr (MODE == MODE_HESS) {
+            if (o.has_h)
+#pragma unroll
+              for (int k = 0; k < T; ++k) dg[k] += o.h[k];
+          }
+        }
+      }
+    }
+    // pipeline prologue: neighbour data of the first incidence
+    double xo_n[N], uo_n[N], a0_n = 0.0;
+    {
+      const uint32_t hi = (uint32_t)(rc_n >> 32);
+      const int o = (int)(hi & 0x7fffffffu);
+      const bool fo = !(hi >> 31);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        xo_n[c] = k0 < k1 ? a.x[(int64_t)o * N + c] : 0.0;
+        if constexpr (MODE == MODE_HVP) uo_n[c] = (k0 < k1 && fo) ? a.w[(int64_t)o * N + c] : 0.0;
+        else uo_n[c] = 0.0;
+      }
+      if (a.ev_a0 && k0 < k1) a0_n = a.ev_a0[(uint32_t)rc_n & 0x7fffffffu];
+    }
+    double* hrow = hbuf + ho;
+    int pos = 0;
+    for (int k = k0; k < k1; ++k) {
+      const uint64_t rc = rc_n;
+      double xo[N], uo[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) { xo[c] = xo_n[c]; uo[c] = uo_n[c]; }
+      const double a0 = a0_n;
+      // prefetch the next incidence (records two ahead)
+      rc_n = rc_nn;
+      if (k + 2 < k1) rc_nn = a.rrec[k + 2];
+      if (k + 1 < k1) {
+        const uint32_t hi = (uint32_t)(rc_n >> 32);
+        const int o = (int)(hi & 0x7fffffffu);
+        const bool fo = !(hi >> 31);
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          xo_n[c] = a.x[(int64_t)o * N + c];
+          if constexpr (MODE == MODE_HVP) uo_n[c] = fo ? a.w[(int64_t)o * N + c] : 0.0;
+        }
+        if (a.ev_a0) a0_n = a.ev_a0[(uint32_t)rc_n & 0x7fffffffu];
+      }
+      const uint32_t lo = (uint32_t)rc, hi = (uint32_t)(rc >> 32);
+      const int64_t e = lo & 0x7fffffffu;
+      const bool first = (lo >> 31) == 0;  // the row is the edge's first vertex
+      const bool fo = !(hi >> 31);
+      double d[N], rr = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        d[c] = xs[c] - xo[c];
+        rr = d[c] * d[c] + rr;
+      }
+      double gam = 0.0, ci_s = 0.0, cd_s = 0.0, dl = 0.0, val = 0.0;
+      double dw = 0.0;
+      if constexpr (MODE == MODE_HVP) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo[c]);
+      }
+      for (int j = 0; j < a.nev; ++j) {
+        const TermDev& t = a.terms[a.ev_idx[j]];
+        const double av = j == 0 && a.ev_a0 ? a0 : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
+        double pv, p1, p2;
+        finite &= radial_term<MODE>(t, av, rr, pv, p1, p2);
+        val += pv;
+        gam += 2.0 * p1;
+        if constexpr (MODE != MODE_GRAD) {
+          double ci = 2.0 * p1, cd = 4.0 * p2, sh = 0.0;
+          if constexpr (PSD) {
+            if (fr && fo) {  // [[A,-A],[-A,A]]: clamp 2A, halve, shift floor/2
+              ci *= 2.0; cd *= 2.0;
+              radial_clamp(ci, cd, rr, a.floor);
+              ci *= 0.5; cd *= 0.5;
+              sh = 0.5 * a.floor;
+            } else if (fr || fo) {
+              radial_clamp(ci, cd, rr, a.floor);
+            }
+          }
+          ci_s += ci;
+          cd_s += cd;
+          dl += sh;
+        }
+      }
+      if constexpr (MODE != MODE_HVP) {
+        if (first) eacc += val;  // an edge's energy counts at its first vertex
+      }
+      if constexpr (MODE == MODE_GRAD || MODE == MODE_HESS) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += gam * d[i];
+      }
+      if constexpr (MODE == MODE_HVP) {  // y_row = M (u_row - u_other) + dl (u_row + u_other)
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo[i]) + cd_s * d[i] * dw + dl * (us[i] + uo[i]);
+      }
+      if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c <= i; ++c) dg[tri(i, c)] += cd_s * d[i] * d[c] + (i == c ? ci_s + dl : 0.0);
+        if (fr && fo) {
+          if (dp != 255 && pos == dp) ++pos;  // leave the diagonal's slot
+          double* dst = hrow + pos * NN;
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int c = 0; c < N; ++c) dst[i * N + c] = -(cd_s * d[i] * d[c]) + (i == c ? dl - ci_s : 0.0);
+          ++pos;
+        }
+      }
+    }
+    double* vout = MODE == MODE_HVP ? a.y : a.grad;
+#pragma unroll
+    for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+    if constexpr (MODE == MODE_HESS) {
+      if (fr && dp != 255) {
+        double* dst = hrow + dp * NN;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
+      }
+      if (len > 0) {
+        fence_proxy_async_smem();
+        row_store_bulk(a.hess + ro * NN, hrow, len * NN);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  }
+  if (!finite) *a.redo = 1;
+  if constexpr (MODE != MODE_HVP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
+    if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
+  }
+  if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // EXACT = false: radial evaluation only; a non-finite lane raises *a.redo.
 // EXACT = true : launched after it; returns at once unless *a.redo is set,
 //                then recomputes every row with the exact K = n dual path.
@@ -489,7 +724,7 @@ void launch_rows(const EvArgs& a, int hd_max, cudaStream_t st) {
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
   const int64_t nb = (a.V + PT - 1) / PT;
   if (!nb) return;
-  auto fast = k_rows_ev<N, MODE, PSD, false>;
+  auto fast = k_rows_fast<N, MODE, PSD>;
   auto exact = k_rows_ev<N, MODE, PSD, true>;
   if (sm) {
     MG_CUDA(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -547,6 +782,13 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.redo = p.redo.p;
   a.floor = c.floor;
   for (int i = 0; i < a.nterms; ++i) a.terms[i] = p.terms[i].dev;
+  a.nev = a.nvt = 0;
+  a.ev_a0 = nullptr;
+  for (int i = 0; i < a.nterms; ++i) {
+    if (p.terms[i].dev.op == MG_OP_EV) a.ev_idx[a.nev++] = i;
+    else a.vt_idx[a.nvt++] = i;
+  }
+  if (a.nev && p.terms[a.ev_idx[0]].dev.type == MG_TERM_SPRING) a.ev_a0 = p.terms[a.ev_idx[0]].dev.a[0];
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
   if (p.n == 3) launch_rows_mode<3>(a, hd, mode, c.psd, c.stream);
   else launch_rows_mode<2>(a, hd, mode, c.psd, c.stream);

@@ -46,16 +46,25 @@ template <int TT> struct Radial { static constexpr bool value = false; };
 template <> struct Radial<MG_TERM_SPRING> { static constexpr bool value = true; };
 template <> struct Radial<MG_TERM_EDGE_LENGTH> { static constexpr bool value = true; };
 
+// phi(r) of a radial term given the element's attribute value a0 (the spring's
+// squared rest length; unused by the edge length)
 template <int TT, class S>
-MG_DI auto term_eval_radial(const TermDev& t, int64_t e, const S& r) {
+MG_DI auto radial_phi(const TermDev& t, double a0, const S& r) {
   if constexpr (TT == MG_TERM_SPRING) {
-    const double l2 = t.a[0][e];
-    auto s = r / l2 - 1.0;
-    return (s * s) * (t.c[0] * l2);
+    auto s = r / a0 - 1.0;
+    return (s * s) * (t.c[0] * a0);
   } else {
     static_assert(TT == MG_TERM_EDGE_LENGTH, "not a radial term");
+    (void)t;
+    (void)a0;
     return r;
   }
+}
+template <int TT> struct RadialAttr { static constexpr bool value = TT == MG_TERM_SPRING; };
+
+template <int TT, class S>
+MG_DI auto term_eval_radial(const TermDev& t, int64_t e, const S& r) {
+  return radial_phi<TT>(t, RadialAttr<TT>::value ? t.a[0][e] : 0.0, r);
 }
 
 template <int TT, int N, class S>

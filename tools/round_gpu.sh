@@ -8,5 +8,5 @@ timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_${tag}.l
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_${tag}.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${tag}.csv python bench.py --profile > gpurun_out/launches_${tag}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^k_patch' -s 2 -c 1 -o gpurun_out/prof_${tag} python bench.py --profile > gpurun_out/ncu_${tag}.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^(k_rows_fast|k_patch)$' -s 0 -c 1 -o gpurun_out/prof_${tag} python bench.py --profile > gpurun_out/ncu_${tag}.log 2>&1
 tail -3 gpurun_out/pytest_gpu_${tag}.log; cat gpurun_out/smoke_${tag}.log | tail -2; cat gpurun_out/bench_${tag}.json
