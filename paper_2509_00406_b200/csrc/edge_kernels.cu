@@ -320,41 +320,62 @@ MG_DI void edge_dual_fof(const EvArgs& a, int64_t e, const double* xa, const dou
   }
 }
 
-// phi, phi', phi'' of EV term j at r (attribute value a0 preloaded)
-template <int MODE>
-MG_DI bool radial_term(const TermDev& t, double a0, double rr, double& pv, double& p1, double& p2) {
-  if constexpr (MODE == MODE_GRAD) {
-    Dg<1> r;
-    r.v = rr;
-    r.g[0] = 1.0;
-    if (t.type == MG_TERM_SPRING) {
-      auto q = radial_phi<MG_TERM_SPRING>(t, a0, r);
-      pv = q.v; p1 = q.g[0];
-    } else {
-      auto q = radial_phi<MG_TERM_EDGE_LENGTH>(t, a0, r);
-      pv = q.v; p1 = q.g[0];
-    }
-    p2 = 0.0;
-    return isfinite(pv) && isfinite(p1);
-  } else {
-    Dh<1, true> r;
-    r.v = rr;
-    r.g[0] = 1.0;
-    if (t.type == MG_TERM_SPRING) {
-      auto q = radial_phi<MG_TERM_SPRING>(t, a0, r);
-      pv = q.v; p1 = q.g[0]; p2 = hess00(q);
-    } else {
-      auto q = radial_phi<MG_TERM_EDGE_LENGTH>(t, a0, r);
-      pv = q.v; p1 = q.g[0]; p2 = hess00(q);
-    }
-    return isfinite(pv) && isfinite(p1) && isfinite(p2);
-  }
+// 1/x to full fp64 precision without the IEEE division sequence: hardware
+// reciprocal estimate + two Newton steps (non-finite / zero inputs give
+// non-finite results, which send the call to the exact kernel)
+MG_DI double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
+// phi, phi', phi'' of a radial term at r; the attribute value (spring: squared
+// rest length) is preloaded. Closed forms of the reference callbacks:
+//   spring  (apps/cloth.py:106-110): s = r/l2 - 1, phi = (s s)(c l2),
+//           phi' = 2 c s, phi'' = 2 c / l2;   edge length (apps/smooth.py:27-28): phi = r.
+// Returns false when a value is non-finite.
+template <int TT>
+MG_DI bool radial_closed(const TermDev& t, double a0, double rr, double& pv, double& p1, double& p2) {
+  if (TT == MG_TERM_SPRING) {
+    const double c = t.c[0];
+    const double u = rcp_fast(a0);
+    const double sv = rr * u - 1.0;
+    pv = (sv * sv) * (c * a0);
+    p1 = 2.0 * c * sv;
+    p2 = 2.0 * c * u;
+  } else {
+    pv = rr;
+    p1 = 1.0;
+    p2 = 0.0;
+  }
+  return isfinite(pv + p1 + p2);
+}
+
+MG_DI bool radial_any(const TermDev& t, double a0, double rr, double& pv, double& p1, double& p2) {
+  return t.type == MG_TERM_SPRING ? radial_closed<MG_TERM_SPRING>(t, a0, rr, pv, p1, p2)
+                                  : radial_closed<MG_TERM_EDGE_LENGTH>(t, a0, rr, pv, p1, p2);
+}
+
+// closed-form clamp with the fast reciprocal
+MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
+  const double lt = ci, ld = ci + cd * r;
+  if (lt > f && ld > f) return;
+  const double mt = lt > f ? lt : f, md = ld > f ? ld : f;
+  ci = mt;
+  cd = r > 0.0 ? (md - mt) * rcp_fast(r) : 0.0;
+}
+
+constexpr int MAXI = 6;  // incidences per row held in registers (the rest are streamed)
+
 // Radial fast kernel: one thread per owned row, d = x_row - x_other (radial
-// terms are even in d, so no orientation bookkeeping), records and neighbour
-// data software-pipelined one incidence ahead.
-template <int N, int MODE, bool PSD>
+// terms are even in d, so no orientation bookkeeping). A row's first MAXI
+// incidences are fetched in two batched levels (records, then neighbour x and
+// edge attributes) so their latencies overlap; EVT fixes the single EV term's
+// type at compile time (0: any mix, dispatched per incidence).
+template <int N, int MODE, bool PSD, int EVT>
 __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs a) {
   constexpr int T = TriN<N>::value, NN = N * N;
   extern __shared__ __align__(16) double hbuf[];
@@ -374,9 +395,11 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
       dp = a.prow_dp[row];
       ho = a.hoff[row];
     }
-    // level 2: own data and the first records
-    uint64_t rc_n = k0 < k1 ? a.rrec[k0] : 0;
-    uint64_t rc_nn = k0 + 1 < k1 ? a.rrec[k0 + 1] : 0;
+    const int cnt = k1 - k0;
+    // level 2: records of the first MAXI incidences, own x / w
+    uint64_t rc[MAXI];
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j) rc[j] = j < cnt ? a.rrec[k0 + j] : 0;
     double xs[N], us[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
@@ -384,12 +407,27 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
       if constexpr (MODE == MODE_HVP) us[c] = fr ? a.w[(int64_t)g * N + c] : 0.0;
       else us[c] = 0.0;
     }
+    // level 3: neighbour x (w) and the edge attribute
+    double xo[MAXI][N], uo[MAXI][N], a0[MAXI];
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j) {
+      const uint32_t hi = (uint32_t)(rc[j] >> 32);
+      const int64_t o = hi & 0x7fffffffu;
+      const bool fo = !(hi >> 31);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        xo[j][c] = j < cnt ? a.x[o * N + c] : 0.0;
+        if constexpr (MODE == MODE_HVP) uo[j][c] = (j < cnt && fo) ? a.w[o * N + c] : 0.0;
+        else uo[j][c] = 0.0;
+      }
+      a0[j] = (j < cnt && a.ev_a0) ? a.ev_a0[(uint32_t)rc[j] & 0x7fffffffu] : 0.0;
+    }
     double vec[N], dg[T];
 #pragma unroll
     for (int i = 0; i < N; ++i) vec[i] = 0.0;
 #pragma unroll
     for (int i = 0; i < T; ++i) dg[i] = 0.0;
-    {  // V terms
+    {  // V terms (their attribute loads overlap the level-3 loads)
       double wv[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) wv[c] = us[c];
@@ -422,63 +460,23 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
         }
       }
     }
-    // pipeline prologue: neighbour data of the first incidence
-    double xo_n[N], uo_n[N], a0_n = 0.0;
-    {
-      const uint32_t hi = (uint32_t)(rc_n >> 32);
-      const int o = (int)(hi & 0x7fffffffu);
-      const bool fo = !(hi >> 31);
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        xo_n[c] = k0 < k1 ? a.x[(int64_t)o * N + c] : 0.0;
-        if constexpr (MODE == MODE_HVP) uo_n[c] = (k0 < k1 && fo) ? a.w[(int64_t)o * N + c] : 0.0;
-        else uo_n[c] = 0.0;
-      }
-      if (a.ev_a0 && k0 < k1) a0_n = a.ev_a0[(uint32_t)rc_n & 0x7fffffffu];
-    }
     double* hrow = hbuf + ho;
     int pos = 0;
-    for (int k = k0; k < k1; ++k) {
-      const uint64_t rc = rc_n;
-      double xo[N], uo[N];
-#pragma unroll
-      for (int c = 0; c < N; ++c) { xo[c] = xo_n[c]; uo[c] = uo_n[c]; }
-      const double a0 = a0_n;
-      // prefetch the next incidence (records two ahead)
-      rc_n = rc_nn;
-      if (k + 2 < k1) rc_nn = a.rrec[k + 2];
-      if (k + 1 < k1) {
-        const uint32_t hi = (uint32_t)(rc_n >> 32);
-        const int o = (int)(hi & 0x7fffffffu);
-        const bool fo = !(hi >> 31);
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-          xo_n[c] = a.x[(int64_t)o * N + c];
-          if constexpr (MODE == MODE_HVP) uo_n[c] = fo ? a.w[(int64_t)o * N + c] : 0.0;
-        }
-        if (a.ev_a0) a0_n = a.ev_a0[(uint32_t)rc_n & 0x7fffffffu];
-      }
-      const uint32_t lo = (uint32_t)rc, hi = (uint32_t)(rc >> 32);
+    // one incidence: contributions to this row
+    auto incidence = [&](uint64_t r64, const double* xo_, const double* uo_, double av) {
+      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
       const int64_t e = lo & 0x7fffffffu;
       const bool first = (lo >> 31) == 0;  // the row is the edge's first vertex
       const bool fo = !(hi >> 31);
       double d[N], rr = 0.0;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        d[c] = xs[c] - xo[c];
+        d[c] = xs[c] - xo_[c];
         rr = d[c] * d[c] + rr;
       }
       double gam = 0.0, ci_s = 0.0, cd_s = 0.0, dl = 0.0, val = 0.0;
-      double dw = 0.0;
-      if constexpr (MODE == MODE_HVP) {
-#pragma unroll
-        for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo[c]);
-      }
-      for (int j = 0; j < a.nev; ++j) {
-        const TermDev& t = a.terms[a.ev_idx[j]];
-        const double av = j == 0 && a.ev_a0 ? a0 : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
-        double pv, p1, p2;
-        finite &= radial_term<MODE>(t, av, rr, pv, p1, p2);
+      auto one_term = [&](bool ok, double pv, double p1, double p2) {
+        finite &= ok;
         val += pv;
         gam += 2.0 * p1;
         if constexpr (MODE != MODE_GRAD) {
@@ -486,16 +484,29 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
           if constexpr (PSD) {
             if (fr && fo) {  // [[A,-A],[-A,A]]: clamp 2A, halve, shift floor/2
               ci *= 2.0; cd *= 2.0;
-              radial_clamp(ci, cd, rr, a.floor);
+              radial_clamp_fast(ci, cd, rr, a.floor);
               ci *= 0.5; cd *= 0.5;
               sh = 0.5 * a.floor;
             } else if (fr || fo) {
-              radial_clamp(ci, cd, rr, a.floor);
+              radial_clamp_fast(ci, cd, rr, a.floor);
             }
           }
           ci_s += ci;
           cd_s += cd;
           dl += sh;
+        }
+      };
+      if constexpr (EVT != 0) {
+        double pv, p1, p2;
+        const bool ok = radial_closed<EVT>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
+        one_term(ok, pv, p1, p2);
+      } else {
+        for (int j = 0; j < a.nev; ++j) {
+          const TermDev& t = a.terms[a.ev_idx[j]];
+          const double at = (j == 0 && a.ev_a0) ? av : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
+          double pv, p1, p2;
+          const bool ok = radial_any(t, at, rr, pv, p1, p2);
+          one_term(ok, pv, p1, p2);
         }
       }
       if constexpr (MODE != MODE_HVP) {
@@ -506,8 +517,11 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
         for (int i = 0; i < N; ++i) vec[i] += gam * d[i];
       }
       if constexpr (MODE == MODE_HVP) {  // y_row = M (u_row - u_other) + dl (u_row + u_other)
+        double dw = 0.0;
 #pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo[i]) + cd_s * d[i] * dw + dl * (us[i] + uo[i]);
+        for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo_[c]);
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo_[i]) + cd_s * d[i] * dw + dl * (us[i] + uo_[i]);
       }
       if constexpr (MODE == MODE_HESS) {
 #pragma unroll
@@ -524,6 +538,23 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
           ++pos;
         }
       }
+    };
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j)
+      if (j < cnt) incidence(rc[j], xo[j], uo[j], a0[j]);
+    for (int k = k0 + MAXI; k < k1; ++k) {  // high-valence rows: streamed
+      const uint64_t r64 = a.rrec[k];
+      const int64_t o = (uint32_t)(r64 >> 32) & 0x7fffffffu;
+      const bool fo = !(r64 >> 63);
+      double x1[N], u1[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        x1[c] = a.x[o * N + c];
+        if constexpr (MODE == MODE_HVP) u1[c] = fo ? a.w[o * N + c] : 0.0;
+        else u1[c] = 0.0;
+      }
+      const double av = a.ev_a0 ? a.ev_a0[(uint32_t)r64 & 0x7fffffffu] : 0.0;
+      incidence(r64, x1, u1, av);
     }
     double* vout = MODE == MODE_HVP ? a.y : a.grad;
 #pragma unroll
@@ -718,13 +749,13 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
   }  // row blocks
 }
 
-template <int N, int MODE, bool PSD>
-void launch_rows(const EvArgs& a, int hd_max, cudaStream_t st) {
+template <int N, int MODE, bool PSD, int EVT>
+void launch_rows_t(const EvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
   const int64_t nb = (a.V + PT - 1) / PT;
   if (!nb) return;
-  auto fast = k_rows_fast<N, MODE, PSD>;
+  auto fast = k_rows_fast<N, MODE, PSD, EVT>;
   auto exact = k_rows_ev<N, MODE, PSD, true>;
   if (sm) {
     MG_CUDA(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -739,6 +770,14 @@ void launch_rows(const EvArgs& a, int hd_max, cudaStream_t st) {
   const int64_t ge = nb < (int64_t)sms * 4 ? nb : (int64_t)sms * 4;
   exact<<<(unsigned)ge, PT, sm, st>>>(a);
   MG_LAUNCH_CHECK();
+}
+
+template <int N, int MODE, bool PSD>
+void launch_rows(const EvArgs& a, int hd_max, cudaStream_t st) {
+  const int t0 = a.nev == 1 ? a.terms[a.ev_idx[0]].type : 0;
+  if (t0 == MG_TERM_SPRING) launch_rows_t<N, MODE, PSD, MG_TERM_SPRING>(a, hd_max, st);
+  else if (t0 == MG_TERM_EDGE_LENGTH) launch_rows_t<N, MODE, PSD, MG_TERM_EDGE_LENGTH>(a, hd_max, st);
+  else launch_rows_t<N, MODE, PSD, 0>(a, hd_max, st);
 }
 
 template <int N>
