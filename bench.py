@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--profile", action="store_true", help="few steps, headline only (for ncu)")
     ap.add_argument("--profile-call", default="psd", choices=["psd", "plain", "hvp", "hvp_psd", "energy"],
-                    help="which call --profile runs")
+                    help="which call --profile / --only runs")
+    ap.add_argument("--only", action="store_true", help="time --profile-call alone (K steps) and print its ms")
     return ap.parse_args()
 
 
@@ -263,7 +264,7 @@ def run_engine(args):
     def step():
         p.eval_terms(psd_floor=FLOOR, sync=False)
 
-    if args.profile and args.profile_call != "psd":
+    if (args.profile or args.only) and args.profile_call != "psd":
         import torch as _t
 
         vd = _t.from_numpy(v).cuda()
@@ -273,6 +274,10 @@ def run_engine(args):
                 "hvp_psd": lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=yd),
                 "energy": lambda: p.eval_energy_only(p.x_device)}[args.profile_call]
 
+    if args.only:
+        ms, _ = time_device(step, steps, max(warmup, 3), dist)
+        print(json.dumps({"call": args.profile_call, "ms": ms, "lib": os.environ.get("MG_LIB", "default")}), flush=True)
+        return
     clk = Clocks(local)  # sampled through warm-up + timed region (same kernel, same load)
     time.sleep(0.3)
     ms, per = time_device(step, steps, max(warmup, 3), dist)

@@ -34,6 +34,8 @@ struct EvArgs {
   int64_t V;  // owned rows (patch order)
   const int32_t* order;      // (V) vertex of each row
   const uint8_t* pfix;       // (V) pinned flag of each row
+  const uint32_t* rmeta;     // (V) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
+  const uint64_t* ell;       // (EV_ELL_K, V) first incidences, slot-major
   const int32_t* rinc_off;   // (V+1)
   const uint64_t* rrec;      // lo: edge | slot << 31, hi: other | pinned(other) << 31
   const int64_t* prow_ro;
@@ -368,7 +370,14 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
   cd = r > 0.0 ? (md - mt) * rcp_fast(r) : 0.0;
 }
 
-constexpr int MAXI = 6;  // incidences per row held in registers (the rest are streamed)
+// incidences per row held in registers (the rest are streamed) and the
+// occupancy target: the Hessian kernel is bounded by its shared-memory row
+// buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
+// for more resident warps
+template <int MODE, bool PSD> struct FastCfg { static constexpr int MAXI = EV_ELL_K, MINB = 1; };
+template <> struct FastCfg<MODE_HVP, false> { static constexpr int MAXI = 4, MINB = 12; };
+template <> struct FastCfg<MODE_HVP, true> { static constexpr int MAXI = 4, MINB = 8; };
+template <> struct FastCfg<MODE_GRAD, false> { static constexpr int MAXI = 4, MINB = 12; };
 
 // Radial fast kernel: one thread per owned row, d = x_row - x_other (radial
 // terms are even in d, so no orientation bookkeeping). A row's first MAXI
@@ -376,30 +385,31 @@ constexpr int MAXI = 6;  // incidences per row held in registers (the rest are s
 // edge attributes) so their latencies overlap; EVT fixes the single EV term's
 // type at compile time (0: any mix, dispatched per incidence).
 template <int N, int MODE, bool PSD, int EVT>
-__global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs a) {
+__global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(const __grid_constant__ EvArgs a) {
   constexpr int T = TriN<N>::value, NN = N * N;
+  constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
   extern __shared__ __align__(16) double hbuf[];
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
   double eacc = 0.0;
   bool finite = true;
   if (row < a.V) {
-    // level 1: static per-row streams
+    // level 1: static per-row streams, all indexed by the row alone
+    // (coalesced): vertex, meta word, row start / buffer offset, ELL records
     const int g = a.order[row];
-    const bool fr = !a.pfix[row];
-    const int k0 = a.rinc_off[row], k1 = a.rinc_off[row + 1];
+    const uint32_t meta = a.rmeta[row];
     int64_t ro = 0;
-    int len = 0, dp = 255, ho = 0;
+    int ho = 0;
     if constexpr (MODE == MODE_HESS) {
       ro = a.prow_ro[row];
-      len = a.prow_len[row];
-      dp = a.prow_dp[row];
       ho = a.hoff[row];
     }
-    const int cnt = k1 - k0;
-    // level 2: records of the first MAXI incidences, own x / w
     uint64_t rc[MAXI];
 #pragma unroll
-    for (int j = 0; j < MAXI; ++j) rc[j] = j < cnt ? a.rrec[k0 + j] : 0;
+    for (int j = 0; j < MAXI; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+    const bool fr = !((meta >> 8) & 1);
+    const int dp = (int)(meta >> 16) & 0xff;
+    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
+    // level 2: own x / w
     double xs[N], us[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
@@ -542,8 +552,8 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
 #pragma unroll
     for (int j = 0; j < MAXI; ++j)
       if (j < cnt) incidence(rc[j], xo[j], uo[j], a0[j]);
-    for (int k = k0 + MAXI; k < k1; ++k) {  // high-valence rows: streamed
-      const uint64_t r64 = a.rrec[k];
+    for (int k = MAXI; k < cnt; ++k) {  // the rest: ELL slots, then the CSR tail
+      const uint64_t r64 = k < EV_ELL_K ? a.ell[(int64_t)k * a.V + row] : a.rrec[a.rinc_off[row] + k];
       const int64_t o = (uint32_t)(r64 >> 32) & 0x7fffffffu;
       const bool fo = !(r64 >> 63);
       double x1[N], u1[N];
@@ -567,6 +577,8 @@ __global__ void __launch_bounds__(PT) k_rows_fast(const __grid_constant__ EvArgs
 #pragma unroll
           for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
       }
+      // blocks written: off-diagonals, plus the diagonal if the walk never passed it
+      const int len = (fr && dp != 255) ? (pos > dp + 1 ? pos : dp + 1) : pos;
       if (len > 0) {
         fence_proxy_async_smem();
         row_store_bulk(a.hess + ro * NN, hrow, len * NN);
@@ -729,6 +741,8 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
 #pragma unroll
           for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
       }
+      // blocks written: off-diagonals, plus the diagonal if the walk never passed it
+      const int len = (fr && dp != 255) ? (pos > dp + 1 ? pos : dp + 1) : pos;
       if (len > 0) {
         fence_proxy_async_smem();
         row_store_bulk(a.hess + ro * NN, hrow, len * NN);
@@ -806,6 +820,8 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.V = m.Vr;
   a.order = m.patches.order.p;
   a.pfix = p.pfix.p;
+  a.rmeta = p.rmeta.p;
+  a.ell = p.ell.p;
   a.rinc_off = p.rinc_off.p;
   a.rrec = p.rrec.p;
   a.prow_ro = p.prow_ro.p;

@@ -110,6 +110,7 @@ struct Term {
 };
 
 constexpr int EV_ROW_BLOCK = 64;  // rows (threads) per CTA of the edge row kernel
+constexpr int EV_ELL_K = 6;       // incidences per row stored slot-major (ELL); the rest stay CSR
 
 struct Problem {
   Mesh* mesh = nullptr;
@@ -143,6 +144,8 @@ struct Problem {
   DBuf<int32_t> rinc_off;      // (Vr+1)
   DBuf<uint64_t> rrec;         // (incidences) lo: edge | slot << 31, hi: other | pinned(other) << 31
   DBuf<uint8_t> pfix;          // (Vr) pinned flag of each row
+  DBuf<uint32_t> rmeta;        // (Vr) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
+  DBuf<uint64_t> ell;          // (EV_ELL_K, Vr) first incidences of each row, slot-major
   DBuf<int64_t> prow_ro;       // (Vr) row start
   DBuf<int32_t> prow_len;      // (Vr) row length (blocks)
   DBuf<uint8_t> prow_dp;       // (Vr) diagonal block position (255: none)

@@ -345,6 +345,25 @@ __global__ void k_vertex_flags(const uint8_t* fixed, const int32_t* vtx, int64_t
   if (i < n) out[i] = fixed ? fixed[vtx[i]] : 0;
 }
 
+// per-row meta word of the edge row kernel: incidence count (saturated at
+// 255), pinned flag, diagonal block position
+__global__ void k_row_meta(const int32_t* rinc_off, const uint8_t* pfix, const uint8_t* pdp, int64_t Vr,
+                           uint32_t* meta) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Vr) return;
+  const int c = rinc_off[i + 1] - rinc_off[i];
+  meta[i] = (uint32_t)(c < 255 ? c : 255) | ((uint32_t)(pfix[i] ? 1 : 0) << 8) | ((uint32_t)(pdp ? pdp[i] : 255) << 16);
+}
+
+// ELL copy of the first K incidences of every row, slot-major (slot k of row i
+// at k * Vr + i: consecutive rows read consecutive words)
+__global__ void k_ell(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr, int K, uint64_t* ell) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Vr) return;
+  const int k0 = rinc_off[i], c = rinc_off[i + 1] - k0;
+  for (int k = 0; k < K; ++k) ell[(int64_t)k * Vr + i] = k < c ? rrec[k0 + k] : 0ull;
+}
+
 __global__ void k_patch_rows(const int32_t* order, const int64_t* ro, const uint8_t* dp, int64_t Vr,
                              int64_t* pro, int32_t* plen, uint8_t* pdp) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -507,6 +526,13 @@ void build_rows_ev(Problem& p, cudaStream_t s) {
     MG_LAUNCH_CHECK();
     p.max_patch_hdoubles = to_host_int(mx.p, s);
   }
+  p.rmeta.alloc(Vr > 0 ? Vr : 1);
+  p.ell.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
+  if (Vr) {
+    k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, Vr, p.rmeta.p);
+    k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
+  }
+  MG_LAUNCH_CHECK();
   MG_CUDA(cudaStreamSynchronize(s));
   p.redo.alloc(1);
   MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
