@@ -96,7 +96,7 @@ class Mesh:
     """
 
     def __init__(self, positions, faces, edges=None, patch_target: int = DEFAULT_PATCH_TARGET,
-                 patch_vertices: int = DEFAULT_PATCH_VERTICES):
+                 patch_vertices: int = DEFAULT_PATCH_VERTICES, owned=None):
         positions = np.array(positions, dtype=np.float64)
         if positions.ndim != 2 or positions.shape[1] != 3:
             raise MeshError(f"positions must be (V, 3), got {positions.shape}")
@@ -124,6 +124,9 @@ class Mesh:
         self._explicit_edges = explicit
         self.patch_target = patch_target
         self.patch_vertices = patch_vertices
+        # multi-GPU shard: rows of the vertices flagged here are assembled on
+        # this device; the others are ribbon (halo) vertices (mg_mesh_set_owned)
+        self.owned = None if owned is None else np.asarray(owned, dtype=bool).reshape(nv)
         self._dev = None
         self._edges = None
         self._edges_device = None
@@ -152,6 +155,9 @@ class Mesh:
             _lib.stream_ptr(), ctypes.byref(handle)))
         self._dev = handle
         self._lib = lib
+        if self.owned is not None:
+            own_d = torch.from_numpy(self.owned.astype(np.uint8)).to(dev)
+            _lib.check(lib.mg_mesh_set_owned(handle, own_d.data_ptr() if nv else None, _lib.stream_ptr()))
         counts = [ctypes.c_int64() for _ in range(4)]
         _lib.check(lib.mg_mesh_counts(handle, *[ctypes.byref(c) for c in counts]))
         ne = counts[1].value

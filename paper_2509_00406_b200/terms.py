@@ -46,6 +46,7 @@ class BuiltinTerm:
     kind: Element = Element.VERTEX
     var_dims: tuple = (2, 3)
     attr_names: tuple = ()
+    attr_domains: tuple = ()  # per attribute: "V" (per vertex), "E" (per edge) or "F" (per face) rows
 
     def params(self, n: int) -> list[float]:
         return []
@@ -57,6 +58,25 @@ class BuiltinTerm:
         if n not in self.var_dims:
             raise ValueError(f"{type(self).__name__} needs var_dim in {self.var_dims}, got {n}")
 
+    def shard(self, vertex_ids, edge_ids, face_ids) -> "BuiltinTerm":
+        """The same term on a submesh: every attribute gathered to the
+        submesh's local vertices / edges / faces (global ids given)."""
+        import copy
+
+        out = copy.copy(self)
+        ids = {"V": vertex_ids, "E": edge_ids, "F": face_ids}
+        for name, dom in zip(self.attr_names, self.attr_domains):
+            arr = getattr(self, name)
+            idx = ids[dom]
+            if hasattr(arr, "detach"):
+                import torch
+
+                sub = arr[torch.as_tensor(idx, device=arr.device)].contiguous()
+            else:
+                sub = np.ascontiguousarray(np.asarray(arr)[idx])
+            setattr(out, name, sub)
+        return out
+
 
 class Inertia(BuiltinTerm):
     """0.5 * m_v * |x_v - t_v|^2 per vertex (ref apps/cloth.py:102-104)."""
@@ -65,6 +85,7 @@ class Inertia(BuiltinTerm):
     op = Op.V
     kind = Element.VERTEX
     attr_names = ("masses", "target")
+    attr_domains = ("V", "V")
 
     def __init__(self, masses, target):
         self.masses = masses
@@ -84,6 +105,7 @@ class Spring(BuiltinTerm):
     op = Op.EV
     kind = Element.EDGE
     attr_names = ("rest_len2",)
+    attr_domains = ("E",)
 
     def __init__(self, rest_len2, coef: float):
         self.rest_len2 = rest_len2
@@ -106,6 +128,7 @@ class Gravity(BuiltinTerm):
     op = Op.V
     kind = Element.VERTEX
     attr_names = ("masses",)
+    attr_domains = ("V",)
 
     def __init__(self, masses, gravity, h2: float):
         self.masses = masses
@@ -141,6 +164,7 @@ class SymDirichlet(BuiltinTerm):
     kind = Element.FACE
     var_dims = (2,)
     attr_names = ("rest_inv", "areas")
+    attr_domains = ("F", "F")
 
     def __init__(self, rest_inv, areas):
         self.rest_inv = rest_inv
@@ -166,6 +190,7 @@ class SphereBarrierStretch(BuiltinTerm):
     kind = Element.FACE
     var_dims = (2,)
     attr_names = ("base", "b1", "b2")
+    attr_domains = ("V", "V", "V")
 
     def __init__(self, base, b1, b2, include_barrier: bool = True, include_stretch: bool = True):
         self.base = base
