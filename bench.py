@@ -8,13 +8,22 @@ what `newton_solve` calls each Newton iteration — on the ClothSim energy
 fp64. A step = one such evaluation. Unit = term-element evaluations / s
 (2V + E per call).
 
-  value  : device time, inputs resident in HBM (x, target, masses, rest
-           lengths; outputs 2.1 GB > L2, so no L2 flush is needed)
-  e2e    : the public API with host buffers: pinned x H2D, eval, energy +
-           gradient D2H, every step
-  roofline: HBM, algorithmic bytes (inputs once + outputs once) / kernel time
+  value   : device time per step (CUDA events on the launching stream, inputs
+            resident in HBM; the 2.6 GB of inputs+outputs exceed the 126 MB L2,
+            so no flush is needed)
+  e2e     : the public API with host buffers: pinned x H2D, eval, energy +
+            gradient D2H, every step
+  roofline: HBM; algorithmic bytes of one call (inputs read once + outputs
+            written once) / the assembly kernel's own device time
+            (library-side CUDA events around that launch, same timed region);
+            traffic = DRAM bytes of the same kernel from the committed ncu capture
   cpu_baseline: the CPU oracle port (oracle/, restating meshgrad) on a bounded
-           sample, all host threads
+            256^2 sample of the same call, all host threads
+
+Multi-GPU (torchrun, N ranks): weak scaling. The global cloth is a
+2048 x (2048 N) grid partitioned by vertex ownership (distributed.py); each
+rank assembles its owned rows after a halo exchange of ribbon x, and the energy
+is all-reduced. Time = max over ranks.
 
 `--impl reference` runs the reference arm: the CPU oracle port on the same
 metric (rank 0 only).
@@ -39,6 +48,7 @@ sys.path.insert(0, str(ROOT))
 
 FLOOR = 1e-9
 GRID = 2048
+METRIC = "term-element evaluations/s, cloth Newton-step grad+Hessian assembly (psd_floor=1e-9)"
 
 
 def parse():
@@ -49,7 +59,7 @@ def parse():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--grid", type=int, default=GRID)
     ap.add_argument("--accumulation", default="deterministic", choices=["deterministic", "atomic"])
-    ap.add_argument("--patch", type=int, default=64, help="owned rows per vertex patch")
+    ap.add_argument("--patch", type=int, default=64, help="owned rows per vertex patch (generic patch path)")
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary workloads")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--profile", action="store_true", help="few steps, headline only (for ncu)")
@@ -61,31 +71,58 @@ def parse():
 
 # ----------------------------------------------------------------- workloads
 
-def cloth_inputs(n, seed=0):
-    from paper_2509_00406_b200.mesh import grid_arrays
+def grid_rect_arrays(nx, ny, spacing):
+    """generate_grid's numbering and split on an nx x ny vertex rectangle."""
+    ii, jj = np.meshgrid(np.arange(nx), np.arange(ny), indexing="xy")
+    pos = np.stack([ii.ravel() * spacing, jj.ravel() * spacing, np.zeros(nx * ny)], axis=1)
+    j, i = np.meshgrid(np.arange(ny - 1), np.arange(nx - 1), indexing="ij")
+    v00 = (j * nx + i).ravel()
+    f = np.empty((2 * (nx - 1) * (ny - 1), 3), np.int64)
+    f[0::2] = np.stack([v00, v00 + 1, v00 + nx + 1], 1)
+    f[1::2] = np.stack([v00, v00 + nx + 1, v00 + nx], 1)
+    return pos, f
 
-    pos, faces = grid_arrays(n, 1.0 / (n - 1))
+
+def cloth_state(pos, n, seed=0):
     rng = np.random.default_rng(seed)
     sig = 0.01 / (n - 1)
     target = pos + sig * rng.normal(size=pos.shape)
     x = (pos + sig * rng.normal(size=pos.shape)).ravel()
     v = np.random.default_rng(1).normal(size=x.size)
+    return target, x, v
+
+
+def cloth_inputs(n, seed=0):
+    from paper_2509_00406_b200.mesh import grid_arrays
+
+    pos, faces = grid_arrays(n, 1.0 / (n - 1))
+    target, x, v = cloth_state(pos, n, seed)
     return pos, faces, target, x, v
 
 
-def cloth_sizes(n):
-    V = n * n
-    E = 3 * n * n - 4 * n + 1
+def cloth_sizes(n, ny=None):
+    ny = n if ny is None else ny
+    V = n * ny
+    E = (n - 1) * ny + n * (ny - 1) + (n - 1) * (ny - 1)
     return V, E
 
 
+# algorithmic bytes per call (SURVEY 8(d)): inputs read once, outputs written once, int32 indices
 def cloth_bytes(V, E, nnzb):
-    # compulsory traffic per call: x, target, masses, rest lengths,
-    # edge endpoints (int32 pairs) read once; grad and Hessian blocks written once
+    # x, target, masses, rest lengths, edge endpoints; grad, Hessian blocks
     return 24 * V + 24 * V + 8 * V + 8 * E + 8 * E + 24 * V + 72 * nnzb
 
 
-def build_engine_cloth(n, accumulation, patch=128):
+def cloth_hvp_bytes(V, E):
+    # x, v, masses, rest lengths, edge endpoints; y
+    return 24 * V + 24 * V + 8 * V + 8 * E + 8 * E + 24 * V
+
+
+def cloth_energy_bytes(V, E):
+    return 24 * V + 24 * V + 8 * V + 8 * E + 8 * E
+
+
+def build_engine_cloth(n, accumulation, patch=64):
     import torch
 
     import paper_2509_00406_b200 as mg
@@ -100,6 +137,30 @@ def build_engine_cloth(n, accumulation, patch=128):
     p.precompute_sparsity()
     p.x = x
     return p, x, v
+
+
+def build_engine_cloth_shard(n, world, rank, accumulation):
+    """Rank `rank`'s shard of the weak-scaling cloth: a 2048 x (2048 world) grid."""
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.distributed import DistributedProblem
+    from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+
+    ny = n * world
+    sp = 1.0 / (n - 1)
+    pos, faces = grid_rect_arrays(n, ny, sp)
+    target, x, v = cloth_state(pos, n)
+    areas = 0.5 * np.linalg.norm(np.cross(pos[faces[:, 1]] - pos[faces[:, 0]], pos[faces[:, 2]] - pos[faces[:, 0]]), axis=1)
+    masses = np.bincount(faces.ravel(), weights=np.repeat(areas / 3.0, 3), minlength=len(pos))
+    edges = mg.mesh._host_edges(faces, None, len(pos))
+    d = pos[edges[:, 1]] - pos[edges[:, 0]]
+    h = 0.01
+    terms = [("V", Inertia(masses, target)), ("EV", Spring(np.einsum("ij,ij->i", d, d), 0.5 * 1e4 * h * h)),
+             ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
+    pins = (n * (ny - 1), n * ny - 1)
+    dp = DistributedProblem(pos, faces, 3, terms, fixed_vertices=pins, accumulation=accumulation)
+    dp.set_x_global(x)
+    dp.problem.precompute_sparsity()
+    return dp, len(pos), len(edges)
 
 
 class Clocks:
@@ -146,6 +207,15 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
 def time_device(fn, steps, warmup, dist=None):
     """Mean ms per step with CUDA events on the current stream; max over ranks."""
     import torch
@@ -171,6 +241,24 @@ def time_device(fn, steps, warmup, dist=None):
         total = float(t.item())
         dist.barrier()
     return total / steps, per
+
+
+def time_with_kernel(p, fn, steps, warmup, dist=None):
+    """(ms per step, ms per main-kernel launch) over the same timed region."""
+    p.set_kernel_timing(False)
+    for _ in range(warmup):
+        fn()
+    p.set_kernel_timing(True)
+    p.kernel_time()  # reset
+    ms, _ = time_device(fn, steps, 0, dist)
+    kt, cnt = p.kernel_time()
+    p.set_kernel_timing(False)
+    return ms, (kt / cnt if cnt else None)
+
+
+def kernel_label(p, call):
+    mode = {"psd": "HESS,psd", "plain": "HESS", "hvp": "HVP", "hvp_psd": "HVP,psd", "energy": "ENERGY"}[call]
+    return f"k_rows_fast<{p.n},{mode},SPRING>"
 
 
 # -------------------------------------------------------------- CPU baseline
@@ -224,7 +312,7 @@ def run_reference(args):
     V, E = cloth_sizes(args.grid)
     val = statistics.median(rates)
     line = {
-        "impl": "reference", "metric": "term-element evaluations/s, cloth Newton-step grad+Hessian assembly (psd_floor=1e-9)",
+        "impl": "reference", "metric": METRIC,
         "value": val, "unit": "term-elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": (2 * V + E) / val * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
@@ -253,84 +341,113 @@ def run_engine(args):
         torch.cuda.set_device(0)
 
     n = args.grid
-    V, E = cloth_sizes(n)
-    units = 2 * V + E
     t_setup = time.perf_counter()
-    p, x, v = build_engine_cloth(n, args.accumulation, args.patch)
+    if world == 1:
+        V, E = cloth_sizes(n)
+        p, x, v = build_engine_cloth(n, args.accumulation, args.patch)
+        dp = None
+        step = lambda: p.eval_terms(psd_floor=FLOOR, sync=False)
+    else:
+        dp, V, E = build_engine_cloth_shard(n, world, rank, args.accumulation)
+        p = dp.problem
+        x = None
+        step = lambda: dp.eval_terms(psd_floor=FLOOR, sync=False)
     t_setup = time.perf_counter() - t_setup
-    nnzb = p.hess.nnz_blocks
-    steps, warmup = (2, 1) if args.profile else (args.steps, args.warmup)
-
-    def step():
-        p.eval_terms(psd_floor=FLOOR, sync=False)
+    units = 2 * V + E  # whole job
+    nnzb_local = p.hess.nnz_blocks
+    steps, warmup = (2, 1) if args.profile else (args.steps, max(args.warmup, 3))
 
     if (args.profile or args.only) and args.profile_call != "psd":
-        import torch as _t
-
-        vd = _t.from_numpy(v).cuda()
-        yd = _t.empty_like(vd)
+        vd = torch.from_numpy(np.random.default_rng(1).normal(size=p.num_dofs)).cuda()
+        yd = torch.empty_like(vd)
         step = {"plain": lambda: p.eval_terms(sync=False),
                 "hvp": lambda: p.hvp(p.x_device, vd, out=yd),
                 "hvp_psd": lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=yd),
                 "energy": lambda: p.eval_energy_only(p.x_device)}[args.profile_call]
-
-    if args.only:
-        ms, _ = time_device(step, steps, max(warmup, 3), dist)
-        print(json.dumps({"call": args.profile_call, "ms": ms, "lib": os.environ.get("MG_LIB", "default")}), flush=True)
-        return
-    clk = Clocks(local)  # sampled through warm-up + timed region (same kernel, same load)
-    time.sleep(0.3)
-    ms, per = time_device(step, steps, max(warmup, 3), dist)
-    clocks = clk.stop()
-    launches = p.launch_count()
-    value = world * units / (ms * 1e-3)
-    bytes_call = cloth_bytes(V, E, nnzb)
-    peak, peak_kind = peaks()
-    achieved = bytes_call / (ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": peak_kind, "algorithmic_bytes_per_launch": bytes_call,
-                "kernel": "k_patch<3,LIGHT,HESS,psd>"}
     if args.profile:
+        ms, _ = time_device(step, steps, warmup, dist)
         print(json.dumps({"profile": True, "ms_per_step": ms}), flush=True)
         return
+    if args.only:
+        ms, kms = time_with_kernel(p, step, steps, warmup, dist)
+        print(json.dumps({"call": args.profile_call, "ms": ms, "kernel_ms": kms,
+                          "lib": os.environ.get("MG_LIB", "default")}), flush=True)
+        return
+
+    clk = Clocks(local)  # sampled through warm-up + timed region (same kernel, same load)
+    time.sleep(0.3)
+    ms, kms = time_with_kernel(p, step, steps, warmup, dist)
+    clocks = clk.stop()
+    launches = p.launch_count() * steps
+    value = units / (ms * 1e-3)
+    peak, peak_kind = peaks()
+    label = kernel_label(p, "psd")
+    if world == 1:
+        bytes_call = cloth_bytes(V, E, nnzb_local)
+        achieved = bytes_call / (kms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": ncu_traffic(label), "peak_source": peak_kind, "kernel": label,
+                    "algorithmic_bytes_per_launch": bytes_call, "kernel_ms": kms,
+                    "kernel_share_of_step": kms / ms,
+                    "bytes_note": "24V x + 24V target + 8V masses + 8E rest lengths + 8E edge ids + 24V grad + 72 nnzb H"}
+    else:
+        roofline = {"bound": "hbm", "kernel": label, "kernel_ms": kms, "note": "per-rank shard; see the N=1 line"}
 
     # e2e through the public API with host buffers
-    x_host = torch.from_numpy(x).pin_memory()
-    g_host = torch.empty(3 * V, dtype=torch.float64).pin_memory()
-    e_host = torch.empty(1, dtype=torch.float64).pin_memory()
+    if world == 1:
+        x_host = torch.from_numpy(x).pin_memory()
+        g_host = torch.empty(p.num_dofs, dtype=torch.float64).pin_memory()
+        e_host = torch.empty(1, dtype=torch.float64).pin_memory()
 
-    def e2e_step():
-        p.x_device.copy_(x_host, non_blocking=True)
-        p.eval_terms(psd_floor=FLOOR, sync=False)
-        g_host.copy_(p.grad_device, non_blocking=True)
-        e_host.copy_(p.energy_device, non_blocking=True)
+        def e2e_step():
+            p.x_device.copy_(x_host, non_blocking=True)
+            p.eval_terms(psd_floor=FLOOR, sync=False)
+            g_host.copy_(p.grad_device, non_blocking=True)
+            e_host.copy_(p.energy_device, non_blocking=True)
+    else:
+        own = len(dp.plan.owned_global)
+        x_host = torch.from_numpy(dp.problem.x.reshape(-1, 3)[np.flatnonzero(dp.plan.owned)].ravel()).pin_memory()
+        x_dev = torch.empty(own * 3, dtype=torch.float64, device="cuda")
+        g_host = torch.empty(own * 3, dtype=torch.float64).pin_memory()
+        e_host = torch.empty(1, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            x_dev.copy_(x_host, non_blocking=True)
+            dp.set_x_owned(x_dev)
+            dp.eval_terms(psd_floor=FLOOR, sync=False)
+            g_host.copy_(dp.grad_owned().reshape(-1), non_blocking=True)
+            e_host.copy_(dp.energy_device, non_blocking=True)
 
     ms_e2e, _ = time_device(e2e_step, max(3, steps // 2), 2, dist)
-    e2e = {"value": world * units / (ms_e2e * 1e-3), "unit": "term-elements/s",
-           "h2d_bytes_per_step": 24 * V, "d2h_bytes_per_step": 24 * V + 8, "ms_per_step": ms_e2e}
+    e2e = {"value": units / (ms_e2e * 1e-3), "unit": "term-elements/s",
+           "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(g_host.numel() * 8 + 8),
+           "ms_per_step": ms_e2e, "path": "Problem.x (pinned H2D) -> eval_terms(psd_floor) -> grad + energy D2H"}
 
     extras = {}
     if not args.no_extras and world == 1:
-        extras = run_extras(p, x, v, V, E, nnzb, steps, warmup, peak)
+        extras = run_extras(p, v, V, E, nnzb_local, steps, peak)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, cores, desc = cpu_oracle_rate(256, reps=3)
         cpu = {"value": r, "unit": "term-elements/s", "cores": cores, "kind": "port", "sample": desc}
     if rank == 0:
+        F = 2 * (n - 1) * (n * world - 1)
         line = {
-            "metric": "term-element evaluations/s, cloth Newton-step grad+Hessian assembly (psd_floor=1e-9)",
+            "metric": METRIC,
             "value": value, "unit": "term-elements/s", "n_gpus": world, "steps": steps, "warmup": warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cloth grid {n}x{n} (V={V}, E={E}, F={2 * (n - 1) ** 2}, nnzb={nnzb}) "
-                                   "Newton-step eval_terms(psd_floor=1e-9), default pins",
-                       "accumulation": args.accumulation, "patch_rows": args.patch, "l2": "inputs+outputs 2.6 GB > 126 MB L2; no flush",
-                       "parallelism": f"replica x{world}" if world > 1 else "1 GPU",
-                       "faces_per_s": world * 2 * (n - 1) ** 2 / (ms * 1e-3), "setup_s": t_setup},
+            "config": {"workload": (f"cloth grid {n}x{n * world} (V={V}, E={E}, F={F}) Newton-step "
+                                    "eval_terms(psd_floor=1e-9), inertia+spring+gravity, 2 pins"),
+                       "accumulation": args.accumulation, "nnzb_per_rank": nnzb_local,
+                       "l2": "inputs+outputs 2.6 GB per GPU > 126 MB L2; no flush",
+                       "parallelism": (f"vertex-partitioned shards x{world} (halo all_to_all + energy all_reduce)"
+                                       if world > 1 else "1 GPU"),
+                       "faces_per_s": F / (ms * 1e-3), "setup_s": t_setup},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches * steps,
+            "gpu_launches": launches,
             "clocks": clocks,
             "extras": extras,
         }
@@ -339,27 +456,26 @@ def run_engine(args):
         dist.destroy_process_group()
 
 
-def run_extras(p, x, v, V, E, nnzb, steps, warmup, peak):
-    """Secondary workloads of the same path, each with its own roofline."""
+def run_extras(p, v, V, E, nnzb, steps, peak):
+    """Secondary calls of the same path, each with its kernel time and HBM fraction."""
     import torch
 
     out = {}
     xd = p.x_device
     vd = torch.from_numpy(v).cuda()
     y = torch.empty_like(vd)
-    k = max(3, steps // 2)
-    ms, _ = time_device(lambda: p.eval_terms(sync=False), k, 2)
-    b = cloth_bytes(V, E, nnzb)
-    out["cloth_grad_hess"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
-                              "hbm_frac": b / (ms * 1e-3) / 1e9 / peak}
-    ms, _ = time_device(lambda: p.hvp(xd, vd, out=y), k, 2)
-    b = 24 * V * 4 + 8 * V + 8 * E + 8 * E  # x, target(unused by H), v, y, masses, rest, edges
-    out["cloth_hvp"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
-                        "hbm_frac": (24 * V * 3 + 8 * V + 16 * E) / (ms * 1e-3) / 1e9 / peak}
-    ms, _ = time_device(lambda: p.hvp(xd, vd, psd_floor=FLOOR, out=y), k, 2)
-    out["cloth_hvp_psd"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3)}
-    ms, _ = time_device(lambda: p.eval_energy_only(xd), k, 2)
-    out["cloth_energy_only"] = {"ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3)}
+    k = max(5, steps // 2)
+    calls = [
+        ("cloth_grad_hess", lambda: p.eval_terms(sync=False), cloth_bytes(V, E, nnzb)),
+        ("cloth_hvp", lambda: p.hvp(xd, vd, out=y), cloth_hvp_bytes(V, E)),
+        ("cloth_hvp_psd", lambda: p.hvp(xd, vd, psd_floor=FLOOR, out=y), cloth_hvp_bytes(V, E)),
+        ("cloth_energy_only", lambda: p.eval_energy_only(xd), cloth_energy_bytes(V, E)),
+    ]
+    for name, fn, b in calls:
+        ms, kms = time_with_kernel(p, fn, k, 3)
+        t = kms if kms else ms
+        out[name] = {"ms": ms, "kernel_ms": kms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
+                     "algorithmic_bytes": b, "hbm_frac": b / (t * 1e-3) / 1e9 / peak}
     return out
 
 

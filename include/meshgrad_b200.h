@@ -156,6 +156,12 @@ MG_API int mg_problem_destroy(mg_problem* prob);
  * most recent mg_eval/mg_energy/mg_hvp call, and the problem's patch stats
  * (patches, owned rows, ribbon vertices, recomputed ribbon elements). */
 MG_API int mg_last_launch_count(const mg_problem* prob, int* launches);
+/* Device timing of the main assembly / HVP kernel (benchmarks): when enabled,
+ * every mg_eval / mg_hvp records CUDA events around that kernel on the call's
+ * stream; mg_problem_kernel_time synchronizes, returns the summed duration
+ * (ms) and the number of launches timed since the previous query, and resets. */
+MG_API int mg_problem_set_timing(mg_problem* prob, int enable);
+MG_API int mg_problem_kernel_time(mg_problem* prob, double* total_ms, int* count);
 MG_API int mg_problem_patch_stats(const mg_problem* prob, int64_t* stats4);
 
 #ifdef __cplusplus

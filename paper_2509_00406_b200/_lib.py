@@ -57,6 +57,8 @@ SIGNATURES = [
     ("mg_problem_destroy", _INT, [_P]),
     ("mg_last_launch_count", _INT, [_P, ctypes.POINTER(_INT)]),
     ("mg_problem_patch_stats", _INT, [_P, _I64P]),
+    ("mg_problem_set_timing", _INT, [_P, _INT]),
+    ("mg_problem_kernel_time", _INT, [_P, ctypes.POINTER(_DBL), ctypes.POINTER(_INT)]),
 ]
 
 

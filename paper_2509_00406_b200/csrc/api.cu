@@ -92,6 +92,31 @@ int64_t partials_needed(const Problem& p) {
 
 }  // namespace
 
+namespace mg {
+static cudaEvent_t take_event(const Problem& p) {
+  if (!p.ev_pool.empty()) {
+    cudaEvent_t e = p.ev_pool.back();
+    p.ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  MG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void timing_begin(const Problem& p, cudaStream_t s) {
+  if (!p.timing) return;
+  p.ev_open = take_event(p);
+  MG_CUDA(cudaEventRecord(p.ev_open, s));
+}
+void timing_end(const Problem& p, cudaStream_t s) {
+  if (!p.timing || !p.ev_open) return;
+  cudaEvent_t e = take_event(p);
+  MG_CUDA(cudaEventRecord(e, s));
+  p.ev_pairs.emplace_back(p.ev_open, e);
+  p.ev_open = nullptr;
+}
+}  // namespace mg
+
 extern "C" {
 
 const char* mg_last_error(void) { return g_err.c_str(); }
@@ -350,8 +375,40 @@ int mg_bsr_matvec(const mg_problem* prob, const double* hess_d, const double* v_
 }
 
 int mg_problem_destroy(mg_problem* prob) {
+  if (prob) {
+    for (auto& pr : prob->p.ev_pairs) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    for (auto e : prob->p.ev_pool) cudaEventDestroy(e);
+  }
   delete prob;
   return MG_OK;
+}
+
+int mg_problem_set_timing(mg_problem* prob, int enable) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  prob->p.timing = enable != 0;
+  return MG_OK;
+}
+
+int mg_problem_kernel_time(mg_problem* prob, double* total_ms, int* count) {
+  if (!prob || !total_ms || !count) return fail(MG_ERR_VALUE, "NULL argument");
+  return guard([&] {
+    Problem& p = prob->p;
+    double t = 0.0;
+    for (auto& pr : p.ev_pairs) {
+      MG_CUDA(cudaEventSynchronize(pr.second));
+      float ms = 0.f;
+      MG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      t += ms;
+      p.ev_pool.push_back(pr.first);
+      p.ev_pool.push_back(pr.second);
+    }
+    *total_ms = t;
+    *count = (int)p.ev_pairs.size();
+    p.ev_pairs.clear();
+  });
 }
 
 int mg_last_launch_count(const mg_problem* prob, int* launches) {

@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
 }
 
 template <int N, int MODE, bool PSD, int EVT>
-void launch_rows_t(const EvArgs& a, int hd_max, cudaStream_t st) {
+void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
   const int64_t nb = (a.V + PT - 1) / PT;
@@ -775,8 +775,10 @@ void launch_rows_t(const EvArgs& a, int hd_max, cudaStream_t st) {
     MG_CUDA(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     MG_CUDA(cudaFuncSetAttribute(exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
+  timing_begin(p, st);
   fast<<<(unsigned)nb, PT, sm, st>>>(a);
   MG_LAUNCH_CHECK();
+  timing_end(p, st);
   // exact re-run only when a lane was non-finite (reads the flag and exits otherwise)
   int dev = 0, sms = 148;
   MG_CUDA(cudaGetDevice(&dev));
@@ -787,24 +789,24 @@ void launch_rows_t(const EvArgs& a, int hd_max, cudaStream_t st) {
 }
 
 template <int N, int MODE, bool PSD>
-void launch_rows(const EvArgs& a, int hd_max, cudaStream_t st) {
+void launch_rows(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
   const int t0 = a.nev == 1 ? a.terms[a.ev_idx[0]].type : 0;
-  if (t0 == MG_TERM_SPRING) launch_rows_t<N, MODE, PSD, MG_TERM_SPRING>(a, hd_max, st);
-  else if (t0 == MG_TERM_EDGE_LENGTH) launch_rows_t<N, MODE, PSD, MG_TERM_EDGE_LENGTH>(a, hd_max, st);
-  else launch_rows_t<N, MODE, PSD, 0>(a, hd_max, st);
+  if (t0 == MG_TERM_SPRING) launch_rows_t<N, MODE, PSD, MG_TERM_SPRING>(p, a, hd_max, st);
+  else if (t0 == MG_TERM_EDGE_LENGTH) launch_rows_t<N, MODE, PSD, MG_TERM_EDGE_LENGTH>(p, a, hd_max, st);
+  else launch_rows_t<N, MODE, PSD, 0>(p, a, hd_max, st);
 }
 
 template <int N>
-void launch_rows_mode(const EvArgs& a, int hd, Mode mode, bool psd, cudaStream_t st) {
+void launch_rows_mode(const Problem& p, const EvArgs& a, int hd, Mode mode, bool psd, cudaStream_t st) {
   switch (mode) {
-    case MODE_GRAD: launch_rows<N, MODE_GRAD, false>(a, hd, st); break;
+    case MODE_GRAD: launch_rows<N, MODE_GRAD, false>(p, a, hd, st); break;
     case MODE_HESS:
-      if (psd) launch_rows<N, MODE_HESS, true>(a, hd, st);
-      else launch_rows<N, MODE_HESS, false>(a, hd, st);
+      if (psd) launch_rows<N, MODE_HESS, true>(p, a, hd, st);
+      else launch_rows<N, MODE_HESS, false>(p, a, hd, st);
       break;
     case MODE_HVP:
-      if (psd) launch_rows<N, MODE_HVP, true>(a, hd, st);
-      else launch_rows<N, MODE_HVP, false>(a, hd, st);
+      if (psd) launch_rows<N, MODE_HVP, true>(p, a, hd, st);
+      else launch_rows<N, MODE_HVP, false>(p, a, hd, st);
       break;
     default: throw Error(MG_ERR_UNSUPPORTED, "edge row kernel assembles grad / Hessian / HVP only");
   }
@@ -845,8 +847,8 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   }
   if (a.nev && p.terms[a.ev_idx[0]].dev.type == MG_TERM_SPRING) a.ev_a0 = p.terms[a.ev_idx[0]].dev.a[0];
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
-  if (p.n == 3) launch_rows_mode<3>(a, hd, mode, c.psd, c.stream);
-  else launch_rows_mode<2>(a, hd, mode, c.psd, c.stream);
+  if (p.n == 3) launch_rows_mode<3>(p, a, hd, mode, c.psd, c.stream);
+  else launch_rows_mode<2>(p, a, hd, mode, c.psd, c.stream);
   return mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
 }
 

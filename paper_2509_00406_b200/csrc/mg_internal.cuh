@@ -152,6 +152,11 @@ struct Problem {
   DBuf<int32_t> hoff;          // (Vr) row-buffer offset (doubles) in its CTA, 16-byte phase matched
   int max_patch_hdoubles = 0;  // max row-buffer doubles of one CTA
   DBuf<int> redo;              // (1) non-finite lane seen by the radial kernel; cleared by the energy reduction
+  // optional device timing of the main assembly kernel (benchmarks)
+  bool timing = false;
+  mutable std::vector<cudaEvent_t> ev_pool;
+  mutable std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
+  mutable cudaEvent_t ev_open = nullptr;
   int64_t recomputed_elements = 0;
 };
 
@@ -199,6 +204,9 @@ int64_t elem_partials_needed(const Term& t);
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 // edge_kernels.cu (two-point edge fast path of the patch-owner assembly)
 int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
+// timing hooks around the main kernel (no-ops unless p.timing)
+void timing_begin(const Problem& p, cudaStream_t s);
+void timing_end(const Problem& p, cudaStream_t s);
 bool patch_supported(const Problem& p);
 // fixed-order reduction of energy partials -> out[0]
 void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag = nullptr);

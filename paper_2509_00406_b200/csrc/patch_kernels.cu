@@ -366,6 +366,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   }
   const int64_t np = m.patches.num;
   const int nvp = p.max_patch_vertices, nb = p.max_patch_blocks;
+  timing_begin(p, c.stream);
   if (p.n == 3) {
     if (used & ~FAM_LIGHT) throw Error(MG_ERR_UNSUPPORTED, "term not available for var_dim 3");
     launch_mode<3, FAM_LIGHT>(a, np, nvp, nb, mode, c.psd, c.stream);
@@ -374,6 +375,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
     else if (used & bit(MG_TERM_SYM_DIRICHLET)) launch_mode<2, FAM_UV>(a, np, nvp, nb, mode, c.psd, c.stream);
     else launch_mode<2, FAM_LIGHT>(a, np, nvp, nb, mode, c.psd, c.stream);
   }
+  timing_end(p, c.stream);
   return mode == MODE_HVP ? 0 : np;
 }
 

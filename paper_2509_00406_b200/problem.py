@@ -432,6 +432,16 @@ class Problem:
         _lib.check(self._lib.mg_last_launch_count(self._h, ctypes.byref(c)))
         return c.value
 
+    def set_kernel_timing(self, enable: bool = True) -> None:
+        """Record device time of the main kernel of every call (benchmarks)."""
+        _lib.check(self._lib.mg_problem_set_timing(self._h, int(bool(enable))))
+
+    def kernel_time(self):
+        """(total ms, launches) of the main kernel since the last query; synchronizes."""
+        t, c = ctypes.c_double(), ctypes.c_int()
+        _lib.check(self._lib.mg_problem_kernel_time(self._h, ctypes.byref(t), ctypes.byref(c)))
+        return t.value, c.value
+
     def patch_stats(self) -> dict:
         arr = (ctypes.c_int64 * 4)()
         _lib.check(self._lib.mg_problem_patch_stats(self._h, arr))
