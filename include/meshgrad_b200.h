@@ -161,6 +161,9 @@ MG_API int mg_last_launch_count(const mg_problem* prob, int* launches);
  * stream; mg_problem_kernel_time synchronizes, returns the summed duration
  * (ms) and the number of launches timed since the previous query, and resets. */
 MG_API int mg_problem_set_timing(mg_problem* prob, int enable);
+/* Number of calls so far whose exact re-run executed (a fast row kernel met a
+ * non-finite lane, or pinned corners under a PSD clamp). Synchronizes. */
+MG_API int mg_problem_exact_runs(const mg_problem* prob, int64_t* runs);
 MG_API int mg_problem_kernel_time(mg_problem* prob, double* total_ms, int* count);
 MG_API int mg_problem_patch_stats(const mg_problem* prob, int64_t* stats4);
 

@@ -58,6 +58,7 @@ SIGNATURES = [
     ("mg_last_launch_count", _INT, [_P, ctypes.POINTER(_INT)]),
     ("mg_problem_patch_stats", _INT, [_P, _I64P]),
     ("mg_problem_set_timing", _INT, [_P, _INT]),
+    ("mg_problem_exact_runs", _INT, [_P, _I64P]),
     ("mg_problem_kernel_time", _INT, [_P, ctypes.POINTER(_DBL), ctypes.POINTER(_INT)]),
 ]
 

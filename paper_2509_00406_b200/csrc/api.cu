@@ -301,7 +301,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
     int64_t np = 0;
     if (p.deterministic && p.layout_ready) {
       np = launch_patch(p, mode, c, 0);
-      launches += p.ev_fast ? 2 : 1;
+      launches += (p.ev_fast || p.fv_fast) ? 2 : 1;
     } else {
       MG_CUDA(cudaMemsetAsync(grad_d, 0, sizeof(double) * p.n * p.mesh->V, s));
       if (p.with_hessian && p.nnzb)
@@ -311,7 +311,8 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
         ++launches;
       }
     }
-    reduce_partials(p.partials.p, np, energy_d, s, p.ev_fast && p.deterministic && p.layout_ready ? p.redo.p : nullptr);
+    reduce_partials(p.partials.p, np, energy_d, s,
+                    (p.ev_fast || p.fv_fast) && p.deterministic && p.layout_ready ? p.redo.p : nullptr);
     p.last_launches = launches + 1;
   });
 }
@@ -353,7 +354,7 @@ int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, 
     if (p.deterministic && p.layout_ready) {
       launch_patch(p, MODE_HVP, c, 0);
       launches = 1;
-      if (p.ev_fast) {
+      if (p.ev_fast || p.fv_fast) {
         MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
         launches = 2;
       }
@@ -384,6 +385,15 @@ int mg_problem_destroy(mg_problem* prob) {
   }
   delete prob;
   return MG_OK;
+}
+
+int mg_problem_exact_runs(const mg_problem* prob, int64_t* runs) {
+  if (!prob || !runs) return fail(MG_ERR_VALUE, "NULL argument");
+  return guard([&] {
+    int h = 0;
+    if (prob->p.exact_runs.p) MG_CUDA(cudaMemcpy(&h, prob->p.exact_runs.p, sizeof(int), cudaMemcpyDeviceToHost));
+    *runs = h;
+  });
 }
 
 int mg_problem_set_timing(mg_problem* prob, int enable) {

@@ -49,6 +49,7 @@ struct EvArgs {
   double* y;
   double* partials;
   int* redo;  // raised by the radial kernel on a non-finite lane
+  int* exact_runs;
   int nev, nvt;                 // compacted term lists (indices into terms)
   int ev_idx[MAXT], vt_idx[MAXT];
   const double* ev_a0;          // per-edge attribute of ev_idx[0] (prefetched), or null
@@ -605,6 +606,7 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
   extern __shared__ __align__(16) double hbuf[];  // this CTA's rows in output layout
   if constexpr (EXACT) {
     if (*(volatile const int*)a.redo == 0) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.exact_runs, 1);
   }
   const int64_t nblk = (a.V + PT - 1) / PT;
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -837,6 +839,7 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.y = c.y;
   a.partials = c.partials + partial_offset;
   a.redo = p.redo.p;
+  a.exact_runs = p.exact_runs.p;
   a.floor = c.floor;
   for (int i = 0; i < a.nterms; ++i) a.terms[i] = p.terms[i].dev;
   a.nev = a.nvt = 0;

@@ -141,6 +141,7 @@ struct Problem {
   // edge row kernel (all EV terms radial, no FV terms): one thread per owned
   // row, rows in patch order; per row its incident edges in column order
   bool ev_fast = false;
+  bool fv_fast = false;        // face row kernel (single SymDirichlet term), generic path as exact fallback
   DBuf<int32_t> rinc_off;      // (Vr+1)
   DBuf<uint64_t> rrec;         // (incidences) lo: edge | slot << 31, hi: other | pinned(other) << 31
   DBuf<uint8_t> pfix;          // (Vr) pinned flag of each row
@@ -152,6 +153,7 @@ struct Problem {
   DBuf<int32_t> hoff;          // (Vr) row-buffer offset (doubles) in its CTA, 16-byte phase matched
   int max_patch_hdoubles = 0;  // max row-buffer doubles of one CTA
   DBuf<int> redo;              // (1) non-finite lane seen by the radial kernel; cleared by the energy reduction
+  DBuf<int> exact_runs;        // (1) calls whose exact re-run executed (diagnostics)
   // optional device timing of the main assembly kernel (benchmarks)
   bool timing = false;
   mutable std::vector<cudaEvent_t> ev_pool;
@@ -178,6 +180,7 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
 void build_pattern(Problem& p, cudaStream_t s);
 void build_patch_layout(Problem& p, cudaStream_t s);
 void build_rows_ev(Problem& p, cudaStream_t s);
+void build_rows_fv(Problem& p, cudaStream_t s);
 void mesh_patches(Mesh& m, cudaStream_t s);
 void mesh_set_owned(Mesh& m, const uint8_t* owned_d, cudaStream_t s);
 int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s);
@@ -204,6 +207,8 @@ int64_t elem_partials_needed(const Term& t);
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 // edge_kernels.cu (two-point edge fast path of the patch-owner assembly)
 int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
+// face_kernels.cu (face row kernel)
+int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 // timing hooks around the main kernel (no-ops unless p.timing)
 void timing_begin(const Problem& p, cudaStream_t s);
 void timing_end(const Problem& p, cudaStream_t s);

@@ -41,6 +41,10 @@ struct PatchArgs {
   int R;
   int nterms;
   int64_t V;
+  int64_t np;        // patches
+  const int* redo;   // non-null: run only if *redo != 0 (exact re-run after a fast kernel)
+  int* exact_runs;   // incremented once per executed re-run
+  int64_t np_total;  // energy partials the reduction reads (> np: zero-fill the rest on a re-run)
   const int32_t* vtx_off;
   const int32_t* vtx;
   const int32_t* hloc;
@@ -202,7 +206,15 @@ constexpr unsigned FAM_ALL = FAM_UV | bit(MG_TERM_SPHERE);
 template <int N, unsigned FAM, int MODE, bool PSD>
 __global__ void __launch_bounds__(PT) k_patch(const __grid_constant__ PatchArgs a, int nvp_max, int blocks_max) {
   extern __shared__ __align__(16) double smem[];
-  const int p = blockIdx.x;
+  if (a.redo && *(volatile const int*)a.redo == 0) return;
+  if (a.redo && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.exact_runs, 1);
+  if constexpr (MODE != MODE_HVP) {
+    for (int64_t i = a.np + blockIdx.x * (int64_t)PT + threadIdx.x; i < a.np_total; i += (int64_t)gridDim.x * PT)
+      a.partials[i] = 0.0;
+  }
+  for (int64_t pp = blockIdx.x; pp < a.np; pp += gridDim.x) {
+  __syncthreads();
+  const int p = (int)pp;
   const int R = a.R;
   const int64_t own0 = (int64_t)p * R;
   const int oc = (int)min((int64_t)R, a.V - own0);
@@ -290,6 +302,7 @@ __global__ void __launch_bounds__(PT) k_patch(const __grid_constant__ PatchArgs 
     const double tot = block_sum(eacc);
     if (threadIdx.x == 0) a.partials[p] = tot;
   }
+  }  // patches
 }
 
 
@@ -305,7 +318,14 @@ void launch_fam(const PatchArgs& a, int64_t np, int nvp_max, int blocks_max, cud
   const size_t sm = smem_bytes(N, MODE, a.R, nvp_max, blocks_max);
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "patch does not fit in shared memory");
   MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  kern<<<(unsigned)np, PT, sm, st>>>(a, nvp_max, blocks_max);
+  int64_t grid = np;
+  if (a.redo) {  // exact re-run: a small persistent grid that exits unless the flag is raised
+    int dev = 0, sms = 148;
+    MG_CUDA(cudaGetDevice(&dev));
+    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = np < (int64_t)sms * 4 ? np : (int64_t)sms * 4;
+  }
+  kern<<<(unsigned)grid, PT, sm, st>>>(a, nvp_max, blocks_max);
   MG_LAUNCH_CHECK();
 }
 
@@ -338,10 +358,16 @@ bool patch_supported(const Problem& p) {
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset) {
   const Mesh& m = *p.mesh;
   if (p.ev_fast) return launch_patch_ev(p, mode, c, partial_offset);
+  int64_t n_fast = 0;
+  if (p.fv_fast) n_fast = launch_patch_fv(p, mode, c, partial_offset);
   PatchArgs a;
   a.R = m.patches.R;
   a.nterms = (int)p.terms.size();
   a.V = m.Vr;
+  a.np = m.patches.num;
+  a.redo = p.fv_fast ? p.redo.p : nullptr;  // after the face row kernel: exact re-run only on its flag
+  a.exact_runs = p.exact_runs.p;
+  a.np_total = n_fast;
   a.vtx_off = p.vtx_off.p;
   a.vtx = p.vtx.p;
   a.hloc = p.hloc.p;
@@ -366,7 +392,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   }
   const int64_t np = m.patches.num;
   const int nvp = p.max_patch_vertices, nb = p.max_patch_blocks;
-  timing_begin(p, c.stream);
+  if (!p.fv_fast) timing_begin(p, c.stream);
   if (p.n == 3) {
     if (used & ~FAM_LIGHT) throw Error(MG_ERR_UNSUPPORTED, "term not available for var_dim 3");
     launch_mode<3, FAM_LIGHT>(a, np, nvp, nb, mode, c.psd, c.stream);
@@ -375,8 +401,9 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
     else if (used & bit(MG_TERM_SYM_DIRICHLET)) launch_mode<2, FAM_UV>(a, np, nvp, nb, mode, c.psd, c.stream);
     else launch_mode<2, FAM_LIGHT>(a, np, nvp, nb, mode, c.psd, c.stream);
   }
-  timing_end(p, c.stream);
-  return mode == MODE_HVP ? 0 : np;
+  if (!p.fv_fast) timing_end(p, c.stream);
+  if (mode == MODE_HVP) return 0;
+  return np > n_fast ? np : n_fast;
 }
 
 }  // namespace mg

@@ -345,14 +345,56 @@ __global__ void k_vertex_flags(const uint8_t* fixed, const int32_t* vtx, int64_t
   if (i < n) out[i] = fixed ? fixed[vtx[i]] : 0;
 }
 
+// Face-incidence records of the face row kernel: for every face and each
+// corner that is an owned row, key = (row, face) (a row's faces in id order),
+// value lo = face | slot << 30, hi = position of the next corner in the row |
+// position of the one after << 8 | pinned corners << 16 (255: no block).
+__global__ void k_row_face_inc(const int32_t* faces, int64_t F, const int32_t* rank, int64_t Vr,
+                               const uint8_t* fixed, const int64_t* ro, const int32_t* col, uint64_t* keys,
+                               uint64_t* vals) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 3 * F) return;
+  const int64_t f = i / 3;
+  const int s = (int)(i % 3);
+  const int v = faces[3 * f + s];
+  const int64_t row = rank[v];
+  if (row >= Vr) {
+    keys[i] = ~0ull;
+    vals[i] = 0;
+    return;
+  }
+  uint32_t pins = 0;
+  for (int q = 0; q < 3; ++q) pins |= (fixed && fixed[faces[3 * f + q]]) ? (1u << q) : 0u;
+  uint32_t pos[2];
+  for (int k = 1; k <= 2; ++k) {
+    const int o = faces[3 * f + (s + k) % 3];
+    uint32_t pk = 255;
+    if (col && !(fixed && (fixed[v] || fixed[o]))) {
+      int64_t lo = ro[v], hi = ro[v + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < o) lo = mid + 1; else hi = mid;
+      }
+      if (lo < ro[v + 1] && col[lo] == o && lo - ro[v] < 255) pk = (uint32_t)(lo - ro[v]);
+    }
+    pos[k - 1] = pk;
+  }
+  keys[i] = ((uint64_t)row << 32) | (uint64_t)f;
+  const uint32_t lo32 = (uint32_t)f | ((uint32_t)s << 30);
+  const uint32_t hi32 = pos[0] | (pos[1] << 8) | (pins << 16);
+  vals[i] = ((uint64_t)hi32 << 32) | lo32;
+}
+
 // per-row meta word of the edge row kernel: incidence count (saturated at
 // 255), pinned flag, diagonal block position
-__global__ void k_row_meta(const int32_t* rinc_off, const uint8_t* pfix, const uint8_t* pdp, int64_t Vr,
-                           uint32_t* meta) {
+__global__ void k_row_meta(const int32_t* rinc_off, const uint8_t* pfix, const uint8_t* pdp, const int32_t* plen,
+                           int64_t Vr, uint32_t* meta) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Vr) return;
   const int c = rinc_off[i + 1] - rinc_off[i];
-  meta[i] = (uint32_t)(c < 255 ? c : 255) | ((uint32_t)(pfix[i] ? 1 : 0) << 8) | ((uint32_t)(pdp ? pdp[i] : 255) << 16);
+  const int l = plen ? plen[i] : 0;
+  meta[i] = (uint32_t)(c < 255 ? c : 255) | ((uint32_t)(pfix[i] ? 1 : 0) << 8) |
+            ((uint32_t)(pdp ? pdp[i] : 255) << 16) | ((uint32_t)(l < 255 ? l : 255) << 24);
 }
 
 // ELL copy of the first K incidences of every row, slot-major (slot k of row i
@@ -529,17 +571,91 @@ void build_rows_ev(Problem& p, cudaStream_t s) {
   p.rmeta.alloc(Vr > 0 ? Vr : 1);
   p.ell.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
   if (Vr) {
-    k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, Vr, p.rmeta.p);
+    k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, p.prow_len.p, Vr, p.rmeta.p);
     k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
   }
   MG_LAUNCH_CHECK();
   MG_CUDA(cudaStreamSynchronize(s));
   p.redo.alloc(1);
   MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
+  if (!p.exact_runs.p) {
+    p.exact_runs.alloc(1);
+    MG_CUDA(cudaMemsetAsync(p.exact_runs.p, 0, sizeof(int), s));
+  }
   MG_CUDA(cudaStreamSynchronize(s));
   p.recomputed_elements = 0;
   p.ev_fast = true;
   p.layout_ready = true;
+}
+
+// Layout of the face row kernel (face_kernels.cu): as build_rows_ev, with
+// face incidences (and row lengths in the meta word, the kernel clears its row).
+void build_rows_fv(Problem& p, cudaStream_t s) {
+  Mesh& m = *p.mesh;
+  PatchSet& ps = m.patches;
+  const int64_t V = m.V, Vr = m.Vr;
+  const int RB = EV_ROW_BLOCK;
+  const int64_t nb = (Vr + RB - 1) / RB;
+  DBuf<int> mx;
+  mx.alloc(1);
+  {
+    DBuf<uint64_t> k1, k2, v1, v2;
+    const int64_t F = m.F;
+    const int64_t n = 3 * F > 0 ? 3 * F : 1;
+    k1.alloc(n); k2.alloc(n); v1.alloc(n); v2.alloc(n);
+    const bool pat = p.with_hessian && p.pattern_ready;
+    if (F) k_row_face_inc<<<grid_for(3 * F), TPB, 0, s>>>(m.faces.p, F, ps.rank.p, Vr, p.any_fixed ? p.fixed.p : nullptr,
+                                                          pat ? p.row_offsets.p : nullptr, pat ? p.col32.p : nullptr,
+                                                          k1.p, v1.p);
+    MG_LAUNCH_CHECK();
+    if (F) {
+      size_t tb = 0;
+      MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, v1.p, v2.p, 3 * F, 0, 64, s));
+      Tmp t(s, tb);
+      MG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, k1.p, k2.p, v1.p, v2.p, 3 * F, 0, 64, s));
+    }
+    p.rinc_off.alloc(Vr + 1);
+    k_lower_bounds_rows<<<grid_for(Vr + 1), TPB, 0, s>>>(k2.p, 3 * F, Vr, p.rinc_off.p);
+    MG_LAUNCH_CHECK();
+    MG_CUDA(cudaStreamSynchronize(s));
+    p.rrec = std::move(v2);
+  }
+  p.pfix.alloc(Vr > 0 ? Vr : 1);
+  if (Vr) k_vertex_flags<<<grid_for(Vr), TPB, 0, s>>>(p.any_fixed ? p.fixed.p : nullptr, ps.order.p, Vr, p.pfix.p);
+  MG_LAUNCH_CHECK();
+  p.max_patch_hdoubles = 0;
+  if (p.with_hessian && p.pattern_ready) {
+    p.diag_pos.alloc(V > 0 ? V : 1);
+    if (V) k_diag_pos<<<grid_for(V), TPB, 0, s>>>(p.row_offsets.p, p.col32.p, V, p.diag_pos.p);
+    p.prow_ro.alloc(Vr > 0 ? Vr : 1);
+    p.prow_len.alloc(Vr > 0 ? Vr : 1);
+    p.prow_dp.alloc(Vr > 0 ? Vr : 1);
+    if (Vr) k_patch_rows<<<grid_for(Vr), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, p.diag_pos.p, Vr, p.prow_ro.p,
+                                                     p.prow_len.p, p.prow_dp.p);
+    MG_LAUNCH_CHECK();
+    p.hoff.alloc(Vr > 0 ? Vr : 1);
+    MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+    if (nb) k_row_smem_offsets<<<grid_for(nb), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, Vr, RB, nb, p.n * p.n,
+                                                           p.hoff.p, mx.p);
+    MG_LAUNCH_CHECK();
+    p.max_patch_hdoubles = to_host_int(mx.p, s);
+  }
+  p.rmeta.alloc(Vr > 0 ? Vr : 1);
+  p.ell.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
+  if (Vr) {
+    k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, p.prow_len.p, Vr, p.rmeta.p);
+    k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
+  }
+  MG_LAUNCH_CHECK();
+  MG_CUDA(cudaStreamSynchronize(s));
+  p.redo.alloc(1);
+  MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
+  if (!p.exact_runs.p) {
+    p.exact_runs.alloc(1);
+    MG_CUDA(cudaMemsetAsync(p.exact_runs.p, 0, sizeof(int), s));
+  }
+  MG_CUDA(cudaStreamSynchronize(s));
+  p.fv_fast = true;
 }
 
 void build_patch_layout(Problem& p, cudaStream_t s) {
@@ -751,6 +867,12 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
     p.max_patch_blocks = to_host_int(mx.p, s);
   }
   MG_CUDA(cudaStreamSynchronize(s));
+  p.fv_fast = false;
+  {
+    bool fv = p.terms.size() == 1 && p.terms[0].dev.type == MG_TERM_SYM_DIRICHLET && p.n == 2 &&
+              m.F < (int64_t(1) << 30) && m.F > 0;
+    if (fv) build_rows_fv(p, s);
+  }
   p.layout_ready = true;
 }
 

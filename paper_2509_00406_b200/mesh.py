@@ -305,4 +305,9 @@ def punctured_icosphere_arrays(subdivisions: int):
     remap[used] = np.arange(len(used))
     p, f = p[used], remap[f]
     uv = np.stack([p[:, 0] / (1 - p[:, 2]), p[:, 1] / (1 - p[:, 2])], axis=1)
+    # det J has the sign of the UV triangle's orientation (the rest frame has
+    # positive orientation): make it positive (ref apps/param.py:77-79)
+    e1, e2 = uv[f[:, 1]] - uv[f[:, 0]], uv[f[:, 2]] - uv[f[:, 0]]
+    if np.max(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]) < 0:
+        uv = uv[:, ::-1].copy()
     return p, f, uv

@@ -442,6 +442,13 @@ class Problem:
         _lib.check(self._lib.mg_problem_kernel_time(self._h, ctypes.byref(t), ctypes.byref(c)))
         return t.value, c.value
 
+    def exact_runs(self) -> int:
+        """Calls whose exact re-run executed (fast row kernels fall back on
+        non-finite lanes); synchronizes."""
+        n = ctypes.c_int64()
+        _lib.check(self._lib.mg_problem_exact_runs(self._h, ctypes.byref(n)))
+        return n.value
+
     def patch_stats(self) -> dict:
         arr = (ctypes.c_int64 * 4)()
         _lib.check(self._lib.mg_problem_patch_stats(self._h, arr))

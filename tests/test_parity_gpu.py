@@ -150,3 +150,27 @@ def test_error_behaviour():
         r.precompute_sparsity()
     with pytest.raises(mg.MeshError, match="repeated"):
         mg.Mesh(np.eye(3), [[0, 0, 1]])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fast_paths_fall_back_only_on_nonfinite(name):
+    """The radial edge / Dirichlet face row kernels must carry every finite
+    golden state themselves (no exact re-run), and hand non-finite ones to the
+    exact kernel (which reproduces the reference's NaN placement)."""
+    d = load(name)
+    p = engine_problem(d)
+    finite = True
+    for s in states(d):
+        x = d[f"s{s}_x"]
+        p.x = x
+        p.eval_terms()
+        if p.with_hessian:
+            p.eval_terms(psd_floor=FLOOR)
+        if f"s{s}_v0" in d:
+            p.hvp(x, d[f"s{s}_v0"])
+        finite &= bool(np.isfinite(d[f"s{s}_grad"]).all() and np.isfinite(d[f"s{s}_energy"]))
+    runs = p.exact_runs()
+    if finite:
+        assert runs == 0, f"{name}: {runs} exact re-runs on finite states"
+    elif name in ("spring_nan", "dirichlet_flip"):
+        assert runs > 0
