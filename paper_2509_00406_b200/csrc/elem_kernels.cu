@@ -230,10 +230,23 @@ void launch_t(int n, const Term& t, Mode mode, bool psd, const ElemArgs& a, cuda
   }
 }
 
-__global__ void k_reduce(const double* partials, int64_t n, double* out, int* clear_flag) {
-  double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
-  const double s = block_sum(acc);
+// Fixed-order sum of the energy partials: thread t owns the contiguous chunk
+// [t*c, (t+1)*c) and sums it with 4 independent accumulators (memory-level
+// parallelism), then the block tree combines the threads in a fixed order.
+__global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int64_t n, double* out,
+                                                 int* clear_flag) {
+  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t b = threadIdx.x * chunk, e = b + chunk < n ? b + chunk : n;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t i = b;
+  for (; i + 3 < e; i += 4) {
+    a0 += partials[i];
+    a1 += partials[i + 1];
+    a2 += partials[i + 2];
+    a3 += partials[i + 3];
+  }
+  for (; i < e; ++i) a0 += partials[i];
+  const double s = block_sum((a0 + a1) + (a2 + a3));
   if (threadIdx.x == 0) {
     out[0] = s;
     if (clear_flag) *clear_flag = 0;

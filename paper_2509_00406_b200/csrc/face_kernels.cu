@@ -77,6 +77,15 @@ MG_DI void row_store_bulk(double* dst, const double* src, int n) {
   }
 }
 
+MG_DI double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // f(J) of the symmetric Dirichlet term on a K = 4 dual over the entries of J
 // (same operation order as terms.cuh / apps/param.py:170-177)
 MG_DI Dh<4, false> dirichlet_J(const double* J, double area) {
@@ -95,8 +104,45 @@ MG_DI Dh<4, false> dirichlet_J(const double* J, double area) {
   return (fro + fro / (det * det)) * area;
 }
 
+// Closed form of the same function and its J-derivatives (F = |J|^2, D = det J,
+// cof = dD/dJ, C2 = d2D/dJ2):
+//   g = 2a [(1 + D^-2) J - F D^-3 cof]
+//   H = 2a [(1 + D^-2) I - 2 D^-3 (J cof^T + cof J^T) + 3 F D^-4 cof cof^T - F D^-3 C2]
+// Returns false unless D > 0 and all values are finite (positive_guard NaNs the
+// reference's value there; the exact kernel then reproduces its NaN pattern).
+template <bool HESS>
+MG_DI bool dirichlet_closed(const double* J, double area, double& val, double* g, double* h) {
+  const double F = J[0] * J[0] + J[1] * J[1] + J[2] * J[2] + J[3] * J[3];
+  const double D = J[0] * J[3] - J[1] * J[2];
+  const double iD = rcp_fast(D), q = iD * iD, r = q * iD;
+  const double cof[4] = {J[3], -J[2], -J[1], J[0]};
+  val = (F + F * q) * area;
+  const double a2 = 2.0 * area, s1 = 1.0 + q, sF = F * r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) g[i] = a2 * (s1 * J[i] - sF * cof[i]);
+  double chk = val + g[0] + g[1] + g[2] + g[3];
+  if constexpr (HESS) {
+    const double t2 = 2.0 * r, t3 = 3.0 * F * q * q;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        double v = -t2 * (J[i] * cof[j] + cof[i] * J[j]) + t3 * cof[i] * cof[j];
+        if (i == j) v += s1;
+        if ((i == 3 && j == 0)) v -= sF;   // C2[0][3] = 1
+        if ((i == 2 && j == 1)) v += sF;   // C2[1][2] = -1
+        h[tri(i, j)] = a2 * v;
+        chk += h[tri(i, j)];
+      }
+  }
+  return D > 0.0 && isfinite(chk);
+}
+
+#ifndef FV_MINB
+#define FV_MINB 8
+#endif
 template <int MODE, bool PSD>
-__global__ void __launch_bounds__(PT) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
+__global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
   constexpr int N = 2, NN = 4;
   extern __shared__ __align__(16) double hbuf[];
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
@@ -127,210 +173,194 @@ __global__ void __launch_bounds__(PT) k_rows_dirichlet(const __grid_constant__ F
     double vec[N] = {0.0, 0.0}, dg[3] = {0.0, 0.0, 0.0};
     const double* R_all = a.t.a[0];
     const double* A_all = a.t.a[1];
-    auto incidence = [&](uint64_t r64) {
-      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
-      const int64_t f = lo & 0x3fffffffu;
-      const int s = (int)(lo >> 30);
-      const int pos1 = (int)(hi & 0xff), pos2 = (int)((hi >> 8) & 0xff);
-      const int pins = (int)((hi >> 16) & 7);
-      const int v0 = a.faces[3 * f], v1 = a.faces[3 * f + 1], v2 = a.faces[3 * f + 2];
-      double X[3][2], U[3][2];
-      const int vv[3] = {v0, v1, v2};
+    // one incidence: face f (record), its corners' x (and w), rest_inv, area
+    struct FaceIn {
+      double X[3][2], U[3][2], R[4], area;
+    };
+    auto load_face = [&](uint64_t r64, const int* v) {
+      FaceIn d;
+      const int64_t f = (uint32_t)r64 & 0x3fffffffu;
+      const int pins = (int)((r64 >> 48) & 7);
 #pragma unroll
       for (int q = 0; q < 3; ++q)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          X[q][c] = a.x[(int64_t)vv[q] * 2 + c];
-          if constexpr (MODE == MODE_HVP) U[q][c] = ((pins >> q) & 1) ? 0.0 : a.w[(int64_t)vv[q] * 2 + c];
-          else U[q][c] = 0.0;
+          d.X[q][c] = a.x[(int64_t)v[q] * 2 + c];
+          if constexpr (MODE == MODE_HVP) d.U[q][c] = ((pins >> q) & 1) ? 0.0 : a.w[(int64_t)v[q] * 2 + c];
+          else d.U[q][c] = 0.0;
         }
-      const double* R = R_all + 4 * f;
-      const double R0 = R[0], R1 = R[1], R2 = R[2], R3 = R[3];
-      const double area = A_all[f];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d.R[k] = R_all[4 * f + k];
+      d.area = A_all[f];
+      return d;
+    };
+    auto sel3 = [](int i, double p0, double p1, double p2) { return i == 0 ? p0 : (i == 1 ? p1 : p2); };
+    auto incidence = [&](uint64_t r64, const FaceIn& d) {
+      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
+      const int s = (int)(lo >> 30);
+      const int pos1 = (int)(hi & 0xff), pos2 = (int)((hi >> 8) & 0xff);
+      const int pins = (int)((hi >> 16) & 7);
+      const double R0 = d.R[0], R1 = d.R[1], R2 = d.R[2], R3 = d.R[3];
       // J = [d1 d2] R, entries (c,k) -> 2c + k
       double J[4];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const double d1 = X[1][c] - X[0][c], d2 = X[2][c] - X[0][c];
+        const double d1 = d.X[1][c] - d.X[0][c], d2 = d.X[2][c] - d.X[0][c];
         J[2 * c] = d1 * R0 + d2 * R2;
         J[2 * c + 1] = d1 * R1 + d2 * R3;
       }
-      // weights W[k][q]: vertex q's coefficient on J[., k]
-      const double W[2][3] = {{-(R0 + R2), R0, R2}, {-(R1 + R3), R1, R3}};
+      // weights of corner q on J[., k]: W[k] = (-(R0k + R1k), R0k, R1k); the
+      // row's corner s and the next two, selected into registers
+      const double Wa0 = -(R0 + R2), Wa1 = -(R1 + R3);
+      double ws[2], w1[2], w2[2];
+      ws[0] = sel3(s, Wa0, R0, R2);
+      ws[1] = sel3(s, Wa1, R1, R3);
+      const int s1 = s == 2 ? 0 : s + 1, s2 = s == 0 ? 2 : s - 1;
+      w1[0] = sel3(s1, Wa0, R0, R2);
+      w1[1] = sel3(s1, Wa1, R1, R3);
+      w2[0] = sel3(s2, Wa0, R0, R2);
+      w2[1] = sel3(s2, Wa1, R1, R3);
       if constexpr (MODE == MODE_GRAD) {
-        Dg<4> j[4];
+        double val, gJ[4];
+        ok &= dirichlet_closed<false>(J, d.area, val, gJ, nullptr);
+        if (s == 0) eacc += val;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          j[q].v = J[q];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) j[q].g[b] = q == b ? 1.0 : 0.0;
-        }
-        auto det = positive_guard(j[0] * j[3] - j[1] * j[2]);
-        auto fro = j[0] * j[0] + 0.0;
-        fro = j[1] * j[1] + fro;
-        fro = j[2] * j[2] + fro;
-        fro = j[3] * j[3] + fro;
-        auto E = (fro + fro / (det * det)) * area;
-        ok &= isfinite(E.v + E.g[0] + E.g[1] + E.g[2] + E.g[3]);
-        if (s == 0) eacc += E.v;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) vec[c] += W[0][s] * E.g[2 * c] + W[1][s] * E.g[2 * c + 1];
-        return;
+        for (int c = 0; c < 2; ++c) vec[c] += ws[0] * gJ[2 * c] + ws[1] * gJ[2 * c + 1];
       } else {
-        const auto E = dirichlet_J(J, area);
-        bool fin = isfinite(E.v);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) fin &= isfinite(E.g[i]);
-#pragma unroll
-        for (int i = 0; i < 10; ++i) fin &= isfinite(E.h[i]);
+        struct {
+          double v, g[4], h[10];
+        } E;
+        bool fin = dirichlet_closed<true>(J, d.area, E.v, E.g, E.h);
         if constexpr (PSD) fin &= pins == 0;  // the reference clamps the pinned-masked block: exact path
         ok &= fin;
         if (MODE == MODE_HESS && s == 0) eacc += E.v;
         if constexpr (MODE == MODE_HESS) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) vec[c] += W[0][s] * E.g[2 * c] + W[1][s] * E.g[2 * c + 1];
+          for (int c = 0; c < 2; ++c) vec[c] += ws[0] * E.g[2 * c] + ws[1] * E.g[2 * c + 1];
         }
-        // block(s, t)[c][c'] of the (possibly clamped) 6x6 Hessian
-        double P[4][4];  // PSD: clamped M; otherwise H_J (full 4x4)
-        double Lw[2][2];
+        // G[(c,k),(c2,b)]: the 4x4 matrix whose (s,t) block contraction gives the
+        // 6x6 Hessian block: unclamped G = H_J with weights W; clamped G = P_f(M)
+        // with weights Q_W (orthonormal basis of 1-perp) plus the floor on 1 1^T / 3
+        double G[4][4];
+        double as[2], a1[2], a2[2];
         if constexpr (PSD) {
-          // Q_W columns u1 = (1,-1,0)/sqrt2, u2 = (1,1,-2)/sqrt6; L_W = W Q_W
-          const double Q[3][2] = {{INV_SQRT2, INV_SQRT6}, {-INV_SQRT2, INV_SQRT6}, {0.0, -2.0 * INV_SQRT6}};
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int b = 0; b < 2; ++b) Lw[k][b] = W[k][0] * Q[0][b] + W[k][1] * Q[1][b] + W[k][2] * Q[2][b];
+          // Q_W rows (corners): (1/sqrt2, 1/sqrt6), (-1/sqrt2, 1/sqrt6), (0, -2/sqrt6); L_W = W Q_W
+          const double Lw00 = (Wa0 - R0) * INV_SQRT2, Lw01 = (Wa0 + R0 - 2.0 * R2) * INV_SQRT6;
+          const double Lw10 = (Wa1 - R1) * INV_SQRT2, Lw11 = (Wa1 + R1 - 2.0 * R3) * INV_SQRT6;
+          const double Lw[2][2] = {{Lw00, Lw01}, {Lw10, Lw11}};
           double M[10];
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int I = 0; I < 4; ++I)
 #pragma unroll
-            for (int aa = 0; aa < 2; ++aa)
+            for (int Jx = 0; Jx <= I; ++Jx) {
+              const int c = I >> 1, aa = I & 1, c2 = Jx >> 1, bb = Jx & 1;
+              double acc = 0.0;
 #pragma unroll
-              for (int c2 = 0; c2 < 2; ++c2)
+              for (int k = 0; k < 2; ++k)
 #pragma unroll
-                for (int bb = 0; bb < 2; ++bb) {
-                  const int I = 2 * c + aa, Jx = 2 * c2 + bb;
-                  if (Jx > I) continue;
-                  double acc = 0.0;
-#pragma unroll
-                  for (int k = 0; k < 2; ++k)
-#pragma unroll
-                    for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * E.h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
-                  M[tri(I, Jx)] = acc;
-                }
+                for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * E.h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
+              M[tri(I, Jx)] = acc;
+            }
           project_if_needed<4>(M, a.floor);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) P[i][j] = M[tri(i, j)];
-          // block(s,t)[c][c'] = sum_{a,b} Q[s][a] Q[t][b] P[(c,a),(c',b)] + f delta_cc' / 3,
-          // evaluated as 0.5 (X(s,t,c,c') + X(t,s,c',c)) so the row kernel's
-          // (r,j) and (j,r) blocks are bitwise transposes
-          auto X = [&](int s_, int t_, int c, int c2) {
-            double acc = 0.0;
-#pragma unroll
-            for (int aa = 0; aa < 2; ++aa)
-#pragma unroll
-              for (int bb = 0; bb < 2; ++bb) acc += Q[s_][aa] * Q[t_][bb] * P[2 * c + aa][2 * c2 + bb];
-            return acc;
-          };
-          auto blk = [&](int t, double* out) {
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int c2 = 0; c2 < 2; ++c2)
-                out[2 * c + c2] = 0.5 * (X(s, t, c, c2) + X(t, s, c2, c)) + (c == c2 ? a.floor * (1.0 / 3.0) : 0.0);
-          };
-          if constexpr (MODE == MODE_HESS) {
-            double b[4];
-            blk(s, b);
-            dg[0] += b[0];
-            dg[1] += b[1];
-            dg[2] += b[3];
-            if (pos1 != 255) {
-              blk((s + 1) % 3, b);
-              double* dst = hrow + pos1 * NN;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) dst[k] += b[k];
-            }
-            if (pos2 != 255) {
-              blk((s + 2) % 3, b);
-              double* dst = hrow + pos2 * NN;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) dst[k] += b[k];
-            }
-          } else {  // HVP with clamp: y_s = sum_t block(s,t) u_t
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-              double b[4];
-              blk(t, b);
-#pragma unroll
-              for (int c = 0; c < 2; ++c) vec[c] += b[2 * c] * U[t][0] + b[2 * c + 1] * U[t][1];
-            }
-          }
+            for (int j = 0; j < 4; ++j) G[i][j] = M[tri(i, j)];
+          as[0] = sel3(s, INV_SQRT2, -INV_SQRT2, 0.0);
+          as[1] = sel3(s, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
+          a1[0] = sel3(s1, INV_SQRT2, -INV_SQRT2, 0.0);
+          a1[1] = sel3(s1, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
+          a2[0] = sel3(s2, INV_SQRT2, -INV_SQRT2, 0.0);
+          a2[1] = sel3(s2, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
         } else {
-          // unclamped: block(s,t)[c][c'] = sum_{k,k'} W[k][s] W[k'][t] H_J[(c,k),(c',k')],
-          // symmetrised like the reference's 0.5 (h + h^T) (problem.py:466), which
-          // also makes the (r,j) and (j,r) blocks bitwise transposes
-          auto X = [&](int s_, int t_, int c, int c2) {
-            double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-              for (int k2 = 0; k2 < 2; ++k2) acc += W[k][s_] * W[k2][t_] * E.h[tri(2 * c + k, 2 * c2 + k2)];
-            return acc;
-          };
-          auto blk = [&](int t, double* out) {
+            for (int j = 0; j < 4; ++j) G[i][j] = E.h[tri(i, j)];
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int c2 = 0; c2 < 2; ++c2) out[2 * c + c2] = 0.5 * (X(s, t, c, c2) + X(t, s, c2, c));
-          };
-          if constexpr (MODE == MODE_HESS) {
-            double b[4];
-            blk(s, b);
-            dg[0] += b[0];
-            dg[1] += b[1];
-            dg[2] += b[3];
-            if (pos1 != 255) {
-              blk((s + 1) % 3, b);
-              double* dst = hrow + pos1 * NN;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) dst[k] += b[k];
-            }
-            if (pos2 != 255) {
-              blk((s + 2) % 3, b);
-              double* dst = hrow + pos2 * NN;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) dst[k] += b[k];
-            }
-          } else {  // HVP: y_s = B_s^T H_J (B u)
-            double bu[4];
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int k = 0; k < 2; ++k) bu[2 * c + k] = W[k][0] * U[0][c] + W[k][1] * U[1][c] + W[k][2] * U[2][c];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              double acc = 0.0;
-#pragma unroll
-              for (int k = 0; k < 2; ++k) {
-                double hb = 0.0;
-#pragma unroll
-                for (int jx = 0; jx < 4; ++jx) hb += E.h[tri(2 * c + k, jx)] * bu[jx];
-                acc += W[k][s] * hb;
-              }
-              vec[c] += acc;
-            }
+          for (int k = 0; k < 2; ++k) {
+            as[k] = ws[k];
+            a1[k] = w1[k];
+            a2[k] = w2[k];
           }
+        }
+        const double fl3 = PSD ? a.floor * (1.0 / 3.0) : 0.0;
+        // block(u,v)[c][c2] = 0.5 (X(u,v,c,c2) + X(v,u,c2,c)), X = sum_{k,k2} u[k] v[k2] G[(c,k),(c2,k2)]:
+        // the reference's symmetrisation, and the (r,j) / (j,r) blocks come out bitwise transposed
+        auto X = [&](const double* u, const double* v, int c, int c2) {
+          return u[0] * (G[2 * c][2 * c2] * v[0] + G[2 * c][2 * c2 + 1] * v[1]) +
+                 u[1] * (G[2 * c + 1][2 * c2] * v[0] + G[2 * c + 1][2 * c2 + 1] * v[1]);
+        };
+        auto blk = [&](const double* u, const double* v, bool diag, double* out) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2)
+              out[2 * c + c2] = 0.5 * (X(u, v, c, c2) + X(v, u, c2, c)) + (diag && c == c2 ? fl3 : 0.0) +
+                                (!diag && c == c2 ? fl3 : 0.0);
+        };
+        if constexpr (MODE == MODE_HESS) {
+          double b[4];
+          blk(as, as, true, b);
+          dg[0] += b[0];
+          dg[1] += b[1];
+          dg[2] += b[3];
+          if (pos1 != 255) {
+            blk(as, a1, false, b);
+            double* dst = hrow + pos1 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] += b[k];
+          }
+          if (pos2 != 255) {
+            blk(as, a2, false, b);
+            double* dst = hrow + pos2 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] += b[k];
+          }
+        } else {  // HVP: y_s = sum_t block(s,t) u_t over the face's corners (masked)
+          double b[4];
+          const double us_[2] = {sel3(s, d.U[0][0], d.U[1][0], d.U[2][0]), sel3(s, d.U[0][1], d.U[1][1], d.U[2][1])};
+          const double u1_[2] = {sel3(s1, d.U[0][0], d.U[1][0], d.U[2][0]), sel3(s1, d.U[0][1], d.U[1][1], d.U[2][1])};
+          const double u2_[2] = {sel3(s2, d.U[0][0], d.U[1][0], d.U[2][0]), sel3(s2, d.U[0][1], d.U[1][1], d.U[2][1])};
+          blk(as, as, true, b);
+          vec[0] += b[0] * us_[0] + b[1] * us_[1];
+          vec[1] += b[2] * us_[0] + b[3] * us_[1];
+          blk(as, a1, false, b);
+          vec[0] += b[0] * u1_[0] + b[1] * u1_[1];
+          vec[1] += b[2] * u1_[0] + b[3] * u1_[1];
+          blk(as, a2, false, b);
+          vec[0] += b[0] * u2_[0] + b[1] * u2_[1];
+          vec[1] += b[2] * u2_[0] + b[3] * u2_[1];
         }
       }
     };
+    // face corner ids of the ELL incidences (one batched level), then the
+    // corners' data streamed one incidence ahead of the compute
     const int ne = cnt < KF ? cnt : KF;
+    int fv[KF][3];
 #pragma unroll
-    for (int j = 0; j < KF; ++j)
-      if (j < ne) incidence(rc[j]);
-    for (int k = KF; k < cnt; ++k) incidence(a.rrec[a.rinc_off[row] + k]);
+    for (int j = 0; j < KF; ++j) {
+      const int64_t f = (uint32_t)rc[j] & 0x3fffffffu;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) fv[j][q] = j < ne ? a.faces[3 * f + q] : 0;
+    }
+    FaceIn cur;
+    if (ne > 0) cur = load_face(rc[0], fv[0]);
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      if (j < ne) {
+        FaceIn nxt;
+        if (j + 1 < ne) nxt = load_face(rc[j + 1], fv[j + 1]);
+        incidence(rc[j], cur);
+        cur = nxt;
+      }
+    }
+    for (int k = KF; k < cnt; ++k) {
+      const uint64_t r64 = a.rrec[a.rinc_off[row] + k];
+      const int64_t f = (uint32_t)r64 & 0x3fffffffu;
+      const int v3[3] = {a.faces[3 * f], a.faces[3 * f + 1], a.faces[3 * f + 2]};
+      incidence(r64, load_face(r64, v3));
+    }
     double* vout = MODE == MODE_HVP ? a.y : a.grad;
 #pragma unroll
     for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
