@@ -150,6 +150,12 @@ MG_API int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int us
  * problem.py:100-106). */
 MG_API int mg_bsr_matvec(const mg_problem* prob, const double* hess_d, const double* v_d, double* y_d,
                   void* stream);
+/* Block-Jacobi preconditioner of the assembled Hessian: inv_d (V, n, n) =
+ * inverse of each row's diagonal block, identity where there is none or it is
+ * singular (BlockSparseMatrix.diagonal_block_inverses, problem.py:118-131). */
+MG_API int mg_bsr_block_jacobi(const mg_problem* prob, const double* hess_d, double* inv_d, void* stream);
+/* y_v = inv_v r_v per vertex (the preconditioner apply, solvers.py:178-186). */
+MG_API int mg_block_apply(const mg_problem* prob, const double* inv_d, const double* r_d, double* y_d, void* stream);
 MG_API int mg_problem_destroy(mg_problem* prob);
 
 /* Introspection for benchmarks/tests: number of kernel launches issued by the

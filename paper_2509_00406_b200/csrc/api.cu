@@ -375,6 +375,17 @@ int mg_bsr_matvec(const mg_problem* prob, const double* hess_d, const double* v_
   return guard([&] { launch_bsr_matvec(prob->p, hess_d, v_d, y_d, S(stream)); });
 }
 
+int mg_bsr_block_jacobi(const mg_problem* prob, const double* hess_d, double* inv_d, void* stream) {
+  if (!prob || !hess_d || !inv_d) return fail(MG_ERR_VALUE, "NULL argument");
+  if (!prob->p.pattern_ready) return fail(MG_ERR_STATE, "sparsity pattern not computed");
+  return guard([&] { launch_block_jacobi(prob->p, hess_d, inv_d, S(stream)); });
+}
+
+int mg_block_apply(const mg_problem* prob, const double* inv_d, const double* r_d, double* y_d, void* stream) {
+  if (!prob || !inv_d || !r_d || !y_d) return fail(MG_ERR_VALUE, "NULL argument");
+  return guard([&] { launch_block_apply(prob->p, inv_d, r_d, y_d, S(stream)); });
+}
+
 int mg_problem_destroy(mg_problem* prob) {
   if (prob) {
     for (auto& pr : prob->p.ev_pairs) {

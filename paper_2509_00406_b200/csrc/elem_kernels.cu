@@ -273,7 +273,94 @@ __global__ void k_bsr_matvec(const int64_t* ro, const int32_t* col, const double
   for (int r = 0; r < N; ++r) y[i * N + r] = acc[r];
 }
 
+// Block-Jacobi preconditioner (BlockSparseMatrix.diagonal_block_inverses,
+// problem.py:118-131; solvers.py:178-186): the inverse of every row's
+// diagonal block, identity where a row has none or the block is singular.
+template <int N>
+__global__ void k_block_jacobi_inv(const int64_t* ro, const int32_t* col, const double* H, int64_t V, double* inv) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  double* out = inv + v * N * N;
+  int64_t lo = ro[v], hi = ro[v + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (col[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  bool ok = lo < ro[v + 1] && col[lo] == v;
+  double a[N * N];
+  if (ok)
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) a[i] = H[lo * N * N + i];
+  double r[N * N];
+  if (ok) {
+    if constexpr (N == 1) {
+      ok = a[0] != 0.0;
+      r[0] = 1.0 / a[0];
+    } else if constexpr (N == 2) {
+      const double det = a[0] * a[3] - a[1] * a[2];
+      ok = det != 0.0;
+      const double id = 1.0 / det;
+      r[0] = a[3] * id; r[1] = -a[1] * id; r[2] = -a[2] * id; r[3] = a[0] * id;
+    } else {
+      const double c00 = a[4] * a[8] - a[5] * a[7], c01 = a[5] * a[6] - a[3] * a[8], c02 = a[3] * a[7] - a[4] * a[6];
+      const double det = a[0] * c00 + a[1] * c01 + a[2] * c02;
+      ok = det != 0.0;
+      const double id = 1.0 / det;
+      r[0] = c00 * id; r[1] = (a[2] * a[7] - a[1] * a[8]) * id; r[2] = (a[1] * a[5] - a[2] * a[4]) * id;
+      r[3] = c01 * id; r[4] = (a[0] * a[8] - a[2] * a[6]) * id; r[5] = (a[2] * a[3] - a[0] * a[5]) * id;
+      r[6] = c02 * id; r[7] = (a[1] * a[6] - a[0] * a[7]) * id; r[8] = (a[0] * a[4] - a[1] * a[3]) * id;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) out[i * N + j] = ok ? r[i * N + j] : (i == j ? 1.0 : 0.0);
+}
+
+template <int N>
+__global__ void k_block_apply(const double* inv, const double* r, double* y, int64_t V) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const double* m = inv + v * N * N;
+  double rv[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) rv[j] = r[v * N + j];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc += m[i * N + j] * rv[j];
+    y[v * N + i] = acc;
+  }
+}
+
 }  // namespace
+
+void launch_block_jacobi(const Problem& p, const double* H, double* inv, cudaStream_t s) {
+  const int64_t V = p.mesh->V;
+  const unsigned grid = (unsigned)((V + 255) / 256);
+  if (!V) return;
+  switch (p.n) {
+    case 1: k_block_jacobi_inv<1><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, inv); break;
+    case 2: k_block_jacobi_inv<2><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, inv); break;
+    case 3: k_block_jacobi_inv<3><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, inv); break;
+    default: throw Error(MG_ERR_UNSUPPORTED, "block Jacobi supports block dims 1..3");
+  }
+  MG_LAUNCH_CHECK();
+}
+
+void launch_block_apply(const Problem& p, const double* inv, const double* r, double* y, cudaStream_t s) {
+  const int64_t V = p.mesh->V;
+  const unsigned grid = (unsigned)((V + 255) / 256);
+  if (!V) return;
+  switch (p.n) {
+    case 1: k_block_apply<1><<<grid, 256, 0, s>>>(inv, r, y, V); break;
+    case 2: k_block_apply<2><<<grid, 256, 0, s>>>(inv, r, y, V); break;
+    case 3: k_block_apply<3><<<grid, 256, 0, s>>>(inv, r, y, V); break;
+    default: throw Error(MG_ERR_UNSUPPORTED, "block Jacobi supports block dims 1..3");
+  }
+  MG_LAUNCH_CHECK();
+}
 
 int64_t elem_partials_needed(const Term& t) { return (t.M + TPB - 1) / TPB; }
 

@@ -216,5 +216,7 @@ bool patch_supported(const Problem& p);
 // fixed-order reduction of energy partials -> out[0]
 void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag = nullptr);
 void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s);
+void launch_block_jacobi(const Problem& p, const double* H, double* inv, cudaStream_t s);
+void launch_block_apply(const Problem& p, const double* inv, const double* r, double* y, cudaStream_t s);
 
 }  // namespace mg

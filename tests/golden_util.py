@@ -12,7 +12,12 @@ FLOOR = 1e-9
 
 
 def cases():
-    return sorted(p.stem for p in GOLDEN.glob("*.npz"))
+    """Problem fixtures (solver trajectories, solver_*.npz, are separate)."""
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith("solver_"))
+
+
+def solver_cases():
+    return sorted(p.stem for p in GOLDEN.glob("solver_*.npz"))
 
 
 def load(name):
