@@ -376,7 +376,7 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
 // buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
 // for more resident warps
 template <int MODE, bool PSD> struct FastCfg { static constexpr int MAXI = EV_ELL_K, MINB = 1; };
-template <> struct FastCfg<MODE_HVP, false> { static constexpr int MAXI = 4, MINB = 12; };
+template <> struct FastCfg<MODE_HVP, false> { static constexpr int MAXI = 4, MINB = 10; };
 template <> struct FastCfg<MODE_HVP, true> { static constexpr int MAXI = 4, MINB = 8; };
 template <> struct FastCfg<MODE_GRAD, false> { static constexpr int MAXI = 4, MINB = 12; };
 
@@ -404,9 +404,9 @@ __global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(cons
       ro = a.prow_ro[row];
       ho = a.hoff[row];
     }
-    uint64_t rc[MAXI];
+    uint64_t rc[EV_ELL_K];
 #pragma unroll
-    for (int j = 0; j < MAXI; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+    for (int j = 0; j < EV_ELL_K; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
     const bool fr = !((meta >> 8) & 1);
     const int dp = (int)(meta >> 16) & 0xff;
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
@@ -418,10 +418,10 @@ __global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(cons
       if constexpr (MODE == MODE_HVP) us[c] = fr ? a.w[(int64_t)g * N + c] : 0.0;
       else us[c] = 0.0;
     }
-    // level 3: neighbour x (w) and the edge attribute
-    double xo[MAXI][N], uo[MAXI][N], a0[MAXI];
-#pragma unroll
-    for (int j = 0; j < MAXI; ++j) {
+    // level 3: neighbour x (w) and the edge attribute, kept MAXI incidences
+    // ahead of the compute (a rolling window over the ELL slots)
+    double xo[EV_ELL_K][N], uo[EV_ELL_K][N], a0[EV_ELL_K];
+    auto issue = [&](int j) {
       const uint32_t hi = (uint32_t)(rc[j] >> 32);
       const int64_t o = hi & 0x7fffffffu;
       const bool fo = !(hi >> 31);
@@ -432,7 +432,9 @@ __global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(cons
         else uo[j][c] = 0.0;
       }
       a0[j] = (j < cnt && a.ev_a0) ? a.ev_a0[(uint32_t)rc[j] & 0x7fffffffu] : 0.0;
-    }
+    };
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j) issue(j);
     double vec[N], dg[T];
 #pragma unroll
     for (int i = 0; i < N; ++i) vec[i] = 0.0;
@@ -551,10 +553,12 @@ __global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(cons
       }
     };
 #pragma unroll
-    for (int j = 0; j < MAXI; ++j)
+    for (int j = 0; j < EV_ELL_K; ++j) {
+      if (j + MAXI < EV_ELL_K) issue(j + MAXI);
       if (j < cnt) incidence(rc[j], xo[j], uo[j], a0[j]);
-    for (int k = MAXI; k < cnt; ++k) {  // the rest: ELL slots, then the CSR tail
-      const uint64_t r64 = k < EV_ELL_K ? a.ell[(int64_t)k * a.V + row] : a.rrec[a.rinc_off[row] + k];
+    }
+    for (int k = EV_ELL_K; k < cnt; ++k) {  // high-valence rows: the CSR tail
+      const uint64_t r64 = a.rrec[a.rinc_off[row] + k];
       const int64_t o = (uint32_t)(r64 >> 32) & 0x7fffffffu;
       const bool fo = !(r64 >> 63);
       double x1[N], u1[N];

@@ -230,22 +230,21 @@ void launch_t(int n, const Term& t, Mode mode, bool psd, const ElemArgs& a, cuda
   }
 }
 
-// Fixed-order sum of the energy partials: thread t owns the contiguous chunk
-// [t*c, (t+1)*c) and sums it with 4 independent accumulators (memory-level
-// parallelism), then the block tree combines the threads in a fixed order.
+// Fixed-order sum of the energy partials: thread t sums the strided set
+// t, t+B, t+2B, ... (coalesced) into 4 independent accumulators (memory-level
+// parallelism), combined in a fixed order; then the block tree.
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int64_t n, double* out,
                                                  int* clear_flag) {
-  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t b = threadIdx.x * chunk, e = b + chunk < n ? b + chunk : n;
+  const int64_t B = blockDim.x;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int64_t i = b;
-  for (; i + 3 < e; i += 4) {
+  int64_t i = threadIdx.x;
+  for (; i + 3 * B < n; i += 4 * B) {
     a0 += partials[i];
-    a1 += partials[i + 1];
-    a2 += partials[i + 2];
-    a3 += partials[i + 3];
+    a1 += partials[i + B];
+    a2 += partials[i + 2 * B];
+    a3 += partials[i + 3 * B];
   }
-  for (; i < e; ++i) a0 += partials[i];
+  for (; i < n; i += B) a0 += partials[i];
   const double s = block_sum((a0 + a1) + (a2 + a3));
   if (threadIdx.x == 0) {
     out[0] = s;
