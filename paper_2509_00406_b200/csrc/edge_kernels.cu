@@ -375,7 +375,10 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
 // occupancy target: the Hessian kernel is bounded by its shared-memory row
 // buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
 // for more resident warps
-template <int MODE, bool PSD> struct FastCfg { static constexpr int MAXI = EV_ELL_K, MINB = 1; };
+#ifndef EV_HESS_MINB
+#define EV_HESS_MINB 1
+#endif
+template <int MODE, bool PSD> struct FastCfg { static constexpr int MAXI = EV_ELL_K, MINB = EV_HESS_MINB; };
 template <> struct FastCfg<MODE_HVP, false> { static constexpr int MAXI = 4, MINB = 10; };
 template <> struct FastCfg<MODE_HVP, true> { static constexpr int MAXI = 4, MINB = 8; };
 template <> struct FastCfg<MODE_GRAD, false> { static constexpr int MAXI = 4, MINB = 12; };
@@ -538,16 +541,29 @@ __global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(cons
       }
       if constexpr (MODE == MODE_HESS) {
 #pragma unroll
+        // t = cd d d^T (6 unique products) feeds both the diagonal sum and the
+        // edge's off-diagonal block -t + (dl - ci) I
+        double cdd[N], t[T];
+#pragma unroll
+        for (int i = 0; i < N; ++i) cdd[i] = cd_s * d[i];
+#pragma unroll
         for (int i = 0; i < N; ++i)
 #pragma unroll
-          for (int c = 0; c <= i; ++c) dg[tri(i, c)] += cd_s * d[i] * d[c] + (i == c ? ci_s + dl : 0.0);
+          for (int c = 0; c <= i; ++c) t[tri(i, c)] = cdd[i] * d[c];
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c <= i; ++c) dg[tri(i, c)] += t[tri(i, c)] + (i == c ? ci_s + dl : 0.0);
         if (fr && fo) {
           if (dp != 255 && pos == dp) ++pos;  // leave the diagonal's slot
-          double* dst = hrow + pos * NN;
+          double blk[NN];
 #pragma unroll
           for (int i = 0; i < N; ++i)
 #pragma unroll
-            for (int c = 0; c < N; ++c) dst[i * N + c] = -(cd_s * d[i] * d[c]) + (i == c ? dl - ci_s : 0.0);
+            for (int c = 0; c < N; ++c) blk[i * N + c] = -t[tri(i, c)] + (i == c ? dl - ci_s : 0.0);
+          double* dst = hrow + pos * NN;
+#pragma unroll
+          for (int k = 0; k < NN; ++k) dst[k] = blk[k];
           ++pos;
         }
       }

@@ -152,6 +152,21 @@ MG_DI void extract_psd(double* H, double floor) {
 #pragma unroll
   for (int i = 0; i < TriN<K>::value; ++i) H[i] = 0.5 * (H[i] + H[i]);
   if (!all_finite<K>(H)) return;
+  {
+    // diagonal block (vertex terms such as inertia m I, or a structural-zero
+    // Hessian): the eigenvalues are the diagonal entries on the coordinate
+    // axes, so the clamp is elementwise and exact
+    bool diag = true;
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < i; ++j) diag &= H[tri(i, j)] == 0.0;
+    if (diag) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) H[tri(i, i)] = H[tri(i, i)] > floor ? H[tri(i, i)] : floor;
+      return;
+    }
+  }
   if constexpr (P == 2) {
     // bitwise two-point structure test
     bool two = true;
