@@ -174,3 +174,60 @@ def test_fast_paths_fall_back_only_on_nonfinite(name):
         assert runs == 0, f"{name}: {runs} exact re-runs on finite states"
     elif name in ("spring_nan", "dirichlet_flip"):
         assert runs > 0
+
+
+@pytest.mark.parametrize("name", ["cloth64", "spring_grid16", "smooth_ico2", "dirichlet_ico2", "sphere_ico2"])
+def test_deterministic_bitwise_and_symmetric(name):
+    """Deterministic mode (the reference default, problem.py:16-21) is bitwise
+    reproducible run to run, and the assembled Hessian is bitwise symmetric
+    (the reference guarantees both, test_problem.py:148-155, 360-369)."""
+    d = load(name)
+    p = engine_problem(d, "deterministic")
+    x = d["s0_x"]
+    p.x = x
+    runs = []
+    for _ in range(3):
+        e = p.eval_terms(psd_floor=FLOOR if p.with_hessian else None)
+        runs.append((e, p.grad.copy(), p.hess.values.copy() if p.with_hessian else None, p.hvp(x, d["s0_v0"])))
+    for e, g, h, y in runs[1:]:
+        assert e == runs[0][0]
+        assert np.array_equal(g, runs[0][1])
+        assert np.array_equal(y, runs[0][3])
+        if h is not None:
+            assert np.array_equal(h, runs[0][2])
+    if p.with_hessian:
+        dense = p.hess.to_dense()
+        assert np.array_equal(dense, dense.T)
+
+
+def test_cloth_large_matches_oracle_at_scale_properties():
+    """Full-size properties on a 512^2 cloth (beyond what the CPU oracle runs in
+    seconds per call): HVP equals the assembled-Hessian matvec, HVP is linear,
+    the energy probe equals eval_terms' energy, and the radial fast path
+    carries the whole call (no exact re-run)."""
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import ClothConfig, cloth_problem, default_pins, lumped_masses
+
+    n = 512
+    pos, faces = mg.grid_arrays(n, 1.0 / (n - 1))
+    mesh = mg.Mesh(pos, faces)
+    rng = np.random.default_rng(3)
+    target = pos + 0.01 / (n - 1) * rng.normal(size=pos.shape)
+    x = (pos + 0.01 / (n - 1) * rng.normal(size=pos.shape)).ravel()
+    cfg = ClothConfig(grid_n=n, spacing=1.0 / (n - 1))
+    p = cloth_problem(cfg, mesh, target, masses=lumped_masses(mesh, 1.0), pinned=default_pins(n))
+    p.x = x
+    e = p.eval_terms()
+    v = torch.from_numpy(rng.normal(size=x.size)).cuda()
+    w = torch.from_numpy(rng.normal(size=x.size)).cuda()
+    hv = p.hvp(p.x_device, v)
+    mv = p.hess.matvec(v)
+    scale = float(hv.abs().max())
+    assert float((hv - mv).abs().max()) <= 1e-10 * scale
+    lin = p.hvp(p.x_device, 2.0 * v - 3.0 * w)
+    ref = 2.0 * hv - 3.0 * p.hvp(p.x_device, w)
+    assert float((lin - ref).abs().max()) <= 1e-10 * float(ref.abs().max())
+    assert abs(p.eval_energy_only(p.x_device) - e) <= 1e-12 * abs(e)
+    assert p.exact_runs() == 0
