@@ -378,10 +378,23 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
 #ifndef EV_HESS_MINB
 #define EV_HESS_MINB 1
 #endif
-template <int MODE, bool PSD> struct FastCfg { static constexpr int MAXI = EV_ELL_K, MINB = EV_HESS_MINB; };
-template <> struct FastCfg<MODE_HVP, false> { static constexpr int MAXI = 4, MINB = 10; };
-template <> struct FastCfg<MODE_HVP, true> { static constexpr int MAXI = 4, MINB = 8; };
-template <> struct FastCfg<MODE_GRAD, false> { static constexpr int MAXI = 4, MINB = 12; };
+#ifndef EV_FLAT_BLOCK
+#define EV_FLAT_BLOCK 64
+#endif
+// MAXI: incidences in flight; BLOCK: threads per CTA (the Hessian kernel's CTA
+// is its row-buffer group, EV_ROW_BLOCK); MINB: CTAs per SM to fit
+template <int MODE, bool PSD> struct FastCfg {
+  static constexpr int MAXI = EV_ELL_K, BLOCK = EV_ROW_BLOCK, MINB = EV_HESS_MINB;
+};
+template <> struct FastCfg<MODE_HVP, false> {
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 640 / EV_FLAT_BLOCK;
+};
+template <> struct FastCfg<MODE_HVP, true> {
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 512 / EV_FLAT_BLOCK;
+};
+template <> struct FastCfg<MODE_GRAD, false> {
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
+};
 
 // Radial fast kernel: one thread per owned row, d = x_row - x_other (radial
 // terms are even in d, so no orientation bookkeeping). A row's first MAXI
@@ -389,9 +402,11 @@ template <> struct FastCfg<MODE_GRAD, false> { static constexpr int MAXI = 4, MI
 // edge attributes) so their latencies overlap; EVT fixes the single EV term's
 // type at compile time (0: any mix, dispatched per incidence).
 template <int N, int MODE, bool PSD, int EVT>
-__global__ void __launch_bounds__(PT, FastCfg<MODE, PSD>::MINB) k_rows_fast(const __grid_constant__ EvArgs a) {
+__global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>::MINB)
+    k_rows_fast(const __grid_constant__ EvArgs a) {
   constexpr int T = TriN<N>::value, NN = N * N;
   constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
+  constexpr int PT = FastCfg<MODE, PSD>::BLOCK;
   extern __shared__ __align__(16) double hbuf[];
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
   double eacc = 0.0;
@@ -798,7 +813,8 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
     MG_CUDA(cudaFuncSetAttribute(exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
   timing_begin(p, st);
-  fast<<<(unsigned)nb, PT, sm, st>>>(a);
+  constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
+  fast<<<(unsigned)((a.V + FB - 1) / FB), FB, sm, st>>>(a);
   MG_LAUNCH_CHECK();
   timing_end(p, st);
   // exact re-run only when a lane was non-finite (reads the flag and exits otherwise)
