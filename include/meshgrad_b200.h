@@ -72,7 +72,8 @@ enum mg_term_type {
   MG_TERM_GRAVITY = 3,
   MG_TERM_EDGE_LENGTH = 4,
   MG_TERM_SYM_DIRICHLET = 5,
-  MG_TERM_SPHERE = 6
+  MG_TERM_SPHERE = 6,
+  MG_TERM_JIT = 100  /* traced user callback (mg_problem_add_jit_term) */
 };
 
 typedef struct mg_mesh mg_mesh;
@@ -123,6 +124,15 @@ MG_API int mg_problem_create(mg_mesh* mesh, int var_dim, int with_hessian, const
 MG_API int mg_problem_add_term(mg_problem* prob, int term_type, int op, const double* params,
                         int num_params, const double* const* attrs_d, int num_attrs,
                         int* term_id);
+/* Register a traced user callback (the reference's general callback protocol,
+ * problem.py:8-14 / 301-310): `image` is a cubin built by
+ * paper_2509_00406_b200/jit.py from csrc/jit_kernel.cuh for this var_dim,
+ * exporting mg_jit_{energy,grad,hess,hess_psd,hvp,hvp_psd}; attrs_d are its
+ * per-element attribute streams (device fp64, caller-owned, at most 64). Problems with a
+ * traced term assemble element-parallel with fp64 atomics. */
+MG_API int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* image,
+                                   const double* const* attrs_d, int num_attrs, int* term_id);
+MG_API int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d);
 /* Rebind one attribute pointer of a registered term (closure arrays that the
  * reference rewrites in place between calls, apps/cloth.py:128, sphere.py:121-127). */
 MG_API int mg_problem_set_attr(mg_problem* prob, int term_id, int slot, const double* attr_d);

@@ -22,6 +22,7 @@ MG_TERM_GRAVITY = 3
 MG_TERM_EDGE_LENGTH = 4
 MG_TERM_SYM_DIRICHLET = 5
 MG_TERM_SPHERE = 6
+MG_TERM_JIT = 100
 
 MG_ERR_VALUE = 1
 MG_ERR_MESH = 2
@@ -47,6 +48,8 @@ SIGNATURES = [
     ("mg_problem_create", _INT, [_P, _INT, _INT, _P, _INT, ctypes.POINTER(_P)]),
     ("mg_problem_add_term", _INT, [_P, _INT, _INT, ctypes.POINTER(_DBL), _INT, ctypes.POINTER(_P), _INT,
                                    ctypes.POINTER(_INT)]),
+    ("mg_problem_add_jit_term", _INT, [_P, _INT, _INT, _P, ctypes.POINTER(_P), _INT, ctypes.POINTER(_INT)]),
+    ("mg_problem_set_jit_attr", _INT, [_P, _INT, _INT, _P]),
     ("mg_problem_set_attr", _INT, [_P, _INT, _INT, _P]),
     ("mg_precompute_sparsity", _INT, [_P, _I64P, _P]),
     ("mg_copy_pattern", _INT, [_P, _P, _P, _P]),

@@ -2,6 +2,7 @@
 #include <cstring>
 #include <string>
 
+#include "jit_abi.h"
 #include "mg_internal.cuh"
 
 using namespace mg;
@@ -250,6 +251,40 @@ int mg_problem_add_term(mg_problem* prob, int term_type, int op, const double* p
   return MG_OK;
 }
 
+int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* image, const double* const* attrs_d,
+                            int num_attrs, int* term_id) {
+  if (!prob || !image) return fail(MG_ERR_VALUE, "problem/image is NULL");
+  if (op != MG_OP_FV && op != MG_OP_EV && op != MG_OP_V)
+    return fail(MG_ERR_UNSUPPORTED, "traced terms support the FV, EV and V ops");
+  if (var_dim != prob->p.n) return fail(MG_ERR_VALUE, "traced module was generated for another var_dim");
+  if (num_attrs < 0 || num_attrs > JIT_MAX_ATTRS) return fail(MG_ERR_VALUE, "at most 64 attribute streams");
+  return guard([&] {
+    Term t;
+    std::memset(&t.dev, 0, sizeof(t.dev));
+    t.dev.type = MG_TERM_JIT;
+    t.dev.op = op;
+    t.dev.P = natural_P(op);
+    t.M = op_count(prob->p.mesh[0], op);
+    t.jit = true;
+    for (int i = 0; i < num_attrs; ++i) t.jit_attrs.push_back(attrs_d[i]);
+    jit_load(t, image);
+    prob->p.terms.push_back(std::move(t));
+    prob->p.pattern_ready = false;
+    prob->p.layout_ready = false;
+    if (term_id) *term_id = (int)prob->p.terms.size() - 1;
+  });
+}
+
+int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  if (term_id < 0 || term_id >= (int)prob->p.terms.size() || !prob->p.terms[term_id].jit)
+    return fail(MG_ERR_VALUE, "not a traced term");
+  auto& at = prob->p.terms[term_id].jit_attrs;
+  if (slot < 0 || slot >= (int)at.size()) return fail(MG_ERR_VALUE, "bad attribute slot");
+  at[slot] = attr_d;
+  return MG_OK;
+}
+
 int mg_problem_set_attr(mg_problem* prob, int term_id, int slot, const double* attr_d) {
   if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
   if (term_id < 0 || term_id >= (int)prob->p.terms.size()) return fail(MG_ERR_VALUE, "bad term id");
@@ -388,6 +423,8 @@ int mg_block_apply(const mg_problem* prob, const double* inv_d, const double* r_
 
 int mg_problem_destroy(mg_problem* prob) {
   if (prob) {
+    for (auto& t : prob->p.terms)
+      if (t.jit) jit_unload(t);
     for (auto& pr : prob->p.ev_pairs) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);

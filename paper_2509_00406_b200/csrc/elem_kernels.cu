@@ -366,6 +366,10 @@ int64_t elem_partials_needed(const Term& t) { return (t.M + TPB - 1) / TPB; }
 int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c,
                     int64_t partial_offset) {
   if (t.M == 0) return 0;
+  if (t.jit) {
+    jit_launch(p, t, mode, c, partial_offset);
+    return mode == MODE_HVP ? 0 : elem_partials_needed(t);
+  }
   ElemArgs a;
   a.x = c.x;
   a.w = c.w;

@@ -107,6 +107,12 @@ struct Term {
   TermDev dev;
   int64_t M = 0;               // elements
   DBuf<int32_t> bids;          // (M,P,P) Hessian block ids, -1 = pinned pair
+  // traced (JIT) term: driver-API module with the six mode kernels and its
+  // per-element attribute streams (caller-owned device arrays)
+  bool jit = false;
+  void* jit_module = nullptr;
+  void* jit_fn[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<const double*> jit_attrs;
 };
 
 constexpr int EV_ROW_BLOCK = 64;  // rows (threads) per CTA of the edge row kernel
@@ -185,6 +191,11 @@ void mesh_patches(Mesh& m, cudaStream_t s);
 void mesh_set_owned(Mesh& m, const uint8_t* owned_d, cudaStream_t s);
 int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s);
 
+// jit_host.cu (traced terms through the driver API)
+struct LaunchCtx;
+void jit_load(Term& t, const void* image);
+void jit_unload(Term& t);
+
 // elem_kernels.cu (element-parallel, atomic accumulation)
 enum Mode { MODE_ENERGY = 0, MODE_GRAD = 1, MODE_HESS = 2, MODE_HVP = 3 };
 struct LaunchCtx {
@@ -202,6 +213,7 @@ struct LaunchCtx {
 // Launch one term element-parallel; returns number of energy partials written.
 int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c,
                     int64_t partial_offset);
+void jit_launch(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 int64_t elem_partials_needed(const Term& t);
 // patch_kernels.cu (deterministic row-owner assembly)
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);

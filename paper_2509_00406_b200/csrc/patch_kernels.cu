@@ -351,7 +351,7 @@ bool patch_supported(const Problem& p) {
   if (p.terms.empty() || p.terms.size() > MAXT) return false;
   if (p.n != 2 && p.n != 3) return false;
   for (auto& t : p.terms)
-    if (t.dev.op == MG_OP_VV) return false;
+    if (t.dev.op == MG_OP_VV || t.jit) return false;
   return p.mesh->patches.num > 0;
 }
 

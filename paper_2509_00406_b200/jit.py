@@ -1,0 +1,264 @@
+"""Tracer + CUDA code generation for arbitrary energy callbacks.
+
+The reference's programming model is a Python callback `fn(handle, nbrs, x)`
+over batched `ActiveVec` / `SmallMatrix` values (problem.py:8-14, 440-452).
+Here such a callback is run ONCE with symbolic scalars:
+
+  * `x[nbr]` yields an ActiveVec of input variables (slot q, component c);
+  * `handle.index` is the real array of element ids, so closure gathers like
+    `rest2[edge.index]` evaluate to (M,) / (M, k) numpy arrays; every such
+    array meeting a symbolic scalar becomes a per-element *attribute stream*
+    (uploaded to the device, read by element id);
+  * scalars and 0-d arrays are constants (emitted as exact hex literals);
+  * `+ - * /`, unary `-`, integer `**`, `abs` and the module functions
+    `sqrt log exp sin cos abs_ positive_guard` are recorded in call order.
+
+The recorded SSA is emitted as a C++ functor over the engine's dual numbers
+(csrc/dual.cuh) — the same operation order as the callback, so each mode
+rounds like the reference's ActiveScalar — and compiled with nvcc for sm_100a
+into a cubin (cached by source hash), which the library loads through the
+driver API (`mg_problem_add_jit_term`). The callback must be a pure function
+of its inputs (the reference asks the same, problem.py:8-14) and must not
+branch on input values.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+CSRC = Path(__file__).resolve().parent / "csrc"
+CACHE = Path(os.environ.get("MG_JIT_CACHE", str(Path(__file__).resolve().parent / "jit_cache")))
+
+__all__ = ["TracedTerm", "trace_callback", "compile_term"]
+
+
+class _Graph:
+    def __init__(self, num_elements):
+        self.M = num_elements
+        self.lines = []
+        self.attrs = []  # (M,) float64 arrays
+        self._attr_ids = {}
+        self._pins = []  # keep operand objects alive so their ids stay unique
+        self.count = 0
+
+    def new(self, expr):
+        name = f"t{self.count}"
+        self.count += 1
+        self.lines.append(f"auto {name} = {expr};")
+        return Sym(self, name)
+
+    def operand(self, v):
+        """C++ expression of an operand (symbol, constant or attribute stream)."""
+        if isinstance(v, Sym):
+            if v.g is not self:
+                raise ValueError("symbols from different traces")
+            return v.name
+        a = np.asarray(v)
+        if a.dtype == bool:
+            a = a.astype(np.float64)
+        if a.ndim == 0 or a.size == 1:
+            return _lit(float(a.reshape(-1)[0]))
+        if a.ndim == 1 and a.shape[0] == self.M:
+            # the same memory (also different views of it) is one stream
+            key = None
+            if isinstance(v, np.ndarray):
+                key = (v.__array_interface__["data"][0], v.strides, v.shape, v.dtype.str)
+            if key is not None and key in self._attr_ids:
+                k = self._attr_ids[key]
+            else:
+                k = len(self.attrs)
+                self.attrs.append(np.ascontiguousarray(a, dtype=np.float64))
+                if key is not None:
+                    self._attr_ids[key] = k
+                    self._pins.append(v)
+            return f"A[{k}][e]"
+        raise ValueError(f"per-element operand must have shape ({self.M},) after indexing, got {a.shape}")
+
+
+def _lit(x: float) -> str:
+    if np.isnan(x):
+        return "mg::nan_d()"
+    if np.isinf(x):
+        return "(1.0 / 0.0)" if x > 0 else "(-1.0 / 0.0)"
+    return f"{float(x).hex()}"
+
+
+class Sym:
+    """Symbolic scalar with the reference ActiveScalar's arithmetic protocol."""
+
+    __slots__ = ("g", "name")
+    __array_ufunc__ = None  # numpy defers to our reflected operators
+
+    def __init__(self, g, name):
+        self.g = g
+        self.name = name
+
+    def _bin(self, other, fmt, reflect=False):
+        a, b = self.g.operand(self), self.g.operand(other)
+        if reflect:
+            a, b = b, a
+        return self.g.new(fmt.format(a=a, b=b))
+
+    def __add__(self, o):
+        return self._bin(o, "{a} + {b}")
+
+    def __radd__(self, o):
+        return self._bin(o, "{a} + {b}", reflect=True)
+
+    def __sub__(self, o):
+        return self._bin(o, "{a} - {b}")
+
+    def __rsub__(self, o):
+        return self._bin(o, "{a} - {b}", reflect=True)
+
+    def __mul__(self, o):
+        return self._bin(o, "{a} * {b}")
+
+    def __rmul__(self, o):
+        return self._bin(o, "{a} * {b}", reflect=True)
+
+    def __truediv__(self, o):
+        return self._bin(o, "{a} / {b}")
+
+    def __rtruediv__(self, o):
+        return self._bin(o, "{a} / {b}", reflect=True)
+
+    def __neg__(self):
+        return self.g.new(f"-{self.name}")
+
+    def __pos__(self):
+        return self
+
+    def __pow__(self, p):
+        if not isinstance(p, (int, np.integer)):
+            raise TypeError("only integer exponents are supported")  # active.py:225-227
+        if p == 1:
+            return self
+        return self.g.new(f"mg::powi({self.name}, {int(p)})")
+
+    def __abs__(self):
+        return self.g.new(f"mg::abs_({self.name})")
+
+    # elementary-function hooks (paper_2509_00406_b200.active dispatch)
+    def _mg_sqrt(self):
+        return self.g.new(f"sqrt({self.name})")
+
+    def _mg_log(self):
+        return self.g.new(f"log({self.name})")
+
+    def _mg_exp(self):
+        return self.g.new(f"exp({self.name})")
+
+    def _mg_sin(self):
+        return self.g.new(f"sin({self.name})")
+
+    def _mg_cos(self):
+        return self.g.new(f"cos({self.name})")
+
+    def _mg_abs(self):
+        return self.__abs__()
+
+    def _mg_positive_guard(self):
+        return self.g.new(f"positive_guard({self.name})")
+
+    def __bool__(self):
+        raise TypeError("traced callbacks cannot branch on input values")
+
+    def __float__(self):
+        raise TypeError("traced callbacks cannot convert inputs to float")
+
+
+class _Handle:
+    __slots__ = ("kind", "index", "slot")
+
+    def __init__(self, kind, index, slot=None):
+        self.kind = kind
+        self.index = index
+        self.slot = slot
+
+
+class _Vars:
+    def __init__(self, vecs):
+        self.vecs = vecs
+
+    def __getitem__(self, h):
+        if getattr(h, "slot", None) is None:
+            raise KeyError("this handle carries no variables")
+        return self.vecs[h.slot]
+
+
+class TracedTerm:
+    """Result of tracing: C++ body, attribute streams, shape."""
+
+    def __init__(self, op: str, P: int, n: int, body: list, ret: str, attrs: list):
+        self.op, self.P, self.n = op, P, n
+        self.body, self.ret, self.attrs = body, ret, attrs
+
+    def source(self) -> str:
+        lines = "\n      ".join(self.body)
+        return f"""// generated by paper_2509_00406_b200/jit.py — traced energy callback
+#include "jit_kernel.cuh"
+
+namespace {{
+struct Traced {{
+  template <int N, class S>
+  MG_DI auto operator()(const double* const* A, int64_t e, const mg::Vec<S, N>* X) const {{
+      using namespace mg;
+      (void)A; (void)e;
+      {lines}
+      return {self.ret};
+  }}
+}};
+}}  // namespace
+
+MG_JIT_INSTANTIATE(Traced, {self.P}, {self.n})
+"""
+
+
+def trace_callback(fn, op: str, n: int, num_elements: int, sel=None) -> TracedTerm:
+    """Run `fn(handle, nbrs, x)` once on symbolic inputs (ref problem.py:440-452).
+    sel: (M, P) vertex ids of the elements (EV / FV), so that a vertex batch's
+    `index` holds the slot's vertex ids like the reference's `_Batch`."""
+    from .active import ActiveVec
+
+    P = {"V": 1, "EV": 2, "FV": 3}[op]
+    g = _Graph(num_elements)
+    index = np.arange(num_elements, dtype=np.int64)
+    vecs = [ActiveVec([Sym(g, f"X[{q}][{c}]") for c in range(n)]) for q in range(P)]
+    kind = {"V": "vertex", "EV": "edge", "FV": "face"}[op]
+    handle = _Handle(kind, index, slot=0 if op == "V" else None)
+    if op != "V" and sel is None:
+        raise ValueError("edge / face callbacks need the element vertex lists")
+    nbrs = (handle,) if op == "V" else tuple(
+        _Handle("vertex", np.ascontiguousarray(np.asarray(sel)[:, q], dtype=np.int64), slot=q) for q in range(P))
+    out = fn(handle, nbrs, _Vars(vecs))
+    if isinstance(out, Sym):
+        ret = out.name
+    else:
+        ret = g.operand(out) if np.ndim(out) == 0 or np.size(out) == 1 else g.new(g.operand(out)).name
+    return TracedTerm(op, P, n, g.lines, ret, g.attrs)
+
+
+def compile_term(tt: TracedTerm) -> bytes:
+    """nvcc the traced functor into an sm_100a cubin (cached by source hash)."""
+    src = tt.source()
+    h = hashlib.sha256(src.encode() + (CSRC / "jit_kernel.cuh").read_bytes() + (CSRC / "dual.cuh").read_bytes()
+                       + (CSRC / "psd.cuh").read_bytes()).hexdigest()[:20]
+    CACHE.mkdir(parents=True, exist_ok=True)
+    cubin = CACHE / f"term_{h}.cubin"
+    if not cubin.exists():
+        cu = CACHE / f"term_{h}.cu"
+        cu.write_text(src)
+        nvcc = os.environ.get("NVCC", "nvcc")
+        cmd = [nvcc, "-cubin", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+               "--expt-relaxed-constexpr", "-I", str(CSRC), "-o", str(cubin) + ".tmp", str(cu)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for traced term:\n{r.stderr[-4000:]}")
+        os.replace(str(cubin) + ".tmp", cubin)
+    return cubin.read_bytes()

@@ -162,7 +162,7 @@ def read_matrix_market(path):
 
 
 class _TermRecord:
-    __slots__ = ("term", "kind", "op", "host_attrs", "dev_attrs", "tid")
+    __slots__ = ("term", "kind", "op", "host_attrs", "dev_attrs", "tid", "traced")
 
     def __init__(self, term, kind, op):
         self.term = term
@@ -171,6 +171,7 @@ class _TermRecord:
         self.host_attrs = []
         self.dev_attrs = []
         self.tid = -1
+        self.traced = None
 
 
 class Problem:
@@ -242,10 +243,7 @@ class Problem:
         if op not in _TERM_OPS:
             raise ValueError(f"{op.name} does not resolve to vertex variables; terms support FV, EV, VV, V")
         if not isinstance(fn, BuiltinTerm):
-            raise NotImplementedError(
-                "arbitrary Python callbacks need the tracer/codegen front-end; register a builtin term "
-                "from paper_2509_00406_b200.terms"
-            )
+            return self._add_traced_term(kind, op, fn)
         if op is not fn.op:
             raise ValueError(f"{type(fn).__name__} is an {fn.op.name} term, registered with {op.name}")
         fn.check_dims(self.n)
@@ -265,6 +263,38 @@ class Problem:
         self._pattern_ready = False
         return len(self._terms) - 1
 
+    def _num_elements(self, op: Op) -> int:
+        return {Op.V: self.mesh.num_vertices, Op.EV: self.mesh.num_edges, Op.FV: self.mesh.num_faces}[op]
+
+    def _element_vertices(self, op: Op):
+        return {Op.V: None, Op.EV: self.mesh.edges, Op.FV: self.mesh.faces}[op]
+
+    def _add_traced_term(self, kind: Element, op: Op, fn) -> int:
+        """A general callback (ref problem.py:8-14, 301-310): traced once on
+        symbolic inputs, compiled to an sm_100a module, launched by the engine
+        (jit.py). Closure arrays indexed by `handle.index` become per-element
+        attribute streams (refresh_attrs() re-gathers them)."""
+        if op not in (Op.V, Op.EV, Op.FV):
+            raise NotImplementedError(f"traced callbacks support the V, EV and FV ops, not {op.name}")
+        from . import jit
+
+        torch = _torch()
+        tt = jit.trace_callback(fn, op.name, self.n, self._num_elements(op), self._element_vertices(op))
+        image = jit.compile_term(tt)
+        rec = _TermRecord(fn, kind, op)
+        rec.traced = tt
+        rec.dev_attrs = [torch.from_numpy(a).to(self._dev) for a in tt.attrs]
+        rec.host_attrs = [None] * len(rec.dev_attrs)
+        buf = ctypes.create_string_buffer(image, len(image))
+        cattrs = (ctypes.c_void_p * max(1, len(rec.dev_attrs)))(*[t.data_ptr() for t in rec.dev_attrs])
+        tid = ctypes.c_int()
+        _lib.check(self._lib.mg_problem_add_jit_term(self._h, _lib.MG_OP[op.name], self.n, buf, cattrs,
+                                                     len(rec.dev_attrs), ctypes.byref(tid)))
+        rec.tid = tid.value
+        self._terms.append(rec)
+        self._pattern_ready = False
+        return len(self._terms) - 1
+
     def _sync_attrs(self):
         if self.live_host_attrs:
             self.refresh_attrs()
@@ -278,7 +308,17 @@ class Problem:
         CUDA tensor attribute in place instead (zero copies), or call this
         after changing a numpy one (or construct with live_host_attrs=True to
         re-upload on every call, at PCIe cost)."""
+        from . import jit
+
         for rec in self._terms:
+            if rec.traced is not None:  # re-gather the closure arrays of a traced callback
+                tt = jit.trace_callback(rec.term, rec.op.name, self.n, self._num_elements(rec.op),
+                                        self._element_vertices(rec.op))
+                if tt.source() != rec.traced.source():
+                    raise ValueError("a traced callback changed its expression; register it again")
+                for dev, host in zip(rec.dev_attrs, tt.attrs):
+                    dev.copy_(_torch().from_numpy(host))
+                continue
             for slot, host in enumerate(rec.host_attrs):
                 if host is not None:
                     src = np.ascontiguousarray(np.asarray(host, dtype=np.float64)).reshape(-1)
