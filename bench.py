@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--accumulation", default="deterministic", choices=["deterministic", "atomic"])
     ap.add_argument("--patch", type=int, default=64, help="owned rows per vertex patch (generic patch path)")
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary workloads")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs 2'/3/4 extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--profile", action="store_true", help="few steps, headline only (for ncu)")
     ap.add_argument("--profile-call", default="psd", choices=["psd", "plain", "hvp", "hvp_psd", "energy"],
@@ -245,6 +246,9 @@ def time_device(fn, steps, warmup, dist=None):
 
 def time_with_kernel(p, fn, steps, warmup, dist=None):
     """(ms per step, ms per main-kernel launch) over the same timed region."""
+    import gc
+
+    gc.collect()  # no deferred destruction (cudaFree) of earlier problems inside the timed region
     p.set_kernel_timing(False)
     for _ in range(warmup):
         fn()
@@ -426,6 +430,10 @@ def run_engine(args):
     extras = {}
     if not args.no_extras and world == 1:
         extras = run_extras(p, v, V, E, nnzb_local, steps, peak)
+        if not args.no_configs:
+            del p
+            torch.cuda.empty_cache()
+            extras.update(run_configs(peak))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, cores, desc = cpu_oracle_rate(256, reps=3)
@@ -476,6 +484,74 @@ def run_extras(p, v, V, E, nnzb, steps, peak):
         t = kms if kms else ms
         out[name] = {"ms": ms, "kernel_ms": kms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
                      "algorithmic_bytes": b, "hbm_frac": b / (t * 1e-3) / 1e9 / peak}
+    return out
+
+
+def run_configs(peak, sub=9):
+    """The other BASELINE workloads, one call each (device ms, main-kernel ms,
+    HBM fraction of the algorithmic bytes): the >= 10M-face cloth (config 2'),
+    symmetric Dirichlet grad+Hessian (config 3) and sphere / smoothing HVPs
+    (config 4) on icosphere(sub)."""
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import (distortion_problem, edge_length_problem, initial_sphere, rest_geometry,
+                                            sphere_problem, tangent_bases)
+
+    out = {}
+
+    def rec(name, p, fn, units, unit, nbytes, k=10):
+        ms, kms = time_with_kernel(p, fn, k, 3)
+        t = kms if kms else ms
+        out[name] = {"ms": ms, "kernel_ms": kms, unit + "_per_s": units / (ms * 1e-3), "algorithmic_bytes": nbytes,
+                     "hbm_frac": nbytes / (t * 1e-3) / 1e9 / peak}
+
+    # config 2': cloth 2240^2 (10.03M faces), Newton step
+    n = 2240
+    p, x, v = build_engine_cloth(n, "deterministic")
+    V, E = cloth_sizes(n)
+    vd = torch.from_numpy(v).cuda()
+    y = torch.empty_like(vd)
+    rec("cloth2240_grad_hess_psd", p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), 2 * V + E, "term_elements",
+        cloth_bytes(V, E, p.hess.nnz_blocks))
+    rec("cloth2240_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), 2 * V + E, "term_elements", cloth_hvp_bytes(V, E))
+    del p, vd, y
+    torch.cuda.empty_cache()
+    # config 3: symmetric Dirichlet on the punctured icosphere
+    pos, faces, uv = mg.punctured_icosphere_arrays(sub)
+    mesh = mg.Mesh(pos, faces)
+    rest_inv, areas = rest_geometry(mesh)
+    p = distortion_problem(mesh, rest_inv, areas, with_hessian=True)
+    p.precompute_sparsity()
+    p.x = uv.ravel()
+    V, F, nnzb = len(pos), len(faces), p.hess.nnz_blocks
+    vd = torch.from_numpy(np.random.default_rng(1).normal(size=2 * V)).cuda()
+    y = torch.empty_like(vd)
+    rec(f"dirichlet_ico{sub}_grad_hess", p, lambda: p.eval_terms(sync=False), F, "faces",
+        16 * V + 12 * F + 32 * F + 8 * F + 16 * V + 32 * nnzb)
+    rec(f"dirichlet_ico{sub}_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces",
+        16 * V + 16 * V + 12 * F + 32 * F + 8 * F + 16 * V)
+    del p, vd, y
+    torch.cuda.empty_cache()
+    # config 4: sphere manifold HVP, smoothing HVP
+    pos, faces = mg.icosphere_arrays(sub)
+    mesh = mg.Mesh(pos, faces)
+    base = initial_sphere(mesh)
+    b1, b2 = tangent_bases(base)
+    p = sphere_problem(mesh, base, b1, b2)
+    V, F = len(pos), len(faces)
+    p.x = 1e-3 * np.random.default_rng(0).normal(size=2 * V)
+    vd = torch.from_numpy(np.random.default_rng(1).normal(size=2 * V)).cuda()
+    y = torch.empty_like(vd)
+    rec(f"sphere_ico{sub}_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces",
+        16 * V + 16 * V + 72 * V + 12 * F + 16 * V)
+    del p, vd, y
+    p = edge_length_problem(mesh)
+    p.x = pos.ravel()
+    E = 3 * F // 2
+    vd = torch.from_numpy(np.random.default_rng(1).normal(size=3 * V)).cuda()
+    y = torch.empty_like(vd)
+    rec(f"smooth_ico{sub}_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), E, "edges", 24 * V + 8 * E + 24 * V)
     return out
 
 

@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 import os
 import time
+import weakref
 
 import numpy as np
 
@@ -57,7 +58,7 @@ class BlockSparseMatrix:
         self.row_offsets = row_offsets
         self.col_indices = col_indices
         self.values_device = values_device
-        self._problem = problem
+        self._problem_ref = weakref.ref(problem) if problem is not None else None
         self._block_rows = np.repeat(np.arange(num_block_rows, dtype=np.int64), np.diff(row_offsets))
 
     @property
@@ -90,6 +91,10 @@ class BlockSparseMatrix:
 
     def block_pairs(self):
         return np.stack([self._block_rows, self.col_indices], axis=1)
+
+    @property
+    def _problem(self):
+        return self._problem_ref() if self._problem_ref is not None else None
 
     def matvec(self, v):
         """H v with the device block-CSR SpMV (problem.py:100-106)."""
