@@ -54,6 +54,8 @@ struct FvArgs {
   int* redo;
   double floor;
   TermDev t;                 // the SymDirichlet term: a[0] rest_inv (F,4), a[1] areas (F)
+  double* vscr;              // sphere: per-vertex retraction (p, pdot), (V, 6)
+  int64_t nv;                // vertices of the (shard) mesh
 };
 
 MG_DI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -388,6 +390,226 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
   if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Sphere barrier + stretch (apps/sphere.py:71-99), BASELINE config 4: gradient
+// and matrix-free HVP in closed form through the per-vertex retraction
+// p = r / |r|, r = s + x0 b1 + x1 b2 (J = dp/dx = (I - p p^T) B / rho, B = [b1 b2]):
+//   face energy  E = -log det[p0 p1 p2] + sum_{a<b} |p_a - p_b|^2  on p-space,
+//   c_s = d det / d p_s (cross products), g_s = -c_s / det + 2 (2 p_s - p_s1 - p_s2),
+//   (grad^2 E pdot)_s = -cdot_s / det + c_s detdot / det^2 + 2 (2 pdot_s - pdot_s1 - pdot_s2),
+//   row: grad_x = J^T sum g_s;  (H u)_x = J^T sum (grad^2 E pdot)_s + (dJ/de)^T sum g_s,
+//   dJ/de = [-(pdot p^T + p pdot^T)/rho - (I - p p^T) rhodot / rho^2] B,  pdot = J u.
+// Faces are recomputed by each corner row (no communication); non-finite
+// faces raise the redo flag (the generic patch kernel then reproduces the
+// reference's NaN placement).
+struct Retract {
+  double p[3], pd[3], rho, rhod;  // p, pdot = J u, |r|, d|r|/de
+};
+
+MG_DI Retract retract(const double* s, const double* b1, const double* b2, double x0, double x1, double u0, double u1) {
+  Retract R;
+  double r[3], rd[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    r[c] = x0 * b1[c] + x1 * b2[c] + s[c];
+    rd[c] = u0 * b1[c] + u1 * b2[c];
+  }
+  R.rho = ::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  const double ir = 1.0 / R.rho;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) R.p[c] = r[c] * ir;
+  const double prd = R.p[0] * rd[0] + R.p[1] * rd[1] + R.p[2] * rd[2];
+  R.rhod = prd;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) R.pd[c] = (rd[c] - R.p[c] * prd) * ir;
+  return R;
+}
+
+MG_DI void cross3(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// per-vertex retraction once per call: p and pdot = J u (u free-masked)
+template <int MODE>
+__global__ void k_sphere_retract(const __grid_constant__ FvArgs a, const uint8_t* fixed) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= a.nv) return;
+  const bool pinned = fixed && fixed[v];
+  double u0 = 0.0, u1 = 0.0;
+  if (MODE == MODE_HVP && !pinned) {
+    u0 = a.w[v * 2];
+    u1 = a.w[v * 2 + 1];
+  }
+  const Retract R = retract(a.t.a[0] + 3 * v, a.t.a[1] + 3 * v, a.t.a[2] + 3 * v, a.x[v * 2], a.x[v * 2 + 1], u0, u1);
+  double* o = a.vscr + 6 * v;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    o[c] = R.p[c];
+    if constexpr (MODE == MODE_HVP) o[3 + c] = R.pd[c];
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvArgs a) {
+  const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
+  double eacc = 0.0;
+  bool ok = true;
+  if (row < a.V) {
+    const int g = a.order[row];
+    const uint32_t meta = a.rmeta[row];
+    uint64_t rc[KF];
+#pragma unroll
+    for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+    const bool fr = !((meta >> 8) & 1);
+    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
+    const bool barrier = a.t.c[0] != 0.0, stretch = a.t.c[1] != 0.0;
+    const double* S = a.t.a[0];
+    const double* B1 = a.t.a[1];
+    const double* B2 = a.t.a[2];
+    double A[3] = {0.0, 0.0, 0.0}, Bs[3] = {0.0, 0.0, 0.0};  // sum (grad^2 E pdot)_s, sum g_s
+    auto corner = [&](int v, bool pinned) {
+      const double x0 = a.x[(int64_t)v * 2], x1 = a.x[(int64_t)v * 2 + 1];
+      double u0 = 0.0, u1 = 0.0;
+      if (MODE == MODE_HVP && !pinned) {
+        u0 = a.w[(int64_t)v * 2];
+        u1 = a.w[(int64_t)v * 2 + 1];
+      }
+      return retract(S + 3 * (int64_t)v, B1 + 3 * (int64_t)v, B2 + 3 * (int64_t)v, x0, x1, u0, u1);
+    };
+    auto incidence = [&](uint64_t r64) {
+      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
+      const int64_t f = lo & 0x3fffffffu;
+      const int s = (int)(lo >> 30);
+      const int pins = (int)((hi >> 16) & 7);
+      Retract P[3];
+      (void)pins;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {  // the corners' retraction from the per-call vertex scratch
+        const double* o = a.vscr + 6 * (int64_t)a.faces[3 * f + q];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          P[q].p[c] = o[c];
+          P[q].pd[c] = MODE == MODE_HVP ? o[3 + c] : 0.0;
+        }
+      }
+      const int s1 = s == 2 ? 0 : s + 1, s2 = s == 0 ? 2 : s - 1;
+      // the row's corner and the next two, selected into registers
+      double ps[3], p1[3], p2[3], ds[3], d1[3], d2[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        ps[c] = s == 0 ? P[0].p[c] : (s == 1 ? P[1].p[c] : P[2].p[c]);
+        p1[c] = s1 == 0 ? P[0].p[c] : (s1 == 1 ? P[1].p[c] : P[2].p[c]);
+        p2[c] = s2 == 0 ? P[0].p[c] : (s2 == 1 ? P[1].p[c] : P[2].p[c]);
+        ds[c] = s == 0 ? P[0].pd[c] : (s == 1 ? P[1].pd[c] : P[2].pd[c]);
+        d1[c] = s1 == 0 ? P[0].pd[c] : (s1 == 1 ? P[1].pd[c] : P[2].pd[c]);
+        d2[c] = s2 == 0 ? P[0].pd[c] : (s2 == 1 ? P[1].pd[c] : P[2].pd[c]);
+      }
+      double val = 0.0, gs[3] = {0.0, 0.0, 0.0}, hs[3] = {0.0, 0.0, 0.0};
+      if (barrier) {
+        // det[p0 p1 p2] = ps . (p1 x p2) for the cyclic order (s, s1, s2)
+        double cs[3], c1[3], c2[3];
+        cross3(p1, p2, cs);
+        cross3(p2, ps, c1);
+        cross3(ps, p1, c2);
+        const double det = ps[0] * cs[0] + ps[1] * cs[1] + ps[2] * cs[2];
+        const double id = 1.0 / det;
+        val += -::log(det);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gs[c] += -cs[c] * id;
+        if constexpr (MODE == MODE_HVP) {
+          double t1[3], t2[3];
+          cross3(d1, p2, t1);
+          cross3(p1, d2, t2);
+          const double detd = cs[0] * ds[0] + cs[1] * ds[1] + cs[2] * ds[2] + c1[0] * d1[0] + c1[1] * d1[1] +
+                              c1[2] * d1[2] + c2[0] * d2[0] + c2[1] * d2[1] + c2[2] * d2[2];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) hs[c] += -(t1[c] + t2[c]) * id + cs[c] * detd * id * id;
+        }
+      }
+      if (stretch) {
+        double e01 = 0.0, e12 = 0.0, e20 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double a01 = ps[c] - p1[c], a12 = p1[c] - p2[c], a20 = p2[c] - ps[c];
+          e01 += a01 * a01;
+          e12 += a12 * a12;
+          e20 += a20 * a20;
+          gs[c] += 2.0 * (2.0 * ps[c] - p1[c] - p2[c]);
+          if constexpr (MODE == MODE_HVP) hs[c] += 2.0 * (2.0 * ds[c] - d1[c] - d2[c]);
+        }
+        val += e01 + e12 + e20;
+      }
+      ok &= isfinite(val + gs[0] + gs[1] + gs[2] + hs[0] + hs[1] + hs[2]);
+      if (MODE == MODE_GRAD && s == 0) eacc += val;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        Bs[c] += gs[c];
+        A[c] += hs[c];
+      }
+    };
+    const int ne = cnt < KF ? cnt : KF;
+#pragma unroll
+    for (int j = 0; j < KF; ++j)
+      if (j < ne) incidence(rc[j]);
+    for (int k = KF; k < cnt; ++k) incidence(a.rrec[a.rinc_off[row] + k]);
+    // the row's own retraction: J, dJ
+    const Retract R = corner(g, !fr);
+    const double* b1 = B1 + 3 * (int64_t)g;
+    const double* b2 = B2 + 3 * (int64_t)g;
+    const double ir = 1.0 / R.rho;
+    // (I - p p^T) v / rho
+    auto proj = [&](const double* v, double* o) {
+      const double pv = R.p[0] * v[0] + R.p[1] * v[1] + R.p[2] * v[2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) o[c] = (v[c] - R.p[c] * pv) * ir;
+    };
+    double out[2];
+    double q[3];
+    if constexpr (MODE == MODE_GRAD) {
+      proj(Bs, q);  // J^T Bs = B^T (I - p p^T) Bs / rho
+      out[0] = q[0] * b1[0] + q[1] * b1[1] + q[2] * b1[2];
+      out[1] = q[0] * b2[0] + q[1] * b2[1] + q[2] * b2[2];
+    } else {
+      double qa[3];
+      proj(A, qa);
+      // dJ^T Bs = B^T [-(p pdot^T + pdot p^T) Bs / rho - (I - p p^T) Bs rhodot / rho^2]
+      const double pB = R.p[0] * Bs[0] + R.p[1] * Bs[1] + R.p[2] * Bs[2];
+      const double dB = R.pd[0] * Bs[0] + R.pd[1] * Bs[1] + R.pd[2] * Bs[2];
+      double qb[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        qb[c] = -(R.p[c] * dB + R.pd[c] * pB) * ir - (Bs[c] - R.p[c] * pB) * R.rhod * ir * ir;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) q[c] = qa[c] + qb[c];
+      out[0] = q[0] * b1[0] + q[1] * b1[1] + q[2] * b1[2];
+      out[1] = q[0] * b2[0] + q[1] * b2[1] + q[2] * b2[2];
+    }
+    double* vout = MODE == MODE_HVP ? a.y : a.grad;
+    vout[(int64_t)g * 2] = fr ? out[0] : 0.0;
+    vout[(int64_t)g * 2 + 1] = fr ? out[1] : 0.0;
+  }
+  if (!ok) *a.redo = 1;
+  if constexpr (MODE != MODE_HVP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
+    if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
+  }
+}
+
+template <int MODE>
+void launch_sphere(const Problem& p, const FvArgs& a, cudaStream_t st) {
+  const int64_t nb = (a.V + PT - 1) / PT;
+  if (!nb) return;
+  timing_begin(p, st);
+  k_sphere_retract<MODE><<<(unsigned)((a.nv + 255) / 256), 256, 0, st>>>(a, p.any_fixed ? p.fixed.p : nullptr);
+  MG_LAUNCH_CHECK();
+  k_rows_sphere<MODE><<<(unsigned)nb, PT, 0, st>>>(a);
+  MG_LAUNCH_CHECK();
+  timing_end(p, st);
+}
+
 template <int MODE, bool PSD>
 void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
@@ -425,7 +647,17 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.redo = p.redo.p;
   a.floor = c.floor;
   a.t = p.terms[0].dev;
+  a.nv = m.V;
+  a.vscr = nullptr;
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
+  if (a.t.type == MG_TERM_SPHERE) {
+    if (p.vscr.n < 6 * m.V) p.vscr.alloc(6 * m.V > 0 ? 6 * m.V : 1);
+    a.vscr = p.vscr.p;
+    if (mode == MODE_GRAD) launch_sphere<MODE_GRAD>(p, a, c.stream);
+    else if (mode == MODE_HVP && !c.psd) launch_sphere<MODE_HVP>(p, a, c.stream);
+    else throw Error(MG_ERR_UNSUPPORTED, "sphere face row kernel: gradient and unclamped HVP only");
+    return mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
+  }
   switch (mode) {
     case MODE_GRAD: launch_fv<MODE_GRAD, false>(p, a, hd, c.stream); break;
     case MODE_HESS:

@@ -160,6 +160,7 @@ struct Problem {
   int max_patch_hdoubles = 0;  // max row-buffer doubles of one CTA
   DBuf<int> redo;              // (1) non-finite lane seen by the radial kernel; cleared by the energy reduction
   DBuf<int> exact_runs;        // (1) calls whose exact re-run executed (diagnostics)
+  mutable DBuf<double> vscr;   // sphere face kernel: per-vertex retraction scratch (V, 6)
   // optional device timing of the main assembly kernel (benchmarks)
   bool timing = false;
   mutable std::vector<cudaEvent_t> ev_pool;

@@ -359,13 +359,16 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   const Mesh& m = *p.mesh;
   if (p.ev_fast) return launch_patch_ev(p, mode, c, partial_offset);
   int64_t n_fast = 0;
-  if (p.fv_fast) n_fast = launch_patch_fv(p, mode, c, partial_offset);
+  // face row kernels: Dirichlet in every mode; sphere for gradient / unclamped HVP
+  const bool fast = p.fv_fast && (p.terms[0].dev.type != MG_TERM_SPHERE || mode == MODE_GRAD ||
+                                  (mode == MODE_HVP && !c.psd));
+  if (fast) n_fast = launch_patch_fv(p, mode, c, partial_offset);
   PatchArgs a;
   a.R = m.patches.R;
   a.nterms = (int)p.terms.size();
   a.V = m.Vr;
   a.np = m.patches.num;
-  a.redo = p.fv_fast ? p.redo.p : nullptr;  // after the face row kernel: exact re-run only on its flag
+  a.redo = fast ? p.redo.p : nullptr;  // after a face row kernel: exact re-run only on its flag
   a.exact_runs = p.exact_runs.p;
   a.np_total = n_fast;
   a.vtx_off = p.vtx_off.p;
@@ -392,7 +395,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   }
   const int64_t np = m.patches.num;
   const int nvp = p.max_patch_vertices, nb = p.max_patch_blocks;
-  if (!p.fv_fast) timing_begin(p, c.stream);
+  if (!fast) timing_begin(p, c.stream);
   if (p.n == 3) {
     if (used & ~FAM_LIGHT) throw Error(MG_ERR_UNSUPPORTED, "term not available for var_dim 3");
     launch_mode<3, FAM_LIGHT>(a, np, nvp, nb, mode, c.psd, c.stream);
@@ -401,7 +404,7 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
     else if (used & bit(MG_TERM_SYM_DIRICHLET)) launch_mode<2, FAM_UV>(a, np, nvp, nb, mode, c.psd, c.stream);
     else launch_mode<2, FAM_LIGHT>(a, np, nvp, nb, mode, c.psd, c.stream);
   }
-  if (!p.fv_fast) timing_end(p, c.stream);
+  if (!fast) timing_end(p, c.stream);
   if (mode == MODE_HVP) return 0;
   return np > n_fast ? np : n_fast;
 }

@@ -869,8 +869,9 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
   MG_CUDA(cudaStreamSynchronize(s));
   p.fv_fast = false;
   {
-    bool fv = p.terms.size() == 1 && p.terms[0].dev.type == MG_TERM_SYM_DIRICHLET && p.n == 2 &&
-              m.F < (int64_t(1) << 30) && m.F > 0;
+    const int t0 = p.terms.size() == 1 ? p.terms[0].dev.type : 0;
+    bool fv = (t0 == MG_TERM_SYM_DIRICHLET || t0 == MG_TERM_SPHERE) && p.n == 2 && m.F < (int64_t(1) << 30) &&
+              m.F > 0;
     if (fv) build_rows_fv(p, s);
   }
   p.layout_ready = true;

@@ -74,7 +74,7 @@ def run_sphere(s, steps, peak):
     b1, b2 = tangent_bases(base)
     p = sphere_problem(mesh, base, b1, b2, with_hessian=False)
     V, F = len(pos), len(faces)
-    p.x = 1e-3 * np.random.default_rng(0).normal(size=2 * V)
+    p.x = 1e-5 * np.random.default_rng(0).normal(size=2 * V)  # tangent noise well below the edge length (no flips)
     setup = time.perf_counter() - t0
     v = torch.from_numpy(np.random.default_rng(1).normal(size=2 * V)).cuda()
     y = torch.empty_like(v)
