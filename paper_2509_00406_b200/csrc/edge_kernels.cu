@@ -407,6 +407,9 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>:
   constexpr int T = TriN<N>::value, NN = N * N;
   constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
   constexpr int PT = FastCfg<MODE, PSD>::BLOCK;
+  // the edge length's Hessian 2 [[I,-I],[-I,I]] does not depend on x
+  // (apps/smooth.py:27-28): its unclamped HVP reads only the direction
+  constexpr bool XFREE = MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH;
   extern __shared__ __align__(16) double hbuf[];
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
   double eacc = 0.0;
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>:
       const bool fo = !(hi >> 31);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        xo[j][c] = j < cnt ? a.x[o * N + c] : 0.0;
+        xo[j][c] = (j < cnt && !XFREE) ? a.x[o * N + c] : 0.0;
         if constexpr (MODE == MODE_HVP) uo[j][c] = (j < cnt && fo) ? a.w[o * N + c] : 0.0;
         else uo[j][c] = 0.0;
       }
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>:
       double d[N], rr = 0.0;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        d[c] = xs[c] - xo_[c];
+        d[c] = XFREE ? 0.0 : xs[c] - xo_[c];
         rr = d[c] * d[c] + rr;
       }
       double gam = 0.0, ci_s = 0.0, cd_s = 0.0, dl = 0.0, val = 0.0;
