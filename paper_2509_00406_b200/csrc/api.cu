@@ -247,6 +247,7 @@ int mg_problem_add_term(mg_problem* prob, int term_type, int op, const double* p
   prob->p.terms.push_back(std::move(t));
   prob->p.pattern_ready = false;
   prob->p.layout_ready = false;
+  prob->p.gather_ready = false;
   if (term_id) *term_id = (int)prob->p.terms.size() - 1;
   return MG_OK;
 }
@@ -271,6 +272,7 @@ int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* i
     prob->p.terms.push_back(std::move(t));
     prob->p.pattern_ready = false;
     prob->p.layout_ready = false;
+    prob->p.gather_ready = false;
     if (term_id) *term_id = (int)prob->p.terms.size() - 1;
   });
 }
@@ -337,6 +339,19 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
     if (p.deterministic && p.layout_ready) {
       np = launch_patch(p, mode, c, 0);
       launches += (p.ev_fast || p.fv_fast) ? 2 : 1;
+    } else if (p.deterministic) {  // element-parallel into scratch, fixed-order gather
+      if (!p.gather_ready) build_gather(p, s);
+      c.scratch = true;
+      for (auto& t : p.terms) {
+        np += launch_elem(p, t, mode, c, np);
+        ++launches;
+      }
+      gather_vec(p, grad_d, s);
+      ++launches;
+      if (p.with_hessian && p.nnzb) {
+        gather_blocks(p, hess_d, s);
+        ++launches;
+      }
     } else {
       MG_CUDA(cudaMemsetAsync(grad_d, 0, sizeof(double) * p.n * p.mesh->V, s));
       if (p.with_hessian && p.nnzb)
@@ -393,6 +408,15 @@ int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, 
         MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
         launches = 2;
       }
+    } else if (p.deterministic) {
+      if (!p.gather_ready) build_gather(p, s);
+      c.scratch = true;
+      for (auto& t : p.terms) {
+        launch_elem(p, t, MODE_HVP, c, 0);
+        ++launches;
+      }
+      gather_vec(p, y_d, s);
+      ++launches;
     } else {
       MG_CUDA(cudaMemsetAsync(y_d, 0, sizeof(double) * p.n * p.mesh->V, s));
       for (auto& t : p.terms) {

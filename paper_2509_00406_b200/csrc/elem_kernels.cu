@@ -29,6 +29,10 @@ struct ElemArgs {
   double* partials;
   double floor;
   int64_t M;
+  // deterministic mode off the patch path: per-element outputs go to scratch
+  // ((M,P,N) vectors, (M,P,P,N,N) blocks) and a fixed-order gather sums them
+  double* sv;
+  double* sh;
 };
 
 // Fixed-order block sum (warp shuffle tree, then warp 0 over the warp sums).
@@ -49,6 +53,13 @@ __device__ double block_sum(double v) {
   return r;  // valid in thread 0
 }
 
+// one slot component of an element's gradient / HVP output: scratch in the
+// deterministic gather mode, fp64 atomic otherwise
+MG_DI void put_vec(const ElemArgs& a, double* out, int64_t e, int P, int q, int N, int c, int v, double val) {
+  if (a.sv) a.sv[(e * P + q) * N + c] = val;
+  else atomicAdd(out + (int64_t)v * N + c, val);
+}
+
 template <int P, int N, int K, class H>
 __device__ __forceinline__ void scatter_hess(const ElemArgs& a, int64_t e, const double* h) {
   const int32_t* b = a.bids + e * P * P;
@@ -58,11 +69,19 @@ __device__ __forceinline__ void scatter_hess(const ElemArgs& a, int64_t e, const
     for (int q2 = 0; q2 < P; ++q2) {
       const int32_t bid = b[q1 * P + q2];
       if (bid >= 0) {
-        double* dst = a.hess + (int64_t)bid * N * N;
+        if (a.sh) {
+          double* dst = a.sh + ((e * P + q1) * P + q2) * N * N;
 #pragma unroll
-        for (int r = 0; r < N; ++r)
+          for (int r = 0; r < N; ++r)
 #pragma unroll
-          for (int c = 0; c < N; ++c) atomicAdd(dst + r * N + c, h[tri(q1 * N + r, q2 * N + c)]);
+            for (int c = 0; c < N; ++c) dst[r * N + c] = h ? h[tri(q1 * N + r, q2 * N + c)] : 0.0;
+        } else if (h) {
+          double* dst = a.hess + (int64_t)bid * N * N;
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int c = 0; c < N; ++c) atomicAdd(dst + r * N + c, h[tri(q1 * N + r, q2 * N + c)]);
+        }
       }
     }
 }
@@ -104,7 +123,7 @@ __global__ void __launch_bounds__(TPB) k_elem(TermDev t, ElemArgs a) {
       for (int q = 0; q < P; ++q)
         if (fr[q])
 #pragma unroll
-          for (int c = 0; c < N; ++c) atomicAdd(a.grad + (int64_t)vid[q] * N + c, r.g[q * N + c]);
+          for (int c = 0; c < N; ++c) put_vec(a, a.grad, e, P, q, N, c, vid[q], r.g[q * N + c]);
     } else if constexpr (MODE == MODE_HESS || (MODE == MODE_HVP && PSD)) {
       Vec<Dh<K, true>, N> X[P];
 #pragma unroll
@@ -123,7 +142,7 @@ __global__ void __launch_bounds__(TPB) k_elem(TermDev t, ElemArgs a) {
         for (int q = 0; q < P; ++q)
           if (fr[q])
 #pragma unroll
-            for (int c = 0; c < N; ++c) atomicAdd(a.grad + (int64_t)vid[q] * N + c, r.g[q * N + c]);
+            for (int c = 0; c < N; ++c) put_vec(a, a.grad, e, P, q, N, c, vid[q], r.g[q * N + c]);
       }
       // _extract (problem.py:454-476): structural zero -> no Hessian unless
       // a PSD floor is requested (then project(0) = floor*I).
@@ -167,9 +186,11 @@ __global__ void __launch_bounds__(TPB) k_elem(TermDev t, ElemArgs a) {
                 double acc = 0.0;
 #pragma unroll
                 for (int j = 0; j < K; ++j) acc += h[tri(q * N + c, j)] * vl[j];
-                atomicAdd(a.y + (int64_t)vid[q] * N + c, acc);
+                put_vec(a, a.y, e, P, q, N, c, vid[q], acc);
               }
         }
+      } else if constexpr (MODE == MODE_HESS) {
+        if (a.sh) scatter_hess<P, N, K, R>(a, e, nullptr);  // structural zero: zero blocks for the gather
       }
     } else {  // MODE_HVP, no PSD: forward-over-forward dual, H never formed
       Vec<Df<K, true>, N> X[P];
@@ -189,7 +210,12 @@ __global__ void __launch_bounds__(TPB) k_elem(TermDev t, ElemArgs a) {
         for (int q = 0; q < P; ++q)
           if (fr[q])
 #pragma unroll
-            for (int c = 0; c < N; ++c) atomicAdd(a.y + (int64_t)vid[q] * N + c, r.gd[q * N + c]);
+            for (int c = 0; c < N; ++c) put_vec(a, a.y, e, P, q, N, c, vid[q], r.gd[q * N + c]);
+      } else if (a.sv) {
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+          for (int c = 0; c < N; ++c) a.sv[(e * P + q) * N + c] = 0.0;
       }
     }
   }
@@ -383,6 +409,8 @@ int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx&
   a.partials = c.partials + partial_offset;
   a.floor = c.floor;
   a.M = t.M;
+  a.sv = c.scratch ? p.gsv.p + t.gv_base : nullptr;
+  a.sh = c.scratch && mode == MODE_HESS ? p.gsh.p + t.gh_base : nullptr;
   switch (t.dev.type) {
     case MG_TERM_INERTIA: launch_t<MG_TERM_INERTIA>(p.n, t, mode, c.psd, a, c.stream); break;
     case MG_TERM_SPRING: launch_t<MG_TERM_SPRING>(p.n, t, mode, c.psd, a, c.stream); break;

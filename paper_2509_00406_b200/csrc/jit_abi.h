@@ -24,6 +24,8 @@ struct JitArgs {
   double floor;
   int64_t M;
   const double* attrs[JIT_MAX_ATTRS];  // per-element attribute streams (device)
+  double* sv;  // deterministic gather mode: (M,P,N) slot vectors, (M,P,P,N,N) blocks
+  double* sh;
 };
 
 }  // namespace mg

@@ -87,6 +87,8 @@ void jit_launch(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c, 
   a.floor = c.floor;
   a.M = t.M;
   for (size_t i = 0; i < t.jit_attrs.size() && i < (size_t)JIT_MAX_ATTRS; ++i) a.attrs[i] = t.jit_attrs[i];
+  a.sv = c.scratch ? p.gsv.p + t.gv_base : nullptr;
+  a.sh = c.scratch && mode == MODE_HESS ? p.gsh.p + t.gh_base : nullptr;
   int k;
   switch (mode) {
     case MODE_ENERGY: k = 0; break;

@@ -55,6 +55,11 @@ template <int K, bool Z> MG_DI Dh<K, false> abs_(const Dh<K, Z>& a) { return cha
 template <int K, bool Z> MG_DI Df<K, false> abs_(const Df<K, Z>& a) { return chainf(a, ::fabs(a.v), jit_sign(a.v), 0.0); }
 MG_DI double positive_guard(double a) { return a > 0.0 ? a : nan_d(); }
 
+MG_DI void jit_put_vec(const JitArgs& a, double* out, int64_t e, int P, int q, int N, int c, int v, double val) {
+  if (a.sv) a.sv[(e * P + q) * N + c] = val;
+  else atomicAdd(out + (int64_t)v * N + c, val);
+}
+
 template <class R> MG_DI double jit_value(const R& r) { return r.v; }
 MG_DI double jit_value(double r) { return r; }
 
@@ -94,7 +99,7 @@ MG_DI void jit_element(const JitArgs& a) {
       for (int q = 0; q < P; ++q)
         if (fr[q])
 #pragma unroll
-          for (int c = 0; c < N; ++c) atomicAdd(a.grad + (int64_t)vid[q] * N + c, r.g[q * N + c]);
+          for (int c = 0; c < N; ++c) jit_put_vec(a, a.grad, e, P, q, N, c, vid[q], r.g[q * N + c]);
     } else if constexpr (MODE == JIT_HESS || (MODE == JIT_HVP && PSD)) {
       Vec<Dh<K, true>, N> X[P];
 #pragma unroll
@@ -113,7 +118,7 @@ MG_DI void jit_element(const JitArgs& a) {
         for (int q = 0; q < P; ++q)
           if (fr[q])
 #pragma unroll
-            for (int c = 0; c < N; ++c) atomicAdd(a.grad + (int64_t)vid[q] * N + c, r.g[q * N + c]);
+            for (int c = 0; c < N; ++c) jit_put_vec(a, a.grad, e, P, q, N, c, vid[q], r.g[q * N + c]);
       }
       if constexpr (!R::kZero || PSD) {
         double h[TriN<K>::value];
@@ -137,11 +142,19 @@ MG_DI void jit_element(const JitArgs& a) {
             for (int q2 = 0; q2 < P; ++q2) {
               const int32_t bid = b[q1 * P + q2];
               if (bid >= 0) {
-                double* dst = a.hess + (int64_t)bid * N * N;
+                if (a.sh) {
+                  double* dst = a.sh + ((e * P + q1) * P + q2) * N * N;
 #pragma unroll
-                for (int rr = 0; rr < N; ++rr)
+                  for (int rr = 0; rr < N; ++rr)
 #pragma unroll
-                  for (int cc = 0; cc < N; ++cc) atomicAdd(dst + rr * N + cc, h[tri(q1 * N + rr, q2 * N + cc)]);
+                    for (int cc = 0; cc < N; ++cc) dst[rr * N + cc] = h[tri(q1 * N + rr, q2 * N + cc)];
+                } else {
+                  double* dst = a.hess + (int64_t)bid * N * N;
+#pragma unroll
+                  for (int rr = 0; rr < N; ++rr)
+#pragma unroll
+                    for (int cc = 0; cc < N; ++cc) atomicAdd(dst + rr * N + cc, h[tri(q1 * N + rr, q2 * N + cc)]);
+                }
               }
             }
         } else {
@@ -158,8 +171,15 @@ MG_DI void jit_element(const JitArgs& a) {
                 double acc = 0.0;
 #pragma unroll
                 for (int j = 0; j < K; ++j) acc += h[tri(q * N + c, j)] * vl[j];
-                atomicAdd(a.y + (int64_t)vid[q] * N + c, acc);
+                jit_put_vec(a, a.y, e, P, q, N, c, vid[q], acc);
               }
+        }
+      } else if constexpr (MODE == JIT_HESS) {
+        if (a.sh) {  // structural-zero Hessian: zero blocks for the gather
+          const int32_t* b = a.bids + e * P * P;
+          for (int k = 0; k < P * P; ++k)
+            if (b[k] >= 0)
+              for (int i = 0; i < N * N; ++i) a.sh[(e * P * P + k) * N * N + i] = 0.0;
         }
       }
     } else {  // JIT_HVP without PSD: forward-over-forward
@@ -180,7 +200,9 @@ MG_DI void jit_element(const JitArgs& a) {
         for (int q = 0; q < P; ++q)
           if (fr[q])
 #pragma unroll
-            for (int c = 0; c < N; ++c) atomicAdd(a.y + (int64_t)vid[q] * N + c, r.gd[q * N + c]);
+            for (int c = 0; c < N; ++c) jit_put_vec(a, a.y, e, P, q, N, c, vid[q], r.gd[q * N + c]);
+      } else if (a.sv) {
+        for (int i = 0; i < P * N; ++i) a.sv[e * P * N + i] = 0.0;
       }
     }
   }

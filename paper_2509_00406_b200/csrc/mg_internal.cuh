@@ -113,6 +113,8 @@ struct Term {
   void* jit_module = nullptr;
   void* jit_fn[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   std::vector<const double*> jit_attrs;
+  // deterministic gather mode: this term's offsets in the problem's scratch
+  int64_t gv_base = 0, gh_base = 0;
 };
 
 constexpr int EV_ROW_BLOCK = 64;  // rows (threads) per CTA of the edge row kernel
@@ -161,6 +163,11 @@ struct Problem {
   DBuf<int> redo;              // (1) non-finite lane seen by the radial kernel; cleared by the energy reduction
   DBuf<int> exact_runs;        // (1) calls whose exact re-run executed (diagnostics)
   mutable DBuf<double> vscr;   // sphere face kernel: per-vertex retraction scratch (V, 6)
+  // deterministic element-parallel mode (gather.cu): per-element output
+  // scratch and, per output row / block, its contributions in fixed order
+  bool gather_ready = false;
+  DBuf<double> gsv, gsh;
+  DBuf<int64_t> gv_off, gv_idx, gh_off, gh_idx;
   // optional device timing of the main assembly kernel (benchmarks)
   bool timing = false;
   mutable std::vector<cudaEvent_t> ev_pool;
@@ -210,6 +217,7 @@ struct LaunchCtx {
   bool psd;
   double floor;
   cudaStream_t stream;
+  bool scratch = false;  // deterministic gather mode: elements write Problem::gsv / gsh
 };
 // Launch one term element-parallel; returns number of energy partials written.
 int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c,
@@ -226,6 +234,10 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
 void timing_begin(const Problem& p, cudaStream_t s);
 void timing_end(const Problem& p, cudaStream_t s);
 bool patch_supported(const Problem& p);
+// gather.cu (deterministic element-parallel accumulation)
+void build_gather(Problem& p, cudaStream_t s);
+void gather_vec(const Problem& p, double* out, cudaStream_t s);
+void gather_blocks(const Problem& p, double* out, cudaStream_t s);
 // fixed-order reduction of energy partials -> out[0]
 void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag = nullptr);
 void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s);

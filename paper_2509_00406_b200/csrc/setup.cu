@@ -278,6 +278,7 @@ void build_pattern(Problem& p, cudaStream_t s) {
   if (keys) cudaFreeAsync(keys, s);
   MG_CUDA(cudaStreamSynchronize(s));
   p.pattern_ready = true;
+  p.gather_ready = false;
 }
 
 }  // namespace mg

@@ -247,7 +247,8 @@ def trace_callback(fn, op: str, n: int, num_elements: int, sel=None) -> TracedTe
 def compile_term(tt: TracedTerm) -> bytes:
     """nvcc the traced functor into an sm_100a cubin (cached by source hash)."""
     src = tt.source()
-    h = hashlib.sha256(src.encode() + (CSRC / "jit_kernel.cuh").read_bytes() + (CSRC / "dual.cuh").read_bytes()
+    h = hashlib.sha256(src.encode() + (CSRC / "jit_kernel.cuh").read_bytes() + (CSRC / "jit_abi.h").read_bytes()
+                       + (CSRC / "dual.cuh").read_bytes()
                        + (CSRC / "psd.cuh").read_bytes()).hexdigest()[:20]
     CACHE.mkdir(parents=True, exist_ok=True)
     cubin = CACHE / f"term_{h}.cubin"
