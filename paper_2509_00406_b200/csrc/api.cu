@@ -87,7 +87,9 @@ int64_t partials_needed(const Problem& p) {
   int64_t need = 1;
   for (auto& t : p.terms) need += elem_partials_needed(t);
   if (p.mesh->patches.num > need) need = p.mesh->patches.num;
-  if ((p.mesh->Vr + 31) / 32 > need) need = (p.mesh->Vr + 31) / 32;  // edge row kernel: one partial per warp
+  // edge row / tile kernels: one partial per warp of (tile-rounded) rows
+  const int64_t nwarps = (p.mesh->Vr + EV_TILE_ROWS - 1) / EV_TILE_ROWS * (EV_TILE_ROWS / 32);
+  if (nwarps > need) need = nwarps;
   return need + 1;
 }
 

@@ -53,6 +53,14 @@ struct EvArgs {
   int nev, nvt;                 // compacted term lists (indices into terms)
   int ev_idx[MAXT], vt_idx[MAXT];
   const double* ev_a0;          // per-edge attribute of ev_idx[0] (prefetched), or null
+  // staged tiles (k_tile_ev): see Problem::tiles_ready
+  const int2* tcnt;
+  const uint32_t* tv;
+  const uint64_t* te;
+  const uint16_t* islot;
+  const uint16_t* islot8;  // (V, 8): a row's first 8 slots, one 16-byte load
+  int max_v, max_e;
+  int64_t np_total;  // energy partials the reduction reads (the exact re-run zero-fills past its own)
   double floor;
   TermDev terms[MAXT];
 };
@@ -634,6 +642,272 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>:
   if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// Staged tile kernel (gradient / HVP), persistent and software-pipelined.
+// Rows are cut into tiles of EV_TILE_ROWS (patch order); tile b owns a padded
+// vertex table (its rows, then its halo) and edge table (every edge incident
+// to one of its rows, once). A CTA walks tiles b, b + grid, ...; while it
+// computes tile i, the gathers of tile i+1 (x, w, the edge attribute) are in
+// flight as cp.async copies into the other shared-memory stage and the table
+// entries of tile i+2 are in flight into registers, so a tile's dependent
+// loads (table -> vertex data) never stall the SM. Per tile:
+//   edges: each edge is evaluated ONCE into a per-edge record: the
+//          contribution to its first vertex (the second gets the negation:
+//          radial blocks are even in d) plus, under a PSD clamp, the
+//          symmetric floor term;
+//   rows:  V terms, then the incidences' records in their fixed order
+//          (bitwise reproducible), one store per output row.
+// The energy counts each edge in the tile of its first vertex.
+#ifndef EV_TILE_MINB
+#define EV_TILE_MINB 4
+#endif
+constexpr int TILE_IPT = 8;  // incidence slots per row in one 16-byte load
+
+MG_DI void cp_async8(void* smem, const void* gmem, bool zero) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(zero ? 0 : 8) : "memory");
+}
+
+// one tile's share of the tables, held by each thread
+struct TileRegs {
+  int nv = 0, ne = 0;
+  uint32_t tv[EV_TILE_VPT];
+  uint64_t te[EV_TILE_EPT];
+  uint4 sl4;
+  uint32_t meta;
+};
+
+template <int N, int MODE, bool PSD, int EVT>
+__global__ void __launch_bounds__(EV_TILE_ROWS, EV_TILE_MINB) k_tile_ev(const __grid_constant__ EvArgs a) {
+  static_assert(MODE == MODE_GRAD || MODE == MODE_HVP, "tile kernel: gradient / HVP");
+  constexpr int TB = EV_TILE_ROWS, VPT = EV_TILE_VPT, EPT = EV_TILE_EPT;
+  constexpr int SW = (MODE == MODE_HVP && PSD) ? 2 * N : N;
+  constexpr bool XFREE = MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH;
+  constexpr bool W = MODE == MODE_HVP;
+  constexpr int XW = (XFREE ? 0 : N) + (W ? N : 0);  // doubles per vertex-table entry
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  const int MV = a.max_v, ME = a.max_e;
+  const int64_t nt = (a.V + TB - 1) / TB;
+  // stage layout (component-major): x (N, MV) | w (N, MV) | attribute (ME) | flags (MV bytes)
+  const int stage_d = XW * MV + ME + (MV + 7) / 8;
+  double* sr = sm + 2 * stage_d;  // (SW, ME) edge records
+  auto sx = [&](int st) { return sm + st * stage_d; };
+  auto sw = [&](int st) { return sm + st * stage_d + (XFREE ? 0 : N * MV); };
+  auto sa0 = [&](int st) { return sm + st * stage_d + XW * MV; };
+  auto sfl = [&](int st) { return reinterpret_cast<uint8_t*>(sm + st * stage_d + XW * MV + ME); };
+
+  auto load_tables = [&](int64_t b, TileRegs& r) {
+    const int2 c = a.tcnt[b];
+    r.nv = c.x;
+    r.ne = c.y;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) r.tv[k] = tid + k * TB < MV ? a.tv[b * MV + tid + k * TB] : 0u;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) r.te[k] = tid + k * TB < ME ? a.te[b * ME + tid + k * TB] : 0ull;
+    const int64_t row = b * TB + tid;
+    r.sl4 = row < a.V ? reinterpret_cast<const uint4*>(a.islot8)[row] : make_uint4(0, 0, 0, 0);
+    r.meta = row < a.V ? a.rmeta[row] : 0u;
+  };
+  auto issue_gathers = [&](int64_t b, const TileRegs& r, int st) {
+    double* x_ = sx(st);
+    double* w_ = sw(st);
+    uint8_t* f_ = sfl(st);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int i = tid + k * TB;
+      if (i < r.nv) {
+        const int64_t gv = r.tv[k] & 0x7fffffffu;
+        const bool f = !(r.tv[k] >> 31);
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          if constexpr (!XFREE) cp_async8(x_ + c * MV + i, a.x + gv * N + c, false);
+          if constexpr (W) cp_async8(w_ + c * MV + i, a.w + gv * N + c, !f);
+        }
+        f_[i] = f;
+      }
+    }
+    if (a.ev_a0) {
+      double* a_ = sa0(st);
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int j = tid + k * TB;
+        if (j < r.ne) cp_async8(a_ + j, a.ev_a0 + (uint32_t)r.te[k], false);
+      }
+    }
+    // the rows' V-term attributes (masses; the inertia target for the gradient) into L1
+    const int64_t row = b * TB + tid;
+    if (row < a.V) {
+      const int64_t g = r.tv[0] & 0x7fffffffu;
+      for (int j = 0; j < a.nvt; ++j) {
+        const TermDev& t = a.terms[a.vt_idx[j]];
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(t.a[0] + g));
+        if (MODE == MODE_GRAD && t.type == MG_TERM_INERTIA) asm volatile("prefetch.global.L1 [%0];" ::"l"(t.a[1] + g * N));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  int64_t b = blockIdx.x;
+  if (b >= nt) return;
+  TileRegs cur, nxt;
+  load_tables(b, cur);
+  issue_gathers(b, cur, 0);
+  if (b + gridDim.x < nt) load_tables(b + gridDim.x, nxt);
+  bool finite = true;
+  for (int it = 0; b < nt; ++it, b += gridDim.x) {
+    const int st = it & 1;
+    const int64_t bn = b + gridDim.x;
+    if (bn < nt) issue_gathers(bn, nxt, st ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    TileRegs use = cur;
+    cur = nxt;
+    if (bn + gridDim.x < nt) load_tables(bn + gridDim.x, nxt);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    // ---- edges of tile b
+    const double* x_ = sx(st);
+    const double* w_ = sw(st);
+    const double* a_ = sa0(st);
+    const uint8_t* f_ = sfl(st);
+    const int64_t rem = a.V - b * TB;
+    const int nrows = rem < TB ? (int)rem : TB;
+    double eacc = 0.0;
+    auto edge = [&](int idx, uint64_t rec) {
+      const uint32_t e = (uint32_t)rec;
+      const int la = (int)((rec >> 32) & 0xffffu), lb = (int)(rec >> 48);
+      const bool fa = f_[la], fb = f_[lb];
+      const double av = a.ev_a0 ? a_[idx] : 0.0;
+      double d[N], rr = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        d[c] = XFREE ? 0.0 : x_[c * MV + la] - x_[c * MV + lb];
+        rr = d[c] * d[c] + rr;
+      }
+      double gam = 0.0, ci_s = 0.0, cd_s = 0.0, dl = 0.0, val = 0.0;
+      auto one_term = [&](bool ok, double pv, double p1, double p2) {
+        finite &= ok;
+        val += pv;
+        gam += 2.0 * p1;
+        if constexpr (MODE == MODE_HVP) {
+          double ci = 2.0 * p1, cd = 4.0 * p2, sh = 0.0;
+          if constexpr (PSD) {
+            if (fa && fb) {  // [[A,-A],[-A,A]]: clamp 2A, halve, shift floor/2
+              ci *= 2.0; cd *= 2.0;
+              radial_clamp_fast(ci, cd, rr, a.floor);
+              ci *= 0.5; cd *= 0.5;
+              sh = 0.5 * a.floor;
+            } else if (fa || fb) {
+              radial_clamp_fast(ci, cd, rr, a.floor);
+            }
+          }
+          ci_s += ci;
+          cd_s += cd;
+          dl += sh;
+        }
+      };
+      if constexpr (EVT != 0) {
+        double pv, p1, p2;
+        const bool ok = radial_closed<EVT>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
+        one_term(ok, pv, p1, p2);
+      } else {
+        for (int j = 0; j < a.nev; ++j) {
+          const TermDev& t = a.terms[a.ev_idx[j]];
+          const double at = (j == 0 && a.ev_a0) ? av : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
+          double pv, p1, p2;
+          const bool ok = radial_any(t, at, rr, pv, p1, p2);
+          one_term(ok, pv, p1, p2);
+        }
+      }
+      if constexpr (MODE == MODE_GRAD) {
+        if (la < nrows) eacc += val;  // the edge's first vertex is a row of this tile
+#pragma unroll
+        for (int c = 0; c < N; ++c) sr[c * ME + idx] = gam * d[c];
+      } else {
+        double dw = 0.0, du[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          du[c] = w_[c * MV + la] - w_[c * MV + lb];
+          dw += d[c] * du[c];
+        }
+#pragma unroll
+        for (int c = 0; c < N; ++c) sr[c * ME + idx] = ci_s * du[c] + cd_s * d[c] * dw;
+        if constexpr (PSD) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) sr[(N + c) * ME + idx] = dl * (w_[c * MV + la] + w_[c * MV + lb]);
+        }
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (tid + k * TB < use.ne) edge(tid + k * TB, use.te[k]);
+    __syncthreads();
+    // ---- rows of tile b
+    const int64_t row = b * TB + tid;
+    if (tid < nrows) {
+      const int g = (int)(use.tv[0] & 0x7fffffffu);
+      const bool fr = f_[tid];
+      double vec[N], xs[N], us[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        vec[c] = 0.0;
+        xs[c] = XFREE ? 0.0 : x_[c * MV + tid];
+        us[c] = W ? w_[c * MV + tid] : 0.0;
+      }
+      {
+        const double* xr[1] = {xs};
+        const double* wr[1] = {us};
+        for (int j = 0; j < a.nvt; ++j) {
+          const TermDev& t = a.terms[a.vt_idx[j]];
+          if (t.type == MG_TERM_INERTIA) {
+            ElemOut<MG_TERM_INERTIA, N, MODE, PSD> o;
+            eval_element<MG_TERM_INERTIA, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
+            eacc += o.val;
+#pragma unroll
+            for (int k = 0; k < N; ++k) vec[k] += o.g[k];
+          } else {
+            ElemOut<MG_TERM_GRAVITY, N, MODE, PSD> o;
+            eval_element<MG_TERM_GRAVITY, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
+            eacc += o.val;
+#pragma unroll
+            for (int k = 0; k < N; ++k) vec[k] += o.g[k];
+          }
+        }
+      }
+      auto inc = [&](uint32_t s16) {
+        const int sl = (int)(s16 & 0x7fff);
+        const bool neg = (s16 >> 15) & 1;  // the row is the edge's second vertex
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const double r = sr[c * ME + sl];
+          double v = neg ? -r : r;
+          if constexpr (MODE == MODE_HVP && PSD) v += sr[(N + c) * ME + sl];
+          vec[c] += v;
+        }
+      };
+      int cnt = (int)(use.meta & 0xff);
+      if (cnt == 255) cnt = a.rinc_off[row + 1] - a.rinc_off[row];
+      const uint32_t w4[4] = {use.sl4.x, use.sl4.y, use.sl4.z, use.sl4.w};
+#pragma unroll
+      for (int j = 0; j < TILE_IPT; ++j)
+        if (j < cnt) inc((w4[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+      if (cnt > TILE_IPT) {
+        const int k0 = a.rinc_off[row];
+        for (int k = TILE_IPT; k < cnt; ++k) inc(a.islot[k0 + k]);
+      }
+      double* vout = MODE == MODE_HVP ? a.y : a.grad;
+#pragma unroll
+      for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+    }
+    if constexpr (MODE == MODE_GRAD) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
+      if ((tid & 31) == 0) a.partials[row >> 5] = eacc;
+    }
+    __syncthreads();  // stage st and the records are rewritten next
+  }
+  if (!finite) *a.redo = 1;
+}
+
 // EXACT = false: radial evaluation only; a non-finite lane raises *a.redo.
 // EXACT = true : launched after it; returns at once unless *a.redo is set,
 //                then recomputes every row with the exact K = n dual path.
@@ -647,6 +921,11 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.exact_runs, 1);
   }
   const int64_t nblk = (a.V + PT - 1) / PT;
+  if constexpr (EXACT && MODE != MODE_HVP) {
+    for (int64_t i = nblk * (PT / 32) + blockIdx.x * (int64_t)PT + threadIdx.x; i < a.np_total;
+         i += (int64_t)gridDim.x * PT)
+      a.partials[i] = 0.0;
+  }
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
   const int64_t row = blk * PT + threadIdx.x;
   double eacc = 0.0;
@@ -803,6 +1082,15 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
   }  // row blocks
 }
 
+// MG_EDGE_TILES=0 selects the per-row kernel for gradient / HVP (A/B runs)
+bool tiles_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MG_EDGE_TILES");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int N, int MODE, bool PSD, int EVT>
 void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
@@ -816,10 +1104,38 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
     MG_CUDA(cudaFuncSetAttribute(exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
   timing_begin(p, st);
-  constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
-  fast<<<(unsigned)((a.V + FB - 1) / FB), FB, sm, st>>>(a);
-  MG_LAUNCH_CHECK();
-  timing_end(p, st);
+  if constexpr (MODE == MODE_HVP && !PSD && EVT != MG_TERM_EDGE_LENGTH) {
+    if (p.tiles_ready && tiles_enabled()) {
+      constexpr int SW = (MODE == MODE_HVP && PSD) ? 2 * N : N;
+      constexpr bool XF = MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH;
+      constexpr int XW = (XF ? 0 : N) + (MODE == MODE_HVP ? N : 0);
+      const size_t stage_d = (size_t)XW * a.max_v + a.max_e + (a.max_v + 7) / 8;
+      const size_t ts = sizeof(double) * (2 * stage_d + (size_t)SW * a.max_e);
+      auto tk = k_tile_ev<N, MODE, PSD, EVT>;
+      if (ts > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "edge tile does not fit in shared memory");
+      MG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ts));
+      int dev = 0, sms = 148, per_sm = 1;
+      MG_CUDA(cudaGetDevice(&dev));
+      MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk, EV_TILE_ROWS, ts));
+      const int64_t nt = (a.V + EV_TILE_ROWS - 1) / EV_TILE_ROWS;
+      int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+      if (grid > nt) grid = nt;
+      tk<<<(unsigned)grid, EV_TILE_ROWS, ts, st>>>(a);
+      MG_LAUNCH_CHECK();
+      timing_end(p, st);
+    } else {
+      constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
+      fast<<<(unsigned)((a.V + FB - 1) / FB), FB, sm, st>>>(a);
+      MG_LAUNCH_CHECK();
+      timing_end(p, st);
+    }
+  } else {
+    constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
+    fast<<<(unsigned)((a.V + FB - 1) / FB), FB, sm, st>>>(a);
+    MG_LAUNCH_CHECK();
+    timing_end(p, st);
+  }
   // exact re-run only when a lane was non-finite (reads the flag and exits otherwise)
   int dev = 0, sms = 148;
   MG_CUDA(cudaGetDevice(&dev));
@@ -883,15 +1199,25 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   for (int i = 0; i < a.nterms; ++i) a.terms[i] = p.terms[i].dev;
   a.nev = a.nvt = 0;
   a.ev_a0 = nullptr;
+  a.tcnt = p.tcnt.p;
+  a.tv = p.tv.p;
+  a.te = p.te.p;
+  a.islot = p.islot.p;
+  a.islot8 = p.islot8.p;
+  a.max_v = p.tile_max_v;
+  a.max_e = p.tile_max_e;
   for (int i = 0; i < a.nterms; ++i) {
     if (p.terms[i].dev.op == MG_OP_EV) a.ev_idx[a.nev++] = i;
     else a.vt_idx[a.nvt++] = i;
   }
   if (a.nev && p.terms[a.ev_idx[0]].dev.type == MG_TERM_SPRING) a.ev_a0 = p.terms[a.ev_idx[0]].dev.a[0];
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
+  // energy partials: one per warp of rows
+  const int64_t np = mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
+  a.np_total = np;
   if (p.n == 3) launch_rows_mode<3>(p, a, hd, mode, c.psd, c.stream);
   else launch_rows_mode<2>(p, a, hd, mode, c.psd, c.stream);
-  return mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
+  return np;
 }
 
 }  // namespace mg

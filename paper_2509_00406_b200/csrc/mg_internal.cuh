@@ -118,6 +118,9 @@ struct Term {
 };
 
 constexpr int EV_ROW_BLOCK = 64;  // rows (threads) per CTA of the edge row kernel
+constexpr int EV_TILE_ROWS = 128;  // rows per tile of the staged edge kernel (edge_kernels.cu)
+constexpr int EV_TILE_VPT = 2;    // vertex-table entries per thread (max_v <= VPT * rows)
+constexpr int EV_TILE_EPT = 5;    // edge-table entries per thread
 constexpr int EV_ELL_K = 6;       // incidences per row stored slot-major (ELL); the rest stay CSR
 
 struct Problem {
@@ -149,6 +152,17 @@ struct Problem {
   // edge row kernel (all EV terms radial, no FV terms): one thread per owned
   // row, rows in patch order; per row its incident edges in column order
   bool ev_fast = false;
+  // staged edge tiles (tile_setup in patch_setup.cu, kernels in edge_kernels.cu):
+  // per tile of EV_TILE_ROWS rows, its vertex table (rows, then halo vertices;
+  // vertex | pinned << 31), its edge table (edge | local a << 32 | local b << 48)
+  // and, per incidence (parallel to rrec), the edge's slot | (row is b) << 15
+  bool tiles_ready = false;
+  DBuf<int32_t> te_off;         // setup only
+  DBuf<int2> tcnt;              // (tiles) vertex / edge table lengths
+  DBuf<uint32_t> tv;            // (tiles, max_v) padded
+  DBuf<uint64_t> te;            // (tiles, max_e) padded
+  DBuf<uint16_t> islot, islot8;
+  int tile_max_v = 0, tile_max_e = 0;
   bool fv_fast = false;        // face row kernel (single SymDirichlet term), generic path as exact fallback
   DBuf<int32_t> rinc_off;      // (Vr+1)
   DBuf<uint64_t> rrec;         // (incidences) lo: edge | slot << 31, hi: other | pinned(other) << 31

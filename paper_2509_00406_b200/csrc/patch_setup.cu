@@ -14,6 +14,9 @@
 //
 // Everything is built with sorts/scans on the device; nothing here affects
 // the numbers, only the order of floating-point summation.
+#include <cstdio>
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "mg_internal.cuh"
@@ -521,6 +524,190 @@ void mesh_patches(Mesh& m, cudaStream_t s) {
 // Layout of the edge row kernel (edge_kernels.cu): rows in patch (Morton)
 // order, per-row incidence records, static per-row streams and the shared-
 // memory row offsets of each ROW_BLOCK-row CTA.
+
+// ---- staged edge tiles (k_tile_hvp in edge_kernels.cu) --------------------
+// Tile b = rows [b T, (b+1) T) in patch order. Its vertex table lists the
+// tile's rows, then the halo (other vertices of the tile's edges); its edge
+// table lists every edge incident to a row of the tile once.
+
+MG_DI int tile_rows(int64_t b, int64_t Vr, int T) {
+  const int64_t r = Vr - b * T;
+  return (int)(r < T ? r : T);
+}
+
+__global__ void k_tile_inc_keys(const int32_t* rinc_off, const uint64_t* rrec, const int32_t* rank, int64_t Vr, int T,
+                                uint64_t* hkeys, uint64_t* ekeys) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= Vr) return;
+  const int64_t b = r / T;
+  for (int k = rinc_off[r]; k < rinc_off[r + 1]; ++k) {
+    const uint64_t rec = rrec[k];
+    const int32_t o = (int32_t)((rec >> 32) & 0x7fffffffu);
+    const int64_t ro = rank[o];
+    const bool inside = ro < Vr && ro / T == b;
+    hkeys[k] = inside ? ~0ull : (((uint64_t)b << 32) | (uint32_t)o);
+    ekeys[k] = ((uint64_t)b << 32) | ((uint32_t)rec & 0x7fffffffu);
+  }
+}
+
+__global__ void k_tile_counts(const int32_t* hoff, const int32_t* eoff, int64_t nt, int64_t Vr, int T, int32_t* cnt,
+                              int* maxv, int* maxe) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b > nt) return;
+  if (b == nt) { cnt[b] = 0; return; }
+  const int nv = tile_rows(b, Vr, T) + hoff[b + 1] - hoff[b];
+  cnt[b] = nv;
+  atomicMax(maxv, nv);
+  atomicMax(maxe, eoff[b + 1] - eoff[b]);
+}
+
+__global__ void k_tile_fill_rows(const int32_t* order, const uint8_t* fixed, int64_t Vr, int T, int MV, uint32_t* tv) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= Vr) return;
+  const int64_t b = r / T;
+  const int32_t g = order[r];
+  tv[b * MV + (r - b * T)] = (uint32_t)g | ((fixed && fixed[g]) ? 0x80000000u : 0u);
+}
+
+__global__ void k_tile_fill_halo(const uint64_t* hkeys, int64_t nh, const int32_t* hoff, const uint8_t* fixed,
+                                 int64_t Vr, int T, int MV, uint32_t* tv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nh) return;
+  const int64_t b = (int64_t)(hkeys[i] >> 32);
+  const uint32_t o = (uint32_t)hkeys[i];
+  tv[b * MV + tile_rows(b, Vr, T) + (i - hoff[b])] = o | ((fixed && fixed[o]) ? 0x80000000u : 0u);
+}
+
+__global__ void k_tile_counts2(const int32_t* cnt, const int32_t* eoff, int64_t nt, int2* tcnt) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nt) return;
+  tcnt[b] = make_int2(cnt[b], eoff[b + 1] - eoff[b]);
+}
+
+MG_DI int64_t seg_find(const uint64_t* keys, int64_t lo, int64_t hi, uint64_t k) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_tile_edges(const uint64_t* ekeys, int64_t ne, const int32_t* edges, const int32_t* rank,
+                             const uint64_t* hkeys, const int32_t* hoff, const int32_t* eoff, int64_t Vr, int T, int ME,
+                             uint64_t* te) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  const int64_t b = (int64_t)(ekeys[i] >> 32);
+  const uint32_t e = (uint32_t)ekeys[i];
+  uint32_t loc[2];
+  for (int q = 0; q < 2; ++q) {
+    const int32_t v = edges[2 * (int64_t)e + q];
+    const int64_t rv = rank[v];
+    if (rv < Vr && rv / T == b) {
+      loc[q] = (uint32_t)(rv - b * T);
+    } else {
+      const int64_t j = seg_find(hkeys, hoff[b], hoff[b + 1], ((uint64_t)b << 32) | (uint32_t)v);
+      loc[q] = (uint32_t)(tile_rows(b, Vr, T) + (j - hoff[b]));
+    }
+  }
+  te[b * ME + (i - eoff[b])] = (uint64_t)e | ((uint64_t)(loc[0] & 0xffffu) << 32) | ((uint64_t)(loc[1] & 0xffffu) << 48);
+}
+
+__global__ void k_tile_islot(const int32_t* rinc_off, const uint64_t* rrec, const uint64_t* ekeys,
+                             const int32_t* eoff, int64_t Vr, int T, uint16_t* islot) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= Vr) return;
+  const int64_t b = r / T;
+  for (int k = rinc_off[r]; k < rinc_off[r + 1]; ++k) {
+    const uint32_t lo = (uint32_t)rrec[k];
+    const int64_t j = seg_find(ekeys, eoff[b], eoff[b + 1], ((uint64_t)b << 32) | (lo & 0x7fffffffu));
+    islot[k] = (uint16_t)((j - eoff[b]) | ((lo >> 31) << 15));
+  }
+}
+
+__global__ void k_tile_islot8(const int32_t* rinc_off, const uint16_t* islot, int64_t Vr, uint16_t* out) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= Vr) return;
+  const int k0 = rinc_off[r], n = rinc_off[r + 1] - k0;
+  for (int j = 0; j < 8; ++j) out[r * 8 + j] = j < n ? islot[k0 + j] : (uint16_t)0;
+}
+
+void build_tiles_ev(Problem& p, cudaStream_t s) {
+  Mesh& m = *p.mesh;
+  const int64_t Vr = m.Vr;
+  const int T = EV_TILE_ROWS;
+  const int64_t nt = (Vr + T - 1) / T;
+  p.tiles_ready = false;
+  if (!nt) return;
+  int64_t ninc = 0;
+  {
+    int32_t h = 0;
+    MG_CUDA(cudaMemcpyAsync(&h, p.rinc_off.p + Vr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    ninc = h;
+  }
+  if (!ninc) return;
+  uint64_t *hk = nullptr, *ek = nullptr;
+  MG_CUDA(cudaMallocAsync(&hk, sizeof(uint64_t) * ninc, s));
+  MG_CUDA(cudaMallocAsync(&ek, sizeof(uint64_t) * ninc, s));
+  k_tile_inc_keys<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.patches.rank.p, Vr, T, hk, ek);
+  MG_LAUNCH_CHECK();
+  int64_t nh = sort_unique(hk, ninc, 64, s);
+  if (nh > 0) {
+    uint64_t last = 0;
+    MG_CUDA(cudaMemcpyAsync(&last, hk + nh - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    if (last == ~0ull) --nh;
+  }
+  const int64_t ne = sort_unique(ek, ninc, 64, s);
+  DBuf<int32_t> hoff, cnt;
+  hoff.alloc(nt + 1);
+  cnt.alloc(nt + 1);
+  p.te_off.alloc(nt + 1);
+  k_lower_bounds<<<grid_for(nt + 1), TPB, 0, s>>>(hk, nh, nt, hoff.p);
+  k_lower_bounds<<<grid_for(nt + 1), TPB, 0, s>>>(ek, ne, nt, p.te_off.p);
+  MG_LAUNCH_CHECK();
+  DBuf<int> mx;
+  mx.alloc(2);
+  MG_CUDA(cudaMemsetAsync(mx.p, 0, 2 * sizeof(int), s));
+  k_tile_counts<<<grid_for(nt + 1), TPB, 0, s>>>(hoff.p, p.te_off.p, nt, Vr, T, cnt.p, mx.p, mx.p + 1);
+  MG_LAUNCH_CHECK();
+  int hm[2] = {0, 0};
+  MG_CUDA(cudaMemcpyAsync(hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  // padded tables (tile b at b * MV / b * ME): the kernel addresses them from
+  // the tile index alone; the pipeline holds a tile's share in registers
+  const int MV = hm[0], ME = hm[1];
+  const bool fits = MV <= EV_TILE_VPT * T && ME <= EV_TILE_EPT * T && nt * MV < (int64_t(1) << 31) &&
+                    nt * (int64_t)MV <= 2 * (Vr + nh) + 64 * nt && nt * (int64_t)ME <= 2 * ne + 64 * nt;
+  if (getenv("MG_DEBUG_TILES"))
+    fprintf(stderr, "edge tiles: %lld tiles, max_v %d, max_e %d, halo %lld, edges %lld, fits %d\n", (long long)nt, MV,
+            ME, (long long)nh, (long long)ne, (int)fits);
+  if (fits) {
+    const uint8_t* fx = p.any_fixed ? p.fixed.p : nullptr;
+    p.tv.alloc(nt * MV);
+    k_tile_fill_rows<<<grid_for(Vr), TPB, 0, s>>>(m.patches.order.p, fx, Vr, T, MV, p.tv.p);
+    if (nh) k_tile_fill_halo<<<grid_for(nh), TPB, 0, s>>>(hk, nh, hoff.p, fx, Vr, T, MV, p.tv.p);
+    p.te.alloc(nt * ME > 0 ? nt * ME : 1);
+    if (ne) k_tile_edges<<<grid_for(ne), TPB, 0, s>>>(ek, ne, m.edges.p, m.patches.rank.p, hk, hoff.p, p.te_off.p, Vr, T,
+                                                      ME, p.te.p);
+    p.tcnt.alloc(nt);
+    k_tile_counts2<<<grid_for(nt), TPB, 0, s>>>(cnt.p, p.te_off.p, nt, p.tcnt.p);
+    p.islot.alloc(ninc);
+    k_tile_islot<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, ek, p.te_off.p, Vr, T, p.islot.p);
+    p.islot8.alloc(Vr * 8);
+    k_tile_islot8<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.islot.p, Vr, p.islot8.p);
+    MG_LAUNCH_CHECK();
+    p.tile_max_v = MV;
+    p.tile_max_e = ME;
+  }
+  MG_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(hk, s);
+  cudaFreeAsync(ek, s);
+  MG_CUDA(cudaStreamSynchronize(s));
+  p.tiles_ready = fits;
+}
+
 void build_rows_ev(Problem& p, cudaStream_t s) {
   Mesh& m = *p.mesh;
   PatchSet& ps = m.patches;
@@ -584,6 +771,7 @@ void build_rows_ev(Problem& p, cudaStream_t s) {
   }
   MG_CUDA(cudaStreamSynchronize(s));
   p.recomputed_elements = 0;
+  build_tiles_ev(p, s);
   p.ev_fast = true;
   p.layout_ready = true;
 }
