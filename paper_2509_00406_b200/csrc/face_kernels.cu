@@ -56,6 +56,8 @@ struct FvArgs {
   TermDev t;                 // the SymDirichlet term: a[0] rest_inv (F,4), a[1] areas (F)
   double* vscr;              // sphere: per-vertex retraction (p, pdot), (V, 6)
   int64_t nv;                // vertices of the (shard) mesh
+  double* fpsd;              // PSD clamp: per face P_f(M), packed 4x4 (F, 10)
+  int64_t nf;                // faces of the (shard) mesh
 };
 
 MG_DI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -140,8 +142,58 @@ MG_DI bool dirichlet_closed(const double* J, double area, double& val, double* g
   return D > 0.0 && isfinite(chk);
 }
 
+// Per-face PSD clamp of the reduced 4x4 matrix M = (I (x) L_W)^T H_J (I (x) L_W)
+// (see the header), once per face: the three owner rows of a face then read
+// P_f(M) instead of each recomputing the eigen-decomposition.
+__global__ void __launch_bounds__(128) k_face_psd(const __grid_constant__ FvArgs a) {
+  const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= a.nf) return;
+  const int v0 = a.faces[3 * f], v1 = a.faces[3 * f + 1], v2 = a.faces[3 * f + 2];
+  double X[3][2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    X[0][c] = a.x[(int64_t)v0 * 2 + c];
+    X[1][c] = a.x[(int64_t)v1 * 2 + c];
+    X[2][c] = a.x[(int64_t)v2 * 2 + c];
+  }
+  const double* Rp = a.t.a[0] + 4 * f;
+  const double R0 = Rp[0], R1 = Rp[1], R2 = Rp[2], R3 = Rp[3];
+  const double area = a.t.a[1][f];
+  double J[4];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double d1 = X[1][c] - X[0][c], d2 = X[2][c] - X[0][c];
+    J[2 * c] = d1 * R0 + d2 * R2;
+    J[2 * c + 1] = d1 * R1 + d2 * R3;
+  }
+  double v, g[4], h[10];
+  const bool fin = dirichlet_closed<true>(J, area, v, g, h);
+  double M[10];
+  const double Wa0 = -(R0 + R2), Wa1 = -(R1 + R3);
+  // Q_W rows (corners): (1/sqrt2, 1/sqrt6), (-1/sqrt2, 1/sqrt6), (0, -2/sqrt6); L_W = W Q_W
+  const double Lw00 = (Wa0 - R0) * INV_SQRT2, Lw01 = (Wa0 + R0 - 2.0 * R2) * INV_SQRT6;
+  const double Lw10 = (Wa1 - R1) * INV_SQRT2, Lw11 = (Wa1 + R1 - 2.0 * R3) * INV_SQRT6;
+  const double Lw[2][2] = {{Lw00, Lw01}, {Lw10, Lw11}};
+#pragma unroll
+  for (int I = 0; I < 4; ++I)
+#pragma unroll
+    for (int Jx = 0; Jx <= I; ++Jx) {
+      const int c = I >> 1, aa = I & 1, c2 = Jx >> 1, bb = Jx & 1;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
+      M[tri(I, Jx)] = acc;
+    }
+  if (fin) project_if_needed<4>(M, a.floor);  // non-finite faces: the row kernel takes the exact path
+  double2* out = reinterpret_cast<double2*>(a.fpsd + f * 10);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) out[k] = make_double2(M[2 * k], M[2 * k + 1]);
+}
+
 #ifndef FV_MINB
-#define FV_MINB 8
+#define FV_MINB 6
 #endif
 template <int MODE, bool PSD>
 __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
@@ -178,11 +230,21 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
     // one incidence: face f (record), its corners' x (and w), rest_inv, area
     struct FaceIn {
       double X[3][2], U[3][2], R[4], area;
+      double M[PSD ? 10 : 1];
     };
     auto load_face = [&](uint64_t r64, const int* v) {
       FaceIn d;
       const int64_t f = (uint32_t)r64 & 0x3fffffffu;
       const int pins = (int)((r64 >> 48) & 7);
+      if constexpr (PSD) {
+        const double2* m2 = reinterpret_cast<const double2*>(a.fpsd + f * 10);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double2 t = m2[k];
+          d.M[2 * k] = t.x;
+          d.M[2 * k + 1] = t.y;
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -229,45 +291,29 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
 #pragma unroll
         for (int c = 0; c < 2; ++c) vec[c] += ws[0] * gJ[2 * c] + ws[1] * gJ[2 * c + 1];
       } else {
-        struct {
-          double v, g[4], h[10];
-        } E;
-        bool fin = dirichlet_closed<true>(J, d.area, E.v, E.g, E.h);
-        if constexpr (PSD) fin &= pins == 0;  // the reference clamps the pinned-masked block: exact path
-        ok &= fin;
-        if (MODE == MODE_HESS && s == 0) eacc += E.v;
-        if constexpr (MODE == MODE_HESS) {
-#pragma unroll
-          for (int c = 0; c < 2; ++c) vec[c] += ws[0] * E.g[2 * c] + ws[1] * E.g[2 * c + 1];
-        }
         // G[(c,k),(c2,b)]: the 4x4 matrix whose (s,t) block contraction gives the
         // 6x6 Hessian block: unclamped G = H_J with weights W; clamped G = P_f(M)
-        // with weights Q_W (orthonormal basis of 1-perp) plus the floor on 1 1^T / 3
+        // (k_face_psd, once per face) with weights Q_W (orthonormal basis of
+        // 1-perp) plus the floor on 1 1^T / 3
         double G[4][4];
         double as[2], a1[2], a2[2];
         if constexpr (PSD) {
-          // Q_W rows (corners): (1/sqrt2, 1/sqrt6), (-1/sqrt2, 1/sqrt6), (0, -2/sqrt6); L_W = W Q_W
-          const double Lw00 = (Wa0 - R0) * INV_SQRT2, Lw01 = (Wa0 + R0 - 2.0 * R2) * INV_SQRT6;
-          const double Lw10 = (Wa1 - R1) * INV_SQRT2, Lw11 = (Wa1 + R1 - 2.0 * R3) * INV_SQRT6;
-          const double Lw[2][2] = {{Lw00, Lw01}, {Lw10, Lw11}};
-          double M[10];
+          double val, gJ[4];
+          bool fin = dirichlet_closed<false>(J, d.area, val, gJ, nullptr);
+          fin &= pins == 0;  // the reference clamps the pinned-masked block: exact path
+          double chk = 0.0;
 #pragma unroll
-          for (int I = 0; I < 4; ++I)
+          for (int k = 0; k < 10; ++k) chk += d.M[k];
+          ok &= fin && isfinite(chk);
+          if (MODE == MODE_HESS && s == 0) eacc += val;
+          if constexpr (MODE == MODE_HESS) {
 #pragma unroll
-            for (int Jx = 0; Jx <= I; ++Jx) {
-              const int c = I >> 1, aa = I & 1, c2 = Jx >> 1, bb = Jx & 1;
-              double acc = 0.0;
-#pragma unroll
-              for (int k = 0; k < 2; ++k)
-#pragma unroll
-                for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * E.h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
-              M[tri(I, Jx)] = acc;
-            }
-          project_if_needed<4>(M, a.floor);
+            for (int c = 0; c < 2; ++c) vec[c] += ws[0] * gJ[2 * c] + ws[1] * gJ[2 * c + 1];
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) G[i][j] = M[tri(i, j)];
+            for (int j = 0; j < 4; ++j) G[i][j] = d.M[tri(i, j)];
           as[0] = sel3(s, INV_SQRT2, -INV_SQRT2, 0.0);
           as[1] = sel3(s, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
           a1[0] = sel3(s1, INV_SQRT2, -INV_SQRT2, 0.0);
@@ -275,6 +321,15 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
           a2[0] = sel3(s2, INV_SQRT2, -INV_SQRT2, 0.0);
           a2[1] = sel3(s2, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
         } else {
+          struct {
+            double v, g[4], h[10];
+          } E;
+          ok &= dirichlet_closed<true>(J, d.area, E.v, E.g, E.h);
+          if (MODE == MODE_HESS && s == 0) eacc += E.v;
+          if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) vec[c] += ws[0] * E.g[2 * c] + ws[1] * E.g[2 * c + 1];
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -619,6 +674,10 @@ void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
   auto kern = k_rows_dirichlet<MODE, PSD>;
   if (sm) MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   timing_begin(p, st);
+  if constexpr (PSD) {
+    if (a.nf) k_face_psd<<<(unsigned)((a.nf + 127) / 128), 128, 0, st>>>(a);
+    MG_LAUNCH_CHECK();
+  }
   kern<<<(unsigned)nb, PT, sm, st>>>(a);
   MG_LAUNCH_CHECK();
   timing_end(p, st);
@@ -649,6 +708,12 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.t = p.terms[0].dev;
   a.nv = m.V;
   a.vscr = nullptr;
+  a.nf = m.F;
+  a.fpsd = nullptr;
+  if (c.psd && mode != MODE_GRAD && a.t.type != MG_TERM_SPHERE) {
+    if (p.fpsd.n < 10 * m.F) p.fpsd.alloc(10 * m.F > 0 ? 10 * m.F : 2);
+    a.fpsd = p.fpsd.p;
+  }
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
   if (a.t.type == MG_TERM_SPHERE) {
     if (p.vscr.n < 6 * m.V) p.vscr.alloc(6 * m.V > 0 ? 6 * m.V : 1);

@@ -177,6 +177,7 @@ struct Problem {
   DBuf<int> redo;              // (1) non-finite lane seen by the radial kernel; cleared by the energy reduction
   DBuf<int> exact_runs;        // (1) calls whose exact re-run executed (diagnostics)
   mutable DBuf<double> vscr;   // sphere face kernel: per-vertex retraction scratch (V, 6)
+  mutable DBuf<double> fpsd;   // Dirichlet face kernel under a PSD clamp: per face P_f(M) (F, 10)
   // deterministic element-parallel mode (gather.cu): per-element output
   // scratch and, per output row / block, its contributions in fixed order
   bool gather_ready = false;
