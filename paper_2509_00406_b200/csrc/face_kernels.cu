@@ -653,6 +653,214 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
   }
 }
 
+
+// Sphere HVP under a PSD clamp (the Newton-CG probe, solvers.py:274-277):
+// face-parallel pass + fixed-order row gather. Per face, the 6x6 Hessian in
+// x comes in closed form from the retraction p = r / |r| (J_q = dp_q/dx_q):
+//   H[q][q'] = J_q^T Hp[q][q'] J_q' + delta_qq' T_q,   T_q[i][j] = g_q . d2p_q/dx_i dx_j,
+//   Hp = -D2 / det + c c^T / det^2  (barrier; c_q = d det / d p_q, D2 = d2 det, cross-product blocks)
+//        + 2 L (x) I_3              (stretch; L the triangle's graph Laplacian),
+// pinned corners' rows / columns zeroed (the reference's masked lift), then
+// clamped (active.py:490-504) and applied to the masked direction; the face's
+// three 2-vectors go to scratch and each owned row sums its faces' entries in
+// its fixed incidence order. Non-finite faces raise the redo flag.
+__global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_constant__ FvArgs a, const uint8_t* fixed,
+                                                            double* yscr) {
+  const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= a.nf) return;
+  int v[3];
+  bool pin[3];
+  double p[3][3], J[3][3][2], B[3][3][2], rho[3], u[3][2];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    v[q] = a.faces[3 * f + q];
+    pin[q] = fixed && fixed[v[q]];
+    const double* S = a.t.a[0] + 3 * (int64_t)v[q];
+    const double* b1 = a.t.a[1] + 3 * (int64_t)v[q];
+    const double* b2 = a.t.a[2] + 3 * (int64_t)v[q];
+    const double x0 = a.x[(int64_t)v[q] * 2], x1 = a.x[(int64_t)v[q] * 2 + 1];
+    u[q][0] = pin[q] ? 0.0 : a.w[(int64_t)v[q] * 2];
+    u[q][1] = pin[q] ? 0.0 : a.w[(int64_t)v[q] * 2 + 1];
+    double r[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      B[q][c][0] = b1[c];
+      B[q][c][1] = b2[c];
+      r[c] = x0 * b1[c] + x1 * b2[c] + S[c];
+    }
+    rho[q] = ::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    const double ir = 1.0 / rho[q];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) p[q][c] = r[c] * ir;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double pb = p[q][0] * B[q][0][j] + p[q][1] * B[q][1][j] + p[q][2] * B[q][2][j];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) J[q][c][j] = (B[q][c][j] - p[q][c] * pb) * ir;
+    }
+  }
+  const bool barrier = a.t.c[0] != 0.0, stretch = a.t.c[1] != 0.0;
+  // p-space gradient and Hessian blocks (upper triangle of blocks)
+  double g[3][3], Hp[3][3][3][3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[q][c] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int q2 = 0; q2 < 3; ++q2)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Hp[q][q2][i][j] = 0.0;
+  double chk = 0.0;
+  if (barrier) {
+    double cc[3][3];
+    cross3(p[1], p[2], cc[0]);
+    cross3(p[2], p[0], cc[1]);
+    cross3(p[0], p[1], cc[2]);
+    const double det = p[0][0] * cc[0][0] + p[0][1] * cc[0][1] + p[0][2] * cc[0][2];
+    const double id = 1.0 / det;
+    chk += ::log(det);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) g[q][c] -= cc[q][c] * id;
+    const double id2 = id * id;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int q2 = 0; q2 < 3; ++q2)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) Hp[q][q2][i][j] += cc[q][i] * cc[q2][j] * id2;
+    // d2 det / dp_q dp_q2 = eps-blocks: (q, q2, third vertex k) cyclic -> -[p_k]x ... written out:
+    // d c_q / d p_q2 for q2 = q+1: -[p_{q+2}]x ; q2 = q+2: +[p_{q+1}]x ; [v]x = [[0,-v2,v1],[v2,0,-v0],[-v1,v0,0]]
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int qa = q == 2 ? 0 : q + 1, qb = q == 0 ? 2 : q - 1;  // q+1, q+2 (mod 3)
+      const double* pk = p[qb];  // for q2 = qa the third vertex is qb
+      // D2[q][qa] = -[p_qb]x  ->  Hp -= id * D2
+      const double X[3][3] = {{0.0, -pk[2], pk[1]}, {pk[2], 0.0, -pk[0]}, {-pk[1], pk[0], 0.0}};
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          Hp[q][qa][i][j] += id * X[i][j];   // -id * (-[p_qb]x)
+          Hp[qa][q][j][i] += id * X[i][j];   // transpose block
+        }
+    }
+  }
+  if (stretch) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int qa = q == 2 ? 0 : q + 1, qb = q == 0 ? 2 : q - 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        g[q][c] += 2.0 * (2.0 * p[q][c] - p[qa][c] - p[qb][c]);
+        Hp[q][q][c][c] += 4.0;
+        Hp[q][qa][c][c] -= 2.0;
+        Hp[q][qb][c][c] -= 2.0;
+      }
+    }
+  }
+  // x-space packed 6x6 (rows / columns 2q + i)
+  double H[21];
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int q2 = 0; q2 <= q; ++q2)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int R = 2 * q + i, C = 2 * q2 + j;
+          if (C > R) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double t = 0.0;
+#pragma unroll
+            for (int l = 0; l < 3; ++l) t += Hp[q][q2][k][l] * J[q2][l][j];
+            acc += J[q][k][i] * t;
+          }
+          if (q == q2) {  // T_q[i][j] = g_q . d2 p_q / dx_i dx_j (symmetrised)
+            auto tij = [&](int ii, int jj) {
+              const double pbi = p[q][0] * B[q][0][ii] + p[q][1] * B[q][1][ii] + p[q][2] * B[q][2][ii];
+              const double rdj = p[q][0] * B[q][0][jj] + p[q][1] * B[q][1][jj] + p[q][2] * B[q][2][jj];
+              double gp = 0.0, gpd = 0.0, pdb = 0.0, gb = 0.0;
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                gp += g[q][c] * p[q][c];
+                gpd += g[q][c] * J[q][c][jj];
+                pdb += J[q][c][jj] * B[q][c][ii];
+                gb += g[q][c] * B[q][c][ii];
+              }
+              const double ir = 1.0 / rho[q];
+              return -(gpd * pbi + gp * pdb) * ir - (gb - gp * pbi) * rdj * ir * ir;
+            };
+            acc += 0.5 * (tij(i, j) + tij(j, i));
+          }
+          H[tri(R, C)] = (pin[q] || pin[q2]) ? 0.0 : acc;
+          chk += H[tri(R, C)];
+        }
+  if (!isfinite(chk)) {
+    *a.redo = 1;
+    return;
+  }
+  project_if_needed<6>(H, a.floor);
+  const double uu[6] = {u[0][0], u[0][1], u[1][0], u[1][1], u[2][0], u[2][1]};
+  double2* out = reinterpret_cast<double2*>(yscr + f * 6);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    double yy[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < 6; ++l) acc += H[tri(2 * q + i, l)] * uu[l];
+      yy[i] = acc;
+    }
+    out[q] = make_double2(yy[0], yy[1]);
+  }
+}
+
+// y_row = sum over the row's faces (fixed incidence order) of the face's entry
+__global__ void __launch_bounds__(PT) k_rows_face_gather(const __grid_constant__ FvArgs a, const double* yscr) {
+  const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
+  if (row >= a.V) return;
+  const int g = a.order[row];
+  const uint32_t meta = a.rmeta[row];
+  const bool fr = !((meta >> 8) & 1);
+  const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
+  uint64_t rc[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+  double2 yv[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) {
+    const uint32_t lo = (uint32_t)rc[j];
+    yv[j] = j < cnt ? reinterpret_cast<const double2*>(yscr + (int64_t)(lo & 0x3fffffffu) * 6)[lo >> 30]
+                    : make_double2(0.0, 0.0);
+  }
+  double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < KF; ++j) {
+    y0 += yv[j].x;
+    y1 += yv[j].y;
+  }
+  for (int k = KF; k < cnt; ++k) {
+    const uint32_t lo = (uint32_t)a.rrec[a.rinc_off[row] + k];
+    const double2 t = reinterpret_cast<const double2*>(yscr + (int64_t)(lo & 0x3fffffffu) * 6)[lo >> 30];
+    y0 += t.x;
+    y1 += t.y;
+  }
+  a.y[(int64_t)g * 2] = fr ? y0 : 0.0;
+  a.y[(int64_t)g * 2 + 1] = fr ? y1 : 0.0;
+}
+
 template <int MODE>
 void launch_sphere(const Problem& p, const FvArgs& a, cudaStream_t st) {
   const int64_t nb = (a.V + PT - 1) / PT;
@@ -720,7 +928,17 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
     a.vscr = p.vscr.p;
     if (mode == MODE_GRAD) launch_sphere<MODE_GRAD>(p, a, c.stream);
     else if (mode == MODE_HVP && !c.psd) launch_sphere<MODE_HVP>(p, a, c.stream);
-    else throw Error(MG_ERR_UNSUPPORTED, "sphere face row kernel: gradient and unclamped HVP only");
+    else if (mode == MODE_HVP) {
+      if (p.fpsd.n < 6 * m.F) p.fpsd.alloc(6 * m.F > 0 ? 6 * m.F : 2);
+      timing_begin(p, c.stream);
+      if (m.F)
+        k_sphere_face_hvp_psd<<<(unsigned)((m.F + 127) / 128), 128, 0, c.stream>>>(a, p.any_fixed ? p.fixed.p : nullptr,
+                                                                                 p.fpsd.p);
+      MG_LAUNCH_CHECK();
+      if (m.Vr) k_rows_face_gather<<<(unsigned)((m.Vr + PT - 1) / PT), PT, 0, c.stream>>>(a, p.fpsd.p);
+      MG_LAUNCH_CHECK();
+      timing_end(p, c.stream);
+    } else throw Error(MG_ERR_UNSUPPORTED, "sphere face kernels: gradient and HVP only");
     return mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
   }
   switch (mode) {

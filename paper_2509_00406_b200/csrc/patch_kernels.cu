@@ -359,9 +359,8 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   const Mesh& m = *p.mesh;
   if (p.ev_fast) return launch_patch_ev(p, mode, c, partial_offset);
   int64_t n_fast = 0;
-  // face row kernels: Dirichlet in every mode; sphere for gradient / unclamped HVP
-  const bool fast = p.fv_fast && (p.terms[0].dev.type != MG_TERM_SPHERE || mode == MODE_GRAD ||
-                                  (mode == MODE_HVP && !c.psd));
+  // face row kernels: Dirichlet in every mode; sphere for gradient / HVP
+  const bool fast = p.fv_fast && (p.terms[0].dev.type != MG_TERM_SPHERE || mode == MODE_GRAD || mode == MODE_HVP);
   if (fast) n_fast = launch_patch_fv(p, mode, c, partial_offset);
   PatchArgs a;
   a.R = m.patches.R;

@@ -98,6 +98,122 @@ MG_DI void jacobi_project(double* A, double floor) {
   (void)T;
 }
 
+// 1/x: hardware estimate + two Newton steps (full fp64 precision for finite,
+// non-zero x; the callers only pass such values)
+MG_DI double psd_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Jacobi rotation zeroing a_pq: t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)),
+// theta = (a_qq - a_pp) / (2 a_pq), written without divisions
+MG_DI void jacobi_angle(double app, double aqq, double apq, double& c, double& s, double& t) {
+  const double d = aqq - app, b = 2.0 * apq;
+  const double h = ::sqrt(d * d + b * b);
+  const double sg = ((d >= 0.0) == (b >= 0.0)) ? 1.0 : -1.0;
+  t = sg * fabs(b) * psd_rcp(fabs(d) + h);
+  c = rsqrt(fma(t, t, 1.0));
+  s = t * c;
+}
+
+// round-robin (circle method) orderings: K/2 disjoint pairs per step, K-1
+// steps per sweep; the pairs of a step are independent, so their angles and
+// updates interleave (instruction-level parallelism on the rotation chain)
+template <int K> struct RoundRobin;
+// pair k of step st: 4-bit fields of a packed code, (0,1),(2,3) / (0,2),(1,3) / ...
+template <> struct RoundRobin<4> {
+  static constexpr int S = 3, PP = 2;
+  static constexpr unsigned long long PC = 0x101020ull, QC = 0x233231ull;
+};
+template <> struct RoundRobin<6> {
+  static constexpr int S = 5, PP = 3;
+  static constexpr unsigned long long PC = 0x210130120410320ull, QC = 0x345254543532451ull;
+};
+MG_DI constexpr int rr_field(unsigned long long code, int i) { return (int)((code >> (4 * i)) & 0xF); }
+
+// In-place: A (packed K x K, symmetric) -> Q max(Lambda, floor) Q^T, parallel
+// ordering (K = 4, 6)
+template <int K>
+MG_DI void jacobi_project_rr(double* A, double floor) {
+  using RR = RoundRobin<K>;
+  double Q[K][K];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) Q[i][j] = (i == j) ? 1.0 : 0.0;
+  double fro2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) fro2 += (i == j ? 1.0 : 2.0) * A[tri(i, j)] * A[tri(i, j)];
+  const double tol2 = fro2 * 1e-30;
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    double off = 0.0;
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < i; ++j) off += A[tri(i, j)] * A[tri(i, j)];
+    if (!(off > tol2)) break;
+#pragma unroll
+    for (int st = 0; st < RR::S; ++st) {
+      double c[RR::PP], sn[RR::PP], t[RR::PP];
+#pragma unroll
+      for (int k = 0; k < RR::PP; ++k) {
+        const int p = rr_field(RR::PC, st * RR::PP + k), q = rr_field(RR::QC, st * RR::PP + k);
+        const double apq = A[tri(q, p)];
+        if (apq != 0.0) {
+          jacobi_angle(A[tri(p, p)], A[tri(q, q)], apq, c[k], sn[k], t[k]);
+        } else {
+          c[k] = 1.0;
+          sn[k] = 0.0;
+          t[k] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RR::PP; ++k) {
+        const int p = rr_field(RR::PC, st * RR::PP + k), q = rr_field(RR::QC, st * RR::PP + k);
+        const double apq = A[tri(q, p)];
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+          if (m != p && m != q) {
+            const double amp = A[tri(m, p)], amq = A[tri(m, q)];
+            A[tri(m, p)] = c[k] * amp - sn[k] * amq;
+            A[tri(m, q)] = sn[k] * amp + c[k] * amq;
+          }
+        }
+        A[tri(p, p)] -= t[k] * apq;
+        A[tri(q, q)] += t[k] * apq;
+        A[tri(q, p)] = 0.0;
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+          const double qmp = Q[m][p], qmq = Q[m][q];
+          Q[m][p] = c[k] * qmp - sn[k] * qmq;
+          Q[m][q] = sn[k] * qmp + c[k] * qmq;
+        }
+      }
+    }
+  }
+  double w[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double l = A[tri(j, j)];
+    w[j] = l > floor ? l : floor;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc += Q[i][j] * w[j] * Q[k][j];
+      A[tri(i, k)] = acc;
+    }
+}
+
 // Is A - floor*I positive definite? (Cholesky in registers.) When it is,
 // max(Lambda, floor) == Lambda and the projector is A itself up to rounding
 // (a misclassification can only happen when an eigenvalue is within rounding
@@ -132,6 +248,7 @@ MG_DI void project_if_needed(double* A, double floor) {
   if (shifted_pd<K>(A, floor)) return;
   if constexpr (K == 2) psd_small::project2(A, floor);
   else if constexpr (K == 3) psd_small::project3(A, floor);
+  else if constexpr (K == 4 || K == 6) jacobi_project_rr<K>(A, floor);
   else jacobi_project<K>(A, floor);
 }
 
