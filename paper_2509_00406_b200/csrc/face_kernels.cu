@@ -700,73 +700,43 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
     }
   }
   const bool barrier = a.t.c[0] != 0.0, stretch = a.t.c[1] != 0.0;
-  // p-space gradient and Hessian blocks (upper triangle of blocks)
-  double g[3][3], Hp[3][3][3][3];
+  // p-space gradient; the Hessian enters only through its x-space blocks
+  //   barrier: Hp = c c^T / det^2 + (1/det) E, E[q][q+1] = [p_{q+2}]x, E[q][q+2] = -[p_{q+1}]x
+  //   stretch: Hp[q][q] = 4 I, Hp[q][q'] = -2 I
+  double g[3][3], jc[3][2];
+  double id = 0.0, chk = 0.0;
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
     for (int c = 0; c < 3; ++c) g[q][c] = 0.0;
-#pragma unroll
-  for (int q = 0; q < 3; ++q)
-#pragma unroll
-    for (int q2 = 0; q2 < 3; ++q2)
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) Hp[q][q2][i][j] = 0.0;
-  double chk = 0.0;
   if (barrier) {
     double cc[3][3];
     cross3(p[1], p[2], cc[0]);
     cross3(p[2], p[0], cc[1]);
     cross3(p[0], p[1], cc[2]);
     const double det = p[0][0] * cc[0][0] + p[0][1] * cc[0][1] + p[0][2] * cc[0][2];
-    const double id = 1.0 / det;
+    id = 1.0 / det;
     chk += ::log(det);
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
+    for (int q = 0; q < 3; ++q) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) g[q][c] -= cc[q][c] * id;
-    const double id2 = id * id;
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int q2 = 0; q2 < 3; ++q2)
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) Hp[q][q2][i][j] += cc[q][i] * cc[q2][j] * id2;
-    // d2 det / dp_q dp_q2 = eps-blocks: (q, q2, third vertex k) cyclic -> -[p_k]x ... written out:
-    // d c_q / d p_q2 for q2 = q+1: -[p_{q+2}]x ; q2 = q+2: +[p_{q+1}]x ; [v]x = [[0,-v2,v1],[v2,0,-v0],[-v1,v0,0]]
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int qa = q == 2 ? 0 : q + 1, qb = q == 0 ? 2 : q - 1;  // q+1, q+2 (mod 3)
-      const double* pk = p[qb];  // for q2 = qa the third vertex is qb
-      // D2[q][qa] = -[p_qb]x  ->  Hp -= id * D2
-      const double X[3][3] = {{0.0, -pk[2], pk[1]}, {pk[2], 0.0, -pk[0]}, {-pk[1], pk[0], 0.0}};
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          Hp[q][qa][i][j] += id * X[i][j];   // -id * (-[p_qb]x)
-          Hp[qa][q][j][i] += id * X[i][j];   // transpose block
-        }
+      for (int i = 0; i < 2; ++i) jc[q][i] = (J[q][0][i] * cc[q][0] + J[q][1][i] * cc[q][1] + J[q][2][i] * cc[q][2]) * id;
     }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) jc[q][0] = jc[q][1] = 0.0;
   }
   if (stretch) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const int qa = q == 2 ? 0 : q + 1, qb = q == 0 ? 2 : q - 1;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        g[q][c] += 2.0 * (2.0 * p[q][c] - p[qa][c] - p[qb][c]);
-        Hp[q][q][c][c] += 4.0;
-        Hp[q][qa][c][c] -= 2.0;
-        Hp[q][qb][c][c] -= 2.0;
-      }
+      for (int c = 0; c < 3; ++c) g[q][c] += 2.0 * (2.0 * p[q][c] - p[qa][c] - p[qb][c]);
     }
   }
-  // x-space packed 6x6 (rows / columns 2q + i)
+  // x-space packed 6x6 (rows / columns 2q + i), blocks q2 <= q
   double H[21];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
@@ -778,24 +748,30 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
         for (int j = 0; j < 2; ++j) {
           const int R = 2 * q + i, C = 2 * q2 + j;
           if (C > R) continue;
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            double t = 0.0;
-#pragma unroll
-            for (int l = 0; l < 3; ++l) t += Hp[q][q2][k][l] * J[q2][l][j];
-            acc += J[q][k][i] * t;
+          double acc = jc[q][i] * jc[q2][j];
+          const double jj = J[q][0][i] * J[q2][0][j] + J[q][1][i] * J[q2][1][j] + J[q][2][i] * J[q2][2][j];
+          if (stretch) acc += (q == q2 ? 4.0 : -2.0) * jj;
+          if (barrier && q != q2) {
+            // q2 = q + 1 (mod 3): + [p_{q+2}]x ; q2 = q + 2: - [p_{q+1}]x
+            const int qa = q == 2 ? 0 : q + 1, qb = q == 0 ? 2 : q - 1;
+            const bool next = q2 == qa;
+            const double* pk = next ? p[qb] : p[qa];
+            double cx[3];
+            const double v3[3] = {J[q2][0][j], J[q2][1][j], J[q2][2][j]};
+            cross3(pk, v3, cx);
+            const double e = J[q][0][i] * cx[0] + J[q][1][i] * cx[1] + J[q][2][i] * cx[2];
+            acc += next ? id * e : -id * e;
           }
           if (q == q2) {  // T_q[i][j] = g_q . d2 p_q / dx_i dx_j (symmetrised)
-            auto tij = [&](int ii, int jj) {
+            auto tij = [&](int ii, int jj2) {
               const double pbi = p[q][0] * B[q][0][ii] + p[q][1] * B[q][1][ii] + p[q][2] * B[q][2][ii];
-              const double rdj = p[q][0] * B[q][0][jj] + p[q][1] * B[q][1][jj] + p[q][2] * B[q][2][jj];
+              const double rdj = p[q][0] * B[q][0][jj2] + p[q][1] * B[q][1][jj2] + p[q][2] * B[q][2][jj2];
               double gp = 0.0, gpd = 0.0, pdb = 0.0, gb = 0.0;
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
                 gp += g[q][c] * p[q][c];
-                gpd += g[q][c] * J[q][c][jj];
-                pdb += J[q][c][jj] * B[q][c][ii];
+                gpd += g[q][c] * J[q][c][jj2];
+                pdb += J[q][c][jj2] * B[q][c][ii];
                 gb += g[q][c] * B[q][c][ii];
               }
               const double ir = 1.0 / rho[q];
