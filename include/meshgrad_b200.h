@@ -129,9 +129,18 @@ MG_API int mg_problem_add_term(mg_problem* prob, int term_type, int op, const do
  * paper_2509_00406_b200/jit.py from csrc/jit_kernel.cuh for this var_dim,
  * exporting mg_jit_{energy,grad,hess,hess_psd,hvp,hvp_psd}; attrs_d are its
  * per-element attribute streams (device fp64, caller-owned, at most 64). Problems with a
- * traced term assemble element-parallel with fp64 atomics. */
+ * traced term assemble element-parallel: into per-element scratch plus a
+ * fixed-order gather when deterministic, with fp64 atomics otherwise. */
 MG_API int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* image,
                                    const double* const* attrs_d, int num_attrs, int* term_id);
+/* A traced VV (vertex-neighbourhood) term over an explicit selection: sel_d is
+ * (M, P) int32 on the device (caller-owned), row = center vertex then its
+ * one-ring ascending (ref problem.py:340-353); the reference groups VV
+ * elements by valence, so register one term per valence group (P = 1 + d,
+ * d <= 32). The module is traced for that P. */
+MG_API int mg_problem_add_jit_term_sel(mg_problem* prob, int op, int var_dim, int P, const int32_t* sel_d, int64_t M,
+                                       const void* image, const double* const* attrs_d, int num_attrs,
+                                       int* term_id);
 MG_API int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d);
 /* Rebind one attribute pointer of a registered term (closure arrays that the
  * reference rewrites in place between calls, apps/cloth.py:128, sphere.py:121-127). */

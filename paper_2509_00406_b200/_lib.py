@@ -49,6 +49,8 @@ SIGNATURES = [
     ("mg_problem_add_term", _INT, [_P, _INT, _INT, ctypes.POINTER(_DBL), _INT, ctypes.POINTER(_P), _INT,
                                    ctypes.POINTER(_INT)]),
     ("mg_problem_add_jit_term", _INT, [_P, _INT, _INT, _P, ctypes.POINTER(_P), _INT, ctypes.POINTER(_INT)]),
+    ("mg_problem_add_jit_term_sel", _INT, [_P, _INT, _INT, _INT, _P, _I64, _P, ctypes.POINTER(_P), _INT,
+                                            ctypes.POINTER(_INT)]),
     ("mg_problem_set_jit_attr", _INT, [_P, _INT, _INT, _P]),
     ("mg_problem_set_attr", _INT, [_P, _INT, _INT, _P]),
     ("mg_precompute_sparsity", _INT, [_P, _I64P, _P]),

@@ -279,6 +279,33 @@ int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* i
   });
 }
 
+int mg_problem_add_jit_term_sel(mg_problem* prob, int op, int var_dim, int P, const int32_t* sel_d, int64_t M,
+                                const void* image, const double* const* attrs_d, int num_attrs, int* term_id) {
+  if (!prob || !image) return fail(MG_ERR_VALUE, "problem/image is NULL");
+  if (op != MG_OP_VV) return fail(MG_ERR_UNSUPPORTED, "explicit selections are for VV neighbourhood terms");
+  if (var_dim != prob->p.n) return fail(MG_ERR_VALUE, "traced module was generated for another var_dim");
+  if (P < 1 || P > 33) return fail(MG_ERR_VALUE, "VV neighbourhoods have 1..33 vertices (valence cap 32)");
+  if (M < 0 || (M > 0 && !sel_d)) return fail(MG_ERR_VALUE, "selection is NULL");
+  if (num_attrs < 0 || num_attrs > JIT_MAX_ATTRS) return fail(MG_ERR_VALUE, "at most 64 attribute streams");
+  return guard([&] {
+    Term t;
+    std::memset(&t.dev, 0, sizeof(t.dev));
+    t.dev.type = MG_TERM_JIT;
+    t.dev.op = op;
+    t.dev.P = P;
+    t.M = M;
+    t.sel = sel_d;
+    t.jit = true;
+    for (int i = 0; i < num_attrs; ++i) t.jit_attrs.push_back(attrs_d[i]);
+    jit_load(t, image);
+    prob->p.terms.push_back(std::move(t));
+    prob->p.pattern_ready = false;
+    prob->p.layout_ready = false;
+    prob->p.gather_ready = false;
+    if (term_id) *term_id = (int)prob->p.terms.size() - 1;
+  });
+}
+
 int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d) {
   if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
   if (term_id < 0 || term_id >= (int)prob->p.terms.size() || !prob->p.terms[term_id].jit)

@@ -401,7 +401,7 @@ int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx&
   a.w = c.w;
   a.fixed = p.any_fixed ? p.fixed.p : nullptr;
   a.owned = p.mesh->owned.p;
-  a.sel = op_sel(*p.mesh, t.dev.op);
+  a.sel = term_sel(*p.mesh, t);
   a.bids = t.bids.p;
   a.grad = c.grad;
   a.hess = c.hess;

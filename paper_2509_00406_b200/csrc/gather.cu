@@ -122,7 +122,7 @@ void build_gather(Problem& p, cudaStream_t s) {
       const Term& t = p.terms[ti];
       const int64_t cnt = t.M * t.dev.P;
       if (cnt)
-        k_vec_keys<<<grid_for(cnt), TPB, 0, s>>>(op_sel(m, t.dev.op), t.dev.P, t.M, (int)ti, n, t.gv_base,
+        k_vec_keys<<<grid_for(cnt), TPB, 0, s>>>(term_sel(m, t), t.dev.P, t.M, (int)ti, n, t.gv_base,
                                                  p.any_fixed ? p.fixed.p : nullptr, m.owned.p, keys.p + o, vals.p + o);
       MG_LAUNCH_CHECK();
       o += cnt;

@@ -113,6 +113,9 @@ struct Term {
   void* jit_module = nullptr;
   void* jit_fn[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   std::vector<const double*> jit_attrs;
+  // explicit element vertex lists (M, P) (caller-owned device array), e.g. the
+  // VV neighbourhoods of one valence group; null: the op's mesh arrays
+  const int32_t* sel = nullptr;
   // deterministic gather mode: this term's offsets in the problem's scratch
   int64_t gv_base = 0, gh_base = 0;
 };
@@ -197,6 +200,7 @@ inline const int32_t* op_sel(const Mesh& m, int op) {
   if (op == MG_OP_EV) return m.edges.p;
   return nullptr;
 }
+inline const int32_t* term_sel(const Mesh& m, const Term& t) { return t.sel ? t.sel : op_sel(m, t.dev.op); }
 inline int64_t op_count(const Mesh& m, int op) {
   if (op == MG_OP_FV) return m.F;
   if (op == MG_OP_EV) return m.E;

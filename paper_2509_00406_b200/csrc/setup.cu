@@ -232,7 +232,7 @@ void build_pattern(Problem& p, cudaStream_t s) {
     int64_t off = 0;
     for (auto& t : p.terms) {
       int64_t cnt = t.M * t.dev.P * t.dev.P;
-      if (cnt) k_pair_keys<<<grid_for(cnt), TPB, 0, s>>>(op_sel(m, t.dev.op), t.dev.P, t.M, V,
+      if (cnt) k_pair_keys<<<grid_for(cnt), TPB, 0, s>>>(term_sel(m, t), t.dev.P, t.M, V,
                                                           p.any_fixed ? p.fixed.p : nullptr, m.owned.p, keys + off);
       MG_LAUNCH_CHECK();
       off += cnt;
@@ -270,7 +270,7 @@ void build_pattern(Problem& p, cudaStream_t s) {
   for (auto& t : p.terms) {
     int64_t cnt = t.M * t.dev.P * t.dev.P;
     t.bids.alloc(cnt > 0 ? cnt : 1);
-    if (cnt) k_bids<<<grid_for(cnt), TPB, 0, s>>>(op_sel(m, t.dev.op), t.dev.P, t.M, V,
+    if (cnt) k_bids<<<grid_for(cnt), TPB, 0, s>>>(term_sel(m, t), t.dev.P, t.M, V,
                                                    p.any_fixed ? p.fixed.p : nullptr, m.owned.p, keys, nnzb, t.bids.p);
     MG_LAUNCH_CHECK();
   }

@@ -220,22 +220,32 @@ MG_JIT_INSTANTIATE(Traced, {self.P}, {self.n})
 """
 
 
-def trace_callback(fn, op: str, n: int, num_elements: int, sel=None) -> TracedTerm:
+def trace_callback(fn, op: str, n: int, num_elements: int, sel=None, index=None) -> TracedTerm:
     """Run `fn(handle, nbrs, x)` once on symbolic inputs (ref problem.py:440-452).
-    sel: (M, P) vertex ids of the elements (EV / FV), so that a vertex batch's
-    `index` holds the slot's vertex ids like the reference's `_Batch`."""
+    sel: (M, P) vertex ids of the elements (EV / FV / VV), so that a vertex
+    batch's `index` holds the slot's vertex ids like the reference's `_Batch`.
+    VV (one valence group): sel rows are the center then its one-ring, `index`
+    the centers; the handle is the center (slot 0), nbrs the ring slots."""
     from .active import ActiveVec
 
-    P = {"V": 1, "EV": 2, "FV": 3}[op]
+    if op == "VV":
+        if sel is None or index is None:
+            raise ValueError("VV callbacks need the group's neighbourhoods and centers")
+        P = int(np.asarray(sel).shape[1])
+    else:
+        P = {"V": 1, "EV": 2, "FV": 3}[op]
     g = _Graph(num_elements)
-    index = np.arange(num_elements, dtype=np.int64)
+    index = np.arange(num_elements, dtype=np.int64) if index is None else np.asarray(index, dtype=np.int64)
     vecs = [ActiveVec([Sym(g, f"X[{q}][{c}]") for c in range(n)]) for q in range(P)]
-    kind = {"V": "vertex", "EV": "edge", "FV": "face"}[op]
-    handle = _Handle(kind, index, slot=0 if op == "V" else None)
+    kind = {"V": "vertex", "VV": "vertex", "EV": "edge", "FV": "face"}[op]
+    handle = _Handle(kind, index, slot=0 if op in ("V", "VV") else None)
     if op != "V" and sel is None:
         raise ValueError("edge / face callbacks need the element vertex lists")
-    nbrs = (handle,) if op == "V" else tuple(
-        _Handle("vertex", np.ascontiguousarray(np.asarray(sel)[:, q], dtype=np.int64), slot=q) for q in range(P))
+    if op == "V":
+        nbrs = (handle,)
+    else:
+        cols = [_Handle("vertex", np.ascontiguousarray(np.asarray(sel)[:, q], dtype=np.int64), slot=q) for q in range(P)]
+        nbrs = tuple(cols[1:]) if op == "VV" else tuple(cols)
     out = fn(handle, nbrs, _Vars(vecs))
     if isinstance(out, Sym):
         ret = out.name

@@ -167,7 +167,7 @@ def read_matrix_market(path):
 
 
 class _TermRecord:
-    __slots__ = ("term", "kind", "op", "host_attrs", "dev_attrs", "tid", "traced")
+    __slots__ = ("term", "kind", "op", "host_attrs", "dev_attrs", "tid", "traced", "groups", "sel", "index", "error")
 
     def __init__(self, term, kind, op):
         self.term = term
@@ -177,6 +177,10 @@ class _TermRecord:
         self.dev_attrs = []
         self.tid = -1
         self.traced = None
+        self.groups = None  # VV: one engine term per valence group (sub-records)
+        self.sel = None     # VV group: (M, P) neighbourhoods (host) and their device copy in dev_attrs' keep-alive
+        self.index = None   # VV group: center vertex ids
+        self.error = None   # deferred layout error (valence cap), raised like the reference at layout time
 
 
 class Problem:
@@ -279,8 +283,8 @@ class Problem:
         symbolic inputs, compiled to an sm_100a module, launched by the engine
         (jit.py). Closure arrays indexed by `handle.index` become per-element
         attribute streams (refresh_attrs() re-gathers them)."""
-        if op not in (Op.V, Op.EV, Op.FV):
-            raise NotImplementedError(f"traced callbacks support the V, EV and FV ops, not {op.name}")
+        if op is Op.VV:
+            return self._add_vv_term(kind, fn)
         from . import jit
 
         torch = _torch()
@@ -300,6 +304,70 @@ class Problem:
         self._pattern_ready = False
         return len(self._terms) - 1
 
+    def _one_rings(self):
+        """Vertex -> one-ring, ascending (ref mesh.py vertex_to_vertex): CSR over the edges."""
+        e = np.asarray(self.mesh.edges, dtype=np.int64).reshape(-1, 2)
+        nv = self.mesh.num_vertices
+        a = np.concatenate([e[:, 0], e[:, 1]])
+        b = np.concatenate([e[:, 1], e[:, 0]])
+        order = np.lexsort((b, a))
+        a, b = a[order], b[order]
+        off = np.zeros(nv + 1, dtype=np.int64)
+        np.cumsum(np.bincount(a, minlength=nv), out=off[1:])
+        return off, b
+
+    def _add_vv_term(self, kind: Element, fn) -> int:
+        """A traced VV term (ref problem.py:340-353): the neighbourhood (center,
+        one-ring ascending) has one arity per valence, so each valence group is
+        traced and registered as its own engine term over an explicit
+        selection; a valence above the cap fails at layout time, as in the
+        reference."""
+        from . import jit
+
+        torch = _torch()
+        rec = _TermRecord(fn, kind, Op.VV)
+        rec.groups = []
+        off, ring = self._one_rings()
+        degs = np.diff(off)
+        if degs.size and degs.max() > self.valence_cap:
+            worst = int(np.argmax(degs))
+            rec.error = ValueError(
+                f"vertex {worst} has valence {int(degs[worst])}, exceeding the cap {self.valence_cap}")
+            self._terms.append(rec)
+            self._pattern_ready = False
+            return len(self._terms) - 1
+        for d in np.unique(degs):
+            ids = np.flatnonzero(degs == d).astype(np.int64)
+            sel = np.empty((len(ids), 1 + int(d)), dtype=np.int64)
+            sel[:, 0] = ids
+            if d:
+                sel[:, 1:] = ring[off[ids][:, None] + np.arange(int(d))]
+            tt = jit.trace_callback(fn, "VV", self.n, len(ids), sel, index=ids)
+            image = jit.compile_term(tt)
+            sub = _TermRecord(fn, kind, Op.VV)
+            sub.traced = tt
+            sub.sel, sub.index = sel, ids
+            sub.dev_attrs = [torch.from_numpy(a).to(self._dev) for a in tt.attrs]
+            sub.host_attrs = [torch.from_numpy(sel.astype(np.int32)).to(self._dev)]  # keeps the selection alive
+            buf = ctypes.create_string_buffer(image, len(image))
+            cattrs = (ctypes.c_void_p * max(1, len(sub.dev_attrs)))(*[t.data_ptr() for t in sub.dev_attrs])
+            tid = ctypes.c_int()
+            _lib.check(self._lib.mg_problem_add_jit_term_sel(
+                self._h, _lib.MG_OP["VV"], self.n, sel.shape[1], sub.host_attrs[0].data_ptr(), len(ids), buf, cattrs,
+                len(sub.dev_attrs), ctypes.byref(tid)))
+            sub.tid = tid.value
+            rec.groups.append(sub)
+        self._terms.append(rec)
+        self._pattern_ready = False
+        return len(self._terms) - 1
+
+    def _check_terms(self):
+        if not self._terms:
+            raise ValueError("no energy terms registered")
+        for rec in self._terms:
+            if rec.error is not None:
+                raise rec.error
+
     def _sync_attrs(self):
         if self.live_host_attrs:
             self.refresh_attrs()
@@ -316,6 +384,14 @@ class Problem:
         from . import jit
 
         for rec in self._terms:
+            if rec.groups is not None:  # VV: every valence group
+                for sub in rec.groups:
+                    tt = jit.trace_callback(rec.term, "VV", self.n, len(sub.index), sub.sel, index=sub.index)
+                    if tt.source() != sub.traced.source():
+                        raise ValueError("a traced callback changed its expression; register it again")
+                    for dev, host in zip(sub.dev_attrs, tt.attrs):
+                        dev.copy_(_torch().from_numpy(host))
+                continue
             if rec.traced is not None:  # re-gather the closure arrays of a traced callback
                 tt = jit.trace_callback(rec.term, rec.op.name, self.n, self._num_elements(rec.op),
                                         self._element_vertices(rec.op))
@@ -377,8 +453,7 @@ class Problem:
 
     def precompute_sparsity(self) -> BlockSparseMatrix:
         """Device-built block pattern (ref problem.py:383-416)."""
-        if not self._terms:
-            raise ValueError("no energy terms registered")
+        self._check_terms()
         torch = _torch()
         nnzb = ctypes.c_int64()
         _lib.check(self._lib.mg_precompute_sparsity(self._h, ctypes.byref(nnzb), _lib.stream_ptr()))
@@ -401,8 +476,7 @@ class Problem:
         (ref problem.py:504-549). With `sync=False` the call stays
         stream-ordered and returns NaN; read `energy_device` later."""
         t0 = time.perf_counter()
-        if not self._terms:
-            raise ValueError("no energy terms registered")
+        self._check_terms()
         if psd_floor is not None and not self.with_hessian:
             raise ValueError("psd_floor requires a Hessian-mode problem")
         if psd_floor is not None and psd_floor <= 0:
@@ -428,8 +502,7 @@ class Problem:
         """Total energy at a trial state; leaves the problem untouched
         (ref problem.py:551-576)."""
         t0 = time.perf_counter()
-        if not self._terms:
-            raise ValueError("no energy terms registered")
+        self._check_terms()
         xd = self._vec_in(x_trial, "trial state must have shape ({},)")
         self._sync_attrs()
         out = _torch().empty(1, dtype=_torch().float64, device=self._dev)
@@ -455,8 +528,7 @@ class Problem:
         numpy in -> numpy out; CUDA tensors in -> CUDA tensor out."""
         t0 = time.perf_counter()
         torch = _torch()
-        if not self._terms:
-            raise ValueError("no energy terms registered")
+        self._check_terms()
         if psd_floor is not None and psd_floor <= 0:
             raise ValueError("floor must be positive")
         host = not isinstance(v, torch.Tensor)
