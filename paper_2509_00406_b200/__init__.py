@@ -20,7 +20,9 @@ from .mesh import (
     generate_icosphere,
     grid_arrays,
     icosphere_arrays,
+    load_obj,
     punctured_icosphere_arrays,
+    save_obj,
 )
 from .problem import BlockSparseMatrix, Problem, read_matrix_market
 from .terms import EdgeLength, Gravity, Inertia, SphereBarrierStretch, Spring, SymDirichlet
@@ -52,10 +54,12 @@ __all__ = [
     "generate_icosphere",
     "grid_arrays",
     "icosphere_arrays",
+    "load_obj",
     "log",
     "positive_guard",
     "punctured_icosphere_arrays",
     "read_matrix_market",
+    "save_obj",
     "sin",
     "sqrt",
 ]

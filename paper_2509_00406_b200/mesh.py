@@ -33,7 +33,9 @@ __all__ = [
     "generate_icosphere",
     "grid_arrays",
     "icosphere_arrays",
+    "load_obj",
     "punctured_icosphere_arrays",
+    "save_obj",
 ]
 
 DEFAULT_VALENCE_CAP = 32
@@ -311,3 +313,61 @@ def punctured_icosphere_arrays(subdivisions: int):
     if np.max(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]) < 0:
         uv = uv[:, ::-1].copy()
     return p, f, uv
+
+
+# ---------------------------------------------------------------- OBJ files
+
+def _obj_records(path):
+    """(line number, tag, fields) of the v / f records of an OBJ file; every
+    other record type (vn, vt, o, g, s, usemtl, ...) and comments are skipped."""
+    with open(path, "r") as fh:
+        for ln, line in enumerate(fh, start=1):
+            fields = line.split()
+            if fields and fields[0] in ("v", "f"):
+                yield ln, fields[0], fields[1:]
+
+
+def load_obj(path, patch_target: int = DEFAULT_PATCH_TARGET) -> "Mesh":
+    """Wavefront OBJ with `v` and triangular `f` records, 1-indexed, /vt/vn
+    suffixes ignored (ref mesh.py:376-418: same accepted input and MeshError
+    texts, with the offending line number)."""
+    pos, tri = [], []
+    for ln, tag, fields in _obj_records(path):
+        if tag == "v":
+            if len(fields) < 3:
+                raise MeshError(f"{path}: line {ln}: vertex record needs 3 coordinates")
+            try:
+                pos.append((float(fields[0]), float(fields[1]), float(fields[2])))
+            except ValueError as exc:
+                raise MeshError(f"{path}: line {ln}: bad vertex coordinate: {exc}") from None
+            continue
+        if len(fields) != 3:
+            raise MeshError(f"{path}: line {ln}: non-triangular face with {len(fields)} vertices")
+        corner = []
+        for ref in fields:
+            head = ref.partition("/")[0]
+            try:
+                k = int(head)
+            except ValueError:
+                raise MeshError(f"{path}: line {ln}: bad face index {head!r}") from None
+            if k < 1:
+                raise MeshError(f"{path}: line {ln}: face indices must be positive (1-indexed)")
+            corner.append(k - 1)
+        tri.append(corner)
+    if not tri:
+        raise MeshError(f"{path}: no faces")
+    try:
+        return Mesh(np.asarray(pos, dtype=np.float64).reshape(-1, 3), np.asarray(tri, dtype=np.int64),
+                    patch_target=patch_target)
+    except MeshError as exc:
+        raise MeshError(f"{path}: {exc}") from None
+
+
+def save_obj(path, positions, faces) -> None:
+    """Vertices then faces, 1-indexed, 6 significant digits (ref mesh.py:421-429)."""
+    p = np.asarray(positions, dtype=np.float64).reshape(-1, 3)
+    f = np.asarray(faces, dtype=np.int64).reshape(-1, 3) + 1
+    lines = [f"v {a:.6g} {b:.6g} {c:.6g}" for a, b, c in p]
+    lines += [f"f {a} {b} {c}" for a, b, c in f]
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + ("\n" if lines else ""))
