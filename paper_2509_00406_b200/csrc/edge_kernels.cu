@@ -379,6 +379,89 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
   cd = r > 0.0 ? (md - mt) * rcp_fast(r) : 0.0;
 }
 
+// Closed forms of the two builtin V terms (apps/cloth.py:102-104, 112-113) in
+// the dual's operation order: inertia 0.5 m |x - t|^2 (gradient m d, Hessian
+// m I exactly as 2 d_i * 0.5 m and 2 * 0.5 m round), gravity -h2 m x.g
+// (structurally zero Hessian: floor I under a clamp, problem.py:463-464).
+// The attribute loads of the first VPRE terms are issued early (vterms_load)
+// so their latency overlaps the incidence gathers. Pinned rows' outputs are
+// dropped by the caller, so no masking here; us is the masked direction.
+constexpr int VPRE = 2;
+template <int N>
+struct VPreload {
+  double m[VPRE], tg[VPRE][N];
+};
+template <int N, int MODE>
+MG_DI VPreload<N> vterms_load(const EvArgs& a, int g) {
+  VPreload<N> v;
+#pragma unroll
+  for (int j = 0; j < VPRE; ++j) {
+    v.m[j] = 0.0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) v.tg[j][c] = 0.0;
+    if (j < a.nvt) {
+      const TermDev& t = a.terms[a.vt_idx[j]];
+      v.m[j] = t.a[0][g];
+      if (MODE != MODE_HVP && t.type == MG_TERM_INERTIA) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) v.tg[j][c] = t.a[1][(int64_t)g * N + c];
+      }
+    }
+  }
+  return v;
+}
+template <int N, int MODE, bool PSD>
+MG_DI void vterm_one(const EvArgs& a, const TermDev& t, double m, const double* tg, const double* xs, const double* us,
+                     double& eacc, double* vec, double* dg) {
+  double hd;  // the term's (clamped) diagonal Hessian entry
+  if (t.type == MG_TERM_INERTIA) {
+    if constexpr (MODE != MODE_HVP) {
+      double d[N], r = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        d[c] = xs[c] - tg[c];
+        r = d[c] * d[c] + r;
+      }
+      eacc += r * (0.5 * m);
+#pragma unroll
+      for (int c = 0; c < N; ++c) vec[c] += d[c] * m;
+    }
+    hd = PSD ? (m > a.floor ? m : a.floor) : m;
+  } else {
+    if constexpr (MODE != MODE_HVP) {
+      double dot = xs[0] * t.c[1];
+#pragma unroll
+      for (int c = 1; c < N; ++c) dot = dot + xs[c] * t.c[1 + c];
+      eacc += (dot * m) * (-t.c[0]);
+#pragma unroll
+      for (int c = 0; c < N; ++c) vec[c] += (t.c[1 + c] * m) * (-t.c[0]);
+    }
+    hd = PSD ? a.floor : 0.0;
+  }
+  if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) dg[tri(c, c)] += hd;
+  } else if constexpr (MODE == MODE_HVP) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) vec[c] += hd * us[c];
+  }
+}
+template <int N, int MODE, bool PSD>
+MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const double* xs, const double* us,
+                         double& eacc, double* vec, double* dg) {
+#pragma unroll
+  for (int j = 0; j < VPRE; ++j)
+    if (j < a.nvt) vterm_one<N, MODE, PSD>(a, a.terms[a.vt_idx[j]], v.m[j], v.tg[j], xs, us, eacc, vec, dg);
+  for (int j = VPRE; j < a.nvt; ++j) {
+    const TermDev& t = a.terms[a.vt_idx[j]];
+    double tg[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+      tg[c] = (MODE != MODE_HVP && t.type == MG_TERM_INERTIA) ? t.a[1][(int64_t)g * N + c] : 0.0;
+    vterm_one<N, MODE, PSD>(a, t, t.a[0][g], tg, xs, us, eacc, vec, dg);
+  }
+}
+
 // incidences per row held in registers (the rest are streamed) and the
 // occupancy target: the Hessian kernel is bounded by its shared-memory row
 // buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
@@ -447,6 +530,7 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>:
       if constexpr (MODE == MODE_HVP) us[c] = fr ? a.w[(int64_t)g * N + c] : 0.0;
       else us[c] = 0.0;
     }
+    const VPreload<N> vpre = vterms_load<N, MODE>(a, g);
     // level 3: neighbour x (w) and the edge attribute, kept MAXI incidences
     // ahead of the compute (a rolling window over the ELL slots)
     double xo[EV_ELL_K][N], uo[EV_ELL_K][N], a0[EV_ELL_K];
@@ -469,39 +553,8 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>:
     for (int i = 0; i < N; ++i) vec[i] = 0.0;
 #pragma unroll
     for (int i = 0; i < T; ++i) dg[i] = 0.0;
-    {  // V terms (their attribute loads overlap the level-3 loads)
-      double wv[N];
-#pragma unroll
-      for (int c = 0; c < N; ++c) wv[c] = us[c];
-      const double* xr[1] = {xs};
-      const double* wr[1] = {wv};
-      for (int j = 0; j < a.nvt; ++j) {
-        const TermDev& t = a.terms[a.vt_idx[j]];
-        if (t.type == MG_TERM_INERTIA) {
-          ElemOut<MG_TERM_INERTIA, N, MODE, PSD> o;
-          eval_element<MG_TERM_INERTIA, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
-          eacc += o.val;
-#pragma unroll
-          for (int k = 0; k < N; ++k) vec[k] += o.g[k];
-          if constexpr (MODE == MODE_HESS) {
-            if (o.has_h)
-#pragma unroll
-              for (int k = 0; k < T; ++k) dg[k] += o.h[k];
-          }
-        } else {
-          ElemOut<MG_TERM_GRAVITY, N, MODE, PSD> o;
-          eval_element<MG_TERM_GRAVITY, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
-          eacc += o.val;
-#pragma unroll
-          for (int k = 0; k < N; ++k) vec[k] += o.g[k];
-          if constexpr (MODE == MODE_HESS) {
-            if (o.has_h)
-#pragma unroll
-              for (int k = 0; k < T; ++k) dg[k] += o.h[k];
-          }
-        }
-      }
-    }
+    // V terms (their attribute loads overlapped the level-3 loads)
+    vterms_closed<N, MODE, PSD>(a, g, vpre, xs, us, eacc, vec, dg);
     double* hrow = hbuf + ho;
     int pos = 0;
     // one incidence: contributions to this row
@@ -853,26 +906,8 @@ __global__ void __launch_bounds__(EV_TILE_ROWS, EV_TILE_MINB) k_tile_ev(const __
         xs[c] = XFREE ? 0.0 : x_[c * MV + tid];
         us[c] = W ? w_[c * MV + tid] : 0.0;
       }
-      {
-        const double* xr[1] = {xs};
-        const double* wr[1] = {us};
-        for (int j = 0; j < a.nvt; ++j) {
-          const TermDev& t = a.terms[a.vt_idx[j]];
-          if (t.type == MG_TERM_INERTIA) {
-            ElemOut<MG_TERM_INERTIA, N, MODE, PSD> o;
-            eval_element<MG_TERM_INERTIA, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
-            eacc += o.val;
-#pragma unroll
-            for (int k = 0; k < N; ++k) vec[k] += o.g[k];
-          } else {
-            ElemOut<MG_TERM_GRAVITY, N, MODE, PSD> o;
-            eval_element<MG_TERM_GRAVITY, N, MODE, PSD>(t, g, &g, xr, wr, &fr, a.floor, o);
-            eacc += o.val;
-#pragma unroll
-            for (int k = 0; k < N; ++k) vec[k] += o.g[k];
-          }
-        }
-      }
+      double dgv[TriN<N>::value];
+      vterms_closed<N, MODE, PSD>(a, g, vterms_load<N, MODE>(a, g), xs, us, eacc, vec, dgv);
       auto inc = [&](uint32_t s16) {
         const int sl = (int)(s16 & 0x7fff);
         const bool neg = (s16 >> 15) & 1;  // the row is the edge's second vertex
