@@ -77,6 +77,7 @@ void ensure_ready(Problem& p, cudaStream_t s) {
 }
 
 void ensure_partials(Problem& p, int64_t need) {
+  need += REDUCE_TAIL;
   if (need > p.partial_cap) {
     p.partials.alloc(need);
     p.partial_cap = need;
@@ -392,7 +393,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
     }
     reduce_partials(p.partials.p, np, energy_d, s,
                     (p.ev_fast || p.fv_fast) && p.deterministic && p.layout_ready ? p.redo.p : nullptr);
-    p.last_launches = launches + 1;
+    p.last_launches = launches + reduce_launches(np);
   });
 }
 
@@ -412,7 +413,7 @@ int mg_energy(mg_problem* prob, const double* x_d, double* energy_d, void* strea
       ++launches;
     }
     reduce_partials(p.partials.p, np, energy_d, s);
-    p.last_launches = launches + 1;
+    p.last_launches = launches + reduce_launches(np);
   });
 }
 

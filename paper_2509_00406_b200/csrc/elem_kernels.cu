@@ -278,6 +278,25 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
   }
 }
 
+// stage 1 of the two-level fixed-order energy sum: CTA b sums the chunk
+// [b C, (b+1) C) (thread t: t, t+256, ...; then the block tree) -> out[b]
+constexpr int RED_CHUNK = 2048;
+__global__ void __launch_bounds__(256) k_reduce_chunks(const double* __restrict__ partials, int64_t n, double* out) {
+  const int64_t base = (int64_t)blockIdx.x * RED_CHUNK;
+  double acc[RED_CHUNK / 256];
+#pragma unroll
+  for (int k = 0; k < RED_CHUNK / 256; ++k) {
+    const int64_t i = base + threadIdx.x + (int64_t)k * 256;
+    acc[k] = i < n ? partials[i] : 0.0;
+  }
+#pragma unroll
+  for (int w = RED_CHUNK / 512; w > 0; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w; ++k) acc[k] += acc[k + w];
+  const double s = block_sum(acc[0]);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 template <int N>
 __global__ void k_bsr_matvec(const int64_t* ro, const int32_t* col, const double* H, const double* v,
                              double* y, int64_t V) {
@@ -424,7 +443,17 @@ int64_t launch_elem(const Problem& p, const Term& t, Mode mode, const LaunchCtx&
 }
 
 void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag) {
-  k_reduce<<<1, 1024, 0, s>>>(partials, n, out, clear_flag);
+  if (n > 4 * RED_CHUNK) {
+    // chunk sums land right after the partials (the buffer carries REDUCE_TAIL spare slots)
+    const int64_t nb = (n + RED_CHUNK - 1) / RED_CHUNK;
+    if (nb > REDUCE_TAIL) throw Error(MG_ERR_UNSUPPORTED, "too many energy partials");
+    double* tmp = const_cast<double*>(partials) + n;
+    k_reduce_chunks<<<(unsigned)nb, 256, 0, s>>>(partials, n, tmp);
+    MG_LAUNCH_CHECK();
+    k_reduce<<<1, 1024, 0, s>>>(tmp, nb, out, clear_flag);
+  } else {
+    k_reduce<<<1, 1024, 0, s>>>(partials, n, out, clear_flag);
+  }
   MG_LAUNCH_CHECK();
 }
 

@@ -258,7 +258,10 @@ void build_gather(Problem& p, cudaStream_t s);
 void gather_vec(const Problem& p, double* out, cudaStream_t s);
 void gather_blocks(const Problem& p, double* out, cudaStream_t s);
 // fixed-order reduction of energy partials -> out[0]
+// (partials buffers carry REDUCE_TAIL spare slots after the largest n: chunk sums)
+constexpr int64_t REDUCE_TAIL = 1 << 16;
 void reduce_partials(const double* partials, int64_t n, double* out, cudaStream_t s, int* clear_flag = nullptr);
+inline int reduce_launches(int64_t n) { return n > 4 * 2048 ? 2 : 1; }
 void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s);
 void launch_block_jacobi(const Problem& p, const double* H, double* inv, cudaStream_t s);
 void launch_block_apply(const Problem& p, const double* inv, const double* r, double* y, cudaStream_t s);
