@@ -40,6 +40,7 @@ struct FvArgs {
   const int32_t* order;
   const uint32_t* rmeta;     // incidence count (sat. 255) | pinned << 8 | diagonal position << 16
   const uint64_t* ell;       // (KF, V) slot-major incidence records
+  const uint64_t* ellv;      // (KF, V) the incidence's other two corners (s+1, s+2)
   const int32_t* rinc_off;   // (V+1) CSR of all incidences
   const uint64_t* rrec;
   const int64_t* prow_ro;
@@ -533,34 +534,39 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
       }
       return retract(S + 3 * (int64_t)v, B1 + 3 * (int64_t)v, B2 + 3 * (int64_t)v, x0, x1, u0, u1);
     };
-    auto incidence = [&](uint64_t r64) {
-      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
-      const int64_t f = lo & 0x3fffffffu;
-      const int s = (int)(lo >> 30);
-      const int pins = (int)((hi >> 16) & 7);
-      Retract P[3];
-      (void)pins;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {  // the corners' retraction from the per-call vertex scratch
-        const double* o = a.vscr + 6 * (int64_t)a.faces[3 * f + q];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          P[q].p[c] = o[c];
-          P[q].pd[c] = MODE == MODE_HVP ? o[3 + c] : 0.0;
-        }
-      }
-      const int s1 = s == 2 ? 0 : s + 1, s2 = s == 0 ? 2 : s - 1;
-      // the row's corner and the next two, selected into registers
-      double ps[3], p1[3], p2[3], ds[3], d1[3], d2[3];
+    // the row's own retraction (p, pdot) once; the other two corners' per incidence
+    double ps[3], ds[3];
+    {
+      const double* o = a.vscr + 6 * (int64_t)g;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        ps[c] = s == 0 ? P[0].p[c] : (s == 1 ? P[1].p[c] : P[2].p[c]);
-        p1[c] = s1 == 0 ? P[0].p[c] : (s1 == 1 ? P[1].p[c] : P[2].p[c]);
-        p2[c] = s2 == 0 ? P[0].p[c] : (s2 == 1 ? P[1].p[c] : P[2].p[c]);
-        ds[c] = s == 0 ? P[0].pd[c] : (s == 1 ? P[1].pd[c] : P[2].pd[c]);
-        d1[c] = s1 == 0 ? P[0].pd[c] : (s1 == 1 ? P[1].pd[c] : P[2].pd[c]);
-        d2[c] = s2 == 0 ? P[0].pd[c] : (s2 == 1 ? P[1].pd[c] : P[2].pd[c]);
+        ps[c] = o[c];
+        ds[c] = MODE == MODE_HVP ? o[3 + c] : 0.0;
       }
+    }
+    struct Other {
+      double p1[3], p2[3], d1[3], d2[3];
+    };
+    auto load_other = [&](int o1, int o2) {
+      Other r;
+      const double* q1 = a.vscr + 6 * (int64_t)o1;
+      const double* q2 = a.vscr + 6 * (int64_t)o2;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        r.p1[c] = q1[c];
+        r.p2[c] = q2[c];
+        r.d1[c] = MODE == MODE_HVP ? q1[3 + c] : 0.0;
+        r.d2[c] = MODE == MODE_HVP ? q2[3 + c] : 0.0;
+      }
+      return r;
+    };
+    auto incidence = [&](uint64_t r64, const Other& O) {
+      const uint32_t lo = (uint32_t)r64;
+      const int s = (int)(lo >> 30);
+      const double* p1 = O.p1;
+      const double* p2 = O.p2;
+      const double* d1 = O.d1;
+      const double* d2 = O.d2;
       double val = 0.0, gs[3] = {0.0, 0.0, 0.0}, hs[3] = {0.0, 0.0, 0.0};
       if (barrier) {
         // det[p0 p1 p2] = ps . (p1 x p2) for the cyclic order (s, s1, s2)
@@ -605,10 +611,27 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
       }
     };
     const int ne = cnt < KF ? cnt : KF;
+    uint64_t ov[KF];
 #pragma unroll
-    for (int j = 0; j < KF; ++j)
-      if (j < ne) incidence(rc[j]);
-    for (int k = KF; k < cnt; ++k) incidence(a.rrec[a.rinc_off[row] + k]);
+    for (int j = 0; j < KF; ++j) ov[j] = a.ellv[(int64_t)j * a.V + row];
+    // corners streamed one incidence ahead of the compute
+    Other cur;
+    if (ne > 0) cur = load_other((int)(uint32_t)ov[0], (int)(ov[0] >> 32));
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      if (j < ne) {
+        Other nxt;
+        if (j + 1 < ne) nxt = load_other((int)(uint32_t)ov[j + 1], (int)(ov[j + 1] >> 32));
+        incidence(rc[j], cur);
+        cur = nxt;
+      }
+    }
+    for (int k = KF; k < cnt; ++k) {
+      const uint64_t r64 = a.rrec[a.rinc_off[row] + k];
+      const int64_t f = (uint32_t)r64 & 0x3fffffffu;
+      const int s = (int)((uint32_t)r64 >> 30);
+      incidence(r64, load_other(a.faces[3 * f + (s + 1) % 3], a.faces[3 * f + (s + 2) % 3]));
+    }
     // the row's own retraction: J, dJ
     const Retract R = corner(g, !fr);
     const double* b1 = B1 + 3 * (int64_t)g;
@@ -881,6 +904,7 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.prow_ro = p.prow_ro.p;
   a.hoff = p.hoff.p;
   a.faces = m.faces.p;
+  a.ellv = p.ellv.p;
   a.x = c.x;
   a.w = c.w;
   a.grad = c.grad;

@@ -409,6 +409,26 @@ __global__ void k_ell(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr,
   for (int k = 0; k < K; ++k) ell[(int64_t)k * Vr + i] = k < c ? rrec[k0 + k] : 0ull;
 }
 
+// face rows: the other two corners (s+1, s+2 mod 3) of each ELL face incidence,
+// so the row kernels skip the faces[] lookup (one dependent level less)
+__global__ void k_ellv(const int32_t* rinc_off, const uint64_t* rrec, const int32_t* faces, int64_t Vr, int K,
+                       uint64_t* ellv) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Vr) return;
+  const int k0 = rinc_off[i], c = rinc_off[i + 1] - k0;
+  for (int k = 0; k < K; ++k) {
+    uint64_t v = 0;
+    if (k < c) {
+      const uint32_t lo = (uint32_t)rrec[k0 + k];
+      const int64_t f = lo & 0x3fffffffu;
+      const int s = (int)(lo >> 30);
+      const uint32_t o1 = (uint32_t)faces[3 * f + (s + 1) % 3], o2 = (uint32_t)faces[3 * f + (s + 2) % 3];
+      v = (uint64_t)o1 | ((uint64_t)o2 << 32);
+    }
+    ellv[(int64_t)k * Vr + i] = v;
+  }
+}
+
 __global__ void k_patch_rows(const int32_t* order, const int64_t* ro, const uint8_t* dp, int64_t Vr,
                              int64_t* pro, int32_t* plen, uint8_t* pdp) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -830,9 +850,11 @@ void build_rows_fv(Problem& p, cudaStream_t s) {
   }
   p.rmeta.alloc(Vr > 0 ? Vr : 1);
   p.ell.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
+  p.ellv.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
   if (Vr) {
     k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, p.prow_len.p, Vr, p.rmeta.p);
     k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
+    k_ellv<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, EV_ELL_K, p.ellv.p);
   }
   MG_LAUNCH_CHECK();
   MG_CUDA(cudaStreamSynchronize(s));
