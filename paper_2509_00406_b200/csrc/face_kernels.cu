@@ -220,10 +220,16 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
     double* hrow = hbuf + ho;
     int nblk = 0;
+    // fan rows (incidences in rotation order around the vertex, setup): each
+    // off-diagonal block's two face contributions meet in registers and the
+    // block is written once; other rows accumulate in the cleared row buffer
+    const bool fan = (meta >> 9) & 1;
+    double carry[4] = {0.0, 0.0, 0.0, 0.0}, first[4] = {0.0, 0.0, 0.0, 0.0};
+    int first_pos = 255, last_pos2 = 255;
     if constexpr (MODE == MODE_HESS) {
-      // the row's blocks: off-diagonals accumulate (two faces per edge), so clear first
       nblk = (int)(((meta >> 24) & 0xff));
-      for (int k = 0; k < nblk * NN; ++k) hrow[k] = 0.0;
+      if (!fan)
+        for (int k = 0; k < nblk * NN; ++k) hrow[k] = 0.0;
     }
     double vec[N] = {0.0, 0.0}, dg[3] = {0.0, 0.0, 0.0};
     const double* R_all = a.t.a[0];
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
       return d;
     };
     auto sel3 = [](int i, double p0, double p1, double p2) { return i == 0 ? p0 : (i == 1 ? p1 : p2); };
-    auto incidence = [&](uint64_t r64, const FaceIn& d) {
+    auto incidence = [&](uint64_t r64, const FaceIn& d, int jidx) {
       const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
       const int s = (int)(lo >> 30);
       const int pos1 = (int)(hi & 0xff), pos2 = (int)((hi >> 8) & 0xff);
@@ -363,17 +369,36 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
           dg[0] += b[0];
           dg[1] += b[1];
           dg[2] += b[3];
-          if (pos1 != 255) {
-            blk(as, a1, false, b);
-            double* dst = hrow + pos1 * NN;
+          if (fan) {
+            // face j's first other corner is face j-1's second: finish that block
+            double b1[4], b2[4];
+            blk(as, a1, false, b1);
+            blk(as, a2, false, b2);
+            if (jidx == 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) dst[k] += b[k];
-          }
-          if (pos2 != 255) {
-            blk(as, a2, false, b);
-            double* dst = hrow + pos2 * NN;
+              for (int k = 0; k < 4; ++k) first[k] = b1[k];
+              first_pos = pos1;
+            } else if (pos1 != 255) {
+              double* dst = hrow + pos1 * NN;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) dst[k] += b[k];
+              for (int k = 0; k < 4; ++k) dst[k] = carry[k] + b1[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) carry[k] = b2[k];
+            last_pos2 = pos2;
+          } else {
+            if (pos1 != 255) {
+              blk(as, a1, false, b);
+              double* dst = hrow + pos1 * NN;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) dst[k] += b[k];
+            }
+            if (pos2 != 255) {
+              blk(as, a2, false, b);
+              double* dst = hrow + pos2 * NN;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) dst[k] += b[k];
+            }
           }
         } else {  // HVP: y_s = sum_t block(s,t) u_t over the face's corners (masked)
           double b[4];
@@ -409,7 +434,7 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
       if (j < ne) {
         FaceIn nxt;
         if (j + 1 < ne) nxt = load_face(rc[j + 1], fv[j + 1]);
-        incidence(rc[j], cur);
+        incidence(rc[j], cur, j);
         cur = nxt;
       }
     }
@@ -417,7 +442,29 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
       const uint64_t r64 = a.rrec[a.rinc_off[row] + k];
       const int64_t f = (uint32_t)r64 & 0x3fffffffu;
       const int v3[3] = {a.faces[3 * f], a.faces[3 * f + 1], a.faces[3 * f + 2]};
-      incidence(r64, load_face(r64, v3));
+      incidence(r64, load_face(r64, v3), k);
+    }
+    if constexpr (MODE == MODE_HESS) {
+      if (fan && cnt > 0) {  // close the fan: the first block meets the last carry, or both stand alone
+        if (last_pos2 == first_pos) {
+          if (first_pos != 255) {
+            double* dst = hrow + first_pos * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = carry[k] + first[k];
+          }
+        } else {
+          if (first_pos != 255) {
+            double* dst = hrow + first_pos * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = first[k];
+          }
+          if (last_pos2 != 255) {
+            double* dst = hrow + last_pos2 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = carry[k];
+          }
+        }
+      }
     }
     double* vout = MODE == MODE_HVP ? a.y : a.grad;
 #pragma unroll

@@ -429,6 +429,58 @@ __global__ void k_ellv(const int32_t* rinc_off, const uint64_t* rrec, const int3
   }
 }
 
+// Face rows: order each row's incidences around its vertex (face j's second
+// other corner is face j+1's first: consistently oriented manifold fans, open
+// or closed, at most 16 faces) and flag the row (meta bit 9); other rows keep
+// face-id order. Records keep their contents, only their order changes.
+__global__ void k_fan_order(const int32_t* rinc_off, uint64_t* rrec, const int32_t* faces, int64_t Vr,
+                            uint32_t* meta) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= Vr) return;
+  const int k0 = rinc_off[r], c = rinc_off[r + 1] - k0;
+  if (c < 1 || c > 16) return;
+  uint64_t rec[16];
+  int o1[16], o2[16];
+  for (int k = 0; k < c; ++k) {
+    rec[k] = rrec[k0 + k];
+    const uint32_t lo = (uint32_t)rec[k];
+    const int64_t f = lo & 0x3fffffffu;
+    const int s = (int)(lo >> 30);
+    o1[k] = faces[3 * f + (s + 1) % 3];
+    o2[k] = faces[3 * f + (s + 2) % 3];
+  }
+  // start: the face whose first other corner ends no other face (open fan), else face 0
+  int start = -1, nstart = 0;
+  for (int k = 0; k < c; ++k) {
+    int preds = 0;
+    for (int j = 0; j < c; ++j) preds += (o2[j] == o1[k]) ? 1 : 0;
+    if (preds > 1) return;  // non-manifold
+    if (preds == 0) {
+      ++nstart;
+      start = k;
+    }
+  }
+  if (nstart > 1) return;  // several fans
+  if (start < 0) start = 0;
+  int order[16];
+  unsigned used = 1u << start;
+  order[0] = start;
+  for (int step = 1; step < c; ++step) {
+    const int cur = order[step - 1];
+    int nxt = -1;
+    for (int j = 0; j < c; ++j)
+      if (!((used >> j) & 1) && o1[j] == o2[cur]) {
+        if (nxt >= 0) return;
+        nxt = j;
+      }
+    if (nxt < 0) return;
+    used |= 1u << nxt;
+    order[step] = nxt;
+  }
+  for (int k = 0; k < c; ++k) rrec[k0 + k] = rec[order[k]];
+  meta[r] |= 1u << 9;
+}
+
 __global__ void k_patch_rows(const int32_t* order, const int64_t* ro, const uint8_t* dp, int64_t Vr,
                              int64_t* pro, int32_t* plen, uint8_t* pdp) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -853,6 +905,8 @@ void build_rows_fv(Problem& p, cudaStream_t s) {
   p.ellv.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
   if (Vr) {
     k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, p.prow_len.p, Vr, p.rmeta.p);
+    if (p.with_hessian && p.pattern_ready)
+      k_fan_order<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, p.rmeta.p);
     k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
     k_ellv<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, EV_ELL_K, p.ellv.p);
   }
