@@ -196,8 +196,13 @@ __global__ void __launch_bounds__(128) k_face_psd(const __grid_constant__ FvArgs
 #ifndef FV_MINB
 #define FV_MINB 6
 #endif
+// CTAs per SM to fit: the clamped Hessian path carries the per-face P_f(M)
+// of two incidences in flight and gets more registers
+template <int MODE, bool PSD> struct FvMinb {
+  static constexpr int v = (PSD && MODE == MODE_HESS) ? 4 : FV_MINB;
+};
 template <int MODE, bool PSD>
-__global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
+__global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
   constexpr int N = 2, NN = 4;
   extern __shared__ __align__(16) double hbuf[];
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
@@ -400,20 +405,35 @@ __global__ void __launch_bounds__(PT, FV_MINB) k_rows_dirichlet(const __grid_con
               for (int k = 0; k < 4; ++k) dst[k] += b[k];
             }
           }
-        } else {  // HVP: y_s = sum_t block(s,t) u_t over the face's corners (masked)
-          double b[4];
-          const double us_[2] = {sel3(s, d.U[0][0], d.U[1][0], d.U[2][0]), sel3(s, d.U[0][1], d.U[1][1], d.U[2][1])};
-          const double u1_[2] = {sel3(s1, d.U[0][0], d.U[1][0], d.U[2][0]), sel3(s1, d.U[0][1], d.U[1][1], d.U[2][1])};
-          const double u2_[2] = {sel3(s2, d.U[0][0], d.U[1][0], d.U[2][0]), sel3(s2, d.U[0][1], d.U[1][1], d.U[2][1])};
-          blk(as, as, true, b);
-          vec[0] += b[0] * us_[0] + b[1] * us_[1];
-          vec[1] += b[2] * us_[0] + b[3] * us_[1];
-          blk(as, a1, false, b);
-          vec[0] += b[0] * u1_[0] + b[1] * u1_[1];
-          vec[1] += b[2] * u1_[0] + b[3] * u1_[1];
-          blk(as, a2, false, b);
-          vec[0] += b[0] * u2_[0] + b[1] * u2_[1];
-          vec[1] += b[2] * u2_[0] + b[3] * u2_[1];
+        } else {
+          // HVP: y_s = sum_t block(s,t) u_t = (I (x) w_s)^T G dJ with dJ = sum_t (w_t (x) u_t)
+          // the face's masked direction in J space (the blocks' symmetrisation is
+          // exact here: G is symmetric), plus the floor term f/3 sum_t u_t under a clamp
+          double wq[3][2];
+          if constexpr (PSD) {
+            wq[0][0] = INV_SQRT2; wq[0][1] = INV_SQRT6;
+            wq[1][0] = -INV_SQRT2; wq[1][1] = INV_SQRT6;
+            wq[2][0] = 0.0; wq[2][1] = -2.0 * INV_SQRT6;
+          } else {
+            wq[0][0] = -(d.R[0] + d.R[2]); wq[0][1] = -(d.R[1] + d.R[3]);
+            wq[1][0] = d.R[0]; wq[1][1] = d.R[1];
+            wq[2][0] = d.R[2]; wq[2][1] = d.R[3];
+          }
+          double dv[4];
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              dv[2 * c + k] = wq[0][k] * d.U[0][c] + wq[1][k] * d.U[1][c] + wq[2][k] * d.U[2][c];
+          double gv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) gv[i] = G[i][0] * dv[0] + G[i][1] * dv[1] + G[i][2] * dv[2] + G[i][3] * dv[3];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            double y = as[0] * gv[2 * c] + as[1] * gv[2 * c + 1];
+            if constexpr (PSD) y += fl3 * (d.U[0][c] + d.U[1][c] + d.U[2][c]);
+            vec[c] += y;
+          }
         }
       }
     };
