@@ -492,8 +492,13 @@ template <> struct FastCfg<MODE_GRAD, false> {
 // incidences are fetched in two batched levels (records, then neighbour x and
 // edge attributes) so their latencies overlap; EVT fixes the single EV term's
 // type at compile time (0: any mix, dispatched per incidence).
+// the x-free edge-length HVP holds only directions: full occupancy (64 registers)
+template <int MODE, bool PSD, int EVT> struct FastMinb {
+  static constexpr int v =
+      (MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH) ? 1024 / EV_FLAT_BLOCK : FastCfg<MODE, PSD>::MINB;
+};
 template <int N, int MODE, bool PSD, int EVT>
-__global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, FastCfg<MODE, PSD>::MINB)
+__global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD, EVT>::v))
     k_rows_fast(const __grid_constant__ EvArgs a) {
   constexpr int T = TriN<N>::value, NN = N * N;
   constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
