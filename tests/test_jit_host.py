@@ -64,3 +64,27 @@ def test_generated_functor_compiles():
     assert len(tt.attrs) == 5  # four rest_inv entries + areas (views of one array dedupe)
     image = jit.compile_term(tt)
     assert image[:4] == b"\x7fELF"
+
+
+def test_vv_trace_uses_center_and_ring_slots():
+    """VV (ref problem.py:340-353, 443-448): the handle is the center (slot 0)
+    and carries the centers' ids; nbrs are the ring slots 1..d."""
+    w = np.arange(10.0)
+    sel = np.array([[3, 1, 4, 5], [7, 2, 6, 8]])
+    ids = sel[:, 0]
+
+    def ring(vertex, nbrs, x):
+        c = x[vertex]
+        total = 0.0
+        for nb in nbrs:
+            total = total + (c - x[nb]).norm2() * w[vertex.index]
+        return total
+
+    tt = jit.trace_callback(ring, "VV", 3, 2, sel, index=ids)
+    assert tt.P == 4
+    body = "\n".join(tt.body)
+    assert "X[0][0] - X[3][0]" in body and "X[4]" not in body
+    # each closure gather is one per-element stream of the group's centers
+    assert tt.attrs and all(np.array_equal(a, w[ids]) for a in tt.attrs)
+    with pytest.raises(ValueError, match="neighbourhoods"):
+        jit.trace_callback(ring, "VV", 3, 2, None)
