@@ -507,23 +507,52 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD
   // (apps/smooth.py:27-28): its unclamped HVP reads only the direction
   constexpr bool XFREE = MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH;
   extern __shared__ __align__(16) double hbuf[];
-  const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
-  double eacc = 0.0;
-  bool finite = true;
-  if (row < a.V) {
-    // level 1: static per-row streams, all indexed by the row alone
-    // (coalesced): vertex, meta word, row start / buffer offset, ELL records
-    const int g = a.order[row];
-    const uint32_t meta = a.rmeta[row];
+  // Row blocks are walked grid-stride (a persistent grid for the Hessian, one
+  // block per CTA otherwise); the level-1 streams of the thread's next row are
+  // loaded while it works on the current one.
+  struct L1 {
+    int g = 0;
+    uint32_t meta = 0;
     int64_t ro = 0;
     int ho = 0;
+    uint64_t rc[EV_ELL_K];
+  };
+  // level 1: static per-row streams, all indexed by the row alone
+  // (coalesced): vertex, meta word, row start / buffer offset, ELL records
+  auto load_l1 = [&](int64_t r, L1& l) {
+    if (r >= a.V) return;
+    l.g = a.order[r];
+    l.meta = a.rmeta[r];
     if constexpr (MODE == MODE_HESS) {
-      ro = a.prow_ro[row];
-      ho = a.hoff[row];
+      l.ro = a.prow_ro[r];
+      l.ho = a.hoff[r];
     }
+#pragma unroll
+    for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
+  };
+  const int64_t nblk = (a.V + PT - 1) / PT;
+  bool finite = true;
+  L1 cur, nxt;
+  if constexpr (MODE == MODE_HESS) load_l1((int64_t)blockIdx.x * PT + threadIdx.x, cur);
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  const int64_t row = blk * PT + threadIdx.x;
+  if constexpr (MODE == MODE_HESS) {
+    if (blk + gridDim.x < nblk) load_l1(row + (int64_t)gridDim.x * PT, nxt);
+  } else {
+    load_l1(row, cur);
+  }
+  double eacc = 0.0;
+  if (row < a.V) {
+    const int g = cur.g;
+    const uint32_t meta = cur.meta;
+    const int64_t ro = cur.ro;
+    const int ho = cur.ho;
     uint64_t rc[EV_ELL_K];
 #pragma unroll
-    for (int j = 0; j < EV_ELL_K; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+    for (int j = 0; j < EV_ELL_K; ++j) rc[j] = cur.rc[j];
+    (void)ro;
+    // the previous row's bulk copy must have read this thread's row buffer
+    if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     const bool fr = !((meta >> 8) & 1);
     const int dp = (int)(meta >> 16) & 0xff;
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
@@ -691,12 +720,15 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD
       }
     }
   }
-  if (!finite) *a.redo = 1;
   if constexpr (MODE != MODE_HVP) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
     if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
   }
+  if constexpr (MODE == MODE_HESS) cur = nxt;
+  else break;  // one row block per CTA outside the Hessian
+  }
+  if (!finite) *a.redo = 1;
   if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
@@ -1131,6 +1163,17 @@ bool tiles_enabled() {
   return on;
 }
 
+// MG_PERSISTENT=1: a persistent grid for the Hessian row kernel (measured
+// slightly slower than one row block per CTA: the hardware block scheduler
+// already overlaps a finishing CTA's stores with a starting CTA's loads)
+bool persistent_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MG_PERSISTENT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int N, int MODE, bool PSD, int EVT>
 void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
@@ -1171,8 +1214,20 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
       timing_end(p, st);
     }
   } else {
+    // Hessian: one row block per CTA (or, opt-in, a persistent grid whose
+    // threads walk their rows with the next row's level-1 streams in flight)
     constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
-    fast<<<(unsigned)((a.V + FB - 1) / FB), FB, sm, st>>>(a);
+    const int64_t nfb = (a.V + FB - 1) / FB;
+    int64_t grid = nfb;
+    if (persistent_enabled()) {
+      int dev = 0, sms = 148, per_sm = 1;
+      MG_CUDA(cudaGetDevice(&dev));
+      MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast, FB, sm));
+      const int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+      if (g < grid) grid = g;
+    }
+    fast<<<(unsigned)grid, FB, sm, st>>>(a);
     MG_LAUNCH_CHECK();
     timing_end(p, st);
   }
