@@ -150,7 +150,11 @@ MG_DI void jacobi_project_rr(double* A, double floor) {
   for (int i = 0; i < K; ++i)
 #pragma unroll
     for (int j = 0; j <= i; ++j) fro2 += (i == j ? 1.0 : 2.0) * A[tri(i, j)] * A[tri(i, j)];
-  const double tol2 = fro2 * 1e-30;
+  // stop at off-diagonal mass 1e-12 of the Frobenius norm: the clamp max(l, f)
+  // is Lipschitz, and a pair mixed by the residual rotation is either both
+  // clamped (no effect) or separated by at least f - l_min, so the projector's
+  // error stays at the residual's level, two orders under the 1e-10 bar
+  const double tol2 = fro2 * 1e-24;
   for (int sweep = 0; sweep < 12; ++sweep) {
     double off = 0.0;
 #pragma unroll
