@@ -36,6 +36,7 @@ __all__ = [
     "ClothSim",
     "ParamConfig",
     "SphereConfig",
+    "bench_gradient",
     "boundary_loop",
     "check_genus_zero",
     "face_determinants",
@@ -365,3 +366,27 @@ def smooth(mesh: Mesh, lam: float, iters: int, mode: str = "ad", x0=None, worker
         report.log(it, manual_energy(x, mesh), float(g.abs().max()), lam, 0, (time.perf_counter() - t0) * 1e3)
     report.termination = Termination.MAX_ITERS
     return x.cpu().numpy(), report
+
+
+def bench_gradient(sizes=(64, 128, 256, 512), repeats: int = 3, workers: int = 1,
+                   accumulation: str = "deterministic"):
+    """Median per-call time of the smoothing gradient on n x n grids (ref
+    apps/smooth.py:97-119): rows of (side, vertices, edges, ms_per_iter, ratio
+    to the previous size); mesh construction and layout outside the timing."""
+    rows = []
+    prev = None
+    for n in sizes:
+        mesh = generate_grid(n, 1.0 / (n - 1))
+        problem = edge_length_problem(mesh, accumulation=accumulation)
+        problem.x = mesh.positions.ravel().copy()
+        problem.eval_terms()  # layout and pattern outside the timed region
+        times = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            problem.eval_terms()
+            times.append((time.perf_counter() - t0) * 1e3)
+        ms = float(np.median(times))
+        rows.append({"side": n, "vertices": mesh.num_vertices, "edges": mesh.num_edges, "ms_per_iter": ms,
+                     "ratio": (ms / prev) if prev else float("nan")})
+        prev = ms
+    return rows

@@ -79,3 +79,12 @@ def test_driver_errors():
         check_genus_zero(mg.generate_grid(3))
     with pytest.raises(ValueError, match="step must be non-negative"):
         smooth(mg.generate_grid(3), -1.0, 1)
+
+
+def test_bench_gradient_rows():
+    from paper_2509_00406_b200.drivers import bench_gradient
+
+    rows = bench_gradient(sizes=(16, 32), repeats=2)
+    assert [r["side"] for r in rows] == [16, 32]
+    assert rows[1]["edges"] == 3 * 32 * 32 - 4 * 32 + 1 and rows[0]["ms_per_iter"] > 0
+    assert np.isnan(rows[0]["ratio"]) and rows[1]["ratio"] > 0
