@@ -121,8 +121,14 @@ struct Term {
 };
 
 constexpr int EV_ROW_BLOCK = 64;  // rows (threads) per CTA of the edge row kernel
-constexpr int EV_TILE_ROWS = 128;  // rows per tile of the staged edge kernel (edge_kernels.cu)
-constexpr int EV_TILE_VPT = 2;    // vertex-table entries per thread (max_v <= VPT * rows)
+#ifndef MG_TILE_ROWS
+#define MG_TILE_ROWS 128
+#endif
+constexpr int EV_TILE_ROWS = MG_TILE_ROWS;  // rows per tile of the staged edge kernel (edge_kernels.cu)
+#ifndef MG_TILE_VPT
+#define MG_TILE_VPT 2
+#endif
+constexpr int EV_TILE_VPT = MG_TILE_VPT;    // vertex-table entries per thread (max_v <= VPT * rows)
 constexpr int EV_TILE_EPT = 5;    // edge-table entries per thread
 constexpr int EV_ELL_K = 6;       // incidences per row stored slot-major (ELL); the rest stay CSR
 
