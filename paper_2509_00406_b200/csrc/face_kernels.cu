@@ -187,7 +187,27 @@ __global__ void __launch_bounds__(128) k_face_psd(const __grid_constant__ FvArgs
         for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
       M[tri(I, Jx)] = acc;
     }
-  if (fin) project_if_needed<4>(M, a.floor);  // non-finite faces: the row kernel takes the exact path
+  // non-finite faces: the row kernel takes the exact path
+  if (fin && !shifted_pd<4>(M, a.floor)) {
+    // only the twist mode of the isotropic energy can be negative: start the
+    // eigen-iteration from J's twist direction [[q, -p], [p, q]] (p = tr-like,
+    // q = skew part of J) mapped through the reduced basis (M = C^T H_J C,
+    // C = I (x) L_W: v0 = C^-1 u_T)
+    const double p = J[0] + J[3], q = J[1] - J[2];
+    const double uT[4] = {q, -p, p, q};
+    const double dl = Lw00 * Lw11 - Lw01 * Lw10;
+    double v0[4];
+    if (dl != 0.0) {
+      const double idl = 1.0 / dl;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // solve sum_a Lw[k][a] y_a = uT[2c+k]
+        const double u0 = uT[2 * c], u1 = uT[2 * c + 1];
+        v0[2 * c] = (Lw11 * u0 - Lw01 * u1) * idl;
+        v0[2 * c + 1] = (-Lw10 * u0 + Lw00 * u1) * idl;
+      }
+    }
+    if (dl == 0.0 || !psd_rank1_update<4>(M, a.floor, v0)) jacobi_project_rr<4>(M, a.floor);
+  }
   double2* out = reinterpret_cast<double2*>(a.fpsd + f * 10);
 #pragma unroll
   for (int k = 0; k < 5; ++k) out[k] = make_double2(M[2 * k], M[2 * k + 1]);

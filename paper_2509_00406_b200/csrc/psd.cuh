@@ -245,6 +245,126 @@ MG_DI bool shifted_pd(const double* A, double floor) {
   return ok;
 }
 
+// One eigenvalue below the floor, from a start vector v0 with a negative
+// Rayleigh quotient (the caller knows the clamped mode's approximate
+// direction): Rayleigh-quotient iteration for (lambda, v), then
+// P_f(A) = A + (f - lambda) v v^T. The error of this update is bounded by the
+// eigenvector residual times |f - lambda| / gap <= 1 (the gap to the next
+// eigenvalue is at least f - lambda), so it is as accurate as the full
+// eigendecomposition. Returns false (A untouched) unless the iteration
+// converged below the floor and A + (s - lambda) v v^T - f I is positive
+// definite for a large s, i.e. no other eigenvalue sits below the floor; the
+// caller then falls back to Jacobi.
+template <int K>
+MG_DI bool psd_rank1_update(double* A, double floor, const double* v0) {
+  double v[K], nrm = 0.0, fro2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) nrm += v0[i] * v0[i];
+  if (!(nrm > 0.0)) return false;
+  nrm = rsqrt(nrm);
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = v0[i] * nrm;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) fro2 += (i == j ? 1.0 : 2.0) * A[tri(i, j)] * A[tri(i, j)];
+  const double scale = ::sqrt(fro2);
+  double rho = 0.0;
+  bool conv = false;
+  for (int it = 0; it < 8; ++it) {
+    double w[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc += A[tri(i, j)] * v[j];
+      w[i] = acc;
+    }
+    rho = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) rho += v[i] * w[i];
+    double res = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) res += (w[i] - rho * v[i]) * (w[i] - rho * v[i]);
+    if (res <= 1e-28 * fro2) {
+      conv = true;
+      break;
+    }
+    // solve (A - rho I) y = v: Gaussian elimination with partial pivoting
+    double B[K][K + 1];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) B[i][j] = A[tri(i, j)] - (i == j ? rho : 0.0);
+      B[i][K] = v[i];
+    }
+    bool sing = false;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      int piv = c;
+      double best = fabs(B[c][c]);
+#pragma unroll
+      for (int r = c + 1; r < K; ++r)
+        if (fabs(B[r][c]) > best) {
+          best = fabs(B[r][c]);
+          piv = r;
+        }
+#pragma unroll
+      for (int r = c + 1; r < K; ++r)
+        if (r == piv)
+#pragma unroll
+          for (int j = 0; j <= K; ++j) {
+            const double t = B[c][j];
+            B[c][j] = B[r][j];
+            B[r][j] = t;
+          }
+      if (!(best > 1e-300)) {
+        sing = true;
+        break;
+      }
+      const double ip = psd_rcp(B[c][c]);
+#pragma unroll
+      for (int r = c + 1; r < K; ++r) {
+        const double f = B[r][c] * ip;
+#pragma unroll
+        for (int j = c; j <= K; ++j) B[r][j] -= f * B[c][j];
+      }
+    }
+    if (sing) {  // rho is an eigenvalue to working precision: v is its vector
+      conv = true;
+      break;
+    }
+    double y[K], yn = 0.0;
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      double acc = B[i][K];
+#pragma unroll
+      for (int j = i + 1; j < K; ++j) acc -= B[i][j] * y[j];
+      y[i] = acc * psd_rcp(B[i][i]);
+      yn += y[i] * y[i];
+    }
+    if (!(yn > 0.0) || !isfinite(yn)) return false;
+    yn = rsqrt(yn);
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] = y[i] * yn;
+  }
+  if (!conv || !(rho < floor)) return false;
+  // no other eigenvalue below the floor: lift v's eigenvalue out of the way and test
+  double T[TriN<K>::value];
+  const double lift = scale + floor - rho;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) T[tri(i, j)] = A[tri(i, j)] + lift * v[i] * v[j];
+  if (!shifted_pd<K>(T, floor)) return false;
+  const double d = floor - rho;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) A[tri(i, j)] += d * v[i] * v[j];
+  return true;
+}
+
 // project in place unless already above the floor; 2x2 / 3x3 blocks (vertex
 // terms, two-point edge terms) use the non-iterative solver of psd_small.h
 template <int K>
