@@ -284,3 +284,70 @@ def test_face_kernels_at_scale_properties():
     fd = (gp - q.grad_device) / (2 * h)
     hv = q.hvp(xd, a)
     assert float((hv - fd).abs().max()) <= 1e-5 * float(hv.abs().max())
+
+
+@pytest.mark.parametrize("k", [7, 12, 40])
+def test_high_valence_rows_match_oracle(k):
+    """A fan mesh whose center has valence k (beyond the 6 ELL slots and the
+    8 register-held tile slots: CSR tails in the edge row, tile and exact
+    kernels), cloth terms with a pinned rim vertex, against the CPU oracle."""
+    import paper_2509_00406_b200 as mg
+    from oracle import OracleProblem
+    from paper_2509_00406_b200 import terms as T
+
+    ang = np.linspace(0, 2 * np.pi, k, endpoint=False)
+    pos = np.concatenate([[[0.0, 0.0, 0.0]], np.stack([np.cos(ang), np.sin(ang), np.zeros(k)], 1)])
+    faces = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)])
+    rng = np.random.default_rng(k)
+    mesh = mg.Mesh(pos, faces)
+    e = mesh.edges
+    l2 = np.einsum("ij,ij->i", pos[e[:, 1]] - pos[e[:, 0]], pos[e[:, 1]] - pos[e[:, 0]])
+    masses = 1.0 + rng.random(k + 1)
+    target = pos + 0.05 * rng.normal(size=pos.shape)
+    terms = [("V", T.Inertia(masses, target)), ("EV", T.Spring(l2, 50.0)),
+             ("V", T.Gravity(masses, np.array([0.0, -9.8, 0.0]), 1e-4))]
+    p = mg.Problem(mesh, 3, fixed_vertices=[3])
+    for op, t in terms:
+        p.add_term(getattr(mg.Element, {"V": "VERTEX", "EV": "EDGE"}[op]), getattr(mg.Op, op), t)
+    o = OracleProblem(k + 1, faces, e, 3, terms, fixed_vertices=[3])
+    x = (pos + 0.1 * rng.normal(size=pos.shape)).ravel()
+    v = rng.normal(size=x.size)
+    p.x = x
+    for floor in (None, FLOOR):
+        en = p.eval_terms(psd_floor=floor)
+        oe, og, oh = o.eval_terms(x, psd_floor=floor)
+        assert rel_scalar(en, oe) <= 1e-10 and rel(p.grad, og) <= 1e-10 and rel(p.hess.values, oh) <= 1e-10
+        assert rel(p.hvp(x, v, psd_floor=floor), o.hvp(x, v, psd_floor=floor)) <= 1e-10
+    assert np.array_equal(p.hess.row_offsets, o.row_offsets) and np.array_equal(p.hess.col_indices, o.col_indices)
+    assert p.exact_runs() == 0  # the fast kernels carried every call
+
+
+@pytest.mark.parametrize("k", [7, 12, 40])
+def test_high_valence_face_rows_match_oracle(k):
+    """Symmetric Dirichlet on a fan whose center has k faces: CSR-tail face
+    incidences, fan-ordered rows (k <= 16) and the accumulating fallback
+    (k = 40), clamped and not, against the CPU oracle."""
+    import paper_2509_00406_b200 as mg
+    from oracle import OracleProblem
+    from paper_2509_00406_b200 import terms as T
+    from paper_2509_00406_b200.apps import rest_geometry
+
+    ang = np.linspace(0, 2 * np.pi, k, endpoint=False)
+    rng = np.random.default_rng(100 + k)
+    pos = np.concatenate([[[0.0, 0.0, 0.0]], np.stack([np.cos(ang), np.sin(ang), 0.1 * rng.random(k)], 1)])
+    faces = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)])
+    mesh = mg.Mesh(pos, faces)
+    rest_inv, areas = rest_geometry(mesh)
+    terms = [("FV", T.SymDirichlet(np.ascontiguousarray(rest_inv).reshape(-1, 4), areas))]
+    p = mg.Problem(mesh, 2)
+    p.add_term(mg.Element.FACE, mg.Op.FV, terms[0][1])
+    o = OracleProblem(k + 1, faces, mesh.edges, 2, terms)
+    x = (pos[:, :2] * (0.8 + 0.4 * rng.random((k + 1, 1)))).ravel()
+    v = rng.normal(size=x.size)
+    p.x = x
+    for floor in (None, FLOOR):
+        en = p.eval_terms(psd_floor=floor)
+        oe, og, oh = o.eval_terms(x, psd_floor=floor)
+        assert rel_scalar(en, oe) <= 1e-10 and rel(p.grad, og) <= 1e-10 and rel(p.hess.values, oh) <= 1e-10
+        assert rel(p.hvp(x, v, psd_floor=floor), o.hvp(x, v, psd_floor=floor)) <= 1e-10
+    assert p.exact_runs() == 0  # the face row kernels carried every call
