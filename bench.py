@@ -237,7 +237,7 @@ def time_device(fn, steps, warmup, dist=None):
     per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
     total = ev[0].elapsed_time(ev[-1])
     if dist is not None:
-        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
         dist.barrier()
@@ -338,8 +338,15 @@ def run_engine(args):
     if world > 1:
         import torch.distributed as tdist
 
-        torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # MG_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo (a functional run
+        # of the N > 1 path on a one-GPU box; its timings are not scaling numbers)
+        if os.environ.get("MG_BENCH_SHARED_GPU") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            tdist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
     else:
         torch.cuda.set_device(0)

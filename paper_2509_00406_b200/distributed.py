@@ -138,6 +138,12 @@ class ShardPlan:
         return [(op, t.shard(self.verts, self.edges, self.faces)) for op, t in terms]
 
 
+def _gloo(group) -> bool:
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
 class HaloExchange:
     """Refresh ribbon rows of a shard-local (num_local, n) array from their
     owners: one all_to_all_single over `group` (works with NCCL and gloo)."""
@@ -164,8 +170,15 @@ class HaloExchange:
             return local
         view = local.view(-1, self.n)
         sendbuf = view.index_select(0, self.send_idx).reshape(-1).contiguous()
-        recvbuf = torch.empty(sum(self.recv_counts), dtype=local.dtype, device=local.device)
+        # NCCL moves device buffers directly; gloo (CPU tests, or several ranks
+        # sharing one GPU) stages them through host memory
+        host = local.is_cuda and _gloo(self.group)
+        if host:
+            sendbuf = sendbuf.cpu()
+        recvbuf = torch.empty(sum(self.recv_counts), dtype=local.dtype, device="cpu" if host else local.device)
         dist.all_to_all_single(recvbuf, sendbuf, self.recv_counts, self.send_counts, group=self.group)
+        if host:
+            recvbuf = recvbuf.to(local.device)
         view.index_copy_(0, self.recv_idx, recvbuf.view(-1, self.n))
         return local
 
@@ -235,7 +248,12 @@ class DistributedProblem:
         self.problem.eval_terms(psd_floor=psd_floor, sync=False)
         e = self.problem.energy_device.clone()
         if dist.is_initialized() and self.plan.world > 1:
-            dist.all_reduce(e, group=self.group)
+            if _gloo(self.group):
+                eh = e.cpu()
+                dist.all_reduce(eh, group=self.group)
+                e = eh.to(e.device)
+            else:
+                dist.all_reduce(e, group=self.group)
         self.energy_device = e
         return float(e.item()) if sync else float("nan")
 
