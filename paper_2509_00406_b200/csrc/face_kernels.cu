@@ -388,6 +388,18 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
               out[2 * c + c2] = 0.5 * (X(u, v, c, c2) + X(v, u, c2, c)) + (diag && c == c2 ? fl3 : 0.0) +
                                 (!diag && c == c2 ? fl3 : 0.0);
         };
+        // off-diagonal block (s, t) evaluated once in the canonical slot order:
+        // the row at the lower slot computes X(w_lo, w_hi), the other row the
+        // same expression transposed — the two blocks come out bitwise
+        // transposed with half the work of the averaged form
+        auto blk_pair = [&](int st, const double* wt, double* out) {
+          const bool lo = s < st;
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2)
+              out[2 * c + c2] = (lo ? X(as, wt, c, c2) : X(wt, as, c2, c)) + (c == c2 ? fl3 : 0.0);
+        };
         if constexpr (MODE == MODE_HESS) {
           double b[4];
           blk(as, as, true, b);
@@ -397,8 +409,8 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
           if (fan) {
             // face j's first other corner is face j-1's second: finish that block
             double b1[4], b2[4];
-            blk(as, a1, false, b1);
-            blk(as, a2, false, b2);
+            blk_pair(s1, a1, b1);
+            blk_pair(s2, a2, b2);
             if (jidx == 0) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) first[k] = b1[k];
@@ -413,13 +425,13 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
             last_pos2 = pos2;
           } else {
             if (pos1 != 255) {
-              blk(as, a1, false, b);
+              blk_pair(s1, a1, b);
               double* dst = hrow + pos1 * NN;
 #pragma unroll
               for (int k = 0; k < 4; ++k) dst[k] += b[k];
             }
             if (pos2 != 255) {
-              blk(as, a2, false, b);
+              blk_pair(s2, a2, b);
               double* dst = hrow + pos2 * NN;
 #pragma unroll
               for (int k = 0; k < 4; ++k) dst[k] += b[k];
