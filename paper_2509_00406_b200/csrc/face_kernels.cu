@@ -58,6 +58,8 @@ struct FvArgs {
   double* vscr;              // sphere: per-vertex retraction (p, pdot), (V, 6)
   int64_t nv;                // vertices of the (shard) mesh
   double* fpsd;              // PSD clamp: per face P_f(M), packed 4x4 (F, 10)
+  double* fpsd6;             // faces with a pinned corner: the clamped masked 6x6, packed (F, 21)
+  const uint8_t* fixed;      // (nv) pinned vertices, or null
   int64_t nf;                // faces of the (shard) mesh
 };
 
@@ -213,6 +215,61 @@ __global__ void __launch_bounds__(128) k_face_psd(const __grid_constant__ FvArgs
   for (int k = 0; k < 5; ++k) out[k] = make_double2(M[2 * k], M[2 * k + 1]);
 }
 
+// Faces with a pinned corner under a clamp (launched only when the problem
+// has pinned vertices): the reference clamps the masked 6x6 (pinned corners'
+// rows / columns zero, problem.py:420-438 + active.py:490-504), which has no
+// translation symmetry left to reduce by, so the full block (packed, rows
+// 2q + c) is clamped and stored for the row kernel.
+__global__ void __launch_bounds__(128) k_face_psd_pinned(const __grid_constant__ FvArgs a) {
+  const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= a.nf) return;
+  const int v0 = a.faces[3 * f], v1 = a.faces[3 * f + 1], v2 = a.faces[3 * f + 2];
+  const bool p0 = a.fixed[v0], p1 = a.fixed[v1], p2 = a.fixed[v2];
+  if (!(p0 || p1 || p2)) return;
+  double X[3][2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    X[0][c] = a.x[(int64_t)v0 * 2 + c];
+    X[1][c] = a.x[(int64_t)v1 * 2 + c];
+    X[2][c] = a.x[(int64_t)v2 * 2 + c];
+  }
+  const double* Rp = a.t.a[0] + 4 * f;
+  const double R0 = Rp[0], R1 = Rp[1], R2 = Rp[2], R3 = Rp[3];
+  const double area = a.t.a[1][f];
+  double J[4];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double d1 = X[1][c] - X[0][c], d2 = X[2][c] - X[0][c];
+    J[2 * c] = d1 * R0 + d2 * R2;
+    J[2 * c + 1] = d1 * R1 + d2 * R3;
+  }
+  double v, g[4], h[10];
+  const bool fin = dirichlet_closed<true>(J, area, v, g, h);
+  const bool pq[3] = {p0, p1, p2};
+  const double W[3][2] = {{-(R0 + R2), -(R1 + R3)}, {R0, R1}, {R2, R3}};
+  double H6[21];
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int q2 = 0; q2 <= q; ++q2)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const int R = 2 * q + c, C = 2 * q2 + c2;
+          if (C > R) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int k2 = 0; k2 < 2; ++k2) acc += W[q][k] * h[tri(2 * c + k, 2 * c2 + k2)] * W[q2][k2];
+          H6[tri(R, C)] = (pq[q] || pq[q2]) ? 0.0 : acc;
+        }
+  if (fin) project_if_needed<6>(H6, a.floor);  // non-finite faces: the row kernel takes the exact path
+#pragma unroll
+  for (int k = 0; k < 21; ++k) a.fpsd6[f * 21 + k] = H6[k];
+}
+
 #ifndef FV_MINB
 #define FV_MINB 6
 #endif
@@ -221,7 +278,7 @@ __global__ void __launch_bounds__(128) k_face_psd(const __grid_constant__ FvArgs
 template <int MODE, bool PSD> struct FvMinb {
   static constexpr int v = (PSD && MODE == MODE_HESS) ? 4 : FV_MINB;
 };
-template <int MODE, bool PSD>
+template <int MODE, bool PSD, bool PIN = false>
 __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
   constexpr int N = 2, NN = 4;
   extern __shared__ __align__(16) double hbuf[];
@@ -329,13 +386,21 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
         // 1-perp) plus the floor on 1 1^T / 3
         double G[4][4];
         double as[2], a1[2], a2[2];
+        // faces with a pinned corner under a clamp: blocks straight from the
+        // clamped masked 6x6 of the pre-pass
+        // (PIN: compiled in only for problems with pinned vertices)
+        const double* P6 = (PSD && PIN && pins != 0) ? a.fpsd6 + ((int64_t)((uint32_t)lo & 0x3fffffffu)) * 21 : nullptr;
         if constexpr (PSD) {
           double val, gJ[4];
           bool fin = dirichlet_closed<false>(J, d.area, val, gJ, nullptr);
-          fin &= pins == 0;  // the reference clamps the pinned-masked block: exact path
           double chk = 0.0;
 #pragma unroll
           for (int k = 0; k < 10; ++k) chk += d.M[k];
+          if (P6) {
+            chk = 0.0;
+#pragma unroll
+            for (int k = 0; k < 21; ++k) chk += P6[k];
+          }
           ok &= fin && isfinite(chk);
           if (MODE == MODE_HESS && s == 0) eacc += val;
           if constexpr (MODE == MODE_HESS) {
@@ -400,17 +465,30 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
             for (int c2 = 0; c2 < 2; ++c2)
               out[2 * c + c2] = (lo ? X(as, wt, c, c2) : X(wt, as, c2, c)) + (c == c2 ? fl3 : 0.0);
         };
+        // block (s, t) of the pinned face's clamped 6x6
+        auto p6blk = [&](int t, double* out) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) out[2 * c + c2] = P6[tri(2 * s + c, 2 * t + c2)];
+        };
         if constexpr (MODE == MODE_HESS) {
           double b[4];
-          blk(as, as, true, b);
+          if (P6) p6blk(s, b);
+          else blk(as, as, true, b);
           dg[0] += b[0];
           dg[1] += b[1];
           dg[2] += b[3];
           if (fan) {
             // face j's first other corner is face j-1's second: finish that block
             double b1[4], b2[4];
-            blk_pair(s1, a1, b1);
-            blk_pair(s2, a2, b2);
+            if (P6) {
+              p6blk(s1, b1);
+              p6blk(s2, b2);
+            } else {
+              blk_pair(s1, a1, b1);
+              blk_pair(s2, a2, b2);
+            }
             if (jidx == 0) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) first[k] = b1[k];
@@ -425,13 +503,15 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
             last_pos2 = pos2;
           } else {
             if (pos1 != 255) {
-              blk_pair(s1, a1, b);
+              if (P6) p6blk(s1, b);
+              else blk_pair(s1, a1, b);
               double* dst = hrow + pos1 * NN;
 #pragma unroll
               for (int k = 0; k < 4; ++k) dst[k] += b[k];
             }
             if (pos2 != 255) {
-              blk_pair(s2, a2, b);
+              if (P6) p6blk(s2, b);
+              else blk_pair(s2, a2, b);
               double* dst = hrow + pos2 * NN;
 #pragma unroll
               for (int k = 0; k < 4; ++k) dst[k] += b[k];
@@ -460,11 +540,23 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
           double gv[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) gv[i] = G[i][0] * dv[0] + G[i][1] * dv[1] + G[i][2] * dv[2] + G[i][3] * dv[3];
+          if (P6) {  // y_s = sum_t P6(s, t) u_t (u masked)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            double y = as[0] * gv[2 * c] + as[1] * gv[2 * c + 1];
-            if constexpr (PSD) y += fl3 * (d.U[0][c] + d.U[1][c] + d.U[2][c]);
-            vec[c] += y;
+            for (int c = 0; c < 2; ++c) {
+              double y = 0.0;
+#pragma unroll
+              for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) y += P6[tri(2 * s + c, 2 * t + c2)] * d.U[t][c2];
+              vec[c] += y;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              double y = as[0] * gv[2 * c] + as[1] * gv[2 * c + 1];
+              if constexpr (PSD) y += fl3 * (d.U[0][c] + d.U[1][c] + d.U[2][c]);
+              vec[c] += y;
+            }
           }
         }
       }
@@ -979,11 +1071,13 @@ void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
   const int64_t nb = (a.V + PT - 1) / PT;
   if (!nb) return;
-  auto kern = k_rows_dirichlet<MODE, PSD>;
+  auto kern = (PSD && a.fpsd6) ? k_rows_dirichlet<MODE, PSD, true> : k_rows_dirichlet<MODE, PSD, false>;
   if (sm) MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   timing_begin(p, st);
   if constexpr (PSD) {
     if (a.nf) k_face_psd<<<(unsigned)((a.nf + 127) / 128), 128, 0, st>>>(a);
+    MG_LAUNCH_CHECK();
+    if (a.nf && a.fpsd6) k_face_psd_pinned<<<(unsigned)((a.nf + 127) / 128), 128, 0, st>>>(a);
     MG_LAUNCH_CHECK();
   }
   kern<<<(unsigned)nb, PT, sm, st>>>(a);
@@ -1019,9 +1113,15 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.vscr = nullptr;
   a.nf = m.F;
   a.fpsd = nullptr;
+  a.fpsd6 = nullptr;
+  a.fixed = p.any_fixed ? p.fixed.p : nullptr;
   if (c.psd && mode != MODE_GRAD && a.t.type != MG_TERM_SPHERE) {
     if (p.fpsd.n < 10 * m.F) p.fpsd.alloc(10 * m.F > 0 ? 10 * m.F : 2);
     a.fpsd = p.fpsd.p;
+    if (p.any_fixed) {
+      if (p.fpsd6.n < 21 * m.F) p.fpsd6.alloc(21 * m.F > 0 ? 21 * m.F : 2);
+      a.fpsd6 = p.fpsd6.p;
+    }
   }
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
   if (a.t.type == MG_TERM_SPHERE) {

@@ -188,6 +188,7 @@ struct Problem {
   DBuf<int> exact_runs;        // (1) calls whose exact re-run executed (diagnostics)
   mutable DBuf<double> vscr;   // sphere face kernel: per-vertex retraction scratch (V, 6)
   mutable DBuf<double> fpsd;   // Dirichlet face kernel under a PSD clamp: per face P_f(M) (F, 10)
+  mutable DBuf<double> fpsd6;  // ... and for faces with a pinned corner the clamped masked 6x6 (F, 21)
   // deterministic element-parallel mode (gather.cu): per-element output
   // scratch and, per output row / block, its contributions in fixed order
   bool gather_ready = false;

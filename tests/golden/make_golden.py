@@ -188,6 +188,12 @@ def case_dirichlet():
     save("dirichlet_ico2", mesh, 2, spec, battery(p, states, vs), extra=extra)
     p = make_distortion_problem(mesh, rest_inv, areas, with_hessian=False)
     save("dirichlet_ico2_grad", mesh, 2, spec, battery(p, states, vs), with_hessian=False, extra=extra)
+    # pinned corners: the reference's masked lift (the app's own callback on a pinned Problem)
+    fn = make_distortion_problem(mesh, rest_inv, areas)._terms[0].fn
+    pins = [0, 7, 31, 60]
+    p = mg.Problem(mesh, 2, with_hessian=True, fixed_vertices=pins)
+    p.add_term(Element.FACE, Op.FV, fn)
+    save("dirichlet_ico2_pinned", mesh, 2, spec, battery(p, states, vs), fixed=pins, extra=extra)
     # one flipped face on a flat 4x4 grid: NaN spreads per field
     g = mg.generate_grid(4, 1.0 / 3)
     ri, ar = rest_geometry(g)
@@ -216,6 +222,11 @@ def case_sphere():
              "attrs": {"base": "a_base", "b1": "a_b1", "b2": "a_b2"}}]
     p = make_sphere_problem(mesh, base, b1, b2, with_hessian=False)
     save("sphere_ico2_grad", mesh, 2, spec, battery(p, [x], vs), with_hessian=False, extra=extra)
+    fn = make_sphere_problem(mesh, base, b1, b2)._terms[0].fn
+    pins = [1, 12, 40, 99]
+    p = mg.Problem(mesh, 2, with_hessian=True, fixed_vertices=pins)
+    p.add_term(Element.FACE, Op.FV, fn)
+    save("sphere_ico2_pinned", mesh, 2, spec, battery(p, [x], vs), fixed=pins, extra=extra)
     # a large tangent step that flips faces: -log(det<0) -> NaN energy, finite grad
     xf = x.copy()
     xf[0:2] = [2.5, -1.5]
