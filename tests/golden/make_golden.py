@@ -260,6 +260,47 @@ def case_additivity():
          extra={"a_ones": np.ones(mesh.num_vertices), "a_zeros": np.zeros((mesh.num_vertices, 3))})
 
 
+def case_mixed():
+    """FV + EV + V terms on one UV problem (n = 2), pinned vertices: the
+    generic patch-owner path (no single-term fast kernel applies)."""
+    p3, f, uv = punctured_icosphere_arrays(1)
+    mesh = mg.Mesh(p3, f)
+    rest_inv, areas = rest_geometry(mesh)
+    from meshgrad.apps.param import jacobian_dets
+
+    if jacobian_dets(uv, mesh, rest_inv).max() < 0:
+        uv = uv[:, ::-1].copy()
+    rng = np.random.default_rng(21)
+    e = mesh.edges
+    l2 = np.einsum("ij,ij->i", uv[e[:, 1]] - uv[e[:, 0]], uv[e[:, 1]] - uv[e[:, 0]]) * 1.1
+    masses = 1.0 + rng.random(mesh.num_vertices)
+    target = uv + 0.01 * rng.normal(size=uv.shape)
+    pins = [2, 9]
+    fn_d = make_distortion_problem(mesh, rest_inv, areas)._terms[0].fn
+
+    def spring(edge, verts, x):
+        d = x[verts[0]] - x[verts[1]]
+        s_ = d.norm2() / l2[edge.index] - 1.0
+        return 0.7 * l2[edge.index] * (s_ * s_)
+
+    def inertia(vertex, nbrs, x):
+        d = x[vertex] - target[vertex.index]
+        return 0.5 * masses[vertex.index] * d.norm2()
+
+    p = mg.Problem(mesh, 2, with_hessian=True, fixed_vertices=pins)
+    p.add_term(Element.FACE, Op.FV, fn_d)
+    p.add_term(Element.EDGE, Op.EV, spring)
+    p.add_term(Element.VERTEX, Op.V, inertia)
+    spec = [{"type": "SymDirichlet", "op": "FV", "attrs": {"rest_inv": "a_rest_inv", "areas": "a_areas"}},
+            {"type": "Spring", "op": "EV", "coef": 0.7, "attrs": {"rest_len2": "a_l2"}},
+            {"type": "Inertia", "op": "V", "attrs": {"masses": "a_masses", "target": "a_target"}}]
+    states = [(uv + 0.003 * rng.normal(size=uv.shape)).ravel()]
+    vs = [rng.normal(size=uv.size)]
+    save("mixed_fv_ev_v", mesh, 2, spec, battery(p, states, vs), fixed=pins,
+         extra={"a_rest_inv": rest_inv.reshape(-1, 4), "a_areas": areas, "a_l2": l2, "a_masses": masses,
+                "a_target": target})
+
+
 if __name__ == "__main__":
     case_springs()
     case_cloth(8, "cloth8")
@@ -269,3 +310,4 @@ if __name__ == "__main__":
     case_sphere()
     case_smooth()
     case_additivity()
+    case_mixed()
