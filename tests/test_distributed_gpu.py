@@ -12,7 +12,8 @@ from golden_util import FLOOR, build_terms, load, rel, rel_scalar
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["cloth64", "spring_grid16", "smooth_ico2", "dirichlet_ico2", "sphere_ico2"]
+CASES = ["cloth64", "spring_grid16", "smooth_ico2", "dirichlet_ico2", "sphere_ico2", "dirichlet_ico2_pinned",
+         "mixed_fv_ev_v"]
 
 
 @pytest.mark.parametrize("mode", ["deterministic", "atomic"])

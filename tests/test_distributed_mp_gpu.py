@@ -61,7 +61,7 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["cloth64", "dirichlet_ico2", "sphere_ico2", "smooth_ico2"])
+@pytest.mark.parametrize("name", ["cloth64", "dirichlet_ico2", "sphere_ico2", "smooth_ico2", "mixed_fv_ev_v"])
 def test_two_process_shards_match_reference(name):
     world = 2
     d = load(name)
