@@ -270,6 +270,29 @@ __global__ void __launch_bounds__(128) k_face_psd_pinned(const __grid_constant__
   for (int k = 0; k < 21; ++k) a.fpsd6[f * 21 + k] = H6[k];
 }
 
+// H_J V of the same function without forming H_J (the HVP's directional
+// derivative of the closed-form gradient along V):
+//   dF = 2 J.V, dD = cof.V,
+//   H_J V = 2a [(1 + D^-2) V - 2 D^-3 dD J - (dF D^-3 - 3 F D^-4 dD) cof - F D^-3 cof(V)]
+// Returns false unless D > 0 and the result is finite.
+MG_DI bool dirichlet_hv_closed(const double* J, const double* V, double area, double* out) {
+  const double F = J[0] * J[0] + J[1] * J[1] + J[2] * J[2] + J[3] * J[3];
+  const double D = J[0] * J[3] - J[1] * J[2];
+  const double iD = rcp_fast(D), q = iD * iD, r = q * iD;
+  const double cof[4] = {J[3], -J[2], -J[1], J[0]};
+  const double cofV[4] = {V[3], -V[2], -V[1], V[0]};
+  const double dF = 2.0 * (J[0] * V[0] + J[1] * V[1] + J[2] * V[2] + J[3] * V[3]);
+  const double dD = cof[0] * V[0] + cof[1] * V[1] + cof[2] * V[2] + cof[3] * V[3];
+  const double a2 = 2.0 * area, s1 = 1.0 + q, tJ = 2.0 * r * dD, tc = dF * r - 3.0 * F * q * q * dD, tv = F * r;
+  double chk = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    out[i] = a2 * (s1 * V[i] - tJ * J[i] - tc * cof[i] - tv * cofV[i]);
+    chk += out[i];
+  }
+  return D > 0.0 && isfinite(chk);
+}
+
 #ifndef FV_MINB
 #define FV_MINB 6
 #endif
@@ -417,6 +440,14 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
           a1[1] = sel3(s1, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
           a2[0] = sel3(s2, INV_SQRT2, -INV_SQRT2, 0.0);
           a2[1] = sel3(s2, INV_SQRT6, INV_SQRT6, -2.0 * INV_SQRT6);
+        } else if constexpr (MODE == MODE_HVP) {
+          // unclamped HVP: only H_J dJ is needed (G unused below)
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            as[k] = ws[k];
+            a1[k] = w1[k];
+            a2[k] = w2[k];
+          }
         } else {
           struct {
             double v, g[4], h[10];
@@ -538,8 +569,12 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
             for (int k = 0; k < 2; ++k)
               dv[2 * c + k] = wq[0][k] * d.U[0][c] + wq[1][k] * d.U[1][c] + wq[2][k] * d.U[2][c];
           double gv[4];
+          if constexpr (PSD) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) gv[i] = G[i][0] * dv[0] + G[i][1] * dv[1] + G[i][2] * dv[2] + G[i][3] * dv[3];
+            for (int i = 0; i < 4; ++i) gv[i] = G[i][0] * dv[0] + G[i][1] * dv[1] + G[i][2] * dv[2] + G[i][3] * dv[3];
+          } else {
+            ok &= dirichlet_hv_closed(J, dv, d.area, gv);
+          }
           if (P6) {  // y_s = sum_t P6(s, t) u_t (u masked)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
