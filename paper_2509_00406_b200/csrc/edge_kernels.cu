@@ -477,8 +477,14 @@ MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const dou
 template <int MODE, bool PSD> struct FastCfg {
   static constexpr int MAXI = EV_ELL_K, BLOCK = EV_ROW_BLOCK, MINB = EV_HESS_MINB;
 };
+#ifndef EV_HVP_MAXI
+#define EV_HVP_MAXI 4
+#endif
+#ifndef EV_HVP_THREADS
+#define EV_HVP_THREADS 512  // measured: 0.269 ms vs 0.288 at 640 (row-kernel spring HVP, 2048^2)
+#endif
 template <> struct FastCfg<MODE_HVP, false> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 640 / EV_FLAT_BLOCK;
+  static constexpr int MAXI = EV_HVP_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_THREADS / EV_FLAT_BLOCK;
 };
 template <> struct FastCfg<MODE_HVP, true> {
   static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 512 / EV_FLAT_BLOCK;
