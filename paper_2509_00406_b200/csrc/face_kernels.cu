@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
         cross3(p2, ps, c1);
         cross3(ps, p1, c2);
         const double det = ps[0] * cs[0] + ps[1] * cs[1] + ps[2] * cs[2];
-        const double id = 1.0 / det;
+        const double id = rcp_fast(det);  // non-finite / zero det -> non-finite, the exact path takes over
         // the value only feeds the gradient call's energy; the HVP needs the
         // derivative factors (finite for any det != 0, like the reference's dual)
         if constexpr (MODE == MODE_GRAD) val += -::log(det);
