@@ -939,8 +939,8 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
       B[q][c][1] = b2[c];
       r[c] = x0 * b1[c] + x1 * b2[c] + S[c];
     }
-    rho[q] = ::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-    const double ir = 1.0 / rho[q];
+    const double ir = 1.0 / ::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    rho[q] = ir;  // 1 / |r| (only the inverse is used below)
 #pragma unroll
     for (int c = 0; c < 3; ++c) p[q][c] = r[c] * ir;
 #pragma unroll
@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
                 pdb += J[q][c][jj2] * B[q][c][ii];
                 gb += g[q][c] * B[q][c][ii];
               }
-              const double ir = 1.0 / rho[q];
+              const double ir = rho[q];
               return -(gpd * pbi + gp * pdb) * ir - (gb - gp * pbi) * rdj * ir * ir;
             };
             acc += 0.5 * (tij(i, j) + tij(j, i));
