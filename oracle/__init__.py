@@ -14,6 +14,6 @@ this oracle against every one of them.
 """
 
 from .dual import Dual, lift_values
-from .engine import OracleProblem
+from .engine import OracleProblem, sparsity_pattern
 
-__all__ = ["Dual", "OracleProblem", "lift_values"]
+__all__ = ["Dual", "OracleProblem", "lift_values", "sparsity_pattern"]

@@ -72,6 +72,34 @@ def derive_edges(faces: np.ndarray, nv: int, explicit=None) -> np.ndarray:
     return np.zeros((0, 2), np.int64)
 
 
+def pattern_keys(nv, sels, fixed=None):
+    """Sorted unique pair keys row*nv + col of every ordered (a, b) vertex
+    pair of every element, both free (problem.py:389-398)."""
+    keyset = []
+    for sel in sels:
+        sel = np.asarray(sel, dtype=np.int64)
+        k = sel[:, :, None] * nv + sel[:, None, :]
+        if fixed is not None:
+            fm = ~fixed[sel]
+            k = k[fm[:, :, None] & fm[:, None, :]]
+        keyset.append(k.ravel())
+    return np.unique(np.concatenate(keyset)) if keyset else np.zeros(0, np.int64)
+
+
+def pattern_from_keys(keys, nv):
+    """int64 row_offsets (nv+1) and col_indices from sorted keys
+    (problem.py:399-402)."""
+    rows, cols = keys // nv, keys % nv
+    ro = np.zeros(nv + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=nv), out=ro[1:])
+    return ro, cols
+
+
+def sparsity_pattern(nv, sels, fixed=None):
+    """(row_offsets, col_indices) of the block Hessian (problem.py:383-402)."""
+    return pattern_from_keys(pattern_keys(nv, sels, fixed), nv)
+
+
 def _pairwise_total(parts) -> float:
     vals = [float(p) for p in parts]
     if not vals:
@@ -91,7 +119,14 @@ class OracleProblem:
     """
 
     def __init__(self, num_vertices, faces, edges, n, terms, with_hessian=True, fixed_vertices=(),
-                 workers=1, accumulation="deterministic", chunk=4096):
+                 workers=1, accumulation="deterministic", chunk=4096, element_ids=None):
+        """`element_ids` (optional, one entry per term, None = all): evaluate
+        only these global element ids of each term. Callbacks still see
+        global ids in `handle.index`, so closure arrays index correctly. A
+        vertex row whose incident elements are all included is complete
+        (gradient, Hessian row, HVP row: problem.py:535-544 scatter only
+        inside an element's own vertices), which is what the at-scale
+        sampled-row parity tests rely on."""
         self.nv = int(num_vertices)
         self.faces = np.asarray(faces, dtype=np.int64).reshape(-1, 3)
         self.edges = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
@@ -104,14 +139,15 @@ class OracleProblem:
         self.chunk = int(chunk)
         self.ndofs = self.n * self.nv
         self.terms = [(op, fn) for op, fn in terms]
-        self.groups = [self._layout(op) for op, _ in self.terms]
+        ids = list(element_ids) if element_ids is not None else [None] * len(self.terms)
+        self.groups = [self._layout(op, i) for (op, _), i in zip(self.terms, ids)]
         self.row_offsets = self.col_indices = None
         self.nnzb = None
         if with_hessian:
             self.precompute_sparsity()
 
     # layout (problem.py:327-379) ----------------------------------------------
-    def _layout(self, op):
+    def _layout(self, op, subset=None):
         if op == "FV":
             sel = self.faces
         elif op == "EV":
@@ -121,6 +157,9 @@ class OracleProblem:
         else:
             raise ValueError(f"oracle supports FV, EV, V terms, not {op}")
         ids = np.arange(len(sel), dtype=np.int64)
+        if subset is not None:
+            ids = np.asarray(subset, dtype=np.int64)
+            sel = sel[ids]
         free = (~self.fixed[sel]).astype(np.float64) if self.fixed.any() else None
         gidx = (sel[:, :, None] * self.n + np.arange(self.n)).reshape(len(ids), -1)
         if free is not None:
@@ -130,17 +169,8 @@ class OracleProblem:
     # sparsity (problem.py:383-416) --------------------------------------------
     def precompute_sparsity(self):
         nv = self.nv
-        keyset = []
-        for g in self.groups:
-            k = g.sel[:, :, None] * nv + g.sel[:, None, :]
-            if g.free is not None:
-                fm = g.free.astype(bool)
-                k = k[fm[:, :, None] & fm[:, None, :]]
-            keyset.append(k.ravel())
-        keys = np.unique(np.concatenate(keyset)) if keyset else np.zeros(0, np.int64)
-        rows, cols = keys // nv, keys % nv
-        ro = np.zeros(nv + 1, dtype=np.int64)
-        np.cumsum(np.bincount(rows, minlength=nv), out=ro[1:])
+        keys = pattern_keys(nv, [g.sel for g in self.groups], self.fixed if self.fixed.any() else None)
+        ro, cols = pattern_from_keys(keys, nv)
         self.row_offsets, self.col_indices, self.nnzb = ro, cols, len(keys)
         for g in self.groups:
             b = np.searchsorted(keys, g.sel[:, :, None] * nv + g.sel[:, None, :])

@@ -100,7 +100,9 @@ def cloth_problem(cfg: ClothConfig, mesh: Mesh, target, masses=None, pinned=None
         pinned = cfg.pinned if cfg.pinned is not None else ()
     p = Problem(mesh, 3, with_hessian=True, fixed_vertices=tuple(pinned), accumulation=accumulation)
     p.add_term(Element.VERTEX, Op.V, Inertia(masses, target))
-    p.add_term(Element.EDGE, Op.EV, Spring(rest_lengths2(mesh), 0.5 * cfg.k * h2))
+    import torch  # rest lengths are derived here, not a caller closure: device-resident, never re-uploaded
+
+    p.add_term(Element.EDGE, Op.EV, Spring(torch.from_numpy(rest_lengths2(mesh)).cuda(), 0.5 * cfg.k * h2))
     p.add_term(Element.VERTEX, Op.V, Gravity(masses, np.asarray(cfg.gravity, dtype=np.float64), h2))
     return p
 

@@ -131,6 +131,9 @@ int mg_mesh_create(const int64_t* faces_d, int64_t num_faces, const int64_t* edg
                    int patch_vertices, void* stream, mg_mesh** out) {
   if (!out) return fail(MG_ERR_VALUE, "out is NULL");
   if (num_vertices < 0 || num_faces < 0 || num_edges < 0) return fail(MG_ERR_VALUE, "negative size");
+  // the face / edge row kernels write one energy partial per 32-row warp; a
+  // patch of >= 32 rows keeps the generic patch kernel's partial count within it
+  if (patch_vertices > 0 && patch_vertices < 32) return fail(MG_ERR_VALUE, "patch_vertices must be >= 32");
   auto* h = new mg_mesh();
   int rc = guard([&] {
     h->m.V = num_vertices;

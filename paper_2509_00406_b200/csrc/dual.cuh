@@ -21,6 +21,14 @@
 // the reference multiplies real zero entries, so 0*Inf -> NaN spreads through
 // a gradient exactly as in numpy.
 //
+// Primal values are computed with explicitly rounded operations
+// (__dadd_rn / __dmul_rn, which the compiler never fuses into an FMA) so a
+// callback's value is bitwise the reference's numpy value for the same
+// operation order. This matters where the primal itself is ill-conditioned:
+// the sphere barrier's det[p0 p1 p2] at icosphere(10) is the difference of
+// O(1) products ~1e-6 apart, and a fused rounding there moves every face
+// gradient by ~1e-10 relative. Derivative parts may fuse.
+//
 // Packed Hessian index for i >= j: i*(i+1)/2 + j. Every product-rule update
 // is computed once per unordered pair, so the assembled blocks are bitwise
 // symmetric by construction (the reference guarantees the same, active.py:19-21).
@@ -44,19 +52,19 @@ struct Dv {
   double v;
 };
 
-template <int K> MG_DI Dv<K> operator+(Dv<K> a, Dv<K> b) { return {a.v + b.v}; }
-template <int K> MG_DI Dv<K> operator+(Dv<K> a, double b) { return {a.v + b}; }
-template <int K> MG_DI Dv<K> operator+(double b, Dv<K> a) { return {a.v + b}; }
-template <int K> MG_DI Dv<K> operator-(Dv<K> a, Dv<K> b) { return {a.v - b.v}; }
-template <int K> MG_DI Dv<K> operator-(Dv<K> a, double b) { return {a.v - b}; }
-template <int K> MG_DI Dv<K> operator-(double b, Dv<K> a) { return {b - a.v}; }
+template <int K> MG_DI Dv<K> operator+(Dv<K> a, Dv<K> b) { return {__dadd_rn(a.v, b.v)}; }
+template <int K> MG_DI Dv<K> operator+(Dv<K> a, double b) { return {__dadd_rn(a.v, b)}; }
+template <int K> MG_DI Dv<K> operator+(double b, Dv<K> a) { return {__dadd_rn(a.v, b)}; }
+template <int K> MG_DI Dv<K> operator-(Dv<K> a, Dv<K> b) { return {__dsub_rn(a.v, b.v)}; }
+template <int K> MG_DI Dv<K> operator-(Dv<K> a, double b) { return {__dsub_rn(a.v, b)}; }
+template <int K> MG_DI Dv<K> operator-(double b, Dv<K> a) { return {__dsub_rn(b, a.v)}; }
 template <int K> MG_DI Dv<K> operator-(Dv<K> a) { return {-a.v}; }
-template <int K> MG_DI Dv<K> operator*(Dv<K> a, Dv<K> b) { return {a.v * b.v}; }
-template <int K> MG_DI Dv<K> operator*(Dv<K> a, double b) { return {a.v * b}; }
-template <int K> MG_DI Dv<K> operator*(double b, Dv<K> a) { return {a.v * b}; }
-template <int K> MG_DI Dv<K> operator/(Dv<K> a, Dv<K> b) { double u = 1.0 / b.v; return {a.v * u}; }
-template <int K> MG_DI Dv<K> operator/(Dv<K> a, double b) { double u = 1.0 / b; return {a.v * u}; }
-template <int K> MG_DI Dv<K> operator/(double a, Dv<K> b) { double u = 1.0 / b.v; return {a * u}; }
+template <int K> MG_DI Dv<K> operator*(Dv<K> a, Dv<K> b) { return {__dmul_rn(a.v, b.v)}; }
+template <int K> MG_DI Dv<K> operator*(Dv<K> a, double b) { return {__dmul_rn(a.v, b)}; }
+template <int K> MG_DI Dv<K> operator*(double b, Dv<K> a) { return {__dmul_rn(a.v, b)}; }
+template <int K> MG_DI Dv<K> operator/(Dv<K> a, Dv<K> b) { double u = 1.0 / b.v; return {__dmul_rn(a.v, u)}; }
+template <int K> MG_DI Dv<K> operator/(Dv<K> a, double b) { double u = 1.0 / b; return {__dmul_rn(a.v, u)}; }
+template <int K> MG_DI Dv<K> operator/(double a, Dv<K> b) { double u = 1.0 / b.v; return {__dmul_rn(a, u)}; }
 template <int K> MG_DI Dv<K> sqrt(Dv<K> a) { return {::sqrt(a.v)}; }
 template <int K> MG_DI Dv<K> log(Dv<K> a) { return {::log(a.v)}; }
 template <int K> MG_DI Dv<K> exp(Dv<K> a) { return {::exp(a.v)}; }
@@ -73,20 +81,20 @@ struct Dg {
 };
 
 template <int K> MG_DI Dg<K> operator+(const Dg<K>& a, const Dg<K>& b) {
-  Dg<K> r; r.v = a.v + b.v;
+  Dg<K> r; r.v = __dadd_rn(a.v, b.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] + b.g[i];
   return r;
 }
-template <int K> MG_DI Dg<K> operator+(const Dg<K>& a, double b) { Dg<K> r = a; r.v = a.v + b; return r; }
+template <int K> MG_DI Dg<K> operator+(const Dg<K>& a, double b) { Dg<K> r = a; r.v = __dadd_rn(a.v, b); return r; }
 template <int K> MG_DI Dg<K> operator+(double b, const Dg<K>& a) { return a + b; }
 template <int K> MG_DI Dg<K> operator-(const Dg<K>& a, const Dg<K>& b) {
-  Dg<K> r; r.v = a.v - b.v;
+  Dg<K> r; r.v = __dsub_rn(a.v, b.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] - b.g[i];
   return r;
 }
-template <int K> MG_DI Dg<K> operator-(const Dg<K>& a, double b) { Dg<K> r = a; r.v = a.v - b; return r; }
+template <int K> MG_DI Dg<K> operator-(const Dg<K>& a, double b) { Dg<K> r = a; r.v = __dsub_rn(a.v, b); return r; }
 template <int K> MG_DI Dg<K> operator-(const Dg<K>& a) {
   Dg<K> r; r.v = -a.v;
 #pragma unroll
@@ -94,20 +102,20 @@ template <int K> MG_DI Dg<K> operator-(const Dg<K>& a) {
   return r;
 }
 template <int K> MG_DI Dg<K> operator-(double b, const Dg<K>& a) {
-  Dg<K> r; r.v = b - a.v;
+  Dg<K> r; r.v = __dsub_rn(b, a.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = -a.g[i];
   return r;
 }
 template <int K> MG_DI Dg<K> operator*(const Dg<K>& a, double c) {
-  Dg<K> r; r.v = a.v * c;
+  Dg<K> r; r.v = __dmul_rn(a.v, c);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] * c;
   return r;
 }
 template <int K> MG_DI Dg<K> operator*(double c, const Dg<K>& a) { return a * c; }
 template <int K> MG_DI Dg<K> operator*(const Dg<K>& a, const Dg<K>& b) {
-  Dg<K> r; r.v = a.v * b.v;
+  Dg<K> r; r.v = __dmul_rn(a.v, b.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] * b.v + b.g[i] * a.v;
   return r;
@@ -115,14 +123,14 @@ template <int K> MG_DI Dg<K> operator*(const Dg<K>& a, const Dg<K>& b) {
 template <int K> MG_DI Dg<K> operator/(const Dg<K>& a, double b) { double u = 1.0 / b; return a * u; }
 template <int K> MG_DI Dg<K> operator/(const Dg<K>& a, const Dg<K>& b) {
   double u = 1.0 / b.v;
-  Dg<K> r; r.v = a.v * u;
+  Dg<K> r; r.v = __dmul_rn(a.v, u);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = (a.g[i] - r.v * b.g[i]) * u;
   return r;
 }
 template <int K> MG_DI Dg<K> operator/(double a, const Dg<K>& b) {
   double u = 1.0 / b.v;
-  Dg<K> r; r.v = a * u;
+  Dg<K> r; r.v = __dmul_rn(a, u);
   double f = -r.v * u;
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = b.g[i] * f;
@@ -192,23 +200,23 @@ MG_DI void h_sub(Dh<K, ZA && ZB>& r, const Dh<K, ZA>& a, const Dh<K, ZB>& b) {
 
 template <int K, bool ZA, bool ZB>
 MG_DI Dh<K, ZA && ZB> operator+(const Dh<K, ZA>& a, const Dh<K, ZB>& b) {
-  Dh<K, ZA && ZB> r; r.v = a.v + b.v;
+  Dh<K, ZA && ZB> r; r.v = __dadd_rn(a.v, b.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] + b.g[i];
   detail::h_add<K, ZA, ZB>(r, a, b);
   return r;
 }
-template <int K, bool Z> MG_DI Dh<K, Z> operator+(const Dh<K, Z>& a, double b) { Dh<K, Z> r = a; r.v = a.v + b; return r; }
+template <int K, bool Z> MG_DI Dh<K, Z> operator+(const Dh<K, Z>& a, double b) { Dh<K, Z> r = a; r.v = __dadd_rn(a.v, b); return r; }
 template <int K, bool Z> MG_DI Dh<K, Z> operator+(double b, const Dh<K, Z>& a) { return a + b; }
 template <int K, bool ZA, bool ZB>
 MG_DI Dh<K, ZA && ZB> operator-(const Dh<K, ZA>& a, const Dh<K, ZB>& b) {
-  Dh<K, ZA && ZB> r; r.v = a.v - b.v;
+  Dh<K, ZA && ZB> r; r.v = __dsub_rn(a.v, b.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] - b.g[i];
   detail::h_sub<K, ZA, ZB>(r, a, b);
   return r;
 }
-template <int K, bool Z> MG_DI Dh<K, Z> operator-(const Dh<K, Z>& a, double b) { Dh<K, Z> r = a; r.v = a.v - b; return r; }
+template <int K, bool Z> MG_DI Dh<K, Z> operator-(const Dh<K, Z>& a, double b) { Dh<K, Z> r = a; r.v = __dsub_rn(a.v, b); return r; }
 template <int K, bool Z> MG_DI Dh<K, Z> operator-(const Dh<K, Z>& a) {
   Dh<K, Z> r; r.v = -a.v;
 #pragma unroll
@@ -220,10 +228,10 @@ template <int K, bool Z> MG_DI Dh<K, Z> operator-(const Dh<K, Z>& a) {
   return r;
 }
 template <int K, bool Z> MG_DI Dh<K, Z> operator-(double b, const Dh<K, Z>& a) {
-  Dh<K, Z> r = -a; r.v = b - a.v; return r;
+  Dh<K, Z> r = -a; r.v = __dsub_rn(b, a.v); return r;
 }
 template <int K, bool Z> MG_DI Dh<K, Z> operator*(const Dh<K, Z>& a, double c) {
-  Dh<K, Z> r; r.v = a.v * c;
+  Dh<K, Z> r; r.v = __dmul_rn(a.v, c);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] * c;
   if constexpr (!Z) {
@@ -238,7 +246,7 @@ template <int K, bool Z> MG_DI Dh<K, Z> operator*(double c, const Dh<K, Z>& a) {
 //   h = (a.h*bv + b.h*av) + (ga gb^T + gb ga^T)
 template <int K, bool ZA, bool ZB>
 MG_DI Dh<K, false> operator*(const Dh<K, ZA>& a, const Dh<K, ZB>& b) {
-  Dh<K, false> r; r.v = a.v * b.v;
+  Dh<K, false> r; r.v = __dmul_rn(a.v, b.v);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] * b.v + b.g[i] * a.v;
 #pragma unroll
@@ -262,7 +270,7 @@ template <int K, bool Z> MG_DI Dh<K, Z> operator/(const Dh<K, Z>& a, double b) {
 template <int K, bool ZA, bool ZB>
 MG_DI Dh<K, false> operator/(const Dh<K, ZA>& a, const Dh<K, ZB>& b) {
   double u = 1.0 / b.v;
-  Dh<K, false> r; r.v = a.v * u;
+  Dh<K, false> r; r.v = __dmul_rn(a.v, u);
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = (a.g[i] - r.v * b.g[i]) * u;
   const double cb = -r.v * u, cs = -u * u, cq = 2.0 * r.v * u * u;
@@ -283,7 +291,7 @@ MG_DI Dh<K, false> operator/(const Dh<K, ZA>& a, const Dh<K, ZB>& b) {
 template <int K, bool Z>
 MG_DI Dh<K, false> operator/(double a, const Dh<K, Z>& b) {
   double u = 1.0 / b.v;
-  Dh<K, false> r; r.v = a * u;
+  Dh<K, false> r; r.v = __dmul_rn(a, u);
   const double cb = -r.v * u, cq = 2.0 * r.v * u * u;
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = b.g[i] * cb;
@@ -348,7 +356,7 @@ struct Df<K, false> {
 
 template <int K, bool ZA, bool ZB>
 MG_DI Df<K, ZA && ZB> operator+(const Df<K, ZA>& a, const Df<K, ZB>& b) {
-  Df<K, ZA && ZB> r; r.v = a.v + b.v; r.vd = a.vd + b.vd;
+  Df<K, ZA && ZB> r; r.v = __dadd_rn(a.v, b.v); r.vd = a.vd + b.vd;
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] + b.g[i];
   if constexpr (!ZA && !ZB) {
@@ -363,7 +371,7 @@ MG_DI Df<K, ZA && ZB> operator+(const Df<K, ZA>& a, const Df<K, ZB>& b) {
   }
   return r;
 }
-template <int K, bool Z> MG_DI Df<K, Z> operator+(const Df<K, Z>& a, double b) { Df<K, Z> r = a; r.v = a.v + b; return r; }
+template <int K, bool Z> MG_DI Df<K, Z> operator+(const Df<K, Z>& a, double b) { Df<K, Z> r = a; r.v = __dadd_rn(a.v, b); return r; }
 template <int K, bool Z> MG_DI Df<K, Z> operator+(double b, const Df<K, Z>& a) { return a + b; }
 template <int K, bool Z> MG_DI Df<K, Z> operator-(const Df<K, Z>& a) {
   Df<K, Z> r; r.v = -a.v; r.vd = -a.vd;
@@ -377,7 +385,7 @@ template <int K, bool Z> MG_DI Df<K, Z> operator-(const Df<K, Z>& a) {
 }
 template <int K, bool ZA, bool ZB>
 MG_DI Df<K, ZA && ZB> operator-(const Df<K, ZA>& a, const Df<K, ZB>& b) {
-  Df<K, ZA && ZB> r; r.v = a.v - b.v; r.vd = a.vd - b.vd;
+  Df<K, ZA && ZB> r; r.v = __dsub_rn(a.v, b.v); r.vd = a.vd - b.vd;
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] - b.g[i];
   if constexpr (!ZA && !ZB) {
@@ -392,10 +400,10 @@ MG_DI Df<K, ZA && ZB> operator-(const Df<K, ZA>& a, const Df<K, ZB>& b) {
   }
   return r;
 }
-template <int K, bool Z> MG_DI Df<K, Z> operator-(const Df<K, Z>& a, double b) { Df<K, Z> r = a; r.v = a.v - b; return r; }
-template <int K, bool Z> MG_DI Df<K, Z> operator-(double b, const Df<K, Z>& a) { Df<K, Z> r = -a; r.v = b - a.v; return r; }
+template <int K, bool Z> MG_DI Df<K, Z> operator-(const Df<K, Z>& a, double b) { Df<K, Z> r = a; r.v = __dsub_rn(a.v, b); return r; }
+template <int K, bool Z> MG_DI Df<K, Z> operator-(double b, const Df<K, Z>& a) { Df<K, Z> r = -a; r.v = __dsub_rn(b, a.v); return r; }
 template <int K, bool Z> MG_DI Df<K, Z> operator*(const Df<K, Z>& a, double c) {
-  Df<K, Z> r; r.v = a.v * c; r.vd = a.vd * c;
+  Df<K, Z> r; r.v = __dmul_rn(a.v, c); r.vd = a.vd * c;
 #pragma unroll
   for (int i = 0; i < K; ++i) r.g[i] = a.g[i] * c;
   if constexpr (!Z) {
@@ -408,7 +416,7 @@ template <int K, bool Z> MG_DI Df<K, Z> operator*(double c, const Df<K, Z>& a) {
 // (H_a bv + H_b av + ga gb^T + gb ga^T) w
 template <int K, bool ZA, bool ZB>
 MG_DI Df<K, false> operator*(const Df<K, ZA>& a, const Df<K, ZB>& b) {
-  Df<K, false> r; r.v = a.v * b.v; r.vd = a.vd * b.v + b.vd * a.v;
+  Df<K, false> r; r.v = __dmul_rn(a.v, b.v); r.vd = a.vd * b.v + b.vd * a.v;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     r.g[i] = a.g[i] * b.v + b.g[i] * a.v;
@@ -424,7 +432,7 @@ template <int K, bool Z> MG_DI Df<K, Z> operator/(const Df<K, Z>& a, double b) {
 template <int K, bool ZA, bool ZB>
 MG_DI Df<K, false> operator/(const Df<K, ZA>& a, const Df<K, ZB>& b) {
   double u = 1.0 / b.v;
-  Df<K, false> r; r.v = a.v * u; r.vd = (a.vd - r.v * b.vd) * u;
+  Df<K, false> r; r.v = __dmul_rn(a.v, u); r.vd = (a.vd - r.v * b.vd) * u;
   const double cb = -r.v * u, cs = -u * u, cq = 2.0 * r.v * u * u;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
@@ -440,7 +448,7 @@ MG_DI Df<K, false> operator/(const Df<K, ZA>& a, const Df<K, ZB>& b) {
 template <int K, bool Z>
 MG_DI Df<K, false> operator/(double a, const Df<K, Z>& b) {
   double u = 1.0 / b.v;
-  Df<K, false> r; r.v = a * u;
+  Df<K, false> r; r.v = __dmul_rn(a, u);
   const double cb = -r.v * u, cq = 2.0 * r.v * u * u;
   r.vd = b.vd * cb;
 #pragma unroll

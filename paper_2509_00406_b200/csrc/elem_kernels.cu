@@ -378,6 +378,76 @@ __global__ void k_block_apply(const double* inv, const double* r, double* y, int
   }
 }
 
+// Any block dim n (traced terms accept var_dim > 3, problem.py:263): one
+// thread per scalar row for the SpMV / apply; Gauss-Jordan with partial
+// pivoting for the diagonal-block inverse (identity on an exactly zero
+// pivot, where numpy.linalg.inv raises and the reference falls back).
+__global__ void k_bsr_matvec_n(const int64_t* ro, const int32_t* col, const double* H, const double* v,
+                               double* y, int64_t V, int n) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= V * n) return;
+  const int64_t i = t / n;
+  const int r = (int)(t - i * n);
+  double acc = 0.0;
+  for (int64_t k = ro[i]; k < ro[i + 1]; ++k) {
+    const double* b = H + (k * n + r) * n;
+    const double* vv = v + (int64_t)col[k] * n;
+    for (int c = 0; c < n; ++c) acc += b[c] * vv[c];
+  }
+  y[t] = acc;
+}
+
+__global__ void k_block_jacobi_inv_n(const int64_t* ro, const int32_t* col, const double* H, int64_t V, int n,
+                                     double* a_scratch, double* inv) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int64_t nn = (int64_t)n * n;
+  double* out = inv + v * nn;
+  double* a = a_scratch + v * nn;
+  int64_t lo = ro[v], hi = ro[v + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (col[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  bool ok = lo < ro[v + 1] && col[lo] == v;
+  for (int64_t i = 0; i < nn; ++i) {
+    a[i] = ok ? H[lo * nn + i] : 0.0;
+    out[i] = (i / n == i % n) ? 1.0 : 0.0;
+  }
+  for (int c = 0; ok && c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (fabs(a[r * n + c]) > fabs(a[piv * n + c])) piv = r;
+    if (a[piv * n + c] == 0.0) { ok = false; break; }
+    if (piv != c)
+      for (int j = 0; j < n; ++j) {
+        double t = a[c * n + j]; a[c * n + j] = a[piv * n + j]; a[piv * n + j] = t;
+        t = out[c * n + j]; out[c * n + j] = out[piv * n + j]; out[piv * n + j] = t;
+      }
+    const double d = 1.0 / a[c * n + c];
+    for (int j = 0; j < n; ++j) { a[c * n + j] *= d; out[c * n + j] *= d; }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = a[r * n + c];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) { a[r * n + j] -= f * a[c * n + j]; out[r * n + j] -= f * out[c * n + j]; }
+    }
+  }
+  if (!ok)
+    for (int64_t i = 0; i < nn; ++i) out[i] = (i / n == i % n) ? 1.0 : 0.0;
+}
+
+__global__ void k_block_apply_n(const double* inv, const double* r, double* y, int64_t V, int n) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= V * n) return;
+  const int64_t v = t / n;
+  const int i = (int)(t - v * n);
+  const double* m = inv + (v * n + i) * n;
+  double acc = 0.0;
+  for (int j = 0; j < n; ++j) acc += m[j] * r[v * n + j];
+  y[t] = acc;
+}
+
 }  // namespace
 
 void launch_block_jacobi(const Problem& p, const double* H, double* inv, cudaStream_t s) {
@@ -388,7 +458,14 @@ void launch_block_jacobi(const Problem& p, const double* H, double* inv, cudaStr
     case 1: k_block_jacobi_inv<1><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, inv); break;
     case 2: k_block_jacobi_inv<2><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, inv); break;
     case 3: k_block_jacobi_inv<3><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, inv); break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "block Jacobi supports block dims 1..3");
+    default: {
+      // elimination scratch, stream-ordered (freed after the kernel on the same stream)
+      double* a = nullptr;
+      MG_CUDA(cudaMallocAsync(&a, sizeof(double) * V * p.n * p.n, s));
+      k_block_jacobi_inv_n<<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, V, p.n, a, inv);
+      MG_LAUNCH_CHECK();
+      MG_CUDA(cudaFreeAsync(a, s));
+    }
   }
   MG_LAUNCH_CHECK();
 }
@@ -401,7 +478,8 @@ void launch_block_apply(const Problem& p, const double* inv, const double* r, do
     case 1: k_block_apply<1><<<grid, 256, 0, s>>>(inv, r, y, V); break;
     case 2: k_block_apply<2><<<grid, 256, 0, s>>>(inv, r, y, V); break;
     case 3: k_block_apply<3><<<grid, 256, 0, s>>>(inv, r, y, V); break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "block Jacobi supports block dims 1..3");
+    default:
+      k_block_apply_n<<<(unsigned)((V * p.n + 255) / 256), 256, 0, s>>>(inv, r, y, V, p.n);
   }
   MG_LAUNCH_CHECK();
 }
@@ -464,7 +542,9 @@ void launch_bsr_matvec(const Problem& p, const double* H, const double* v, doubl
     case 1: k_bsr_matvec<1><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V); break;
     case 2: k_bsr_matvec<2><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V); break;
     case 3: k_bsr_matvec<3><<<grid, 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V); break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "bsr matvec supports block dims 1..3");
+    default:
+      k_bsr_matvec_n<<<(unsigned)((V * p.n + 255) / 256), 256, 0, s>>>(p.row_offsets.p, p.col32.p, H, v, y, V,
+                                                                       p.n);
   }
   MG_LAUNCH_CHECK();
 }

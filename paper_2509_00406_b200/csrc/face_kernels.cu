@@ -688,18 +688,44 @@ struct Retract {
   double p[3], pd[3], rho, rhod;  // p, pdot = J u, |r|, d|r|/de
 };
 
+// Reference-order, unfused primal of the retraction and of the barrier's
+// determinant. At BASELINE size (icosphere(10), edge ~1.1e-3) det[p0 p1 p2]
+// ~1e-6 is a difference of O(1) products, so its rounding (~1e-10 relative)
+// moves every face gradient by as much, and the six faces around a vertex
+// cancel to a gradient ~25x smaller. Computing p and det with exactly the
+// reference's operations (apps/sphere.py:69-71: r = (x0 b1 + x1 b2) + s,
+// p = r * (1/sqrt(r.r)); active.py:445-453 cofactor expansion in face
+// order; numpy never fuses a multiply-add) makes both bitwise equal to the
+// reference's, leaving only well-conditioned differences.
+MG_DI double rmul(double a, double b) { return __dmul_rn(a, b); }
+MG_DI double radd(double a, double b) { return __dadd_rn(a, b); }
+MG_DI double rsub(double a, double b) { return __dsub_rn(a, b); }
+
+MG_DI double retract_ref(const double* s, const double* b1, const double* b2, double x0, double x1, double* r,
+                         double* p) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) r[c] = radd(radd(rmul(x0, b1[c]), rmul(x1, b2[c])), s[c]);
+  const double rho = ::sqrt(radd(radd(rmul(r[0], r[0]), rmul(r[1], r[1])), rmul(r[2], r[2])));
+  const double ir = 1.0 / rho;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) p[c] = rmul(r[c], ir);
+  return rho;
+}
+
+// SmallMatrix.from_columns(p0, p1, p2).det() (m_ij = p_j[i])
+MG_DI double det_ref(const double* p0, const double* p1, const double* p2) {
+  return radd(rsub(rmul(p0[0], rsub(rmul(p1[1], p2[2]), rmul(p2[1], p1[2]))),
+                   rmul(p1[0], rsub(rmul(p0[1], p2[2]), rmul(p2[1], p0[2])))),
+              rmul(p2[0], rsub(rmul(p0[1], p1[2]), rmul(p1[1], p0[2]))));
+}
+
 MG_DI Retract retract(const double* s, const double* b1, const double* b2, double x0, double x1, double u0, double u1) {
   Retract R;
   double r[3], rd[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    r[c] = x0 * b1[c] + x1 * b2[c] + s[c];
-    rd[c] = u0 * b1[c] + u1 * b2[c];
-  }
-  R.rho = ::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  R.rho = retract_ref(s, b1, b2, x0, x1, r, R.p);
   const double ir = 1.0 / R.rho;
 #pragma unroll
-  for (int c = 0; c < 3; ++c) R.p[c] = r[c] * ir;
+  for (int c = 0; c < 3; ++c) rd[c] = u0 * b1[c] + u1 * b2[c];
   const double prd = R.p[0] * rd[0] + R.p[1] * rd[1] + R.p[2] * rd[2];
   R.rhod = prd;
 #pragma unroll
@@ -800,7 +826,15 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
         cross3(p1, p2, cs);
         cross3(p2, ps, c1);
         cross3(ps, p1, c2);
-        const double det = ps[0] * cs[0] + ps[1] * cs[1] + ps[2] * cs[2];
+        // the determinant in the face's own corner order (slot s is this row)
+        double f0[3], f1[3], f2[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          f0[c] = s == 0 ? ps[c] : (s == 1 ? p2[c] : p1[c]);
+          f1[c] = s == 0 ? p1[c] : (s == 1 ? ps[c] : p2[c]);
+          f2[c] = s == 0 ? p2[c] : (s == 1 ? p1[c] : ps[c]);
+        }
+        const double det = det_ref(f0, f1, f2);
         const double id = rcp_fast(det);  // non-finite / zero det -> non-finite, the exact path takes over
         // the value only feeds the gradient call's energy; the HVP needs the
         // derivative factors (finite for any det != 0, like the reference's dual)
@@ -937,12 +971,9 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
     for (int c = 0; c < 3; ++c) {
       B[q][c][0] = b1[c];
       B[q][c][1] = b2[c];
-      r[c] = x0 * b1[c] + x1 * b2[c] + S[c];
     }
-    const double ir = 1.0 / ::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    const double ir = 1.0 / retract_ref(S, b1, b2, x0, x1, r, p[q]);
     rho[q] = ir;  // 1 / |r| (only the inverse is used below)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) p[q][c] = r[c] * ir;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const double pb = p[q][0] * B[q][0][j] + p[q][1] * B[q][1][j] + p[q][2] * B[q][2][j];
@@ -965,7 +996,7 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
     cross3(p[1], p[2], cc[0]);
     cross3(p[2], p[0], cc[1]);
     cross3(p[0], p[1], cc[2]);
-    const double det = p[0][0] * cc[0][0] + p[0][1] * cc[0][1] + p[0][2] * cc[0][2];
+    const double det = det_ref(p[0], p[1], p[2]);
     id = 1.0 / det;
     chk += ::log(det);
 #pragma unroll

@@ -75,7 +75,9 @@ class ClothSim:
         self.rest_len2 = rest_lengths2(self.mesh)
         self._target = torch.from_numpy(np.ascontiguousarray(self.mesh.positions, dtype=np.float64)).cuda()
         self._pin_idx = torch.tensor(list(self.pinned), dtype=torch.int64, device="cuda")
-        self.problem = cloth_problem(cfg, self.mesh, self._target, masses=self.masses, pinned=self.pinned,
+        self.problem = cloth_problem(cfg, self.mesh, self._target, masses=torch.from_numpy(
+                                         np.ascontiguousarray(self.masses, dtype=np.float64)).cuda(),
+                                     pinned=self.pinned,
                                      accumulation=accumulation)
         self.problem.precompute_sparsity()
 

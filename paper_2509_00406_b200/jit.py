@@ -61,9 +61,10 @@ class _Graph:
         a = np.asarray(v)
         if a.dtype == bool:
             a = a.astype(np.float64)
-        if a.ndim == 0 or a.size == 1:
+        per_element = a.ndim == 1 and a.shape[0] == self.M
+        if not per_element and (a.ndim == 0 or a.size == 1):  # with M == 1 a (1,) array is still a stream
             return _lit(float(a.reshape(-1)[0]))
-        if a.ndim == 1 and a.shape[0] == self.M:
+        if per_element:
             # the same memory (also different views of it) is one stream
             key = None
             if isinstance(v, np.ndarray):
@@ -254,22 +255,45 @@ def trace_callback(fn, op: str, n: int, num_elements: int, sel=None, index=None)
     return TracedTerm(op, P, n, g.lines, ret, g.attrs)
 
 
+_NVCC_FLAGS = ["-cubin", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "--expt-relaxed-constexpr"]
+_toolchain_key = None
+
+
+def _toolchain() -> bytes:
+    """Everything a cubin depends on besides the generated source: every
+    header under csrc/ (jit_kernel.cuh includes dual.cuh, psd.cuh,
+    psd_small.h, ...), the nvcc flags and the nvcc version."""
+    global _toolchain_key
+    if _toolchain_key is None:
+        nvcc = os.environ.get("NVCC", "nvcc")
+        try:
+            ver = subprocess.run([nvcc, "--version"], capture_output=True, text=True).stdout
+        except OSError:
+            ver = "no-nvcc"
+        parts = [nvcc.encode(), " ".join(_NVCC_FLAGS).encode(), ver.encode()]
+        for hdr in sorted(list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))):
+            parts += [hdr.name.encode(), hdr.read_bytes()]
+        _toolchain_key = b"\0".join(parts)
+    return _toolchain_key
+
+
 def compile_term(tt: TracedTerm) -> bytes:
-    """nvcc the traced functor into an sm_100a cubin (cached by source hash)."""
+    """nvcc the traced functor into an sm_100a cubin (cached by source +
+    toolchain hash; compiled under a per-process name, then renamed)."""
     src = tt.source()
-    h = hashlib.sha256(src.encode() + (CSRC / "jit_kernel.cuh").read_bytes() + (CSRC / "jit_abi.h").read_bytes()
-                       + (CSRC / "dual.cuh").read_bytes()
-                       + (CSRC / "psd.cuh").read_bytes()).hexdigest()[:20]
+    h = hashlib.sha256(src.encode() + _toolchain()).hexdigest()[:20]
     CACHE.mkdir(parents=True, exist_ok=True)
     cubin = CACHE / f"term_{h}.cubin"
     if not cubin.exists():
-        cu = CACHE / f"term_{h}.cu"
+        tag = f"{os.getpid()}_{os.urandom(4).hex()}"
+        cu = CACHE / f"term_{h}.{tag}.cu"
+        tmp = CACHE / f"term_{h}.{tag}.cubin.tmp"
         cu.write_text(src)
         nvcc = os.environ.get("NVCC", "nvcc")
-        cmd = [nvcc, "-cubin", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
-               "--expt-relaxed-constexpr", "-I", str(CSRC), "-o", str(cubin) + ".tmp", str(cu)]
+        cmd = [nvcc, *_NVCC_FLAGS, "-I", str(CSRC), "-o", str(tmp), str(cu)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for traced term:\n{r.stderr[-4000:]}")
-        os.replace(str(cubin) + ".tmp", cubin)
+        os.replace(tmp, cubin)
+        os.replace(cu, CACHE / f"term_{h}.cu")
     return cubin.read_bytes()

@@ -99,6 +99,8 @@ class Mesh:
 
     def __init__(self, positions, faces, edges=None, patch_target: int = DEFAULT_PATCH_TARGET,
                  patch_vertices: int = DEFAULT_PATCH_VERTICES, owned=None):
+        if patch_vertices < 32:
+            raise MeshError("patch_vertices must be >= 32 (one energy partial per 32-row warp)")
         positions = np.array(positions, dtype=np.float64)
         if positions.ndim != 2 or positions.shape[1] != 3:
             raise MeshError(f"positions must be (V, 3), got {positions.shape}")

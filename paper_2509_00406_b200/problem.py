@@ -101,7 +101,11 @@ class BlockSparseMatrix:
         torch = _torch()
         p = self._problem
         host = not isinstance(v, torch.Tensor)
-        vd = _as_device(v, torch, torch.device("cuda")).reshape(-1)
+        n = self.num_block_rows * self.block_dim
+        if (v.numel() if not host else np.size(v)) != n:
+            raise ValueError(f"cannot reshape array of size {np.size(v) if host else v.numel()} into shape ({n},)")
+        vd = _as_device(v if not host else np.asarray(v, dtype=np.float64).reshape(-1), torch,
+                        torch.device("cuda")).reshape(-1)
         y = torch.empty_like(vd)
         _lib.check(p._lib.mg_bsr_matvec(p._h, self.values_device.data_ptr(), vd.data_ptr(), y.data_ptr(),
                                         _lib.stream_ptr()))
@@ -191,7 +195,7 @@ class Problem:
     def __init__(self, mesh: Mesh, var_dim: int, with_hessian: bool = True,
                  fixed_vertices=(), accumulation: str = "deterministic",
                  workers: int = 1, valence_cap: int = DEFAULT_VALENCE_CAP,
-                 chunk_elements: int = 4096, live_host_attrs: bool = False):
+                 chunk_elements: int = 4096, live_host_attrs: bool = True):
         if var_dim < 1:
             raise ValueError("var_dim must be at least 1")
         if accumulation not in ("deterministic", "atomic"):
@@ -370,20 +374,32 @@ class Problem:
 
     def _sync_attrs(self):
         if self.live_host_attrs:
-            self.refresh_attrs()
+            self.refresh_attrs(only_host=True)
 
-    def refresh_attrs(self):
+    def refresh_attrs(self, only_host: bool = False):
         """Re-upload the host (numpy) attribute arrays of every term.
 
         The reference's callbacks read their closure arrays live on every call
-        (ClothSim.step rewrites `target` in place, apps/cloth.py:128). Here a
-        numpy attribute is snapshotted to the device at `add_term`; mutate a
-        CUDA tensor attribute in place instead (zero copies), or call this
-        after changing a numpy one (or construct with live_host_attrs=True to
-        re-upload on every call, at PCIe cost)."""
+        (ClothSim.step rewrites `target` in place, apps/cloth.py:128; the
+        sphere app rewrites its bases, apps/sphere.py:123-126). By default
+        (`live_host_attrs=True`) every call does the same: numpy attributes of
+        builtin terms are copied to the device again and traced callbacks with
+        closure arrays are re-gathered. CUDA tensor attributes are read in
+        place by the kernels (zero copies) — the fast way to mutate state.
+        With `live_host_attrs=False` numpy attributes are snapshots taken at
+        `add_term`, refreshed only by calling this method."""
         from . import jit
 
         for rec in self._terms:
+            if only_host:
+                if rec.groups is not None:
+                    live = any(sub.dev_attrs for sub in rec.groups)
+                elif rec.traced is not None:
+                    live = bool(rec.dev_attrs)  # without closure arrays a traced callback is constants only
+                else:
+                    live = any(h is not None for h in rec.host_attrs)
+                if not live:
+                    continue
             if rec.groups is not None:  # VV: every valence group
                 for sub in rec.groups:
                     tt = jit.trace_callback(rec.term, "VV", self.n, len(sub.index), sub.sel, index=sub.index)
@@ -536,6 +552,10 @@ class Problem:
         xd = self._vec_in(x, msg)
         vd = self._vec_in(v, msg)
         self._sync_attrs()
+        if out is not None and not (isinstance(out, torch.Tensor) and out.dtype == torch.float64
+                                    and out.device == vd.device and out.is_contiguous()
+                                    and out.numel() == self._num_dofs):
+            raise ValueError(f"out must be a contiguous float64 CUDA tensor of {self._num_dofs} entries")
         y = out if out is not None else torch.empty(self._num_dofs, dtype=torch.float64, device=self._dev)
         _lib.check(self._lib.mg_hvp(self._h, xd.data_ptr(), vd.data_ptr(), int(psd_floor is not None),
                                     float(psd_floor or 0.0), y.data_ptr(), _lib.stream_ptr()))

@@ -9,10 +9,10 @@ Each class is both
     the reference's operation order, over the scalar-generic containers of
     `active.py`. The CPU oracle (tests only) runs exactly this callable.
 
-Attribute arrays may be numpy arrays (re-uploaded on every call, like the
-reference re-reading closure arrays that `ClothSim.step` / the sphere
-`post_step` rewrite in place) or CUDA torch tensors (used by reference, zero
-copies).
+Attribute arrays may be numpy arrays (re-uploaded on every call by default,
+`Problem(live_host_attrs=True)`, like the reference re-reading closure arrays
+that `ClothSim.step` / the sphere `post_step` rewrite in place) or CUDA torch
+tensors (read in place by the kernels, zero copies).
 """
 
 from __future__ import annotations

@@ -58,30 +58,44 @@ def test_traced_callbacks_match_reference(name):
                 assert rel(p.hvp(x, d[f"s{s}_v0"], psd_floor=FLOOR), d[f"s{s}_hvp_psd0"]) <= 1e-10
 
 
-def test_traced_closure_refresh():
-    """A closure array mutated in place (ClothSim.step's target rewrite,
-    apps/cloth.py:128) is re-read after refresh_attrs()."""
+@pytest.mark.parametrize("traced", [True, False])
+def test_numpy_closure_mutated_in_place(traced):
+    """A numpy closure array mutated in place between calls (ClothSim.step's
+    target rewrite, apps/cloth.py:128) is seen by the next eval_terms, as in
+    the reference, for traced callbacks and builtin terms alike. With
+    live_host_attrs=False the arrays are snapshots until refresh_attrs()."""
     import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200 import terms as T
 
     d = load("cloth8")
-    target = d["a_target"].copy()
     masses = d["a_masses"]
 
-    def inertia(v, nbrs, x):
-        dd = x[v] - target[v.index]
-        return 0.5 * masses[v.index] * dd.norm2()
+    def expect(x, target):
+        dx = x.reshape(-1, 3) - target
+        return 0.5 * np.sum(masses[:, None] * dx * dx)
 
-    p = mg.Problem(engine_mesh(d), 3)
-    p.add_term(mg.Element.VERTEX, mg.Op.V, inertia)
-    x = d["s0_x"]
-    p.x = x
-    e0 = p.eval_terms()
-    target += 0.5
-    p.refresh_attrs()
-    e1 = p.eval_terms()
-    dx = x.reshape(-1, 3) - target
-    assert abs(e1 - 0.5 * np.sum(masses[:, None] * dx * dx)) <= 1e-12 * abs(e1)
-    assert e1 != e0
+    for live in (True, False):
+        target = d["a_target"].copy()
+
+        def inertia(v, nbrs, x):
+            dd = x[v] - target[v.index]
+            return 0.5 * masses[v.index] * dd.norm2()
+
+        p = mg.Problem(engine_mesh(d), 3, live_host_attrs=live)
+        p.add_term(mg.Element.VERTEX, mg.Op.V, inertia if traced else T.Inertia(masses, target))
+        x = d["s0_x"]
+        p.x = x
+        e0 = p.eval_terms()
+        assert abs(e0 - expect(x, target)) <= 1e-12 * abs(e0)
+        target += 0.5  # in place, like target[:] = ... in the reference app
+        e1 = p.eval_terms()
+        if live:
+            assert abs(e1 - expect(x, target)) <= 1e-12 * abs(e1) and e1 != e0
+            assert abs(p.eval_energy_only(x) - e1) <= 1e-12 * abs(e1)
+        else:
+            assert e1 == e0  # snapshot semantics
+            p.refresh_attrs()
+            assert abs(p.eval_terms() - expect(x, target)) <= 1e-12 * abs(e1)
 
 
 @pytest.mark.parametrize("name", CASES)
