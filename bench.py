@@ -527,7 +527,7 @@ def run_configs(peak, sub=9):
     # config 3: symmetric Dirichlet on the punctured icosphere
     pos, faces, uv = mg.punctured_icosphere_arrays(sub)
     mesh = mg.Mesh(pos, faces)
-    rest_inv, areas = rest_geometry(mesh)
+    rest_inv, areas = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in rest_geometry(mesh))
     p = distortion_problem(mesh, rest_inv, areas, with_hessian=True)
     p.precompute_sparsity()
     p.x = uv.ravel()
@@ -545,6 +545,7 @@ def run_configs(peak, sub=9):
     mesh = mg.Mesh(pos, faces)
     base = initial_sphere(mesh)
     b1, b2 = tangent_bases(base)
+    base, b1, b2 = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (base, b1, b2))
     p = sphere_problem(mesh, base, b1, b2)
     V, F = len(pos), len(faces)
     p.x = 1e-5 * np.random.default_rng(0).normal(size=2 * V)  # tangent noise well below the edge length (no flips)

@@ -110,6 +110,20 @@ MG_API int mg_mesh_copy_vertex_patches(const mg_mesh* mesh, int32_t* patch_d, vo
  * and an element's energy counts only where its first vertex is owned, so the
  * per-shard energies sum to the global energy. Call before creating problems
  * on the mesh. Synchronizes `stream`. */
+/* Row processing order of the assembly kernels (never changes results beyond
+ * summation order; the outputs stay in the caller's numbering). AUTO (the
+ * default at mg_mesh_create) keeps the caller's vertex numbering when it is
+ * translation-regular (>= half the edges (i,j) have (i+1,j+1) as an edge:
+ * structured grids, where consecutive rows' neighbour gathers coalesce) and
+ * uses a Morton order of the positions otherwise. Setting it rebuilds the
+ * patches; call before creating problems on the mesh. No reference
+ * counterpart (the reference's patch order, mesh.py:252-279, only affects
+ * rounding too). */
+enum mg_row_order { MG_ROW_AUTO = 0, MG_ROW_MORTON = 1, MG_ROW_IDENTITY = 2 };
+MG_API int mg_mesh_set_row_order(mg_mesh* mesh, int order, void* stream);
+/* resolved order (MG_ROW_MORTON / MG_ROW_IDENTITY) and the regularity score */
+MG_API int mg_mesh_row_order(const mg_mesh* mesh, int* order, double* regularity);
+
 MG_API int mg_mesh_set_owned(mg_mesh* mesh, const uint8_t* owned_d, void* stream);
 MG_API int mg_mesh_destroy(mg_mesh* mesh);
 

@@ -44,6 +44,8 @@ SIGNATURES = [
     ("mg_mesh_copy_edges", _INT, [_P, _P, _P]),
     ("mg_mesh_copy_vertex_patches", _INT, [_P, _P, _P]),
     ("mg_mesh_set_owned", _INT, [_P, _P, _P]),
+    ("mg_mesh_set_row_order", _INT, [_P, _INT, _P]),
+    ("mg_mesh_row_order", _INT, [_P, ctypes.POINTER(_INT), ctypes.POINTER(ctypes.c_double)]),
     ("mg_mesh_destroy", _INT, [_P]),
     ("mg_problem_create", _INT, [_P, _INT, _INT, _P, _INT, ctypes.POINTER(_P)]),
     ("mg_problem_add_term", _INT, [_P, _INT, _INT, ctypes.POINTER(_DBL), _INT, ctypes.POINTER(_P), _INT,

@@ -143,7 +143,11 @@ def jacobian_dets(uv: np.ndarray, mesh: Mesh, rest_inv: np.ndarray) -> np.ndarra
 def distortion_problem(mesh: Mesh, rest_inv, areas, with_hessian: bool = False,
                        accumulation: str = "deterministic") -> Problem:
     p = Problem(mesh, 2, with_hessian=with_hessian, accumulation=accumulation)
-    p.add_term(Element.FACE, Op.FV, SymDirichlet(np.ascontiguousarray(rest_inv).reshape(-1, 4), areas))
+    if hasattr(rest_inv, "detach"):  # CUDA tensor: read in place by the kernels
+        ri = rest_inv.reshape(-1, 4)
+    else:  # numpy: a view, so in-place rewrites of the caller's array are seen (live attributes)
+        ri = np.ascontiguousarray(rest_inv).reshape(-1, 4)
+    p.add_term(Element.FACE, Op.FV, SymDirichlet(ri, areas))
     return p
 
 

@@ -188,6 +188,24 @@ int mg_mesh_set_owned(mg_mesh* mesh, const uint8_t* owned_d, void* stream) {
   return guard([&] { mesh_set_owned(mesh->m, owned_d, S(stream)); });
 }
 
+int mg_mesh_set_row_order(mg_mesh* mesh, int order, void* stream) {
+  if (!mesh) return fail(MG_ERR_VALUE, "mesh is NULL");
+  if (order < MG_ROW_AUTO || order > MG_ROW_IDENTITY) return fail(MG_ERR_VALUE, "unknown row order");
+  return guard([&] {
+    if (mesh->m.row_order == order) return;
+    mesh->m.row_order = order;
+    mesh_patches(mesh->m, S(stream));
+    MG_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int mg_mesh_row_order(const mg_mesh* mesh, int* order, double* regularity) {
+  if (!mesh || !order) return fail(MG_ERR_VALUE, "NULL argument");
+  *order = mesh->m.row_order_used;
+  if (regularity) *regularity = mesh->m.regularity;
+  return MG_OK;
+}
+
 int mg_mesh_destroy(mg_mesh* mesh) {
   delete mesh;
   return MG_OK;

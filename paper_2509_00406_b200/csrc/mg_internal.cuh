@@ -101,6 +101,13 @@ struct Mesh {
   DBuf<double> pos;      // (V,3) or empty
   PatchSet patches;
   int patch_vertices = 128;
+  // row processing order: MG_ROW_AUTO picks the caller's numbering when it is
+  // translation-regular (consecutive rows have shifted neighbourhoods, as in
+  // a structured grid: a warp's neighbour gathers are then contiguous), else
+  // Morton order of the positions; row_order_used is the resolved choice
+  int row_order = 0;       // MG_ROW_AUTO / MG_ROW_MORTON / MG_ROW_IDENTITY
+  int row_order_used = 0;
+  double regularity = 0.0;  // fraction of edges (i,j) whose (i+1,j+1) is an edge
 };
 
 struct Term {

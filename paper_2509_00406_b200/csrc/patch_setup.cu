@@ -14,6 +14,8 @@
 //
 // Everything is built with sorts/scans on the device; nothing here affects
 // the numbers, only the order of floating-point summation.
+#include <cstring>
+#include <cstdlib>
 #include <cstdio>
 #include <cstdlib>
 
@@ -522,6 +524,25 @@ int to_host_int(const int* d, cudaStream_t s) {
   return h;
 }
 
+// translation regularity of the caller's numbering: edges (i,j) (sorted,
+// canonical) whose shifted pair (i+1,j+1) is also an edge
+__global__ void k_edge_regularity(const int32_t* edges, int64_t E, unsigned long long* hits) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool hit = false;
+  if (e < E) {
+    const int32_t a = edges[2 * e] + 1, b = edges[2 * e + 1] + 1;
+    int64_t lo = e + 1, hi = E;  // (a,b) sorts after (a-1,b-1)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      const int32_t ma = edges[2 * mid], mb = edges[2 * mid + 1];
+      if (ma < a || (ma == a && mb < b)) lo = mid + 1; else hi = mid;
+    }
+    hit = lo < E && edges[2 * lo] == a && edges[2 * lo + 1] == b;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(hits, (unsigned long long)__popc(m));
+}
+
 int key_bits(int64_t v) {
   int b = 1;
   while ((int64_t(1) << b) <= v) ++b;
@@ -550,13 +571,34 @@ void mesh_patches(Mesh& m, cudaStream_t s) {
   ps.rank.alloc(V > 0 ? V : 1);
   ps.patch_of_vertex.alloc(V > 0 ? V : 1);
   if (V == 0) return;
-  if (m.pos.p || owned) {
+  // row order (mg_row_order): explicit, the MG_ROW_ORDER env knob, or the
+  // regularity test of the caller's numbering
+  int order = m.row_order;
+  const char* ro_env = getenv("MG_ROW_ORDER");
+  if (ro_env && !strcmp(ro_env, "identity")) order = MG_ROW_IDENTITY;
+  if (ro_env && !strcmp(ro_env, "morton")) order = MG_ROW_MORTON;
+  if (m.E > 0) {
+    DBuf<unsigned long long> hits;
+    hits.alloc(1);
+    MG_CUDA(cudaMemsetAsync(hits.p, 0, sizeof(unsigned long long), s));
+    k_edge_regularity<<<grid_for(m.E), TPB, 0, s>>>(m.edges.p, m.E, hits.p);
+    MG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    MG_CUDA(cudaMemcpyAsync(&h, hits.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    m.regularity = (double)h / (double)m.E;
+  }
+  if (order == MG_ROW_AUTO) order = m.regularity >= 0.5 ? MG_ROW_IDENTITY : MG_ROW_MORTON;
+  if (!m.pos.p) order = MG_ROW_IDENTITY;
+  m.row_order_used = order;
+  const bool ident = order == MG_ROW_IDENTITY;
+  if ((m.pos.p && !ident) || owned) {
     DBuf<uint64_t> code, code2;
     DBuf<int32_t> ids;
     code.alloc(V);
     code2.alloc(V);
     ids.alloc(V);
-    if (m.pos.p) {
+    if (m.pos.p && !ident) {
       const int nb = 256;
       DBuf<double> part, box;
       part.alloc(6 * nb);

@@ -98,7 +98,10 @@ class Mesh:
     """
 
     def __init__(self, positions, faces, edges=None, patch_target: int = DEFAULT_PATCH_TARGET,
-                 patch_vertices: int = DEFAULT_PATCH_VERTICES, owned=None):
+                 patch_vertices: int = DEFAULT_PATCH_VERTICES, owned=None, row_order: str = "auto"):
+        if row_order not in _ROW_ORDERS:
+            raise MeshError(f"row_order must be one of {sorted(_ROW_ORDERS)}")
+        self.row_order = row_order
         if patch_vertices < 32:
             raise MeshError("patch_vertices must be >= 32 (one energy partial per 32-row warp)")
         positions = np.array(positions, dtype=np.float64)
@@ -159,6 +162,8 @@ class Mesh:
             _lib.stream_ptr(), ctypes.byref(handle)))
         self._dev = handle
         self._lib = lib
+        if self.row_order != "auto":
+            _lib.check(lib.mg_mesh_set_row_order(handle, _ROW_ORDERS[self.row_order], _lib.stream_ptr()))
         if self.owned is not None:
             own_d = torch.from_numpy(self.owned.astype(np.uint8)).to(dev)
             _lib.check(lib.mg_mesh_set_owned(handle, own_d.data_ptr() if nv else None, _lib.stream_ptr()))
@@ -172,6 +177,15 @@ class Mesh:
         self._edges_device = e
         self._edges = e.cpu().numpy()
         return self
+
+    def row_order_used(self):
+        """(resolved row order, translation regularity of the numbering):
+        the assembly kernels walk rows in the caller's numbering when it is
+        regular (structured grids), else in Morton order (mg_mesh_row_order)."""
+        self.to_device()
+        o, r = ctypes.c_int(), ctypes.c_double()
+        _lib.check(self._lib.mg_mesh_row_order(self._dev, ctypes.byref(o), ctypes.byref(r)))
+        return {1: "morton", 2: "identity"}[o.value], r.value
 
     def __del__(self):
         if getattr(self, "_dev", None) is not None:
@@ -218,6 +232,9 @@ class Mesh:
 
 
 # generators -----------------------------------------------------------------
+
+
+_ROW_ORDERS = {"auto": 0, "morton": 1, "identity": 2}
 
 
 def grid_arrays(n: int, spacing: float = 1.0):
