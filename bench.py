@@ -11,14 +11,30 @@ fp64. A step = one such evaluation. Unit = term-element evaluations / s
   value   : device time per step (CUDA events on the launching stream, inputs
             resident in HBM; the 2.6 GB of inputs+outputs exceed the 126 MB L2,
             so no flush is needed)
-  e2e     : the public API with host buffers: pinned x H2D, eval, energy +
-            gradient D2H, every step
+  e2e     : the public API with host buffers, every step: pinned x H2D, eval,
+            energy + gradient + the 2.1 GB of Hessian values D2H into pinned
+            host memory (the reference's eval_terms leaves all three in host
+            memory); extras.cloth_e2e_h_on_device is the same without the
+            Hessian copy (a consumer that keeps H on the device)
   roofline: HBM; algorithmic bytes of one call (inputs read once + outputs
             written once) / the assembly kernel's own device time
             (library-side CUDA events around that launch, same timed region);
-            traffic = DRAM bytes of the same kernel from the committed ncu capture
-  cpu_baseline: the CPU oracle port (oracle/, restating meshgrad) on a bounded
-            256^2 sample of the same call, all host threads
+            traffic = DRAM bytes of the same kernel from the committed ncu
+            capture (profiles/ncu_kernels.json)
+  cpu_baseline: the CPU oracle port (oracle/, restating meshgrad's numpy
+            path) on the SAME 2048^2 problem, all host threads, atomic
+            accumulation (the reference CLI default): a bounded sample = a
+            fixed stride of the call's 4096-element chunks, so the per-element
+            rate is the full call's (the sample's elements / its time)
+  extras  : the other calls of the path (grad+H, HVP, HVP(psd), energy probe),
+            BASELINE configs 2' (cloth 2240^2, 10.0M faces), 3 (symmetric
+            Dirichlet, punctured icosphere(10), 21M faces), 4 (sphere and
+            smoothing HVPs, icosphere(10)) and 5 (cloth 7072^2, 100M faces,
+            gradient + HVP) with a roofline object each: HBM fraction of the
+            algorithmic bytes and, for the face kernels, the FP64 fraction of
+            the ncu-executed flops (dadd + dmul + 2 dfma) against the measured
+            FP64 peak (profiles/fp64_peak.json); `bound` is the unit ncu shows
+            busier
 
 Multi-GPU (torchrun, N ranks): weak scaling. The global cloth is a
 2048 x (2048 N) grid partitioned by vertex ownership (distributed.py); each
@@ -26,7 +42,9 @@ rank assembles its owned rows after a halo exchange of ribbon x, and the energy
 is all-reduced. Time = max over ranks.
 
 `--impl reference` runs the reference arm: the CPU oracle port on the same
-metric (rank 0 only).
+2048^2 problem and call (rank 0 only), each step a fixed-stride 1/16 sample of
+the call's chunks; its extras time each of the five calls once at full size
+(all threads, atomic) and a workers=1 deterministic sample of each.
 """
 
 from __future__ import annotations
@@ -58,10 +76,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--grid", type=int, default=GRID)
+    ap.add_argument("--sub", type=int, default=10, help="icosphere subdivisions of configs 3-4 (BASELINE: 10)")
+    ap.add_argument("--grid5", type=int, default=7072, help="cloth grid of config 5 (BASELINE: 7072, 100M faces)")
     ap.add_argument("--accumulation", default="deterministic", choices=["deterministic", "atomic"])
     ap.add_argument("--patch", type=int, default=64, help="owned rows per vertex patch (generic patch path)")
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary workloads")
-    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs 2'/3/4 extras")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs 2'/3/4/5 extras")
+    ap.add_argument("--no-config5", action="store_true", help="skip the 100M-face config 5 extra")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--profile", action="store_true", help="few steps, headline only (for ncu)")
     ap.add_argument("--profile-call", default="psd", choices=["psd", "plain", "hvp", "hvp_psd", "energy"],
@@ -208,13 +229,47 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture."""
+def fp64_peak():
+    """FP64 FMA throughput measured on this pool's B200 by tools/fp64_peak
+    (MEASURED_PEAKS.json carries no FP64 figure); nominal 37 TF/s otherwise."""
     try:
-        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
-        return d.get(kernel)
+        d = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())
+        return float(d["fp64_tflops"]), "measured (tools/fp64_peak, profiles/fp64_peak.json)"
     except Exception:
-        return None
+        return 37.0, "nominal"
+
+
+def ncu_kernel(label):
+    """Per-launch ncu facts of a kernel from the committed captures
+    (profiles/ncu_kernels.json): DRAM bytes, executed FP64 flops, DRAM% and
+    FP64-pipe% (which unit binds)."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_kernels.json").read_text())
+        return d.get(label) or {}
+    except Exception:
+        return {}
+
+
+def roofline_obj(label, kernel_ms, nbytes, hbm_peak, hbm_src, note=None):
+    """Roofline object of one launch: the HBM fraction of the algorithmic
+    bytes always; the FP64 fraction of the ncu-executed flops when the
+    capture has them; `bound` = the unit ncu shows busier."""
+    nk = ncu_kernel(label)
+    achieved = nbytes / (kernel_ms * 1e-3) / 1e9
+    r = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+         "traffic": nk.get("traffic"), "peak_source": hbm_src, "kernel": label,
+         "algorithmic_bytes_per_launch": nbytes, "kernel_ms": kernel_ms, "hbm_frac": achieved / hbm_peak}
+    if nk.get("fp64_flops"):
+        fpk, fsrc = fp64_peak()
+        tf = nk["fp64_flops"] / (kernel_ms * 1e-3) / 1e12
+        r.update({"fp64_flops_per_launch": nk["fp64_flops"], "fp64_tflops": tf, "fp64_peak": fpk,
+                  "fp64_peak_source": fsrc, "fp64_frac": tf / fpk,
+                  "ncu_dram_pct": nk.get("dram_pct"), "ncu_fp64_pipe_pct": nk.get("fp64_pipe_pct")})
+        if (nk.get("fp64_pipe_pct") or 0) > (nk.get("dram_pct") or 0):
+            r.update({"bound": "fp64", "achieved": tf, "peak": fpk, "unit": "TFLOP/s", "frac": tf / fpk})
+    if note:
+        r["bytes_note"] = note
+    return r
 
 
 def time_device(fn, steps, warmup, dist=None):
@@ -265,67 +320,160 @@ def kernel_label(p, call):
     return f"k_rows_fast<{p.n},{mode},SPRING>"
 
 
+
+
 # -------------------------------------------------------------- CPU baseline
 
-def cpu_oracle_rate(n_sample, reps=1, psd=True):
-    """Oracle port (oracle/) on a cloth n_sample^2 grid, all host threads."""
-    from oracle import OracleProblem
-    from oracle.engine import default_workers
-    from paper_2509_00406_b200.apps import default_pins, lumped_masses
-    from paper_2509_00406_b200.mesh import Mesh, _host_edges
-    from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+def cpu_info():
+    info = {"cpu_count": os.cpu_count(), "numpy": np.__version__}
+    try:
+        info["affinity"] = len(os.sched_getaffinity(0))
+    except AttributeError:
+        pass
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                info["model"] = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return info
 
-    pos, faces, target, x, _ = cloth_inputs(n_sample)
-    nv = len(pos)
-    edges = _host_edges(faces, None, nv)
-    mesh = Mesh(pos, faces)
-    mesh._edges = edges
-    masses = lumped_masses(mesh, 1.0)
-    d = pos[edges[:, 1]] - pos[edges[:, 0]]
-    l2 = np.einsum("ij,ij->i", d, d)
-    h = 0.01
-    terms = [("V", Inertia(masses, target)), ("EV", Spring(l2, 0.5 * 1e4 * h * h)),
-             ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
-    workers = default_workers()
-    op = OracleProblem(nv, faces, edges, 3, terms, with_hessian=True, fixed_vertices=default_pins(n_sample),
-                       workers=workers, accumulation="atomic")
-    op.eval_terms(x, psd_floor=FLOOR if psd else None)  # warm-up (layout outside the timed region)
-    ts = []
-    for _ in range(reps):
+
+class CpuCloth:
+    """The CPU oracle port (oracle/: the reference's numpy pipeline restated)
+    on the same cloth problem as the engine's headline: same mesh, terms,
+    pins and state. Setup (layout + pattern) is outside every timed region,
+    as in the reference (apps/smooth.py:104)."""
+
+    def __init__(self, n, workers, accumulation):
+        from oracle import OracleProblem
+        from paper_2509_00406_b200.apps import default_pins
+        from paper_2509_00406_b200.mesh import _host_edges
+        from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+
+        pos, faces, target, x, v = cloth_inputs(n)
+        nv = len(pos)
+        edges = _host_edges(faces, None, nv)
+        areas = 0.5 * np.linalg.norm(np.cross(pos[faces[:, 1]] - pos[faces[:, 0]], pos[faces[:, 2]] - pos[faces[:, 0]]),
+                                     axis=1)
+        masses = np.bincount(faces.ravel(), weights=np.repeat(areas / 3.0, 3), minlength=nv)
+        d = pos[edges[:, 1]] - pos[edges[:, 0]]
+        h = 0.01
+        terms = [("V", Inertia(masses, target)), ("EV", Spring(np.einsum("ij,ij->i", d, d), 0.5 * 1e4 * h * h)),
+                 ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
+        self.workers = workers
+        self.op = OracleProblem(nv, faces, edges, 3, terms, with_hessian=True, fixed_vertices=default_pins(n),
+                                workers=workers, accumulation=accumulation)
+        self.x, self.v = x, v
+        self.units = 2 * nv + len(edges)
+        self.sizes = [sl.stop - sl.start for _, _, _, sl in self.op._tasks()]
+
+    def call(self, name):
+        o, x, v = self.op, self.x, self.v
+        return {"eval_terms": lambda: o.eval_terms(x),
+                "eval_terms_psd": lambda: o.eval_terms(x, psd_floor=FLOOR),
+                "hvp": lambda: o.hvp(x, v),
+                "hvp_psd": lambda: o.hvp(x, v, psd_floor=FLOOR),
+                "energy_only": lambda: o.eval_energy_only(x)}[name]
+
+    def sample(self, name, stride, k):
+        """(term-elements, seconds) of one call restricted to chunks k, k+stride, ..."""
+        self.op.task_slice = slice(k % stride, None, stride) if stride > 1 else None
+        units = sum(self.sizes[k % stride::stride]) if stride > 1 else self.units
         t0 = time.perf_counter()
-        op.eval_terms(x, psd_floor=FLOOR if psd else None)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
-    units = 2 * nv + len(edges)
-    return units / t, workers, f"cloth {n_sample}x{n_sample} ({units} term-elements), eval_terms(psd_floor=1e-9), median of {reps}"
+        self.call(name)()
+        dt = time.perf_counter() - t0
+        self.op.task_slice = None
+        return units, dt
+
+    def rate(self, name, stride, steps, warmup):
+        for k in range(warmup):
+            self.sample(name, stride, k)
+        rates = []
+        for k in range(steps):
+            u, dt = self.sample(name, stride, warmup + k)
+            rates.append(u / dt)
+        return statistics.median(rates), rates
+
+
+def cpu_baseline_line(n, stride=64, steps=3):
+    """cpu_baseline of the engine arm: the oracle port on the same problem, all
+    host threads, a 1/stride chunk sample of eval_terms(psd_floor) per step."""
+    from oracle.engine import default_workers
+
+    workers = default_workers()
+    ref = CpuCloth(n, workers, "atomic")
+    val, _ = ref.rate("eval_terms_psd", stride, steps, 1)
+    return {"value": val, "unit": "term-elements/s", "cores": workers, "kind": "port",
+            "sample": (f"cloth {n}x{n} (the headline problem, {ref.units} term-elements per full call), "
+                       f"eval_terms(psd_floor=1e-9), atomic, {workers} threads; each sample = every {stride}th of the "
+                       f"call's {len(ref.sizes)} 4096-element chunks (~{ref.units // stride} term-elements), "
+                       f"median of {steps} after 1 warm-up"),
+            "host": cpu_info()}
 
 
 # ------------------------------------------------------------------- arms
 
 def run_reference(args):
+    """The reference arm: the oracle port (oracle/, the reference's numpy path
+    restated and pinned to the reference's own outputs) on the SAME 2048^2
+    problem and call as the engine arm, all host threads (atomic, the
+    reference CLI default, cli.py:25,34-35). Each step = the call restricted
+    to a fixed-stride 1/16 of its chunks (a bounded sample; the per-element
+    rate is the full call's). Extras: each of the five calls once at full
+    size, and a workers=1 deterministic 1/64 sample of each."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sample = 256
-    rates = []
-    for _ in range(args.warmup):
-        cpu_oracle_rate(sample, reps=1)
-    for _ in range(args.steps):
-        r, cores, desc = cpu_oracle_rate(sample, reps=1)
-        rates.append(r)
-    V, E = cloth_sizes(args.grid)
-    val = statistics.median(rates)
+    from oracle.engine import default_workers
+
+    workers = default_workers()
+    t_setup = time.perf_counter()
+    ref = CpuCloth(args.grid, workers, "atomic")
+    t_setup = time.perf_counter() - t_setup
+    stride = 16
+    val, rates = ref.rate("eval_terms_psd", stride, args.steps, args.warmup)
+    ms = ref.units / val * 1e3
+    desc = (f"each step: eval_terms(psd_floor=1e-9) on every {stride}th of the full 2048^2 call's "
+            f"{len(ref.sizes)} 4096-element chunks (~{ref.units // stride} term-elements), {workers} threads, atomic; "
+            f"ms_per_step = the full call's time at the measured rate")
+    extras = {"setup_s": t_setup}
+    full = {}
+    for name in ("eval_terms", "eval_terms_psd", "hvp", "hvp_psd", "energy_only"):
+        u, dt = ref.sample(name, 1, 0)
+        full[name] = {"s": dt, "term_elements_per_s": u / dt}
+    extras["full_calls_all_threads"] = full
+    ref1 = CpuCloth.__new__(CpuCloth)
+    ref1.__dict__.update(ref.__dict__)
+    ref.op.workers, ref.op.accumulation = 1, "deterministic"
+    one = {}
+    for name in ("eval_terms", "eval_terms_psd", "hvp", "hvp_psd", "energy_only"):
+        u, dt = ref.sample(name, 64, 0)
+        one[name] = {"sample_s": dt, "term_elements_per_s": u / dt, "full_call_s_at_rate": ref.units / (u / dt)}
+    extras["workers1_deterministic_1_64_sample"] = one
     line = {
         "impl": "reference", "metric": METRIC,
         "value": val, "unit": "term-elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": (2 * V + E) / val * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cloth grid {args.grid}x{args.grid} Newton-step eval_terms(psd_floor=1e-9)",
-                   "sample": f"each step: {desc}"},
-        "cpu_baseline": {"value": val, "unit": "term-elements/s", "cores": cores, "kind": "port", "sample": desc},
+        "config": headline_config(args.grid, 1, args.accumulation),
+        "cpu_baseline": {"value": val, "unit": "term-elements/s", "cores": workers, "kind": "port", "sample": desc,
+                         "host": cpu_info()},
         "e2e": {"value": val, "unit": "term-elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extras": extras,
     }
     print(json.dumps(line), flush=True)
+
+
+def headline_config(n, world, accumulation):
+    V, E = cloth_sizes(n, n * world)
+    F = 2 * (n - 1) * (n * world - 1)
+    return {"workload": (f"cloth grid {n}x{n * world} (V={V}, E={E}, F={F}) Newton-step "
+                         "eval_terms(psd_floor=1e-9), inertia+spring+gravity, 2 pins"),
+            "accumulation": accumulation,
+            "l2": "inputs+outputs 2.6 GB per GPU > 126 MB L2; no flush",
+            "parallelism": (f"vertex-partitioned shards x{world} (halo all_to_all + energy all_reduce)"
+                            if world > 1 else "1 GPU")}
 
 
 def run_engine(args):
@@ -394,27 +542,29 @@ def run_engine(args):
     peak, peak_kind = peaks()
     label = kernel_label(p, "psd")
     if world == 1:
-        bytes_call = cloth_bytes(V, E, nnzb_local)
-        achieved = bytes_call / (kms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": ncu_traffic(label), "peak_source": peak_kind, "kernel": label,
-                    "algorithmic_bytes_per_launch": bytes_call, "kernel_ms": kms,
-                    "kernel_share_of_step": kms / ms,
-                    "bytes_note": "24V x + 24V target + 8V masses + 8E rest lengths + 8E edge ids + 24V grad + 72 nnzb H"}
+        roofline = roofline_obj(label, kms, cloth_bytes(V, E, nnzb_local), peak, peak_kind,
+                                "24V x + 24V target + 8V masses + 8E rest lengths + 8E edge ids + 24V grad + 72 nnzb H")
+        roofline["kernel_share_of_step"] = kms / ms
     else:
         roofline = {"bound": "hbm", "kernel": label, "kernel_ms": kms, "note": "per-rank shard; see the N=1 line"}
 
     # e2e through the public API with host buffers
+    extras = {}
     if world == 1:
         x_host = torch.from_numpy(x).pin_memory()
         g_host = torch.empty(p.num_dofs, dtype=torch.float64).pin_memory()
         e_host = torch.empty(1, dtype=torch.float64).pin_memory()
+        h_host = torch.empty_like(p.hess.values_device, device="cpu").pin_memory()
 
-        def e2e_step():
+        def e2e_step(with_h=True):
             p.x_device.copy_(x_host, non_blocking=True)
             p.eval_terms(psd_floor=FLOOR, sync=False)
             g_host.copy_(p.grad_device, non_blocking=True)
             e_host.copy_(p.energy_device, non_blocking=True)
+            if with_h:
+                h_host.copy_(p.hess.values_device, non_blocking=True)
+        d2h = int(g_host.numel() * 8 + 8 + h_host.numel() * 8)
+        path = "Problem.x (pinned H2D) -> eval_terms(psd_floor) -> energy + grad + Hessian values D2H (pinned)"
     else:
         own = len(dp.plan.owned_global)
         x_host = torch.from_numpy(dp.problem.x.reshape(-1, 3)[np.flatnonzero(dp.plan.owned)].ravel()).pin_memory()
@@ -422,43 +572,48 @@ def run_engine(args):
         g_host = torch.empty(own * 3, dtype=torch.float64).pin_memory()
         e_host = torch.empty(1, dtype=torch.float64).pin_memory()
 
-        def e2e_step():
+        def e2e_step(with_h=False):
             x_dev.copy_(x_host, non_blocking=True)
             dp.set_x_owned(x_dev)
             dp.eval_terms(psd_floor=FLOOR, sync=False)
             g_host.copy_(dp.grad_owned().reshape(-1), non_blocking=True)
             e_host.copy_(dp.energy_device, non_blocking=True)
+        d2h = int(g_host.numel() * 8 + 8)
+        path = "owned x (pinned H2D) -> halo -> eval_terms(psd_floor) -> energy + owned grad D2H"
 
     ms_e2e, _ = time_device(e2e_step, max(3, steps // 2), 2, dist)
     e2e = {"value": units / (ms_e2e * 1e-3), "unit": "term-elements/s",
-           "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(g_host.numel() * 8 + 8),
-           "ms_per_step": ms_e2e, "path": "Problem.x (pinned H2D) -> eval_terms(psd_floor) -> grad + energy D2H"}
+           "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": d2h,
+           "ms_per_step": ms_e2e, "path": path}
+    if world == 1:
+        ms_dev_h, _ = time_device(lambda: e2e_step(False), max(3, steps // 2), 2, dist)
+        extras["cloth_e2e_h_on_device"] = {
+            "ms": ms_dev_h, "term_elements_per_s": units / (ms_dev_h * 1e-3),
+            "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(g_host.numel() * 8 + 8),
+            "path": "as e2e, but the Hessian stays on the device"}
+        del h_host
 
-    extras = {}
     if not args.no_extras and world == 1:
-        extras = run_extras(p, v, V, E, nnzb_local, steps, peak)
-        if not args.no_configs:
-            del p
-            torch.cuda.empty_cache()
-            extras.update(run_configs(peak))
+        extras.update(run_extras(p, v, V, E, nnzb_local, steps, peak, peak_kind))
+    if not args.no_configs and world == 1:
+        del p
+        gc_cuda()
+        extras.update(run_configs(peak, peak_kind, args.sub))
+        if not args.no_config5:
+            extras.update(run_config5(peak, peak_kind, args.grid5))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r, cores, desc = cpu_oracle_rate(256, reps=3)
-        cpu = {"value": r, "unit": "term-elements/s", "cores": cores, "kind": "port", "sample": desc}
+        cpu = cpu_baseline_line(n)
     if rank == 0:
-        F = 2 * (n - 1) * (n * world - 1)
+        cfg = headline_config(n, world, args.accumulation)
+        cfg.update({"nnzb_per_rank": nnzb_local, "faces_per_s": 2 * (n - 1) * (n * world - 1) / (ms * 1e-3),
+                    "setup_s": t_setup})
         line = {
             "metric": METRIC,
             "value": value, "unit": "term-elements/s", "n_gpus": world, "steps": steps, "warmup": warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": (f"cloth grid {n}x{n * world} (V={V}, E={E}, F={F}) Newton-step "
-                                    "eval_terms(psd_floor=1e-9), inertia+spring+gravity, 2 pins"),
-                       "accumulation": args.accumulation, "nnzb_per_rank": nnzb_local,
-                       "l2": "inputs+outputs 2.6 GB per GPU > 126 MB L2; no flush",
-                       "parallelism": (f"vertex-partitioned shards x{world} (halo all_to_all + energy all_reduce)"
-                                       if world > 1 else "1 GPU"),
-                       "faces_per_s": F / (ms * 1e-3), "setup_s": t_setup},
+            "config": cfg,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -471,34 +626,53 @@ def run_engine(args):
         dist.destroy_process_group()
 
 
-def run_extras(p, v, V, E, nnzb, steps, peak):
-    """Secondary calls of the same path, each with its kernel time and HBM fraction."""
+def gc_cuda():
+    import gc
+
     import torch
 
-    out = {}
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def call_record(p, fn, units, unit, nbytes, label, peak, peak_kind, steps=10, extra=None):
+    ms, kms = time_with_kernel(p, fn, steps, 3)
+    t = kms if kms else ms
+    r = {"ms": ms, "kernel_ms": kms, unit + "_per_s": units / (ms * 1e-3), "algorithmic_bytes": nbytes,
+         "hbm_frac": nbytes / (t * 1e-3) / 1e9 / peak, "roofline": roofline_obj(label, t, nbytes, peak, peak_kind)}
+    if extra:
+        r.update(extra)
+    return r
+
+
+def run_extras(p, v, V, E, nnzb, steps, peak, peak_kind):
+    """The headline problem's other calls, each with its kernel time and roofline."""
+    import torch
+
     xd = p.x_device
     vd = torch.from_numpy(v).cuda()
     y = torch.empty_like(vd)
     k = max(5, steps // 2)
-    calls = [
-        ("cloth_grad_hess", lambda: p.eval_terms(sync=False), cloth_bytes(V, E, nnzb)),
-        ("cloth_hvp", lambda: p.hvp(xd, vd, out=y), cloth_hvp_bytes(V, E)),
-        ("cloth_hvp_psd", lambda: p.hvp(xd, vd, psd_floor=FLOOR, out=y), cloth_hvp_bytes(V, E)),
-        ("cloth_energy_only", lambda: p.eval_energy_only(xd), cloth_energy_bytes(V, E)),
-    ]
-    for name, fn, b in calls:
-        ms, kms = time_with_kernel(p, fn, k, 3)
-        t = kms if kms else ms
-        out[name] = {"ms": ms, "kernel_ms": kms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3),
-                     "algorithmic_bytes": b, "hbm_frac": b / (t * 1e-3) / 1e9 / peak}
-    return out
+    te = 2 * V + E
+    return {
+        "cloth_grad_hess": call_record(p, lambda: p.eval_terms(sync=False), te, "term_elements",
+                                       cloth_bytes(V, E, nnzb), kernel_label(p, "plain"), peak, peak_kind, k),
+        "cloth_hvp": call_record(p, lambda: p.hvp(xd, vd, out=y), te, "term_elements", cloth_hvp_bytes(V, E),
+                                 kernel_label(p, "hvp"), peak, peak_kind, k),
+        "cloth_hvp_psd": call_record(p, lambda: p.hvp(xd, vd, psd_floor=FLOOR, out=y), te, "term_elements",
+                                     cloth_hvp_bytes(V, E), kernel_label(p, "hvp_psd"), peak, peak_kind, k),
+        "cloth_energy_only": call_record(p, lambda: p.eval_energy_only(xd), te, "term_elements",
+                                         cloth_energy_bytes(V, E), "k_elem energy (3 launches)", peak, peak_kind, k),
+    }
 
 
-def run_configs(peak, sub=9):
-    """The other BASELINE workloads, one call each (device ms, main-kernel ms,
-    HBM fraction of the algorithmic bytes): the >= 10M-face cloth (config 2'),
-    symmetric Dirichlet grad+Hessian (config 3) and sphere / smoothing HVPs
-    (config 4) on icosphere(sub)."""
+def run_configs(peak, peak_kind, sub=10):
+    """The other BASELINE workloads at their BASELINE sizes, per call: device
+    ms, main-kernel ms, rate and a roofline object. Config 2' is the >= 10M
+    face cloth (2240^2), config 3 symmetric Dirichlet grad + Hessian on the
+    punctured icosphere(10), config 4 the sphere and smoothing HVPs on
+    icosphere(10)."""
     import torch
 
     import paper_2509_00406_b200 as mg
@@ -506,60 +680,155 @@ def run_configs(peak, sub=9):
                                             sphere_problem, tangent_bases)
 
     out = {}
-
-    def rec(name, p, fn, units, unit, nbytes, k=10):
-        ms, kms = time_with_kernel(p, fn, k, 3)
-        t = kms if kms else ms
-        out[name] = {"ms": ms, "kernel_ms": kms, unit + "_per_s": units / (ms * 1e-3), "algorithmic_bytes": nbytes,
-                     "hbm_frac": nbytes / (t * 1e-3) / 1e9 / peak}
-
-    # config 2': cloth 2240^2 (10.03M faces), Newton step
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    # config 2': cloth 2240^2 (10.03M faces)
     n = 2240
+    t0 = time.perf_counter()
     p, x, v = build_engine_cloth(n, "deterministic")
+    st = time.perf_counter() - t0
     V, E = cloth_sizes(n)
-    vd = torch.from_numpy(v).cuda()
-    y = torch.empty_like(vd)
-    rec("cloth2240_grad_hess_psd", p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), 2 * V + E, "term_elements",
-        cloth_bytes(V, E, p.hess.nnz_blocks))
-    rec("cloth2240_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), 2 * V + E, "term_elements", cloth_hvp_bytes(V, E))
+    vd, y = dev(v), torch.empty(3 * V, dtype=torch.float64, device="cuda")
+    ex = {"V": V, "E": E, "F": 2 * (n - 1) ** 2, "setup_s": st}
+    out["cloth2240_grad_hess_psd"] = call_record(
+        p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), 2 * V + E, "term_elements",
+        cloth_bytes(V, E, p.hess.nnz_blocks), kernel_label(p, "psd"), peak, peak_kind, extra=ex)
+    out["cloth2240_grad_hess"] = call_record(
+        p, lambda: p.eval_terms(sync=False), 2 * V + E, "term_elements", cloth_bytes(V, E, p.hess.nnz_blocks),
+        kernel_label(p, "plain"), peak, peak_kind)
+    out["cloth2240_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), 2 * V + E, "term_elements",
+                                       cloth_hvp_bytes(V, E), kernel_label(p, "hvp"), peak, peak_kind)
+    out["cloth2240_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), 2 * V + E,
+                                           "term_elements", cloth_hvp_bytes(V, E), kernel_label(p, "hvp_psd"), peak,
+                                           peak_kind)
     del p, vd, y
-    torch.cuda.empty_cache()
-    # config 3: symmetric Dirichlet on the punctured icosphere
+    gc_cuda()
+    # config 3: symmetric Dirichlet on the punctured icosphere (stereographic UV, all det J > 0)
+    t0 = time.perf_counter()
     pos, faces, uv = mg.punctured_icosphere_arrays(sub)
     mesh = mg.Mesh(pos, faces)
-    rest_inv, areas = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in rest_geometry(mesh))
+    rest_inv, areas = (dev(a) for a in rest_geometry(mesh))
     p = distortion_problem(mesh, rest_inv, areas, with_hessian=True)
     p.precompute_sparsity()
     p.x = uv.ravel()
     V, F, nnzb = len(pos), len(faces), p.hess.nnz_blocks
-    vd = torch.from_numpy(np.random.default_rng(1).normal(size=2 * V)).cuda()
+    st = time.perf_counter() - t0
+    vd = dev(np.random.default_rng(1).normal(size=2 * V))
     y = torch.empty_like(vd)
-    rec(f"dirichlet_ico{sub}_grad_hess", p, lambda: p.eval_terms(sync=False), F, "faces",
-        16 * V + 12 * F + 32 * F + 8 * F + 16 * V + 32 * nnzb)
-    rec(f"dirichlet_ico{sub}_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces",
-        16 * V + 16 * V + 12 * F + 32 * F + 8 * F + 16 * V)
-    del p, vd, y
-    torch.cuda.empty_cache()
-    # config 4: sphere manifold HVP, smoothing HVP
+    b_hess = 16 * V + 12 * F + 32 * F + 8 * F + 16 * V + 32 * nnzb
+    b_hvp = 16 * V + 16 * V + 12 * F + 32 * F + 8 * F + 16 * V
+    ex = {"V": V, "F": F, "nnzb": nnzb, "setup_s": st, "row_order": mesh.row_order_used()[0],
+          "bytes_note": "16V uv + 12F faces + 32F rest_inv + 8F areas + 16V grad + 32 nnzb H (HVP: + 16V v, y for grad/H)"}
+    pre = f"dirichlet_ico{sub}"
+    out[pre + "_grad_hess"] = call_record(p, lambda: p.eval_terms(sync=False), F, "faces", b_hess,
+                                          "k_rows_dirichlet<HESS>", peak, peak_kind, extra=ex)
+    out[pre + "_grad_hess_psd"] = call_record(p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), F, "faces",
+                                              b_hess, "k_face_psd + k_rows_dirichlet<HESS,psd>", peak, peak_kind)
+    out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces", b_hvp,
+                                    "k_rows_dirichlet<HVP>", peak, peak_kind)
+    out[pre + "_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), F, "faces", b_hvp,
+                                        "k_face_psd + k_rows_dirichlet<HVP,psd>", peak, peak_kind)
+    del p, vd, y, mesh
+    gc_cuda()
+    # config 4: sphere manifold HVP (and its gradient), smoothing HVP (and gradient)
+    t0 = time.perf_counter()
     pos, faces = mg.icosphere_arrays(sub)
     mesh = mg.Mesh(pos, faces)
     base = initial_sphere(mesh)
     b1, b2 = tangent_bases(base)
-    base, b1, b2 = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (base, b1, b2))
-    p = sphere_problem(mesh, base, b1, b2)
+    p = sphere_problem(mesh, dev(base), dev(b1), dev(b2))
     V, F = len(pos), len(faces)
-    p.x = 1e-5 * np.random.default_rng(0).normal(size=2 * V)  # tangent noise well below the edge length (no flips)
-    vd = torch.from_numpy(np.random.default_rng(1).normal(size=2 * V)).cuda()
+    p.x = 1e-5 * np.random.default_rng(0).normal(size=2 * V)  # tangent noise below the 1.1e-3 edge (no flips)
+    st = time.perf_counter() - t0
+    vd = dev(np.random.default_rng(1).normal(size=2 * V))
     y = torch.empty_like(vd)
-    rec(f"sphere_ico{sub}_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces",
-        16 * V + 16 * V + 72 * V + 12 * F + 16 * V)
+    b_grad = 16 * V + 72 * V + 12 * F + 16 * V
+    b_hvp = 16 * V + 16 * V + 72 * V + 12 * F + 16 * V
+    ex = {"V": V, "F": F, "setup_s": st, "bytes_note": "16V x + 72V base/b1/b2 + 12F faces + 16V out (HVP: + 16V v)"}
+    pre = f"sphere_ico{sub}"
+    out[pre + "_grad"] = call_record(p, lambda: p.eval_terms(sync=False), F, "faces", b_grad,
+                                     "k_rows_sphere<GRAD>", peak, peak_kind, extra=ex)
+    out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces", b_hvp,
+                                    "k_rows_sphere<HVP>", peak, peak_kind)
+    out[pre + "_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), F, "faces", b_hvp,
+                                        "k_sphere_face_hvp_psd", peak, peak_kind)
     del p, vd, y
+    gc_cuda()
     p = edge_length_problem(mesh)
     p.x = pos.ravel()
     E = 3 * F // 2
-    vd = torch.from_numpy(np.random.default_rng(1).normal(size=3 * V)).cuda()
+    vd = dev(np.random.default_rng(1).normal(size=3 * V))
     y = torch.empty_like(vd)
-    rec(f"smooth_ico{sub}_hvp", p, lambda: p.hvp(p.x_device, vd, out=y), E, "edges", 24 * V + 8 * E + 24 * V)
+    pre = f"smooth_ico{sub}"
+    out[pre + "_grad"] = call_record(p, lambda: p.eval_terms(sync=False), E, "edges", 24 * V + 8 * E + 24 * V,
+                                     "k_rows_fast<3,GRAD,EDGE_LENGTH>", peak, peak_kind,
+                                     extra={"bytes_note": "24V x + 8E edge ids + 24V grad"})
+    out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), E, "edges", 24 * V + 8 * E + 24 * V,
+                                    "k_rows_fast<3,HVP,EDGE_LENGTH>", peak, peak_kind,
+                                    extra={"bytes_note": "24V v + 8E edge ids + 24V y (the Hessian is constant)"})
+    del p, vd, y, mesh
+    gc_cuda()
+    return out
+
+
+def run_config5(peak, peak_kind, n=7072):
+    """BASELINE config 5 at N=1: cloth on generate_grid(7072) (50.0M vertices,
+    150M edges, 100M faces), gradient-mode problem: eval_terms (energy +
+    gradient) and the Newton-CG HVP, plain and clamped. Inputs are built on
+    the device (lumped masses and rest lengths from the device mesh)."""
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import default_pins
+    from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+
+    t0 = time.perf_counter()
+    pos, faces = mg.grid_arrays(n, 1.0 / (n - 1))
+    mesh = mg.Mesh(pos, faces)
+    mesh.to_device()
+    pos_d = torch.from_numpy(pos).cuda()
+    f_d = torch.from_numpy(faces).cuda()
+    del faces
+    cr = torch.linalg.cross(pos_d[f_d[:, 1]] - pos_d[f_d[:, 0]], pos_d[f_d[:, 2]] - pos_d[f_d[:, 0]])
+    area3 = (0.5 * torch.linalg.vector_norm(cr, dim=1) / 3.0).repeat_interleave(3)
+    del cr
+    masses = torch.zeros(len(pos), dtype=torch.float64, device="cuda").index_add_(0, f_d.reshape(-1), area3)
+    del area3, f_d
+    e_d = mesh._edges_device
+    dd = pos_d[e_d[:, 1]] - pos_d[e_d[:, 0]]
+    l2 = (dd * dd).sum(dim=1)
+    del dd
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    sig = 0.01 / (n - 1)
+    target = (pos_d + sig * torch.randn(pos_d.shape, generator=gen, device="cuda", dtype=torch.float64)).contiguous()
+    x = (pos_d + sig * torch.randn(pos_d.shape, generator=gen, device="cuda", dtype=torch.float64)).reshape(-1)
+    vd = torch.randn(x.numel(), generator=gen, device="cuda", dtype=torch.float64)
+    h = 0.01
+    p = mg.Problem(mesh, 3, with_hessian=False, fixed_vertices=default_pins(n))
+    p.add_term(mg.Element.VERTEX, mg.Op.V, Inertia(masses, target))
+    p.add_term(mg.Element.EDGE, mg.Op.EV, Spring(l2, 0.5 * 1e4 * h * h))
+    p.add_term(mg.Element.VERTEX, mg.Op.V, Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))
+    p.x = x
+    del pos_d
+    torch.cuda.synchronize()
+    st = time.perf_counter() - t0
+    V, E = cloth_sizes(n)
+    y = torch.empty_like(vd)
+    te = 2 * V + E
+    ex = {"V": V, "E": E, "F": 2 * (n - 1) ** 2, "setup_s": st, "problem": "gradient mode (with_hessian=False)",
+          "inputs": "device-built (torch seeded generator); masses / rest lengths from the device mesh",
+          "gpu_mem_gb": torch.cuda.max_memory_allocated() / 1e9}
+    out = {
+        "cloth7072_grad": call_record(p, lambda: p.eval_terms(sync=False), te, "term_elements",
+                                      cloth_energy_bytes(V, E) + 24 * V, "k_rows_fast<3,GRAD,SPRING>", peak,
+                                      peak_kind, extra=ex),
+        "cloth7072_hvp": call_record(p, lambda: p.hvp(p.x_device, vd, out=y), te, "term_elements",
+                                     cloth_hvp_bytes(V, E), "k_rows_fast<3,HVP,SPRING>", peak, peak_kind),
+        "cloth7072_hvp_psd": call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), te,
+                                         "term_elements", cloth_hvp_bytes(V, E), "k_rows_fast<3,HVP,psd,SPRING>",
+                                         peak, peak_kind),
+    }
+    del p, vd, y, x, target, masses, l2, mesh
+    gc_cuda()
     return out
 
 

@@ -137,6 +137,7 @@ class OracleProblem:
         self.workers = max(1, int(workers))
         self.accumulation = accumulation
         self.chunk = int(chunk)
+        self.task_slice = None
         self.ndofs = self.n * self.nv
         self.terms = [(op, fn) for op, fn in terms]
         ids = list(element_ids) if element_ids is not None else [None] * len(self.terms)
@@ -243,6 +244,8 @@ class OracleProblem:
 
     def _run(self, fn):
         tasks = self._tasks()
+        if self.task_slice is not None:  # a bounded sample of the call's chunks (bench CPU baseline)
+            tasks = tasks[self.task_slice]
         if self.workers <= 1 or len(tasks) <= 1:
             for t in tasks:
                 yield fn(t)
@@ -293,6 +296,8 @@ class OracleProblem:
                 np.add.at(gpad, gidx.ravel(), gr.ravel())
             if blocks is not None:
                 np.add.at(hpad, bids, blocks)
+        if self.task_slice is not None:  # a timed sample: views (the reference returns its buffers, no copy)
+            return self._reduce(parts), gpad[: self.ndofs], (hpad[: self.nnzb] if hpad is not None else None)
         return self._reduce(parts), gpad[: self.ndofs].copy(), (hpad[: self.nnzb].copy() if hpad is not None else None)
 
     def eval_energy_only(self, x):
@@ -327,7 +332,7 @@ class OracleProblem:
         for gidx, y in self._run(work):
             if y is not None:
                 np.add.at(ypad, gidx.ravel(), y.ravel())
-        return ypad[: self.ndofs].copy()
+        return ypad[: self.ndofs] if self.task_slice is not None else ypad[: self.ndofs].copy()
 
 
 def default_workers():

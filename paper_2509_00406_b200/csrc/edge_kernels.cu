@@ -348,13 +348,16 @@ MG_DI double rcp_fast(double x) {
 //   spring  (apps/cloth.py:106-110): s = r/l2 - 1, phi = (s s)(c l2),
 //           phi' = 2 c s, phi'' = 2 c / l2;   edge length (apps/smooth.py:27-28): phi = r.
 // Returns false when a value is non-finite.
-template <int TT>
+// NEEDV = false (HVP): the value is not formed and only the derivative
+// factors are checked (an infinite value with finite derivatives leaves the
+// reference's Hessian finite too)
+template <int TT, bool NEEDV = true>
 MG_DI bool radial_closed(const TermDev& t, double a0, double rr, double& pv, double& p1, double& p2) {
   if (TT == MG_TERM_SPRING) {
     const double c = t.c[0];
     const double u = rcp_fast(a0);
     const double sv = rr * u - 1.0;
-    pv = (sv * sv) * (c * a0);
+    pv = NEEDV ? (sv * sv) * (c * a0) : 0.0;
     p1 = 2.0 * c * sv;
     p2 = 2.0 * c * u;
   } else {
@@ -362,7 +365,7 @@ MG_DI bool radial_closed(const TermDev& t, double a0, double rr, double& pv, dou
     p1 = 1.0;
     p2 = 0.0;
   }
-  return isfinite(pv + p1 + p2);
+  return NEEDV ? isfinite(pv + p1 + p2) : isfinite(p1 + p2);
 }
 
 MG_DI bool radial_any(const TermDev& t, double a0, double rr, double& pv, double& p1, double& p2) {
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD
   // (coalesced): vertex, meta word, row start / buffer offset, ELL records
   auto load_l1 = [&](int64_t r, L1& l) {
     if (r >= a.V) return;
-    l.g = a.order[r];
+    l.g = a.order ? a.order[r] : (int)r;  // null: identity row order
     l.meta = a.rmeta[r];
     if constexpr (MODE == MODE_HESS) {
       l.ro = a.prow_ro[r];
@@ -559,20 +562,21 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD
     (void)ro;
     // the previous row's bulk copy must have read this thread's row buffer
     if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    const bool fr = !((meta >> 8) & 1);
-    const int dp = (int)(meta >> 16) & 0xff;
-    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
-    // level 2: own x / w
+    // level 2: own x / w, issued before anything waits on the meta word (with
+    // the identity row order g is the row itself, so these do not wait on
+    // level 1 at all); the pinned mask is applied after the load
     double xs[N], us[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       xs[c] = a.x[(int64_t)g * N + c];
-      if constexpr (MODE == MODE_HVP) us[c] = fr ? a.w[(int64_t)g * N + c] : 0.0;
+      if constexpr (MODE == MODE_HVP) us[c] = a.w[(int64_t)g * N + c];
       else us[c] = 0.0;
     }
     const VPreload<N> vpre = vterms_load<N, MODE>(a, g);
     // level 3: neighbour x (w) and the edge attribute, kept MAXI incidences
-    // ahead of the compute (a rolling window over the ELL slots)
+    // ahead of the compute (a rolling window over the ELL slots). Unused ELL
+    // slots hold record 0 (edge 0, vertex 0), so the loads are unconditional
+    // (no wait on the incidence count) and their values are never used.
     double xo[EV_ELL_K][N], uo[EV_ELL_K][N], a0[EV_ELL_K];
     auto issue = [&](int j) {
       const uint32_t hi = (uint32_t)(rc[j] >> 32);
@@ -580,14 +584,25 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD
       const bool fo = !(hi >> 31);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        xo[j][c] = (j < cnt && !XFREE) ? a.x[o * N + c] : 0.0;
-        if constexpr (MODE == MODE_HVP) uo[j][c] = (j < cnt && fo) ? a.w[o * N + c] : 0.0;
-        else uo[j][c] = 0.0;
+        xo[j][c] = !XFREE ? a.x[o * N + c] : 0.0;
+        if constexpr (MODE == MODE_HVP) {
+          const double wv = a.w[o * N + c];
+          uo[j][c] = fo ? wv : 0.0;
+        } else {
+          uo[j][c] = 0.0;
+        }
       }
-      a0[j] = (j < cnt && a.ev_a0) ? a.ev_a0[(uint32_t)rc[j] & 0x7fffffffu] : 0.0;
+      a0[j] = a.ev_a0 ? a.ev_a0[(uint32_t)rc[j] & 0x7fffffffu] : 0.0;
     };
 #pragma unroll
     for (int j = 0; j < MAXI; ++j) issue(j);
+    const bool fr = !((meta >> 8) & 1);
+    const int dp = (int)(meta >> 16) & 0xff;
+    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
+    if constexpr (MODE == MODE_HVP) {
+#pragma unroll
+      for (int c = 0; c < N; ++c) us[c] = fr ? us[c] : 0.0;
+    }
     double vec[N], dg[T];
 #pragma unroll
     for (int i = 0; i < N; ++i) vec[i] = 0.0;
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD
       };
       if constexpr (EVT != 0) {
         double pv, p1, p2;
-        const bool ok = radial_closed<EVT>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
+        const bool ok = radial_closed<EVT, MODE != MODE_HVP>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
         one_term(ok, pv, p1, p2);
       } else {
         for (int j = 0; j < a.nev; ++j) {
@@ -906,7 +921,7 @@ __global__ void __launch_bounds__(EV_TILE_ROWS, EV_TILE_MINB) k_tile_ev(const __
       };
       if constexpr (EVT != 0) {
         double pv, p1, p2;
-        const bool ok = radial_closed<EVT>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
+        const bool ok = radial_closed<EVT, MODE != MODE_HVP>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
         one_term(ok, pv, p1, p2);
       } else {
         for (int j = 0; j < a.nev; ++j) {
@@ -1012,7 +1027,7 @@ __global__ void __launch_bounds__(PT) k_rows_ev(const __grid_constant__ EvArgs a
   double eacc = 0.0;
   bool finite = true;
   if (row < a.V) {
-    const int g = a.order[row];
+    const int g = a.order ? a.order[row] : (int)row;
     const bool fr = !a.pfix[row];
     const int k0 = a.rinc_off[row], k1 = a.rinc_off[row + 1];
     int64_t ro = 0;
@@ -1281,7 +1296,7 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   EvArgs a;
   a.nterms = (int)p.terms.size();
   a.V = m.Vr;
-  a.order = m.patches.order.p;
+  a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr : m.patches.order.p;
   a.pfix = p.pfix.p;
   a.rmeta = p.rmeta.p;
   a.ell = p.ell.p;

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
   double eacc = 0.0;
   bool ok = true;
   if (row < a.V) {
-    const int g = a.order[row];
+    const int g = a.order ? a.order[row] : (int)row;
     const uint32_t meta = a.rmeta[row];
     int64_t ro = 0;
     int ho = 0;
@@ -317,9 +317,12 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
       ro = a.prow_ro[row];
       ho = a.hoff[row];
     }
-    uint64_t rc[KF];
+    uint64_t rc[KF], ov[KF];
 #pragma unroll
-    for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+    for (int j = 0; j < KF; ++j) {
+      rc[j] = a.ell[(int64_t)j * a.V + row];
+      ov[j] = a.ellv[(int64_t)j * a.V + row];
+    }
     const bool fr = !((meta >> 8) & 1);
     const int dp = (int)(meta >> 16) & 0xff;
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
@@ -598,13 +601,17 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
     };
     // face corner ids of the ELL incidences (one batched level), then the
     // corners' data streamed one incidence ahead of the compute
+    // (the other two corners come from the ELL other-corner records, so no
+    // dependent faces[] lookup; the row's own vertex is corner s)
     const int ne = cnt < KF ? cnt : KF;
     int fv[KF][3];
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
-      const int64_t f = (uint32_t)rc[j] & 0x3fffffffu;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) fv[j][q] = j < ne ? a.faces[3 * f + q] : 0;
+      const int s = (int)((uint32_t)rc[j] >> 30);
+      const int o1 = (int)(uint32_t)ov[j], o2 = (int)(ov[j] >> 32);
+      fv[j][0] = s == 0 ? g : (s == 1 ? o2 : o1);
+      fv[j][1] = s == 0 ? o1 : (s == 1 ? g : o2);
+      fv[j][2] = s == 0 ? o2 : (s == 1 ? o1 : g);
     }
     FaceIn cur;
     if (ne > 0) cur = load_face(rc[0], fv[0]);
@@ -765,7 +772,7 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
   double eacc = 0.0;
   bool ok = true;
   if (row < a.V) {
-    const int g = a.order[row];
+    const int g = a.order ? a.order[row] : (int)row;
     const uint32_t meta = a.rmeta[row];
     uint64_t rc[KF];
 #pragma unroll
@@ -1089,7 +1096,7 @@ __global__ void __launch_bounds__(128) k_sphere_face_hvp_psd(const __grid_consta
 __global__ void __launch_bounds__(PT) k_rows_face_gather(const __grid_constant__ FvArgs a, const double* yscr) {
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
   if (row >= a.V) return;
-  const int g = a.order[row];
+  const int g = a.order ? a.order[row] : (int)row;
   const uint32_t meta = a.rmeta[row];
   const bool fr = !((meta >> 8) & 1);
   const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
@@ -1157,7 +1164,7 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   const Mesh& m = *p.mesh;
   FvArgs a;
   a.V = m.Vr;
-  a.order = m.patches.order.p;
+  a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr : m.patches.order.p;
   a.rmeta = p.rmeta.p;
   a.ell = p.ell.p;
   a.rinc_off = p.rinc_off.p;

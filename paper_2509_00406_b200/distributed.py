@@ -19,53 +19,74 @@ Design: "owner computes".
     Gradient / Hessian / HVP rows are complete on their owner: nothing else is
     communicated (ribbon elements are recomputed instead).
 
-`ShardPlan` and `HaloExchange` are device-agnostic host logic (numpy / torch)
-and are tested with gloo on CPU; `DistributedProblem` runs the CUDA engine.
+`ShardPlan` (torch ops: built on the GPU by DistributedProblem, on the CPU in
+the gloo tests; send lists from one exchange of the recv lists) and
+`HaloExchange` are tested with gloo on CPU; `DistributedProblem` runs the CUDA
+engine. x is exchanged only when its owned rows changed since the last call.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-from .mesh import _host_edges
-
 __all__ = ["DistributedProblem", "HaloExchange", "ShardPlan", "morton_owner"]
 
 
-def _spread3(v: np.ndarray) -> np.ndarray:
-    v = v.astype(np.uint64) & np.uint64(0x1FFFFF)
-    v = (v | (v << np.uint64(32))) & np.uint64(0x1F00000000FFFF)
-    v = (v | (v << np.uint64(16))) & np.uint64(0x1F0000FF0000FF)
-    v = (v | (v << np.uint64(8))) & np.uint64(0x100F00F00F00F00F)
-    v = (v | (v << np.uint64(4))) & np.uint64(0x10C30C30C30C30C3)
-    v = (v | (v << np.uint64(2))) & np.uint64(0x1249249249249249)
+_SPREAD = ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F), (4, 0x10C30C30C30C30C3),
+           (2, 0x1249249249249249))
+
+
+def _spread3(v):
+    """Interleave the low 21 bits of v with two zero bits each (torch int64)."""
+    v = v & 0x1FFFFF
+    for sh, mask in _SPREAD:
+        v = (v | (v << sh)) & mask
     return v
 
 
-def morton_owner(positions: np.ndarray, world: int) -> np.ndarray:
-    """Rank owning each vertex: Morton order of the positions cut into
-    `world` contiguous, count-balanced ranges (ties broken by vertex id)."""
-    nv = len(positions)
+def _morton_owner_t(pos, world: int):
+    """Owner rank of every vertex (torch, on pos's device): Morton order of the
+    positions cut into `world` contiguous count-balanced ranges, ties broken
+    by vertex id (a stable sort of the codes)."""
+    import torch
+
+    nv = pos.shape[0]
+    owner = torch.zeros(nv, dtype=torch.int32, device=pos.device)
     if world <= 1 or nv == 0:
-        return np.zeros(nv, dtype=np.int32)
-    p = np.asarray(positions, dtype=np.float64)
-    lo, hi = p.min(axis=0), p.max(axis=0)
-    ext = np.where(hi > lo, hi - lo, 1.0)
-    t = np.clip((p - lo) / ext, 0.0, 1.0)
-    q = (t * 2097151.0).astype(np.uint64)
-    code = (_spread3(q[:, 0]) << np.uint64(2)) | (_spread3(q[:, 1]) << np.uint64(1)) | _spread3(q[:, 2])
-    order = np.lexsort((np.arange(nv), code))
-    owner = np.empty(nv, dtype=np.int32)
-    bounds = (np.arange(world + 1) * nv) // world
+        return owner
+    lo, hi = pos.min(dim=0).values, pos.max(dim=0).values
+    ext = torch.where(hi > lo, hi - lo, torch.ones_like(hi))
+    q = ((pos - lo) / ext).clamp(0.0, 1.0).mul(2097151.0).to(torch.int64)
+    code = (_spread3(q[:, 0]) << 2) | (_spread3(q[:, 1]) << 1) | _spread3(q[:, 2])
+    order = torch.sort(code, stable=True).indices
+    bounds = [(r * nv) // world for r in range(world + 1)]
     for r in range(world):
         owner[order[bounds[r]:bounds[r + 1]]] = r
     return owner
 
 
-class ShardPlan:
-    """One rank's view of the partition.
+def morton_owner(positions, world: int) -> np.ndarray:
+    """Rank owning each vertex (numpy in / out; see _morton_owner_t)."""
+    import torch
 
-    Attributes (local = index into this shard's vertex list `verts`):
+    return _morton_owner_t(torch.from_numpy(np.asarray(positions, dtype=np.float64)), world).numpy()
+
+
+def _edge_keys(faces, nv):
+    import torch
+
+    if faces.shape[0] == 0:
+        return torch.zeros(0, dtype=torch.int64, device=faces.device)
+    sides = torch.cat([faces[:, [0, 1]], faces[:, [1, 2]], faces[:, [2, 0]]])
+    lo, hi = sides.min(dim=1).values, sides.max(dim=1).values
+    return torch.unique(lo * nv + hi)  # sorted, canonical (mesh.py:184-202)
+
+
+class ShardPlan:
+    """One rank's view of the partition, built with torch ops on `device`
+    (the GPU in production: O(mesh) device work per rank; CPU in the gloo
+    tests). Attributes are numpy (local = index into this shard's vertex
+    list `verts`):
       verts        global ids of the shard's vertices (sorted): owned + ribbon
       owned        (len(verts),) bool, True for vertices this rank owns
       faces        global ids of the shard's faces; local_faces their (F,3) local corners
@@ -74,53 +95,104 @@ class ShardPlan:
       send[q]      local ids of owned vertices that rank q holds as ribbon
       recv[q]      local ids of this shard's ribbon vertices owned by rank q
     Both lists are sorted by global id, so sender and receiver agree on order.
+    With `group` (or the default group) initialised over the same world, the
+    send lists come from one exchange of the recv lists (each rank builds only
+    its own shard); otherwise every peer's shard is derived locally.
     """
 
-    def __init__(self, positions, faces, edges, world: int, rank: int, owner=None):
-        positions = np.asarray(positions, dtype=np.float64)
-        faces = np.asarray(faces, dtype=np.int64).reshape(-1, 3)
-        nv = len(positions)
+    def __init__(self, positions, faces, edges, world: int, rank: int, owner=None, device=None, group=None):
+        import torch
+
+        dev = torch.device(device) if device is not None else torch.device("cpu")
+        t = lambda a, dt: torch.as_tensor(np.asarray(a), dtype=dt, device=dev) if not torch.is_tensor(a) else a.to(dev, dt)
+        pos = t(positions, torch.float64).reshape(-1, 3)
+        faces_t = t(faces, torch.int64).reshape(-1, 3) if faces is not None and np.size(faces) else \
+            torch.zeros((0, 3), dtype=torch.int64, device=dev)
+        nv = pos.shape[0]
         self.world, self.rank, self.num_global_vertices = world, rank, nv
-        self.global_edges = _host_edges(faces, edges, nv) if (len(faces) or edges is not None) else np.zeros((0, 2), np.int64)
-        self.owner = morton_owner(positions, world) if owner is None else np.asarray(owner, dtype=np.int32)
-        self.face_free = len(faces) == 0
-        elems = faces if not self.face_free else self.global_edges
-        own_of = self.owner[elems] if len(elems) else np.zeros((0, elems.shape[1]), np.int32)
+        self.face_free = faces_t.shape[0] == 0
+        if not self.face_free:
+            gkeys = _edge_keys(faces_t, nv)
+        elif edges is not None and np.size(edges):
+            e = t(edges, torch.int64).reshape(-1, 2)
+            gkeys = torch.unique(e.min(dim=1).values * nv + e.max(dim=1).values)
+        else:
+            gkeys = torch.zeros(0, dtype=torch.int64, device=dev)
+        gedges = torch.stack([gkeys // nv, gkeys % nv], dim=1) if nv else gkeys.reshape(0, 2)
+        self.global_edges = gedges.cpu().numpy()
+        own_t = _morton_owner_t(pos, world) if owner is None else t(owner, torch.int32)
+        self.owner = own_t.cpu().numpy()
+        elems = gedges if self.face_free else faces_t
+        own_of = own_t[elems].to(torch.int64)
 
         def shard_of(q):
-            sel = np.flatnonzero(np.any(own_of == q, axis=1)) if len(elems) else np.zeros(0, np.int64)
-            vs = np.unique(np.concatenate([np.flatnonzero(self.owner == q), elems[sel].ravel()]))
+            sel = torch.nonzero((own_of == q).any(dim=1)).reshape(-1)
+            vs = torch.unique(torch.cat([torch.nonzero(own_t == q).reshape(-1), elems[sel].reshape(-1)]))
             return sel, vs
 
         sel, verts = shard_of(rank)
-        self.verts = verts
-        self.owned = self.owner[verts] == rank
-        g2l = np.full(nv, -1, dtype=np.int64)
-        g2l[verts] = np.arange(len(verts))
-        self._g2l = g2l
+        g2l = torch.full((nv,), -1, dtype=torch.int64, device=dev)
+        g2l[verts] = torch.arange(verts.numel(), device=dev)
+        owned_t = own_t[verts] == rank
         if self.face_free:
             self.faces = np.zeros(0, np.int64)
             self.local_faces = np.zeros((0, 3), np.int64)
-            self.edges = sel
+            edge_ids = sel
         else:
-            self.faces = sel
-            self.local_faces = g2l[faces[sel]]
-            le = _host_edges(self.local_faces, None, len(verts))
-            ge = verts[le]
-            key_g = self.global_edges[:, 0] * nv + self.global_edges[:, 1]
-            self.edges = np.searchsorted(key_g, ge[:, 0] * nv + ge[:, 1])
-        self.local_edges = g2l[self.global_edges[self.edges]] if len(self.edges) else np.zeros((0, 2), np.int64)
-        # halo lists: what every peer's shard holds of mine, and what I hold of theirs
-        mine = np.flatnonzero(self.owner == rank)
+            self.faces = sel.cpu().numpy()
+            lf = g2l[faces_t[sel]]
+            self.local_faces = lf.cpu().numpy()
+            lkeys = _edge_keys(lf, verts.numel())
+            gl = verts[lkeys // max(verts.numel(), 1)] * nv + verts[lkeys % max(verts.numel(), 1)]
+            edge_ids = torch.searchsorted(gkeys, gl)
+        self.edges = edge_ids.cpu().numpy()
+        self.local_edges = g2l[gedges[edge_ids]].cpu().numpy() if edge_ids.numel() else np.zeros((0, 2), np.int64)
+        self.verts = verts.cpu().numpy()
+        self.owned = owned_t.cpu().numpy()
+        self._g2l = g2l.cpu().numpy()
+        # halo lists: recv from my ribbon; send by exchanging recv lists (or deriving peers' shards)
+        ribbon = verts[~owned_t]
+        rib_owner = own_t[ribbon]
         self.send, self.recv = {}, {}
         for q in range(world):
-            if q == rank:
-                continue
-            _, vq = shard_of(q)
-            need = np.intersect1d(vq, mine, assume_unique=True)       # my owned vertices in q's shard
-            have = verts[(~self.owned) & (self.owner[verts] == q)]    # q's vertices in my shard
-            self.send[q] = g2l[need]
-            self.recv[q] = g2l[have]
+            if q != rank:
+                self.recv[q] = g2l[ribbon[rib_owner == q]].cpu().numpy()
+        import torch.distributed as dist
+
+        if world > 1 and dist.is_initialized() and dist.get_world_size(group) == world:
+            self.send = self._exchange_send(ribbon, rib_owner, g2l, group)
+        else:
+            mine = torch.nonzero(own_t == rank).reshape(-1)
+            for q in range(world):
+                if q == rank:
+                    continue
+                _, vq = shard_of(q)
+                need = vq[torch.isin(vq, mine)]  # my owned vertices in q's shard, sorted
+                self.send[q] = g2l[need].cpu().numpy()
+
+    def _exchange_send(self, ribbon, rib_owner, g2l, group):
+        """Each rank tells every owner which of its vertices it holds as ribbon
+        (global ids, sorted); what arrives from q is my send list to q."""
+        import torch
+        import torch.distributed as dist
+
+        world = self.world
+        cpu = dist.get_backend(group) == "gloo"
+        dev = torch.device("cpu") if cpu else ribbon.device
+        order = torch.argsort(rib_owner.to(torch.int64) * self.num_global_vertices + ribbon)
+        ids = ribbon[order].to(dev)
+        counts = torch.bincount(rib_owner.to(torch.int64), minlength=world).to(dev)
+        rcounts = torch.empty_like(counts)
+        dist.all_to_all_single(rcounts, counts, group=group)
+        got = torch.empty(int(rcounts.sum()), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(got, ids, rcounts.tolist(), counts.tolist(), group=group)
+        send, off = {}, 0
+        g2l_d = g2l.to(dev)
+        for q, c in enumerate(rcounts.tolist()):
+            if q != self.rank:
+                send[q] = g2l_d[got[off:off + c]].cpu().numpy()
+            off += c
+        return send
 
     @property
     def num_local(self) -> int:
@@ -202,7 +274,7 @@ class DistributedProblem:
         if plan is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
             rank = dist.get_rank(group) if dist.is_initialized() else 0
-            plan = ShardPlan(positions, faces, edges, world, rank)
+            plan = ShardPlan(positions, faces, edges, world, rank, device="cuda", group=group)
         self.plan = plan
         pl = self.plan
         self.n = var_dim
@@ -223,12 +295,14 @@ class DistributedProblem:
         self.halo = HaloExchange(pl, var_dim, torch.device("cuda"), group)
         self._owned_rows = torch.as_tensor(np.flatnonzero(pl.owned), device="cuda")
         self._v_local = None
+        self._x_fresh = False  # ribbon rows of x hold their owners' current values
 
     # state -------------------------------------------------------------------
 
     def set_x_global(self, x_global) -> None:
         """Set the shard's x from a full global state (every rank passes the same array)."""
         self.problem.x = np.asarray(x_global, dtype=np.float64).reshape(-1, self.n)[self.plan.verts].ravel()
+        self._x_fresh = True
 
     def set_x_owned(self, x_owned) -> None:
         """Set this rank's owned rows (device tensor or array, owned-row order); ribbon rows
@@ -238,13 +312,19 @@ class DistributedProblem:
         xl = self.problem.x_device.view(-1, self.n)
         src = torch.as_tensor(x_owned, dtype=torch.float64, device=xl.device).view(-1, self.n)
         xl.index_copy_(0, self._owned_rows, src)
+        self._x_fresh = False
+
+    def _sync_x(self):
+        if not self._x_fresh:
+            self.halo.exchange(self.problem.x_device)
+            self._x_fresh = True
 
     # calls -------------------------------------------------------------------
 
     def eval_terms(self, psd_floor=None, sync: bool = True):
         import torch.distributed as dist
 
-        self.halo.exchange(self.problem.x_device)
+        self._sync_x()
         self.problem.eval_terms(psd_floor=psd_floor, sync=False)
         e = self.problem.energy_device.clone()
         if dist.is_initialized() and self.plan.world > 1:
@@ -270,7 +350,7 @@ class DistributedProblem:
         vl = self._v_local.view(-1, self.n)
         vl.index_copy_(0, self._owned_rows, torch.as_tensor(v_owned, dtype=torch.float64, device=vl.device).view(-1, self.n))
         self.halo.exchange(self._v_local)
-        self.halo.exchange(self.problem.x_device)
+        self._sync_x()  # x only when its owned rows changed since the last exchange
         y = self.problem.hvp(self.problem.x_device, self._v_local, psd_floor=psd_floor)
         return y.view(-1, self.n).index_select(0, self._owned_rows)
 

@@ -3,6 +3,8 @@ import csv
 import subprocess
 import sys
 
+FP64_PEAK = 34.116e12  # tools/fp64_peak on this pool's B200 (profiles/fp64_peak.json)
+
 
 def ncu(rep, *args):
     return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
@@ -28,6 +30,18 @@ def main(rep, top=25):
         if x in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                  "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "gpu__time_duration.sum"):
             print(f"  {x}: {v[i]} {u[i]}")
+    fp = {}
+    for i, x in enumerate(h):
+        for op in ("dadd", "dmul", "dfma"):
+            if x == f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum":
+                fp[op] = float(v[i].replace(",", ""))
+        if x == "gpu__time_duration.sum":
+            scale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}
+            dur = float(v[i].replace(",", "")) * scale.get(u[i], 1e-3)
+    if len(fp) == 3:
+        flops = fp["dadd"] + fp["dmul"] + 2 * fp["dfma"]
+        print(f"  fp64 executed flops (dadd+dmul+2 dfma): {flops:.4g}; at the kernel's duration "
+              f"{flops / dur / 1e12:.2f} TFLOP/s = {flops / dur / FP64_PEAK:.3f} of the measured {FP64_PEAK / 1e12:.1f} TFLOP/s")
     st = []
     for i, x in enumerate(h):
         if x.startswith("smsp__pcsamp_warps_issue_stalled") and not x.endswith("not_issued"):
