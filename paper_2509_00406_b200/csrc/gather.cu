@@ -67,6 +67,19 @@ __global__ void k_gather(const int64_t* off, const int64_t* idx, const double* s
   for (int i = 0; i < W; ++i) out[r * W + i] = acc[i];
 }
 
+// any width (var_dim > 3: the reference accepts any var_dim, problem.py:263):
+// one thread per output scalar, same fixed contribution order
+__global__ void k_gather_n(const int64_t* off, const int64_t* idx, const double* scr, int64_t rows, int W,
+                           double* out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * W) return;
+  const int64_t r = t / W;
+  const int i = (int)(t - r * W);
+  double acc = 0.0;
+  for (int64_t k = off[r]; k < off[r + 1]; ++k) acc += scr[idx[k] + i];
+  out[t] = acc;
+}
+
 // sort (key, value) pairs and drop the ~0 keys; returns the kept count
 int64_t sort_pairs(DBuf<uint64_t>& k, DBuf<int64_t>& v, int64_t n, cudaStream_t s) {
   if (n == 0) return 0;
@@ -165,7 +178,7 @@ void gather_vec(const Problem& p, double* out, cudaStream_t s) {
     case 1: k_gather<1><<<grid_for(V), TPB, 0, s>>>(p.gv_off.p, p.gv_idx.p, p.gsv.p, V, out); break;
     case 2: k_gather<2><<<grid_for(V), TPB, 0, s>>>(p.gv_off.p, p.gv_idx.p, p.gsv.p, V, out); break;
     case 3: k_gather<3><<<grid_for(V), TPB, 0, s>>>(p.gv_off.p, p.gv_idx.p, p.gsv.p, V, out); break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "deterministic gather supports var_dim 1..3");
+    default: k_gather_n<<<grid_for(V * p.n), TPB, 0, s>>>(p.gv_off.p, p.gv_idx.p, p.gsv.p, V, p.n, out);
   }
   MG_LAUNCH_CHECK();
 }
@@ -177,7 +190,8 @@ void gather_blocks(const Problem& p, double* out, cudaStream_t s) {
     case 1: k_gather<1><<<grid_for(nb), TPB, 0, s>>>(p.gh_off.p, p.gh_idx.p, p.gsh.p, nb, out); break;
     case 2: k_gather<4><<<grid_for(nb), TPB, 0, s>>>(p.gh_off.p, p.gh_idx.p, p.gsh.p, nb, out); break;
     case 3: k_gather<9><<<grid_for(nb), TPB, 0, s>>>(p.gh_off.p, p.gh_idx.p, p.gsh.p, nb, out); break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "deterministic gather supports var_dim 1..3");
+    default:
+      k_gather_n<<<grid_for(nb * p.n * p.n), TPB, 0, s>>>(p.gh_off.p, p.gh_idx.p, p.gsh.p, nb, p.n * p.n, out);
   }
   MG_LAUNCH_CHECK();
 }
