@@ -601,6 +601,10 @@ def run_engine(args):
         extras.update(run_configs(peak, peak_kind, args.sub))
         if not args.no_config5:
             extras.update(run_config5(peak, peak_kind, args.grid5))
+    if world > 1 and not args.no_config5:
+        del p, dp
+        gc_cuda()
+        extras.update(run_config5_dist(world, rank, dist, args.grid5))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_line(n)
@@ -830,6 +834,64 @@ def run_config5(peak, peak_kind, n=7072):
     del p, vd, y, x, target, masses, l2, mesh
     gc_cuda()
     return out
+
+
+def run_config5_dist(world, rank, dist, n=7072, steps=10):
+    """Config 5 on `world` ranks: the same 7072^2 cloth (gradient mode),
+    vertex-partitioned (device-built shard plans), interior rows assembled
+    while the ribbon exchange is in flight (DistributedProblem overlap);
+    strong scaling: the whole-job rate over the max-over-ranks device time."""
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import default_pins
+    from paper_2509_00406_b200.distributed import DistributedProblem
+    from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+
+    t0 = time.perf_counter()
+    pos, faces = mg.grid_arrays(n, 1.0 / (n - 1))
+    pos_d = torch.from_numpy(pos).cuda()
+    f_d = torch.from_numpy(faces).cuda()
+    cr = torch.linalg.cross(pos_d[f_d[:, 1]] - pos_d[f_d[:, 0]], pos_d[f_d[:, 2]] - pos_d[f_d[:, 0]])
+    area3 = (0.5 * torch.linalg.vector_norm(cr, dim=1) / 3.0).repeat_interleave(3)
+    del cr
+    masses = torch.zeros(len(pos), dtype=torch.float64, device="cuda").index_add_(0, f_d.reshape(-1), area3)
+    del area3
+    sides = torch.cat([f_d[:, [0, 1]], f_d[:, [1, 2]], f_d[:, [2, 0]]])
+    keys = torch.unique(sides.min(dim=1).values * len(pos) + sides.max(dim=1).values)
+    del sides, f_d
+    e0, e1 = keys // len(pos), keys % len(pos)
+    dd = pos_d[e1] - pos_d[e0]
+    l2 = (dd * dd).sum(dim=1)
+    del dd, keys, e0, e1
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    sig = 0.01 / (n - 1)
+    target = (pos_d + sig * torch.randn(pos_d.shape, generator=gen, device="cuda", dtype=torch.float64)).contiguous()
+    x = (pos_d + sig * torch.randn(pos_d.shape, generator=gen, device="cuda", dtype=torch.float64)).reshape(-1)
+    v = torch.randn(x.numel(), generator=gen, device="cuda", dtype=torch.float64)
+    h = 0.01
+    terms = [("V", Inertia(masses, target)), ("EV", Spring(l2, 0.5 * 1e4 * h * h)),
+             ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
+    dp = DistributedProblem(pos, faces, 3, terms, fixed_vertices=default_pins(n), with_hessian=False, overlap=True)
+    dp.set_x_global(x.cpu().numpy())
+    own = torch.as_tensor(dp.plan.owned_global, device="cuda")
+    v_own = v.view(-1, 3).index_select(0, own).contiguous()
+    y_own = torch.empty_like(v_own)
+    del pos_d, x, v, target, masses, l2
+    gc_cuda()
+    st = time.perf_counter() - t0
+    V, E = cloth_sizes(n)
+    te = 2 * V + E
+    out = {"setup_s": st, "owned_rows": len(dp.plan.owned_global), "interior_rows": dp.interior_rows,
+           "boundary_rows": dp.boundary_rows, "halo_bytes_per_exchange": dp.halo.bytes_per_call,
+           "scaling": "strong (one 7072^2 mesh over all ranks)"}
+    ms, _ = time_device(lambda: dp.eval_terms(sync=False), steps, 3, dist)
+    out["grad"] = {"ms": ms, "term_elements_per_s": te / (ms * 1e-3)}
+    ms, _ = time_device(lambda: dp.hvp_owned(v_own, out=y_own), steps, 3, dist)
+    out["hvp"] = {"ms": ms, "term_elements_per_s": te / (ms * 1e-3)}
+    del dp
+    gc_cuda()
+    return {f"cloth{n}_strong": out}
 
 
 def main():

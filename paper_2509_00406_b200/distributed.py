@@ -233,13 +233,15 @@ class HaloExchange:
         self.recv_idx = cat([plan.recv[q] for q in peers if q in plan.recv])
         self.bytes_per_call = 8 * (sum(self.send_counts) + sum(self.recv_counts))
 
-    def exchange(self, local):
-        """local: (num_local * n,) or (num_local, n) tensor; ribbon rows overwritten in place."""
+    def start(self, local):
+        """Post the exchange of `local`'s ribbon rows; returns a handle for
+        finish(). With NCCL the transfer runs on the communicator's stream
+        while the caller keeps launching work on the current stream."""
         import torch
         import torch.distributed as dist
 
         if self.plan.world <= 1 or not dist.is_initialized():
-            return local
+            return None
         view = local.view(-1, self.n)
         sendbuf = view.index_select(0, self.send_idx).reshape(-1).contiguous()
         # NCCL moves device buffers directly; gloo (CPU tests, or several ranks
@@ -248,10 +250,24 @@ class HaloExchange:
         if host:
             sendbuf = sendbuf.cpu()
         recvbuf = torch.empty(sum(self.recv_counts), dtype=local.dtype, device="cpu" if host else local.device)
-        dist.all_to_all_single(recvbuf, sendbuf, self.recv_counts, self.send_counts, group=self.group)
+        work = dist.all_to_all_single(recvbuf, sendbuf, self.recv_counts, self.send_counts, group=self.group,
+                                      async_op=True)
+        return (view, recvbuf, work, host, sendbuf)
+
+    def finish(self, handle):
+        """Wait for a posted exchange (the current stream waits on the
+        communicator's) and write the ribbon rows."""
+        if handle is None:
+            return
+        view, recvbuf, work, host, _ = handle
+        work.wait()
         if host:
-            recvbuf = recvbuf.to(local.device)
+            recvbuf = recvbuf.to(view.device)
         view.index_copy_(0, self.recv_idx, recvbuf.view(-1, self.n))
+
+    def exchange(self, local):
+        """local: (num_local * n,) or (num_local, n) tensor; ribbon rows overwritten in place."""
+        self.finish(self.start(local))
         return local
 
 
@@ -264,7 +280,13 @@ class DistributedProblem:
 
     def __init__(self, positions, faces, var_dim: int, terms, fixed_vertices=(), edges=None,
                  with_hessian: bool = True, accumulation: str = "deterministic", group=None, plan=None,
-                 patch_vertices: int = 128):
+                 patch_vertices: int = 128, overlap: bool = False):
+        """overlap (gradient-mode problems, deterministic accumulation): the
+        owned rows are split into interior rows (no ribbon vertex in any
+        incident element) and boundary rows, assembled by two engine problems
+        on the same shard and sharing x / gradient / HVP buffers; the interior
+        kernel runs while the ribbon exchange is in flight, the boundary
+        kernel after it lands."""
         import torch
         import torch.distributed as dist
 
@@ -287,11 +309,40 @@ class DistributedProblem:
             mesh = Mesh(positions[pl.verts], pl.local_faces, owned=pl.owned, patch_vertices=patch_vertices)
         fixed_g = np.zeros(pl.num_global_vertices, dtype=bool)
         fixed_g[list(fixed_vertices)] = True
-        self.problem = Problem(mesh, var_dim, with_hessian=with_hessian,
-                               fixed_vertices=np.flatnonzero(fixed_g[pl.verts]).tolist(), accumulation=accumulation)
+        fixed_l = np.flatnonzero(fixed_g[pl.verts]).tolist()
         kinds = {"V": Element.VERTEX, "EV": Element.EDGE, "FV": Element.FACE}
-        for op, t in pl.shard_terms(terms):
-            self.problem.add_term(kinds[op], getattr(Op, op), t)
+        sterms = pl.shard_terms(terms)
+        self.overlap = bool(overlap) and pl.world > 1
+        if self.overlap and (with_hessian or accumulation != "deterministic"):
+            raise ValueError("overlap needs a gradient-mode problem with deterministic accumulation")
+        if self.overlap:
+            elems = pl.local_edges if pl.face_free else pl.local_faces
+            touch = (~pl.owned)[elems].any(axis=1)  # elements with a ribbon vertex
+            boundary = np.zeros(pl.num_local, dtype=bool)
+            boundary[elems[touch].ravel()] = True
+            boundary &= pl.owned
+            interior = pl.owned & ~boundary
+            sub = []
+            for own in (interior, boundary):
+                if pl.face_free:
+                    m = Mesh(positions[pl.verts], np.zeros((0, 3)), edges=pl.local_edges, owned=own,
+                             patch_vertices=patch_vertices)
+                else:
+                    m = Mesh(positions[pl.verts], pl.local_faces, owned=own, patch_vertices=patch_vertices)
+                q = Problem(m, var_dim, with_hessian=False, fixed_vertices=fixed_l, accumulation=accumulation)
+                for op, t in sterms:
+                    q.add_term(kinds[op], getattr(Op, op), t)
+                sub.append(q)
+            self.problem, self._boundary = sub
+            self._boundary.x_device = self.problem.x_device  # one x / gradient for both row sets
+            self._boundary.grad_device = self.problem.grad_device
+            self.interior_rows, self.boundary_rows = int(interior.sum()), int(boundary.sum())
+        else:
+            self.problem = Problem(mesh, var_dim, with_hessian=with_hessian, fixed_vertices=fixed_l,
+                                   accumulation=accumulation)
+            for op, t in sterms:
+                self.problem.add_term(kinds[op], getattr(Op, op), t)
+            self._boundary = None
         self.halo = HaloExchange(pl, var_dim, torch.device("cuda"), group)
         self._owned_rows = torch.as_tensor(np.flatnonzero(pl.owned), device="cuda")
         self._v_local = None
@@ -324,9 +375,17 @@ class DistributedProblem:
     def eval_terms(self, psd_floor=None, sync: bool = True):
         import torch.distributed as dist
 
-        self._sync_x()
-        self.problem.eval_terms(psd_floor=psd_floor, sync=False)
-        e = self.problem.energy_device.clone()
+        if self._boundary is not None:  # interior rows under the in-flight ribbon exchange
+            h = None if self._x_fresh else self.halo.start(self.problem.x_device)
+            self.problem.eval_terms(psd_floor=psd_floor, sync=False)
+            self.halo.finish(h)
+            self._x_fresh = True
+            self._boundary.eval_terms(psd_floor=psd_floor, sync=False)
+            e = self.problem.energy_device + self._boundary.energy_device
+        else:
+            self._sync_x()
+            self.problem.eval_terms(psd_floor=psd_floor, sync=False)
+            e = self.problem.energy_device.clone()
         if dist.is_initialized() and self.plan.world > 1:
             if _gloo(self.group):
                 eh = e.cpu()
@@ -341,18 +400,33 @@ class DistributedProblem:
         """(owned, n) gradient rows of this rank (device tensor)."""
         return self.problem.grad_device.view(-1, self.n).index_select(0, self._owned_rows)
 
-    def hvp_owned(self, v_owned, psd_floor=None):
+    def hvp_owned(self, v_owned, psd_floor=None, out=None):
         """y = H v restricted to owned rows; v given on owned rows (halo-exchanged here)."""
         import torch
 
         if self._v_local is None:
             self._v_local = torch.zeros_like(self.problem.x_device)
+            self._y_local = torch.empty_like(self.problem.x_device)
         vl = self._v_local.view(-1, self.n)
         vl.index_copy_(0, self._owned_rows, torch.as_tensor(v_owned, dtype=torch.float64, device=vl.device).view(-1, self.n))
-        self.halo.exchange(self._v_local)
-        self._sync_x()  # x only when its owned rows changed since the last exchange
-        y = self.problem.hvp(self.problem.x_device, self._v_local, psd_floor=psd_floor)
-        return y.view(-1, self.n).index_select(0, self._owned_rows)
+        if self._boundary is not None:
+            hv = self.halo.start(self._v_local)
+            hx = None if self._x_fresh else self.halo.start(self.problem.x_device)
+            self.problem.hvp(self.problem.x_device, self._v_local, psd_floor=psd_floor, out=self._y_local)
+            self.halo.finish(hv)
+            self.halo.finish(hx)
+            self._x_fresh = True
+            self._boundary.hvp(self.problem.x_device, self._v_local, psd_floor=psd_floor, out=self._y_local)
+            y = self._y_local
+        else:
+            self.halo.exchange(self._v_local)
+            self._sync_x()  # x only when its owned rows changed since the last exchange
+            y = self.problem.hvp(self.problem.x_device, self._v_local, psd_floor=psd_floor, out=self._y_local)
+        rows = y.view(-1, self.n).index_select(0, self._owned_rows)
+        if out is not None:
+            out.view(-1, self.n).copy_(rows)
+            return out
+        return rows
 
     def hvp_from_global(self, v_global, psd_floor=None):
         """Owned rows of H v for a full global v (every rank passes the same

@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, overlap=False):
     import os
     import sys
     from pathlib import Path
@@ -45,7 +45,7 @@ def _worker(rank, world, port, name, q):
         faces = d["faces"]
         edges = d["edges"] if not len(faces) else None
         dp = DistributedProblem(d["positions"], faces, n, build_terms(d), fixed_vertices=d["fixed"].tolist(),
-                                edges=edges, with_hessian=bool(d["with_hessian"]))
+                                edges=edges, with_hessian=bool(d["with_hessian"]) and not overlap, overlap=overlap)
         own = dp.plan.owned_global
         x, v = d["s0_x"].reshape(-1, n), d["s0_v0"].reshape(-1, n)
         dp.set_x_owned(x[own])  # ribbon rows of x arrive through the halo exchange
@@ -61,14 +61,19 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["cloth64", "dirichlet_ico2", "sphere_ico2", "smooth_ico2", "mixed_fv_ev_v"])
-def test_two_process_shards_match_reference(name):
+CASES = [(n, False) for n in ("cloth64", "dirichlet_ico2", "sphere_ico2", "smooth_ico2", "mixed_fv_ev_v")]
+# overlap: interior rows assembled while the ribbon exchange is in flight (gradient-mode shards)
+CASES += [(n, True) for n in ("cloth64", "sphere_ico2", "smooth_ico2", "mixed_fv_ev_v")]
+
+
+@pytest.mark.parametrize("name,overlap", CASES)
+def test_two_process_shards_match_reference(name, overlap):
     world = 2
     d = load(name)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
