@@ -595,6 +595,9 @@ def run_engine(args):
 
     if not args.no_extras and world == 1:
         extras.update(run_extras(p, v, V, E, nnzb_local, steps, peak, peak_kind))
+        for k, r in run_traced(n, max(5, steps // 2), peak, peak_kind).items():
+            r["vs_builtin_newton_step"] = r["newton_step_ms"] / ms
+            extras[k] = r
     if not args.no_configs and world == 1:
         del p
         gc_cuda()
@@ -669,6 +672,52 @@ def run_extras(p, v, V, E, nnzb, steps, peak, peak_kind):
         "cloth_energy_only": call_record(p, lambda: p.eval_energy_only(xd), te, "term_elements",
                                          cloth_energy_bytes(V, E), "k_elem energy (3 launches)", peak, peak_kind, k),
     }
+
+
+def run_traced(n, steps, peak, peak_kind):
+    """The same cloth Newton step with the terms registered as reference-style
+    Python callbacks (the builtin terms' __call__ bodies are the reference
+    app's formulas, apps/cloth.py:102-113): traced once, compiled by nvcc for
+    sm_100a, assembled (a) by the problem's generated patch module
+    (jit_patch.cuh) and (b) by the element-parallel kernels with fixed-order
+    gather. Closure arrays are snapshots (live_host_attrs=False) so the timed
+    region holds only device work."""
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import default_pins, lumped_masses, rest_lengths2
+    from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
+
+    pos, faces, target, x, v = cloth_inputs(n)
+    V, E = cloth_sizes(n)
+    out = {}
+    for path, env in (("patch", "0"), ("element", str(1 << 62))):
+        os.environ["MG_JIT_PATCH_MIN"] = env
+        t0 = time.perf_counter()
+        mesh = mg.Mesh(pos, faces)
+        masses = lumped_masses(mesh, 1.0)
+        h2 = 0.01 * 0.01
+        terms = [Inertia(masses, target), Spring(rest_lengths2(mesh), 0.5 * 1e4 * h2),
+                 Gravity(masses, np.array([0.0, -9.8, 0.0]), h2)]
+        p = mg.Problem(mesh, 3, fixed_vertices=default_pins(n), live_host_attrs=False)
+        for t in terms:
+            p.add_term(t.kind, t.op, lambda hd, nb, xx, _t=t: _t(hd, nb, xx))  # plain callbacks: traced
+        p.precompute_sparsity()
+        p.x = x
+        p.eval_terms(psd_floor=FLOOR)
+        st = time.perf_counter() - t0
+        vd = torch.from_numpy(v).cuda()
+        y = torch.empty_like(vd)
+        ms, _ = time_device(lambda: p.eval_terms(psd_floor=FLOOR, sync=False), steps, 3)
+        ms_h, _ = time_device(lambda: p.hvp(p.x_device, vd, out=y), steps, 3)
+        out[f"cloth_traced_{path}"] = {
+            "newton_step_ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3), "hvp_ms": ms_h,
+            "setup_and_compile_s": st, "patch_module": p.patch_module,
+            "hbm_frac_newton_step": cloth_bytes(V, E, p.hess.nnz_blocks) / (ms * 1e-3) / 1e9 / peak}
+        del p, vd, y, mesh
+        gc_cuda()
+    os.environ.pop("MG_JIT_PATCH_MIN", None)
+    return out
 
 
 def run_configs(peak, peak_kind, sub=10):

@@ -155,6 +155,15 @@ MG_API int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const 
 MG_API int mg_problem_add_jit_term_sel(mg_problem* prob, int op, int var_dim, int P, const int32_t* sel_d, int64_t M,
                                        const void* image, const double* const* attrs_d, int num_attrs,
                                        int* term_id);
+/* Traced terms on the patch-owner path: `image` is a cubin generated by
+ * paper_2509_00406_b200/jit.py for THIS problem's traced terms (in
+ * registration order; csrc/jit_patch.cuh) exporting mg_patch_{grad, hess,
+ * hess_psd, hvp, hvp_psd}. With it, eval / hvp assemble the traced terms
+ * with the same deterministic patch kernel body as the builtin terms instead
+ * of element-parallel scratch + gather. NULL drops it; adding a term drops
+ * it. Every term must be traced (V / EV / FV). Same numbers as the element
+ * path up to summation order (reference problem.py:504-617). */
+MG_API int mg_problem_set_patch_module(mg_problem* prob, const void* image);
 MG_API int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d);
 /* Rebind one attribute pointer of a registered term (closure arrays that the
  * reference rewrites in place between calls, apps/cloth.py:128, sphere.py:121-127). */

@@ -269,6 +269,7 @@ int mg_problem_add_term(mg_problem* prob, int term_type, int op, const double* p
   for (int i = 0; i < num_attrs; ++i) t.dev.a[i] = attrs_d[i];
   t.M = op_count(prob->p.mesh[0], op);
   prob->p.terms.push_back(std::move(t));
+  jit_patch_unload(prob->p);  // a generated patch module covers the terms it was built for
   prob->p.pattern_ready = false;
   prob->p.layout_ready = false;
   prob->p.gather_ready = false;
@@ -294,6 +295,7 @@ int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* i
     for (int i = 0; i < num_attrs; ++i) t.jit_attrs.push_back(attrs_d[i]);
     jit_load(t, image);
     prob->p.terms.push_back(std::move(t));
+  jit_patch_unload(prob->p);  // a generated patch module covers the terms it was built for
     prob->p.pattern_ready = false;
     prob->p.layout_ready = false;
     prob->p.gather_ready = false;
@@ -321,10 +323,26 @@ int mg_problem_add_jit_term_sel(mg_problem* prob, int op, int var_dim, int P, co
     for (int i = 0; i < num_attrs; ++i) t.jit_attrs.push_back(attrs_d[i]);
     jit_load(t, image);
     prob->p.terms.push_back(std::move(t));
+  jit_patch_unload(prob->p);  // a generated patch module covers the terms it was built for
     prob->p.pattern_ready = false;
     prob->p.layout_ready = false;
     prob->p.gather_ready = false;
     if (term_id) *term_id = (int)prob->p.terms.size() - 1;
+  });
+}
+
+int mg_problem_set_patch_module(mg_problem* prob, const void* image) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  return guard([&] {
+    Problem& p = prob->p;
+    if (!image) {
+      jit_patch_unload(p);
+    } else {
+      for (auto& t : p.terms)
+        if (!t.jit || t.dev.op == MG_OP_VV) throw Error(MG_ERR_VALUE, "a patch module needs every term traced (no VV)");
+      jit_patch_load(p, image);
+    }
+    p.layout_ready = false;  // the next call builds (or drops) the patch layout
   });
 }
 
@@ -335,6 +353,7 @@ int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const doubl
   auto& at = prob->p.terms[term_id].jit_attrs;
   if (slot < 0 || slot >= (int)at.size()) return fail(MG_ERR_VALUE, "bad attribute slot");
   at[slot] = attr_d;
+  prob->p.jattr_dirty = true;
   return MG_OK;
 }
 
@@ -500,6 +519,7 @@ int mg_problem_destroy(mg_problem* prob) {
   if (prob) {
     for (auto& t : prob->p.terms)
       if (t.jit) jit_unload(t);
+    jit_patch_unload(prob->p);
     for (auto& pr : prob->p.ev_pairs) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);

@@ -10,27 +10,50 @@ namespace mg {
 // Evaluate one element: dual result -> value + per-slot contributions.
 //   MODE_GRAD: g[K];  MODE_HESS: g[K] and packed h (valid flag);
 //   MODE_HVP: hv[K] (H v, PSD-clamped if requested).
-template <int TT, int N, int MODE, bool PSD>
-struct ElemOut {
-  static constexpr int P = TermInfo<TT>::P, K = P * N;
+template <int P_, int N, int MODE, bool PSD>
+struct ElemOutP {
+  static constexpr int P = P_, K = P * N;
   double val;
   double g[K];
   double h[(MODE == MODE_HESS) ? TriN<K>::value : 1];
   bool has_h;
 };
+template <int TT, int N, int MODE, bool PSD>
+using ElemOut = ElemOutP<TermInfo<TT>::P, N, MODE, PSD>;
+
+// the term as an evaluator: ev(e, vid, X) -> dual result (builtin terms here;
+// traced callbacks supply their generated functor, jit_patch.cuh)
+template <int TT, int N>
+struct BuiltinEval {
+  const TermDev& t;
+  template <class S>
+  MG_DI auto operator()(int64_t e, const int* vid, const Vec<S, N>* X) const { return term_eval<TT, N>(t, e, vid, X); }
+};
+
+template <int P, int N, int MODE, bool PSD, class EV>
+__device__ __forceinline__ void eval_element_f(const EV& ev, int64_t e, const int* vid, const double* const* xr,
+                                               const double* const* wr, const bool* fr, double floor,
+                                               ElemOutP<P, N, MODE, PSD>& o);
 
 template <int TT, int N, int MODE, bool PSD>
 __device__ __forceinline__ void eval_element(const TermDev& t, int64_t e, const int* vid, const double* const* xr,
                                              const double* const* wr, const bool* fr, double floor,
                                              ElemOut<TT, N, MODE, PSD>& o) {
-  constexpr int P = TermInfo<TT>::P, K = P * N;
+  eval_element_f<TermInfo<TT>::P, N, MODE, PSD>(BuiltinEval<TT, N>{t}, e, vid, xr, wr, fr, floor, o);
+}
+
+template <int P, int N, int MODE, bool PSD, class EV>
+__device__ __forceinline__ void eval_element_f(const EV& ev, int64_t e, const int* vid, const double* const* xr,
+                                               const double* const* wr, const bool* fr, double floor,
+                                               ElemOutP<P, N, MODE, PSD>& o) {
+  constexpr int K = P * N;
   if constexpr (MODE == MODE_ENERGY) {
     Vec<Dv<K>, N> X[P];
 #pragma unroll
     for (int q = 0; q < P; ++q)
 #pragma unroll
       for (int c = 0; c < N; ++c) X[q][c].v = xr[q][c];
-    o.val = term_eval<TT, N>(t, e, vid, X).v;
+    o.val = ev(e, vid, X).v;
   } else if constexpr (MODE == MODE_GRAD) {
     Vec<Dg<K>, N> X[P];
 #pragma unroll
@@ -41,7 +64,7 @@ __device__ __forceinline__ void eval_element(const TermDev& t, int64_t e, const 
 #pragma unroll
         for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
       }
-    auto r = term_eval<TT, N>(t, e, vid, X);
+    auto r = ev(e, vid, X);
     o.val = r.v;
 #pragma unroll
     for (int i = 0; i < K; ++i) o.g[i] = r.g[i];
@@ -55,7 +78,7 @@ __device__ __forceinline__ void eval_element(const TermDev& t, int64_t e, const 
 #pragma unroll
         for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
       }
-    auto r = term_eval<TT, N>(t, e, vid, X);
+    auto r = ev(e, vid, X);
     using R = decltype(r);
     o.val = r.v;
     if constexpr (MODE == MODE_HESS) {
@@ -112,7 +135,7 @@ __device__ __forceinline__ void eval_element(const TermDev& t, int64_t e, const 
 #pragma unroll
         for (int i = 0; i < K; ++i) X[q][c].g[i] = (i == q * N + c) ? 1.0 : 0.0;
       }
-    auto r = term_eval<TT, N>(t, e, vid, X);
+    auto r = ev(e, vid, X);
     using R = decltype(r);
     o.val = r.v;
 #pragma unroll

@@ -19,6 +19,7 @@ typedef int (*PFN_launch)(void*, unsigned, unsigned, unsigned, unsigned, unsigne
                           void**, void**);
 typedef int (*PFN_unload)(void*);
 typedef int (*PFN_errstr)(int, const char**);
+typedef int (*PFN_setattr)(void*, int, int);
 
 struct Driver {
   PFN_load load = nullptr;
@@ -26,6 +27,7 @@ struct Driver {
   PFN_launch launch = nullptr;
   PFN_unload unload = nullptr;
   PFN_errstr errstr = nullptr;
+  PFN_setattr setattr = nullptr;
 };
 
 Driver& driver() {
@@ -41,6 +43,7 @@ Driver& driver() {
       d.launch = (PFN_launch)dlsym(h, "cuLaunchKernel");
       d.unload = (PFN_unload)dlsym(h, "cuModuleUnload");
       d.errstr = (PFN_errstr)dlsym(h, "cuGetErrorString");
+      d.setattr = (PFN_setattr)dlsym(h, "cuFuncSetAttribute");
     }
   }
   if (!d.load || !d.getfn || !d.launch) throw Error(MG_ERR_CUDA, "CUDA driver API (libcuda) unavailable");
@@ -100,6 +103,38 @@ void jit_launch(const Problem& p, const Term& t, Mode mode, const LaunchCtx& c, 
   const unsigned grid = (unsigned)((t.M + JIT_TPB - 1) / JIT_TPB);
   if (grid) drv_check(driver().launch(t.jit_fn[k], grid, 1, 1, JIT_TPB, 1, 1, 0, c.stream, params, nullptr),
                       "cuLaunchKernel");
+}
+
+const char* kPatchNames[5] = {"mg_patch_grad", "mg_patch_hess", "mg_patch_hess_psd", "mg_patch_hvp",
+                              "mg_patch_hvp_psd"};
+
+void jit_patch_load(Problem& p, const void* image) {
+  MG_CUDA(cudaFree(nullptr));
+  Driver& d = driver();
+  jit_patch_unload(p);
+  drv_check(d.load(&p.patch_module, image), "cuModuleLoadData (patch module)");
+  for (int i = 0; i < 5; ++i) drv_check(d.getfn(&p.patch_fn[i], p.patch_module, kPatchNames[i]), kPatchNames[i]);
+  p.jattr_dirty = true;
+}
+
+void jit_patch_unload(Problem& p) {
+  if (p.patch_module && driver().unload) driver().unload(p.patch_module);
+  p.patch_module = nullptr;
+  for (auto& f : p.patch_fn) f = nullptr;
+}
+
+void jit_patch_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t np, int nvp_max, int blocks_max,
+                      size_t smem, cudaStream_t s) {
+  Driver& d = driver();
+  const int k = mode == MODE_GRAD ? 0 : mode == MODE_HESS ? (psd ? 2 : 1) : (psd ? 4 : 3);
+  if (mode != MODE_GRAD && mode != MODE_HESS && mode != MODE_HVP)
+    throw Error(MG_ERR_UNSUPPORTED, "traced patch kernels assemble grad / Hessian / HVP only");
+  if (d.setattr) drv_check(d.setattr(p.patch_fn[k], 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */,
+                                     (int)smem), "cuFuncSetAttribute");
+  void* params[3] = {args, &nvp_max, &blocks_max};
+  if (np > 0)
+    drv_check(d.launch(p.patch_fn[k], (unsigned)np, 1, 1, 128, 1, 1, (unsigned)smem, s, params, nullptr),
+              "cuLaunchKernel (patch module)");
 }
 
 }  // namespace mg

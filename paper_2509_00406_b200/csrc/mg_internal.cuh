@@ -207,6 +207,12 @@ struct Problem {
   mutable std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
   mutable cudaEvent_t ev_open = nullptr;
   int64_t recomputed_elements = 0;
+  // traced terms on the patch path (jit_patch.cuh): the problem's generated
+  // patch module (5 mode kernels) and its terms' attribute-pointer table
+  void* patch_module = nullptr;
+  void* patch_fn[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  mutable DBuf<const double*> jattr;
+  mutable bool jattr_dirty = true;
 };
 
 // element vertex ids of an op (nullptr for V: the element is the vertex)
@@ -237,9 +243,17 @@ int64_t sort_unique(uint64_t*& keys, int64_t n, int end_bit, cudaStream_t s);
 struct LaunchCtx;
 void jit_load(Term& t, const void* image);
 void jit_unload(Term& t);
+void jit_patch_load(Problem& p, const void* image);
+void jit_patch_unload(Problem& p);
+
 
 // elem_kernels.cu (element-parallel, atomic accumulation)
 enum Mode { MODE_ENERGY = 0, MODE_GRAD = 1, MODE_HESS = 2, MODE_HVP = 3 };
+// launch the problem's traced patch kernel for a mode (args: the filled
+// patch::PatchArgs, passed as void* to keep this header light)
+void jit_patch_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t np, int nvp_max,
+                      int blocks_max, size_t smem, cudaStream_t s);
+
 struct LaunchCtx {
   const double* x;
   const double* w;     // hvp direction

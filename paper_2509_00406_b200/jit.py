@@ -200,13 +200,10 @@ class TracedTerm:
         self.op, self.P, self.n = op, P, n
         self.body, self.ret, self.attrs = body, ret, attrs
 
-    def source(self) -> str:
+    def functor(self, name: str = "Traced") -> str:
+        """The recorded SSA as a C++ functor over the engine's duals."""
         lines = "\n      ".join(self.body)
-        return f"""// generated by paper_2509_00406_b200/jit.py — traced energy callback
-#include "jit_kernel.cuh"
-
-namespace {{
-struct Traced {{
+        return f"""struct {name} {{
   template <int N, class S>
   MG_DI auto operator()(const double* const* A, int64_t e, const mg::Vec<S, N>* X) const {{
       using namespace mg;
@@ -214,10 +211,58 @@ struct Traced {{
       {lines}
       return {self.ret};
   }}
-}};
+}};"""
+
+    def source(self) -> str:
+        return f"""// generated by paper_2509_00406_b200/jit.py — traced energy callback
+#include "jit_kernel.cuh"
+
+namespace {{
+{self.functor()}
 }}  // namespace
 
 MG_JIT_INSTANTIATE(Traced, {self.P}, {self.n})
+"""
+
+
+def patch_source(terms: list, n: int) -> str:
+    """One module for a problem's traced terms on the patch-owner path
+    (csrc/jit_patch.cuh): a functor per term and a policy that runs the V
+    terms, then the EV / FV terms, in registration order (like the builtin
+    patch kernel), each with its own attribute streams (a.jattr + t * 64)."""
+    funcs = "\n".join(t.functor(f"T{i}") for i, t in enumerate(terms))
+    vt, et = [], []
+    for i, t in enumerate(terms):
+        ev = f"mg::patch::JitEval<T{i}, N>{{a.jattr + {i} * mg::patch::JATTR}}"
+        if t.op == "V":
+            vt.append(f"mg::patch::run_vterm_g<N, MODE, PSD>(a, {ev}, s, oc, eacc);")
+        elif t.op in ("EV", "FV"):
+            lay = "a.ev" if t.op == "EV" else "a.fv"
+            et.append(f"mg::patch::run_eterm_g<{t.P}, N, MODE, PSD>(a, {ev}, {lay}, p, s, oc, eacc);")
+        else:
+            raise ValueError("patch modules take V / EV / FV traced terms")
+    j = "\n    "
+    return f"""// generated by paper_2509_00406_b200/jit.py — a problem's traced terms on the patch path
+#include "jit_patch.cuh"
+
+namespace {{
+{funcs}
+
+struct Policy {{
+  template <int N, int MODE, bool PSD>
+  MG_DI static void vterms(const mg::patch::PatchArgs& a, const mg::patch::Smem& s, int oc, double& eacc) {{
+    (void)a; (void)s; (void)oc; (void)eacc;
+    {j.join(vt)}
+  }}
+  template <int N, int MODE, bool PSD>
+  MG_DI static void eterms(const mg::patch::PatchArgs& a, int p, const mg::patch::Smem& s, int oc, double& eacc) {{
+    (void)a; (void)p; (void)s; (void)oc; (void)eacc;
+    {j.join(et)}
+  }}
+}};
+}}  // namespace
+
+MG_PATCH_JIT_INSTANTIATE(Policy, {n})
 """
 
 
@@ -280,7 +325,15 @@ def _toolchain() -> bytes:
 def compile_term(tt: TracedTerm) -> bytes:
     """nvcc the traced functor into an sm_100a cubin (cached by source +
     toolchain hash; compiled under a per-process name, then renamed)."""
-    src = tt.source()
+    return compile_source(tt.source())
+
+
+def compile_patch(terms: list, n: int) -> bytes:
+    """The patch-path module of a problem's traced terms (patch_source)."""
+    return compile_source(patch_source(terms, n))
+
+
+def compile_source(src: str) -> bytes:
     h = hashlib.sha256(src.encode() + _toolchain()).hexdigest()[:20]
     CACHE.mkdir(parents=True, exist_ok=True)
     cubin = CACHE / f"term_{h}.cubin"

@@ -232,6 +232,8 @@ class Problem:
         self.energy: float = float("nan")
         self._terms: list[_TermRecord] = []
         self._pattern_ready = False
+        self._patch_checked = False
+        self.patch_module = False  # traced terms run through a generated patch module
         self.stats = {
             "eval_terms_calls": 0, "eval_terms_ms": 0.0,
             "energy_only_calls": 0, "energy_only_ms": 0.0,
@@ -253,6 +255,7 @@ class Problem:
         a builtin term from `paper_2509_00406_b200.terms`."""
         if SOURCE_KIND[op] is not kind:
             raise ValueError(f"{op.name} iterates over {SOURCE_KIND[op].value} elements, not {kind.value}")
+        self._patch_checked = self.patch_module = False  # the library drops a generated patch module on add
         if op not in _TERM_OPS:
             raise ValueError(f"{op.name} does not resolve to vertex variables; terms support FV, EV, VV, V")
         if not isinstance(fn, BuiltinTerm):
@@ -274,6 +277,7 @@ class Problem:
         rec.tid = tid.value
         self._terms.append(rec)
         self._pattern_ready = False
+        self._patch_checked = self.patch_module = False
         return len(self._terms) - 1
 
     def _num_elements(self, op: Op) -> int:
@@ -306,6 +310,7 @@ class Problem:
         rec.tid = tid.value
         self._terms.append(rec)
         self._pattern_ready = False
+        self._patch_checked = self.patch_module = False
         return len(self._terms) - 1
 
     def _one_rings(self):
@@ -371,6 +376,31 @@ class Problem:
         for rec in self._terms:
             if rec.error is not None:
                 raise rec.error
+        if not self._patch_checked:
+            self._patch_checked = True
+            self._use_patch_module()
+
+    def _use_patch_module(self):
+        """Traced terms on the patch-owner path: when every term is a traced
+        V / EV / FV callback, deterministic accumulation, and the problem has
+        at least MG_JIT_PATCH_MIN elements (default 65536; smaller problems
+        keep the element-parallel kernels, compiled once per term), generate
+        and compile one module with all the problem's functors and hand it to
+        the library (mg_problem_set_patch_module)."""
+        from . import jit
+
+        recs = self._terms
+        if self.accumulation != "deterministic" or not all(r.traced is not None and r.groups is None for r in recs):
+            return
+        if len(recs) > 8 or self.mesh.num_vertices == 0:
+            return
+        total = sum(self._num_elements(r.op) for r in recs)
+        if total < int(os.environ.get("MG_JIT_PATCH_MIN", "65536")):
+            return
+        image = jit.compile_patch([r.traced for r in recs], self.n)
+        buf = ctypes.create_string_buffer(image, len(image))
+        _lib.check(self._lib.mg_problem_set_patch_module(self._h, buf))
+        self.patch_module = True
 
     def _sync_attrs(self):
         if self.live_host_attrs:

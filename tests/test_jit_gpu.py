@@ -27,8 +27,13 @@ def traced_problem(d):
     return p
 
 
+@pytest.mark.parametrize("path", ["element", "patch"])
 @pytest.mark.parametrize("name", CASES)
-def test_traced_callbacks_match_reference(name):
+def test_traced_callbacks_match_reference(name, path, monkeypatch):
+    """Both engine paths for traced terms: element-parallel kernels (one
+    module per term, fixed-order gather) and the problem's generated patch
+    module (jit_patch.cuh; forced here at golden sizes by MG_JIT_PATCH_MIN=0)."""
+    monkeypatch.setenv("MG_JIT_PATCH_MIN", "0" if path == "patch" else str(1 << 62))
     d = load(name)
     p = traced_problem(d)
     assert all(r.traced is not None for r in p._terms)
@@ -36,6 +41,9 @@ def test_traced_callbacks_match_reference(name):
         h = p.precompute_sparsity()
         assert np.array_equal(h.row_offsets, d["row_offsets"])
         assert np.array_equal(h.col_indices, d["col_indices"])
+    else:
+        p.eval_terms()
+    assert p.patch_module == (path == "patch")
     for s in states(d):
         x = d[f"s{s}_x"]
         p.x = x
