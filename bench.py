@@ -678,8 +678,10 @@ def run_traced(n, steps, peak, peak_kind):
     """The same cloth Newton step with the terms registered as reference-style
     Python callbacks (the builtin terms' __call__ bodies are the reference
     app's formulas, apps/cloth.py:102-113): traced once, compiled by nvcc for
-    sm_100a, assembled (a) by the problem's generated patch module
-    (jit_patch.cuh) and (b) by the element-parallel kernels with fixed-order
+    sm_100a, assembled (a) by the generated edge row module (jit_rows.cuh:
+    the tracer proves the spring radial, phi(r) on a one-variable
+    second-order dual), (b) by the problem's generated patch module
+    (jit_patch.cuh) and (c) by the element-parallel kernels with fixed-order
     gather. Closure arrays are snapshots (live_host_attrs=False) so the timed
     region holds only device work."""
     import torch
@@ -691,8 +693,9 @@ def run_traced(n, steps, peak, peak_kind):
     pos, faces, target, x, v = cloth_inputs(n)
     V, E = cloth_sizes(n)
     out = {}
-    for path, env in (("patch", "0"), ("element", str(1 << 62))):
+    for path, env, rows in (("rows", "0", "1"), ("patch", "0", "0"), ("element", str(1 << 62), "0")):
         os.environ["MG_JIT_PATCH_MIN"] = env
+        os.environ["MG_JIT_ROWS"] = rows
         t0 = time.perf_counter()
         mesh = mg.Mesh(pos, faces)
         masses = lumped_masses(mesh, 1.0)
@@ -712,11 +715,12 @@ def run_traced(n, steps, peak, peak_kind):
         ms_h, _ = time_device(lambda: p.hvp(p.x_device, vd, out=y), steps, 3)
         out[f"cloth_traced_{path}"] = {
             "newton_step_ms": ms, "term_elements_per_s": (2 * V + E) / (ms * 1e-3), "hvp_ms": ms_h,
-            "setup_and_compile_s": st, "patch_module": p.patch_module,
+            "setup_and_compile_s": st, "patch_module": p.patch_module, "row_module": p.row_module,
             "hbm_frac_newton_step": cloth_bytes(V, E, p.hess.nnz_blocks) / (ms * 1e-3) / 1e9 / peak}
         del p, vd, y, mesh
         gc_cuda()
     os.environ.pop("MG_JIT_PATCH_MIN", None)
+    os.environ.pop("MG_JIT_ROWS", None)
     return out
 
 

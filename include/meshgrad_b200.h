@@ -164,6 +164,17 @@ MG_API int mg_problem_add_jit_term_sel(mg_problem* prob, int op, int var_dim, in
  * it. Every term must be traced (V / EV / FV). Same numbers as the element
  * path up to summation order (reference problem.py:504-617). */
 MG_API int mg_problem_set_patch_module(mg_problem* prob, const void* image);
+/* Traced terms on the edge row kernel: `image` is a cubin generated by
+ * paper_2509_00406_b200/jit.py (csrc/jit_rows.cuh) for THIS problem's traced
+ * terms when every EV callback depends on x only through |x_i - x_j|^2 (the
+ * tracer proves it on the recorded operations) and the others are V terms;
+ * it exports mg_rows_{grad, hess, hess_psd, hvp, hvp_psd} and needs the
+ * problem's patch module as its exact re-run (non-finite lanes). Replaces
+ * the per-element evaluation of Problem.eval_terms / hvp (reference
+ * problem.py:504-549, 578-617) by one thread per row with phi(r) on a
+ * one-variable second-order dual; results agree with the full-dual path to
+ * rounding. NULL drops it; adding a term drops it. */
+MG_API int mg_problem_set_row_module(mg_problem* prob, const void* image);
 MG_API int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d);
 /* Rebind one attribute pointer of a registered term (closure arrays that the
  * reference rewrites in place between calls, apps/cloth.py:128, sphere.py:121-127). */

@@ -269,7 +269,8 @@ int mg_problem_add_term(mg_problem* prob, int term_type, int op, const double* p
   for (int i = 0; i < num_attrs; ++i) t.dev.a[i] = attrs_d[i];
   t.M = op_count(prob->p.mesh[0], op);
   prob->p.terms.push_back(std::move(t));
-  jit_patch_unload(prob->p);  // a generated patch module covers the terms it was built for
+  jit_patch_unload(prob->p);  // a generated patch / row module covers the terms it was built for
+    jit_rows_unload(prob->p);
   prob->p.pattern_ready = false;
   prob->p.layout_ready = false;
   prob->p.gather_ready = false;
@@ -295,7 +296,8 @@ int mg_problem_add_jit_term(mg_problem* prob, int op, int var_dim, const void* i
     for (int i = 0; i < num_attrs; ++i) t.jit_attrs.push_back(attrs_d[i]);
     jit_load(t, image);
     prob->p.terms.push_back(std::move(t));
-  jit_patch_unload(prob->p);  // a generated patch module covers the terms it was built for
+  jit_patch_unload(prob->p);  // a generated patch / row module covers the terms it was built for
+    jit_rows_unload(prob->p);
     prob->p.pattern_ready = false;
     prob->p.layout_ready = false;
     prob->p.gather_ready = false;
@@ -323,7 +325,8 @@ int mg_problem_add_jit_term_sel(mg_problem* prob, int op, int var_dim, int P, co
     for (int i = 0; i < num_attrs; ++i) t.jit_attrs.push_back(attrs_d[i]);
     jit_load(t, image);
     prob->p.terms.push_back(std::move(t));
-  jit_patch_unload(prob->p);  // a generated patch module covers the terms it was built for
+  jit_patch_unload(prob->p);  // a generated patch / row module covers the terms it was built for
+    jit_rows_unload(prob->p);
     prob->p.pattern_ready = false;
     prob->p.layout_ready = false;
     prob->p.gather_ready = false;
@@ -343,6 +346,22 @@ int mg_problem_set_patch_module(mg_problem* prob, const void* image) {
       jit_patch_load(p, image);
     }
     p.layout_ready = false;  // the next call builds (or drops) the patch layout
+  });
+}
+
+int mg_problem_set_row_module(mg_problem* prob, const void* image) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  return guard([&] {
+    Problem& p = prob->p;
+    if (!image) {
+      jit_rows_unload(p);
+    } else {
+      for (auto& t : p.terms)
+        if (!t.jit || (t.dev.op != MG_OP_V && t.dev.op != MG_OP_EV))
+          throw Error(MG_ERR_VALUE, "a row module needs every term traced, V or EV");
+      jit_rows_load(p, image);
+    }
+    p.layout_ready = false;  // the next call builds (or drops) the row layout
   });
 }
 
@@ -408,7 +427,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
     int64_t np = 0;
     if (p.deterministic && p.layout_ready) {
       np = launch_patch(p, mode, c, 0);
-      launches += (p.ev_fast || p.fv_fast) ? 2 : 1;
+      launches += (p.ev_fast || p.fv_fast || p.ev_jit) ? 2 : 1;
     } else if (p.deterministic) {  // element-parallel into scratch, fixed-order gather
       if (!p.gather_ready) build_gather(p, s);
       c.scratch = true;
@@ -432,7 +451,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
       }
     }
     reduce_partials(p.partials.p, np, energy_d, s,
-                    (p.ev_fast || p.fv_fast) && p.deterministic && p.layout_ready ? p.redo.p : nullptr);
+                    (p.ev_fast || p.fv_fast || p.ev_jit) && p.deterministic && p.layout_ready ? p.redo.p : nullptr);
     p.last_launches = launches + reduce_launches(np);
   });
 }
@@ -474,7 +493,7 @@ int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, 
     if (p.deterministic && p.layout_ready) {
       launch_patch(p, MODE_HVP, c, 0);
       launches = 1;
-      if (p.ev_fast || p.fv_fast) {
+      if (p.ev_fast || p.fv_fast || p.ev_jit) {
         MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
         launches = 2;
       }
@@ -520,6 +539,7 @@ int mg_problem_destroy(mg_problem* prob) {
     for (auto& t : prob->p.terms)
       if (t.jit) jit_unload(t);
     jit_patch_unload(prob->p);
+    jit_rows_unload(prob->p);
     for (auto& pr : prob->p.ev_pairs) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);

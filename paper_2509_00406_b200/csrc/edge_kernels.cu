@@ -18,6 +18,9 @@
 // edge is evaluated by each of its two owner rows (recompute instead of
 // communicate). The energy counts every element once (edges at their first
 // vertex) through fixed-order per-warp partials.
+#include <cstring>
+
+#include "edge_rows.cuh"
 #include "elem_eval.cuh"
 #include "mg_internal.cuh"
 #include "psd.cuh"
@@ -26,44 +29,7 @@ namespace mg {
 
 namespace {
 
-constexpr int PT = EV_ROW_BLOCK;  // rows (threads) per CTA
-constexpr int MAXT = 8;
-
-struct EvArgs {
-  int nterms;
-  int64_t V;  // owned rows (patch order)
-  const int32_t* order;      // (V) vertex of each row
-  const uint8_t* pfix;       // (V) pinned flag of each row
-  const uint32_t* rmeta;     // (V) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
-  const uint64_t* ell;       // (EV_ELL_K, V) first incidences, slot-major
-  const int32_t* rinc_off;   // (V+1)
-  const uint64_t* rrec;      // lo: edge | slot << 31, hi: other | pinned(other) << 31
-  const int64_t* prow_ro;
-  const int32_t* prow_len;
-  const uint8_t* prow_dp;
-  const int32_t* hoff;
-  const double* x;
-  const double* w;
-  double* grad;
-  double* hess;
-  double* y;
-  double* partials;
-  int* redo;  // raised by the radial kernel on a non-finite lane
-  int* exact_runs;
-  int nev, nvt;                 // compacted term lists (indices into terms)
-  int ev_idx[MAXT], vt_idx[MAXT];
-  const double* ev_a0;          // per-edge attribute of ev_idx[0] (prefetched), or null
-  // staged tiles (k_tile_ev): see Problem::tiles_ready
-  const int2* tcnt;
-  const uint32_t* tv;
-  const uint64_t* te;
-  const uint16_t* islot;
-  const uint16_t* islot8;  // (V, 8): a row's first 8 slots, one 16-byte load
-  int max_v, max_e;
-  int64_t np_total;  // energy partials the reduction reads (the exact re-run zero-fills past its own)
-  double floor;
-  TermDev terms[MAXT];
-};
+using namespace rows;
 
 // per-edge record (doubles) and per-row V-term accumulator widths
 template <int N, int MODE, bool PSD>
@@ -74,29 +40,6 @@ struct EvRec {
   static constexpr int VW = MODE == MODE_HESS ? N + T : N;
 };
 
-MG_DI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// dst[0..n) = src[0..n) (doubles), src in shared memory with the same 16-byte
-// phase as dst: 8-byte head / tail stores plus one bulk (TMA) copy of the
-// aligned middle. The caller waits for the bulk group before leaving.
-MG_DI void row_store_bulk(double* dst, const double* src, int n) {
-  int k0 = 0;
-  if (reinterpret_cast<uintptr_t>(dst) & 15) {
-    if (n > 0) dst[0] = src[0];
-    k0 = 1;
-  }
-  int m = n - k0;
-  if (m <= 0) return;
-  if (m & 1) {
-    dst[n - 1] = src[n - 1];
-    --m;
-  }
-  if (m > 0) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src + k0);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                 :: "l"(dst + k0), "r"(sa), "r"((uint32_t)m * 8u) : "memory");
-  }
-}
 
 template <class Q>
 MG_DI double hess00(const Q& q) {
@@ -331,17 +274,6 @@ MG_DI void edge_dual_fof(const EvArgs& a, int64_t e, const double* xa, const dou
   }
 }
 
-// 1/x to full fp64 precision without the IEEE division sequence: hardware
-// reciprocal estimate + two Newton steps (non-finite / zero inputs give
-// non-finite results, which send the call to the exact kernel)
-MG_DI double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 // phi, phi', phi'' of a radial term at r; the attribute value (spring: squared
 // rest length) is preloaded. Closed forms of the reference callbacks:
@@ -373,14 +305,6 @@ MG_DI bool radial_any(const TermDev& t, double a0, double rr, double& pv, double
                                   : radial_closed<MG_TERM_EDGE_LENGTH>(t, a0, rr, pv, p1, p2);
 }
 
-// closed-form clamp with the fast reciprocal
-MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
-  const double lt = ci, ld = ci + cd * r;
-  if (lt > f && ld > f) return;
-  const double mt = lt > f ? lt : f, md = ld > f ? ld : f;
-  ci = mt;
-  cd = r > 0.0 ? (md - mt) * rcp_fast(r) : 0.0;
-}
 
 // Closed forms of the two builtin V terms (apps/cloth.py:102-104, 112-113) in
 // the dual's operation order: inertia 0.5 m |x - t|^2 (gradient m d, Hessian
@@ -465,292 +389,45 @@ MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const dou
   }
 }
 
-// incidences per row held in registers (the rest are streamed) and the
-// occupancy target: the Hessian kernel is bounded by its shared-memory row
-// buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
-// for more resident warps
-#ifndef EV_HESS_MINB
-#define EV_HESS_MINB 1
-#endif
-#ifndef EV_FLAT_BLOCK
-#define EV_FLAT_BLOCK 64
-#endif
-// MAXI: incidences in flight; BLOCK: threads per CTA (the Hessian kernel's CTA
-// is its row-buffer group, EV_ROW_BLOCK); MINB: CTAs per SM to fit
-template <int MODE, bool PSD> struct FastCfg {
-  static constexpr int MAXI = EV_ELL_K, BLOCK = EV_ROW_BLOCK, MINB = EV_HESS_MINB;
-};
-#ifndef EV_HVP_MAXI
-#define EV_HVP_MAXI 4
-#endif
-#ifndef EV_HVP_THREADS
-#define EV_HVP_THREADS 512  // measured: 0.269 ms vs 0.288 at 640 (row-kernel spring HVP, 2048^2)
-#endif
-template <> struct FastCfg<MODE_HVP, false> {
-  static constexpr int MAXI = EV_HVP_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_THREADS / EV_FLAT_BLOCK;
-};
-template <> struct FastCfg<MODE_HVP, true> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 512 / EV_FLAT_BLOCK;
-};
-template <> struct FastCfg<MODE_GRAD, false> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
+// The builtin terms as a row-kernel policy (edge_rows.cuh): closed forms of
+// the V terms with early attribute loads, and the radial closed forms of the
+// EV terms; EVT fixes the single EV term's type at compile time (0: any mix,
+// dispatched per incidence).
+template <int EVT>
+struct BuiltinRows {
+  static constexpr bool kXFreeHvp = EVT == MG_TERM_EDGE_LENGTH;
+  template <int N, int MODE>
+  MG_DI static VPreload<N> vload(const EvArgs& a, int g) { return vterms_load<N, MODE>(a, g); }
+  template <int N, int MODE, bool PSD>
+  MG_DI static void vterms(const EvArgs& a, int g, bool, const VPreload<N>& v, const double* xs, const double* us,
+                           double& eacc, double* vec, double* dg) {
+    vterms_closed<N, MODE, PSD>(a, g, v, xs, us, eacc, vec, dg);
+  }
+  template <int MODE>
+  MG_DI static double eload(const EvArgs& a, uint32_t e) { return a.ev_a0 ? a.ev_a0[e] : 0.0; }
+  template <int MODE, bool NEEDV, class F>
+  MG_DI static void eterms(const EvArgs& a, double av, double rr, uint32_t e, F&& one) {
+    if constexpr (EVT != 0) {
+      double pv, p1, p2;
+      const bool ok = radial_closed<EVT, NEEDV>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
+      one(ok, pv, p1, p2);
+    } else {
+      for (int j = 0; j < a.nev; ++j) {
+        const TermDev& t = a.terms[a.ev_idx[j]];
+        const double at = (j == 0 && a.ev_a0) ? av : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
+        double pv, p1, p2;
+        const bool ok = radial_any(t, at, rr, pv, p1, p2);
+        one(ok, pv, p1, p2);
+      }
+    }
+  }
 };
 
-// Radial fast kernel: one thread per owned row, d = x_row - x_other (radial
-// terms are even in d, so no orientation bookkeeping). A row's first MAXI
-// incidences are fetched in two batched levels (records, then neighbour x and
-// edge attributes) so their latencies overlap; EVT fixes the single EV term's
-// type at compile time (0: any mix, dispatched per incidence).
-// the x-free edge-length HVP holds only directions: full occupancy (64 registers)
-template <int MODE, bool PSD, int EVT> struct FastMinb {
-  static constexpr int v =
-      (MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH) ? 1024 / EV_FLAT_BLOCK : FastCfg<MODE, PSD>::MINB;
-};
 template <int N, int MODE, bool PSD, int EVT>
-__global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK, (FastMinb<MODE, PSD, EVT>::v))
+__global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK,
+                                  (FastMinb<MODE, PSD, BuiltinRows<EVT>::kXFreeHvp>::v))
     k_rows_fast(const __grid_constant__ EvArgs a) {
-  constexpr int T = TriN<N>::value, NN = N * N;
-  constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
-  constexpr int PT = FastCfg<MODE, PSD>::BLOCK;
-  // the edge length's Hessian 2 [[I,-I],[-I,I]] does not depend on x
-  // (apps/smooth.py:27-28): its unclamped HVP reads only the direction
-  constexpr bool XFREE = MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH;
-  extern __shared__ __align__(16) double hbuf[];
-  // Row blocks are walked grid-stride (a persistent grid for the Hessian, one
-  // block per CTA otherwise); the level-1 streams of the thread's next row are
-  // loaded while it works on the current one.
-  struct L1 {
-    int g = 0;
-    uint32_t meta = 0;
-    int64_t ro = 0;
-    int ho = 0;
-    uint64_t rc[EV_ELL_K];
-  };
-  // level 1: static per-row streams, all indexed by the row alone
-  // (coalesced): vertex, meta word, row start / buffer offset, ELL records
-  auto load_l1 = [&](int64_t r, L1& l) {
-    if (r >= a.V) return;
-    l.g = a.order ? a.order[r] : (int)r;  // null: identity row order
-    l.meta = a.rmeta[r];
-    if constexpr (MODE == MODE_HESS) {
-      l.ro = a.prow_ro[r];
-      l.ho = a.hoff[r];
-    }
-#pragma unroll
-    for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
-  };
-  const int64_t nblk = (a.V + PT - 1) / PT;
-  bool finite = true;
-  L1 cur, nxt;
-  if constexpr (MODE == MODE_HESS) load_l1((int64_t)blockIdx.x * PT + threadIdx.x, cur);
-  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-  const int64_t row = blk * PT + threadIdx.x;
-  if constexpr (MODE == MODE_HESS) {
-    if (blk + gridDim.x < nblk) load_l1(row + (int64_t)gridDim.x * PT, nxt);
-  } else {
-    load_l1(row, cur);
-  }
-  double eacc = 0.0;
-  if (row < a.V) {
-    const int g = cur.g;
-    const uint32_t meta = cur.meta;
-    const int64_t ro = cur.ro;
-    const int ho = cur.ho;
-    uint64_t rc[EV_ELL_K];
-#pragma unroll
-    for (int j = 0; j < EV_ELL_K; ++j) rc[j] = cur.rc[j];
-    (void)ro;
-    // the previous row's bulk copy must have read this thread's row buffer
-    if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    // level 2: own x / w, issued before anything waits on the meta word (with
-    // the identity row order g is the row itself, so these do not wait on
-    // level 1 at all); the pinned mask is applied after the load
-    double xs[N], us[N];
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      xs[c] = a.x[(int64_t)g * N + c];
-      if constexpr (MODE == MODE_HVP) us[c] = a.w[(int64_t)g * N + c];
-      else us[c] = 0.0;
-    }
-    const VPreload<N> vpre = vterms_load<N, MODE>(a, g);
-    // level 3: neighbour x (w) and the edge attribute, kept MAXI incidences
-    // ahead of the compute (a rolling window over the ELL slots). Unused ELL
-    // slots hold record 0 (edge 0, vertex 0), so the loads are unconditional
-    // (no wait on the incidence count) and their values are never used.
-    double xo[EV_ELL_K][N], uo[EV_ELL_K][N], a0[EV_ELL_K];
-    auto issue = [&](int j) {
-      const uint32_t hi = (uint32_t)(rc[j] >> 32);
-      const int64_t o = hi & 0x7fffffffu;
-      const bool fo = !(hi >> 31);
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        xo[j][c] = !XFREE ? a.x[o * N + c] : 0.0;
-        if constexpr (MODE == MODE_HVP) {
-          const double wv = a.w[o * N + c];
-          uo[j][c] = fo ? wv : 0.0;
-        } else {
-          uo[j][c] = 0.0;
-        }
-      }
-      a0[j] = a.ev_a0 ? a.ev_a0[(uint32_t)rc[j] & 0x7fffffffu] : 0.0;
-    };
-#pragma unroll
-    for (int j = 0; j < MAXI; ++j) issue(j);
-    const bool fr = !((meta >> 8) & 1);
-    const int dp = (int)(meta >> 16) & 0xff;
-    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
-    if constexpr (MODE == MODE_HVP) {
-#pragma unroll
-      for (int c = 0; c < N; ++c) us[c] = fr ? us[c] : 0.0;
-    }
-    double vec[N], dg[T];
-#pragma unroll
-    for (int i = 0; i < N; ++i) vec[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < T; ++i) dg[i] = 0.0;
-    // V terms (their attribute loads overlapped the level-3 loads)
-    vterms_closed<N, MODE, PSD>(a, g, vpre, xs, us, eacc, vec, dg);
-    double* hrow = hbuf + ho;
-    int pos = 0;
-    // one incidence: contributions to this row
-    auto incidence = [&](uint64_t r64, const double* xo_, const double* uo_, double av) {
-      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
-      const int64_t e = lo & 0x7fffffffu;
-      const bool first = (lo >> 31) == 0;  // the row is the edge's first vertex
-      const bool fo = !(hi >> 31);
-      double d[N], rr = 0.0;
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        d[c] = XFREE ? 0.0 : xs[c] - xo_[c];
-        rr = d[c] * d[c] + rr;
-      }
-      double gam = 0.0, ci_s = 0.0, cd_s = 0.0, dl = 0.0, val = 0.0;
-      auto one_term = [&](bool ok, double pv, double p1, double p2) {
-        finite &= ok;
-        val += pv;
-        gam += 2.0 * p1;
-        if constexpr (MODE != MODE_GRAD) {
-          double ci = 2.0 * p1, cd = 4.0 * p2, sh = 0.0;
-          if constexpr (PSD) {
-            if (fr && fo) {  // [[A,-A],[-A,A]]: clamp 2A, halve, shift floor/2
-              ci *= 2.0; cd *= 2.0;
-              radial_clamp_fast(ci, cd, rr, a.floor);
-              ci *= 0.5; cd *= 0.5;
-              sh = 0.5 * a.floor;
-            } else if (fr || fo) {
-              radial_clamp_fast(ci, cd, rr, a.floor);
-            }
-          }
-          ci_s += ci;
-          cd_s += cd;
-          dl += sh;
-        }
-      };
-      if constexpr (EVT != 0) {
-        double pv, p1, p2;
-        const bool ok = radial_closed<EVT, MODE != MODE_HVP>(a.terms[a.ev_idx[0]], av, rr, pv, p1, p2);
-        one_term(ok, pv, p1, p2);
-      } else {
-        for (int j = 0; j < a.nev; ++j) {
-          const TermDev& t = a.terms[a.ev_idx[j]];
-          const double at = (j == 0 && a.ev_a0) ? av : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
-          double pv, p1, p2;
-          const bool ok = radial_any(t, at, rr, pv, p1, p2);
-          one_term(ok, pv, p1, p2);
-        }
-      }
-      if constexpr (MODE != MODE_HVP) {
-        if (first) eacc += val;  // an edge's energy counts at its first vertex
-      }
-      if constexpr (MODE == MODE_GRAD || MODE == MODE_HESS) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += gam * d[i];
-      }
-      if constexpr (MODE == MODE_HVP) {  // y_row = M (u_row - u_other) + dl (u_row + u_other)
-        double dw = 0.0;
-#pragma unroll
-        for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo_[c]);
-#pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo_[i]) + cd_s * d[i] * dw + dl * (us[i] + uo_[i]);
-      }
-      if constexpr (MODE == MODE_HESS) {
-#pragma unroll
-        // t = cd d d^T (6 unique products) feeds both the diagonal sum and the
-        // edge's off-diagonal block -t + (dl - ci) I
-        double cdd[N], t[T];
-#pragma unroll
-        for (int i = 0; i < N; ++i) cdd[i] = cd_s * d[i];
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int c = 0; c <= i; ++c) t[tri(i, c)] = cdd[i] * d[c];
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int c = 0; c <= i; ++c) dg[tri(i, c)] += t[tri(i, c)] + (i == c ? ci_s + dl : 0.0);
-        if (fr && fo) {
-          if (dp != 255 && pos == dp) ++pos;  // leave the diagonal's slot
-          double blk[NN];
-#pragma unroll
-          for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int c = 0; c < N; ++c) blk[i * N + c] = -t[tri(i, c)] + (i == c ? dl - ci_s : 0.0);
-          double* dst = hrow + pos * NN;
-#pragma unroll
-          for (int k = 0; k < NN; ++k) dst[k] = blk[k];
-          ++pos;
-        }
-      }
-    };
-#pragma unroll
-    for (int j = 0; j < EV_ELL_K; ++j) {
-      if (j + MAXI < EV_ELL_K) issue(j + MAXI);
-      if (j < cnt) incidence(rc[j], xo[j], uo[j], a0[j]);
-    }
-    for (int k = EV_ELL_K; k < cnt; ++k) {  // high-valence rows: the CSR tail
-      const uint64_t r64 = a.rrec[a.rinc_off[row] + k];
-      const int64_t o = (uint32_t)(r64 >> 32) & 0x7fffffffu;
-      const bool fo = !(r64 >> 63);
-      double x1[N], u1[N];
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        x1[c] = a.x[o * N + c];
-        if constexpr (MODE == MODE_HVP) u1[c] = fo ? a.w[o * N + c] : 0.0;
-        else u1[c] = 0.0;
-      }
-      const double av = a.ev_a0 ? a.ev_a0[(uint32_t)r64 & 0x7fffffffu] : 0.0;
-      incidence(r64, x1, u1, av);
-    }
-    double* vout = MODE == MODE_HVP ? a.y : a.grad;
-#pragma unroll
-    for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
-    if constexpr (MODE == MODE_HESS) {
-      if (fr && dp != 255) {
-        double* dst = hrow + dp * NN;
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-          for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
-      }
-      // blocks written: off-diagonals, plus the diagonal if the walk never passed it
-      const int len = (fr && dp != 255) ? (pos > dp + 1 ? pos : dp + 1) : pos;
-      if (len > 0) {
-        fence_proxy_async_smem();
-        row_store_bulk(a.hess + ro * NN, hrow, len * NN);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
-  }
-  if constexpr (MODE != MODE_HVP) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
-    if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
-  }
-  if constexpr (MODE == MODE_HESS) cur = nxt;
-  else break;  // one row block per CTA outside the Hessian
-  }
-  if (!finite) *a.redo = 1;
-  if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  rows_fast_body<N, MODE, PSD, BuiltinRows<EVT>>(a);
 }
 
 // Staged tile kernel, persistent and software-pipelined. Dispatched for the
@@ -1290,10 +967,12 @@ void launch_rows_mode(const Problem& p, const EvArgs& a, int hd, Mode mode, bool
 
 }  // namespace
 
-int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset) {
+namespace {
+
+void fill_ev_args(const Problem& p, const LaunchCtx& c, int64_t partial_offset, EvArgs& a) {
   const Mesh& m = *p.mesh;
   if (p.terms.size() > MAXT) throw Error(MG_ERR_UNSUPPORTED, "at most 8 terms per problem on the patch path");
-  EvArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.nterms = (int)p.terms.size();
   a.V = m.Vr;
   a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr : m.patches.order.p;
@@ -1329,6 +1008,14 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
     if (p.terms[i].dev.op == MG_OP_EV) a.ev_idx[a.nev++] = i;
     else a.vt_idx[a.nvt++] = i;
   }
+}
+
+}  // namespace
+
+int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset) {
+  const Mesh& m = *p.mesh;
+  EvArgs a;
+  fill_ev_args(p, c, partial_offset, a);
   if (a.nev && p.terms[a.ev_idx[0]].dev.type == MG_TERM_SPRING) a.ev_a0 = p.terms[a.ev_idx[0]].dev.a[0];
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
   // energy partials: one per warp of rows
@@ -1336,6 +1023,47 @@ int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.np_total = np;
   if (p.n == 3) launch_rows_mode<3>(p, a, hd, mode, c.psd, c.stream);
   else launch_rows_mode<2>(p, a, hd, mode, c.psd, c.stream);
+  return np;
+}
+
+// Traced terms with radial EV callbacks (jit_rows.cuh): the same row layout
+// and kernel body, the problem's generated policy; the attribute streams of
+// all its terms, in term order, in EvArgs::js. No exact re-run here: the
+// caller launches the traced patch module gated on the redo flag.
+bool rows_jit_supported(const Problem& p) {
+  if (!p.row_module || p.terms.empty() || p.terms.size() > (size_t)MAXT) return false;
+  if (p.n != 2 && p.n != 3) return false;
+  size_t streams = 0;
+  bool any_ev = false;
+  for (auto& t : p.terms) {
+    if (!t.jit || (t.dev.op != MG_OP_V && t.dev.op != MG_OP_EV)) return false;
+    any_ev |= t.dev.op == MG_OP_EV;
+    streams += t.jit_attrs.size();
+  }
+  return any_ev && streams <= (size_t)MAX_JS && p.mesh->E < (int64_t(1) << 31);
+}
+
+int64_t launch_rows_jit(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset) {
+  const Mesh& m = *p.mesh;
+  EvArgs a;
+  fill_ev_args(p, c, partial_offset, a);
+  int js = 0;
+  for (auto& t : p.terms)
+    for (auto* ptr : t.jit_attrs) {
+      if (js >= MAX_JS) throw Error(MG_ERR_UNSUPPORTED, "row module: too many attribute streams");
+      a.js[js++] = ptr;
+    }
+  const int64_t np = mode == MODE_HVP ? 0 : (m.Vr + 31) / 32;
+  a.np_total = np;
+  const size_t sm = mode == MODE_HESS ? (size_t)p.max_patch_hdoubles * 8 + 16 : 0;
+  if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
+  constexpr int B = EV_ROW_BLOCK;
+  static_assert(FastCfg<MODE_HESS, false>::BLOCK == B && FastCfg<MODE_HVP, false>::BLOCK == B &&
+                FastCfg<MODE_HVP, true>::BLOCK == B && FastCfg<MODE_GRAD, false>::BLOCK == B,
+                "row module launches assume one block size");
+  timing_begin(p, c.stream);
+  jit_rows_launch(p, mode, c.psd, &a, (m.Vr + B - 1) / B, B, sm, c.stream);
+  timing_end(p, c.stream);
   return np;
 }
 

@@ -1,0 +1,387 @@
+// Edge row kernel body, shared by the library's builtin radial terms
+// (edge_kernels.cu) and traced callbacks whose edge terms the tracer proved
+// radial (jit_rows.cuh, compiled at runtime with the generated functors).
+// See edge_kernels.cu for the algorithm. A policy type supplies the terms:
+//
+//   static constexpr bool kXFreeHvp;   // EV Hessian independent of x (the
+//                                      // unclamped HVP reads directions only)
+//   template <int N, int MODE> static auto vload(const EvArgs&, int g);
+//       V-term attribute loads, issued before the incidence gathers
+//   template <int N, int MODE, bool PSD> static void vterms(a, g, fr, pre, xs, us, eacc, vec, dg);
+//       the row's V terms: energy, gradient / H u into vec, Hessian into dg
+//   template <int MODE> static auto eload(const EvArgs&, uint32_t e);
+//       per-edge attribute loads of one incidence (issued with the gathers)
+//   template <int MODE, bool NEEDV, class EP, class F> static void eterms(a, ep, rr, e, one);
+//       phi, phi', phi'' of every radial EV term at r = |d|^2, handed to
+//       one(ok, phi, phi', phi'')
+#pragma once
+#include "mg_internal.cuh"
+
+namespace mg {
+namespace rows {
+
+constexpr int PT = EV_ROW_BLOCK;  // rows (threads) per CTA
+constexpr int MAXT = 8;
+constexpr int MAX_JS = 24;        // traced attribute streams of a row module (all terms)
+
+struct EvArgs {
+  int nterms;
+  int64_t V;  // owned rows (patch order)
+  const int32_t* order;      // (V) vertex of each row
+  const uint8_t* pfix;       // (V) pinned flag of each row
+  const uint32_t* rmeta;     // (V) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
+  const uint64_t* ell;       // (EV_ELL_K, V) first incidences, slot-major
+  const int32_t* rinc_off;   // (V+1)
+  const uint64_t* rrec;      // lo: edge | slot << 31, hi: other | pinned(other) << 31
+  const int64_t* prow_ro;
+  const int32_t* prow_len;
+  const uint8_t* prow_dp;
+  const int32_t* hoff;
+  const double* x;
+  const double* w;
+  double* grad;
+  double* hess;
+  double* y;
+  double* partials;
+  int* redo;  // raised by the radial kernel on a non-finite lane
+  int* exact_runs;
+  int nev, nvt;                 // compacted term lists (indices into terms)
+  int ev_idx[MAXT], vt_idx[MAXT];
+  const double* ev_a0;          // per-edge attribute of ev_idx[0] (prefetched), or null
+  // staged tiles (k_tile_ev): see Problem::tiles_ready
+  const int2* tcnt;
+  const uint32_t* tv;
+  const uint64_t* te;
+  const uint16_t* islot;
+  const uint16_t* islot8;  // (V, 8): a row's first 8 slots, one 16-byte load
+  int max_v, max_e;
+  int64_t np_total;  // energy partials the reduction reads (the exact re-run zero-fills past its own)
+  double floor;
+  TermDev terms[MAXT];
+  const double* js[MAX_JS];  // traced terms: attribute streams of the row module, terms in order
+};
+
+MG_DI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// dst[0..n) = src[0..n) (doubles), src in shared memory with the same 16-byte
+// phase as dst: 8-byte head / tail stores plus one bulk (TMA) copy of the
+// aligned middle. The caller waits for the bulk group before leaving.
+MG_DI void row_store_bulk(double* dst, const double* src, int n) {
+  int k0 = 0;
+  if (reinterpret_cast<uintptr_t>(dst) & 15) {
+    if (n > 0) dst[0] = src[0];
+    k0 = 1;
+  }
+  int m = n - k0;
+  if (m <= 0) return;
+  if (m & 1) {
+    dst[n - 1] = src[n - 1];
+    --m;
+  }
+  if (m > 0) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src + k0);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(dst + k0), "r"(sa), "r"((uint32_t)m * 8u) : "memory");
+  }
+}
+
+// 1/x to full fp64 precision without the IEEE division sequence: hardware
+// reciprocal estimate + two Newton steps (non-finite / zero inputs give
+// non-finite results, which send the call to the exact kernel)
+MG_DI double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Closed-form clamp of a radial block c_i I + c_d d d^T (r = |d|^2): the
+// transverse eigenvalue is c_i, the axial one c_i + c_d r. Already above the
+// floor -> unchanged (the reference's eigh recomposition equals the input to
+// rounding); otherwise Q max(L, f) Q^T = m_t I + (m_d - m_t) d d^T / r.
+MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
+  const double lt = ci, ld = ci + cd * r;
+  if (lt > f && ld > f) return;
+  const double mt = lt > f ? lt : f, md = ld > f ? ld : f;
+  ci = mt;
+  cd = r > 0.0 ? (md - mt) * rcp_fast(r) : 0.0;
+}
+
+// incidences per row held in registers (the rest are streamed) and the
+// occupancy target: the Hessian kernel is bounded by its shared-memory row
+// buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
+// for more resident warps
+#ifndef EV_HESS_MINB
+#define EV_HESS_MINB 1
+#endif
+#ifndef EV_FLAT_BLOCK
+#define EV_FLAT_BLOCK 64
+#endif
+// MAXI: incidences in flight; BLOCK: threads per CTA (the Hessian kernel's CTA
+// is its row-buffer group, EV_ROW_BLOCK); MINB: CTAs per SM to fit
+template <int MODE, bool PSD> struct FastCfg {
+  static constexpr int MAXI = EV_ELL_K, BLOCK = EV_ROW_BLOCK, MINB = EV_HESS_MINB;
+};
+#ifndef EV_HVP_MAXI
+#define EV_HVP_MAXI 4
+#endif
+#ifndef EV_HVP_THREADS
+#define EV_HVP_THREADS 512  // measured: 0.269 ms vs 0.288 at 640 (row-kernel spring HVP, 2048^2)
+#endif
+template <> struct FastCfg<MODE_HVP, false> {
+  static constexpr int MAXI = EV_HVP_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_THREADS / EV_FLAT_BLOCK;
+};
+template <> struct FastCfg<MODE_HVP, true> {
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 512 / EV_FLAT_BLOCK;
+};
+template <> struct FastCfg<MODE_GRAD, false> {
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
+};
+// the x-free HVP holds only directions: full occupancy (64 registers)
+template <int MODE, bool PSD, bool XFREE_HVP> struct FastMinb {
+  static constexpr int v = (MODE == MODE_HVP && !PSD && XFREE_HVP) ? 1024 / EV_FLAT_BLOCK : FastCfg<MODE, PSD>::MINB;
+};
+
+// Radial row kernel body: one thread per owned row, d = x_row - x_other
+// (radial terms are even in d, so no orientation bookkeeping). A row's first
+// MAXI incidences are fetched in two batched levels (records, then neighbour
+// x and edge attributes) so their latencies overlap.
+template <int N, int MODE, bool PSD, class Pol>
+MG_DI void rows_fast_body(const EvArgs& a) {
+  constexpr int T = TriN<N>::value, NN = N * N;
+  constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
+  constexpr int PTB = FastCfg<MODE, PSD>::BLOCK;
+  // e.g. the edge length's Hessian 2 [[I,-I],[-I,I]] does not depend on x
+  // (apps/smooth.py:27-28): its unclamped HVP reads only the direction
+  constexpr bool XFREE = MODE == MODE_HVP && !PSD && Pol::kXFreeHvp;
+  extern __shared__ __align__(16) double hbuf[];
+  // Row blocks are walked grid-stride (a persistent grid for the Hessian, one
+  // block per CTA otherwise); the level-1 streams of the thread's next row are
+  // loaded while it works on the current one.
+  struct L1 {
+    int g = 0;
+    uint32_t meta = 0;
+    int64_t ro = 0;
+    int ho = 0;
+    uint64_t rc[EV_ELL_K];
+  };
+  // level 1: static per-row streams, all indexed by the row alone
+  // (coalesced): vertex, meta word, row start / buffer offset, ELL records
+  auto load_l1 = [&](int64_t r, L1& l) {
+    if (r >= a.V) return;
+    l.g = a.order ? a.order[r] : (int)r;  // null: identity row order
+    l.meta = a.rmeta[r];
+    if constexpr (MODE == MODE_HESS) {
+      l.ro = a.prow_ro[r];
+      l.ho = a.hoff[r];
+    }
+#pragma unroll
+    for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
+  };
+  const int64_t nblk = (a.V + PTB - 1) / PTB;
+  bool finite = true;
+  L1 cur, nxt;
+  if constexpr (MODE == MODE_HESS) load_l1((int64_t)blockIdx.x * PTB + threadIdx.x, cur);
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  const int64_t row = blk * PTB + threadIdx.x;
+  if constexpr (MODE == MODE_HESS) {
+    if (blk + gridDim.x < nblk) load_l1(row + (int64_t)gridDim.x * PTB, nxt);
+  } else {
+    load_l1(row, cur);
+  }
+  double eacc = 0.0;
+  if (row < a.V) {
+    const int g = cur.g;
+    const uint32_t meta = cur.meta;
+    const int64_t ro = cur.ro;
+    const int ho = cur.ho;
+    uint64_t rc[EV_ELL_K];
+#pragma unroll
+    for (int j = 0; j < EV_ELL_K; ++j) rc[j] = cur.rc[j];
+    (void)ro;
+    // the previous row's bulk copy must have read this thread's row buffer
+    if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    // level 2: own x / w, issued before anything waits on the meta word (with
+    // the identity row order g is the row itself, so these do not wait on
+    // level 1 at all); the pinned mask is applied after the load
+    double xs[N], us[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      xs[c] = a.x[(int64_t)g * N + c];
+      if constexpr (MODE == MODE_HVP) us[c] = a.w[(int64_t)g * N + c];
+      else us[c] = 0.0;
+    }
+    const auto vpre = Pol::template vload<N, MODE>(a, g);
+    // level 3: neighbour x (w) and the edge attributes, kept MAXI incidences
+    // ahead of the compute (a rolling window over the ELL slots). Unused ELL
+    // slots hold record 0 (edge 0, vertex 0), so the loads are unconditional
+    // (no wait on the incidence count) and their values are never used.
+    using EP = decltype(Pol::template eload<MODE>(a, 0u));
+    double xo[EV_ELL_K][N], uo[EV_ELL_K][N];
+    EP ep[EV_ELL_K];
+    auto issue = [&](int j) {
+      const uint32_t hi = (uint32_t)(rc[j] >> 32);
+      const int64_t o = hi & 0x7fffffffu;
+      const bool fo = !(hi >> 31);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        xo[j][c] = !XFREE ? a.x[o * N + c] : 0.0;
+        if constexpr (MODE == MODE_HVP) {
+          const double wv = a.w[o * N + c];
+          uo[j][c] = fo ? wv : 0.0;
+        } else {
+          uo[j][c] = 0.0;
+        }
+      }
+      ep[j] = Pol::template eload<MODE>(a, (uint32_t)rc[j] & 0x7fffffffu);
+    };
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j) issue(j);
+    const bool fr = !((meta >> 8) & 1);
+    const int dp = (int)(meta >> 16) & 0xff;
+    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
+    if constexpr (MODE == MODE_HVP) {
+#pragma unroll
+      for (int c = 0; c < N; ++c) us[c] = fr ? us[c] : 0.0;
+    }
+    double vec[N], dg[T];
+#pragma unroll
+    for (int i = 0; i < N; ++i) vec[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < T; ++i) dg[i] = 0.0;
+    // V terms (their attribute loads overlapped the level-3 loads)
+    Pol::template vterms<N, MODE, PSD>(a, g, fr, vpre, xs, us, eacc, vec, dg);
+    double* hrow = hbuf + ho;
+    int pos = 0;
+    // one incidence: contributions to this row
+    auto incidence = [&](uint64_t r64, const double* xo_, const double* uo_, const EP& av) {
+      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
+      const uint32_t e = lo & 0x7fffffffu;
+      const bool first = (lo >> 31) == 0;  // the row is the edge's first vertex
+      const bool fo = !(hi >> 31);
+      double d[N], rr = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        d[c] = XFREE ? 0.0 : xs[c] - xo_[c];
+        rr = d[c] * d[c] + rr;
+      }
+      double gam = 0.0, ci_s = 0.0, cd_s = 0.0, dl = 0.0, val = 0.0;
+      auto one_term = [&](bool ok, double pv, double p1, double p2) {
+        finite &= ok;
+        val += pv;
+        gam += 2.0 * p1;
+        if constexpr (MODE != MODE_GRAD) {
+          double ci = 2.0 * p1, cd = 4.0 * p2, sh = 0.0;
+          if constexpr (PSD) {
+            if (fr && fo) {  // [[A,-A],[-A,A]]: clamp 2A, halve, shift floor/2
+              ci *= 2.0; cd *= 2.0;
+              radial_clamp_fast(ci, cd, rr, a.floor);
+              ci *= 0.5; cd *= 0.5;
+              sh = 0.5 * a.floor;
+            } else if (fr || fo) {
+              radial_clamp_fast(ci, cd, rr, a.floor);
+            }
+          }
+          ci_s += ci;
+          cd_s += cd;
+          dl += sh;
+        }
+      };
+      Pol::template eterms<MODE, MODE != MODE_HVP>(a, av, rr, e, one_term);
+      if constexpr (MODE != MODE_HVP) {
+        if (first) eacc += val;  // an edge's energy counts at its first vertex
+      }
+      if constexpr (MODE == MODE_GRAD || MODE == MODE_HESS) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += gam * d[i];
+      }
+      if constexpr (MODE == MODE_HVP) {  // y_row = M (u_row - u_other) + dl (u_row + u_other)
+        double dw = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo_[c]);
+#pragma unroll
+        for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo_[i]) + cd_s * d[i] * dw + dl * (us[i] + uo_[i]);
+      }
+      if constexpr (MODE == MODE_HESS) {
+        // t = cd d d^T (6 unique products) feeds both the diagonal sum and the
+        // edge's off-diagonal block -t + (dl - ci) I
+        double cdd[N], t[T];
+#pragma unroll
+        for (int i = 0; i < N; ++i) cdd[i] = cd_s * d[i];
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c <= i; ++c) t[tri(i, c)] = cdd[i] * d[c];
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c <= i; ++c) dg[tri(i, c)] += t[tri(i, c)] + (i == c ? ci_s + dl : 0.0);
+        if (fr && fo) {
+          if (dp != 255 && pos == dp) ++pos;  // leave the diagonal's slot
+          double blk[NN];
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int c = 0; c < N; ++c) blk[i * N + c] = -t[tri(i, c)] + (i == c ? dl - ci_s : 0.0);
+          double* dst = hrow + pos * NN;
+#pragma unroll
+          for (int k = 0; k < NN; ++k) dst[k] = blk[k];
+          ++pos;
+        }
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < EV_ELL_K; ++j) {
+      if (j + MAXI < EV_ELL_K) issue(j + MAXI);
+      if (j < cnt) incidence(rc[j], xo[j], uo[j], ep[j]);
+    }
+    for (int k = EV_ELL_K; k < cnt; ++k) {  // high-valence rows: the CSR tail
+      const uint64_t r64 = a.rrec[a.rinc_off[row] + k];
+      const int64_t o = (uint32_t)(r64 >> 32) & 0x7fffffffu;
+      const bool fo = !(r64 >> 63);
+      double x1[N], u1[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        x1[c] = a.x[o * N + c];
+        if constexpr (MODE == MODE_HVP) u1[c] = fo ? a.w[o * N + c] : 0.0;
+        else u1[c] = 0.0;
+      }
+      const EP av = Pol::template eload<MODE>(a, (uint32_t)r64 & 0x7fffffffu);
+      incidence(r64, x1, u1, av);
+    }
+    double* vout = MODE == MODE_HVP ? a.y : a.grad;
+#pragma unroll
+    for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+    if constexpr (MODE == MODE_HESS) {
+      if (fr && dp != 255) {
+        double* dst = hrow + dp * NN;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
+      }
+      // blocks written: off-diagonals, plus the diagonal if the walk never passed it
+      const int len = (fr && dp != 255) ? (pos > dp + 1 ? pos : dp + 1) : pos;
+      if (len > 0) {
+        fence_proxy_async_smem();
+        row_store_bulk(a.hess + ro * NN, hrow, len * NN);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  }
+  if constexpr (MODE != MODE_HVP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
+    if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
+  }
+  if constexpr (MODE == MODE_HESS) cur = nxt;
+  else break;  // one row block per CTA outside the Hessian
+  }
+  if (!finite) *a.redo = 1;
+  if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+}  // namespace rows
+}  // namespace mg

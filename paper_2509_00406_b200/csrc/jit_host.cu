@@ -124,7 +124,7 @@ void jit_patch_unload(Problem& p) {
 }
 
 void jit_patch_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t np, int nvp_max, int blocks_max,
-                      size_t smem, cudaStream_t s) {
+                      size_t smem, cudaStream_t s, int64_t grid) {
   Driver& d = driver();
   const int k = mode == MODE_GRAD ? 0 : mode == MODE_HESS ? (psd ? 2 : 1) : (psd ? 4 : 3);
   if (mode != MODE_GRAD && mode != MODE_HESS && mode != MODE_HVP)
@@ -132,9 +132,41 @@ void jit_patch_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t
   if (d.setattr) drv_check(d.setattr(p.patch_fn[k], 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */,
                                      (int)smem), "cuFuncSetAttribute");
   void* params[3] = {args, &nvp_max, &blocks_max};
-  if (np > 0)
-    drv_check(d.launch(p.patch_fn[k], (unsigned)np, 1, 1, 128, 1, 1, (unsigned)smem, s, params, nullptr),
+  if (grid < 0 || grid > np) grid = np;
+  if (grid > 0)
+    drv_check(d.launch(p.patch_fn[k], (unsigned)grid, 1, 1, 128, 1, 1, (unsigned)smem, s, params, nullptr),
               "cuLaunchKernel (patch module)");
+}
+
+const char* kRowNames[5] = {"mg_rows_grad", "mg_rows_hess", "mg_rows_hess_psd", "mg_rows_hvp", "mg_rows_hvp_psd"};
+
+void jit_rows_load(Problem& p, const void* image) {
+  MG_CUDA(cudaFree(nullptr));
+  Driver& d = driver();
+  jit_rows_unload(p);
+  drv_check(d.load(&p.row_module, image), "cuModuleLoadData (row module)");
+  for (int i = 0; i < 5; ++i) drv_check(d.getfn(&p.row_fn[i], p.row_module, kRowNames[i]), kRowNames[i]);
+}
+
+void jit_rows_unload(Problem& p) {
+  if (p.row_module && driver().unload) driver().unload(p.row_module);
+  p.row_module = nullptr;
+  for (auto& f : p.row_fn) f = nullptr;
+  p.ev_jit = false;
+}
+
+void jit_rows_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t grid, int block, size_t smem,
+                     cudaStream_t s) {
+  Driver& d = driver();
+  if (mode != MODE_GRAD && mode != MODE_HESS && mode != MODE_HVP)
+    throw Error(MG_ERR_UNSUPPORTED, "traced row kernels assemble grad / Hessian / HVP only");
+  const int k = mode == MODE_GRAD ? 0 : mode == MODE_HESS ? (psd ? 2 : 1) : (psd ? 4 : 3);
+  if (d.setattr) drv_check(d.setattr(p.row_fn[k], 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */,
+                                     (int)smem), "cuFuncSetAttribute");
+  void* params[1] = {args};
+  if (grid > 0)
+    drv_check(d.launch(p.row_fn[k], (unsigned)grid, 1, 1, (unsigned)block, 1, 1, (unsigned)smem, s, params, nullptr),
+              "cuLaunchKernel (row module)");
 }
 
 }  // namespace mg

@@ -213,6 +213,12 @@ struct Problem {
   void* patch_fn[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   mutable DBuf<const double*> jattr;
   mutable bool jattr_dirty = true;
+  // traced terms on the edge row kernel (jit_rows.cuh): every EV callback
+  // radial (proved by the tracer), V terms at the row; the patch module is
+  // the exact re-run. ev_jit: its row layout is built.
+  void* row_module = nullptr;
+  void* row_fn[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool ev_jit = false;
 };
 
 // element vertex ids of an op (nullptr for V: the element is the vertex)
@@ -233,7 +239,7 @@ void mesh_build(Mesh& m, const int64_t* faces_d, const int64_t* edges_d, int64_t
                 const double* pos_d, cudaStream_t s);
 void build_pattern(Problem& p, cudaStream_t s);
 void build_patch_layout(Problem& p, cudaStream_t s);
-void build_rows_ev(Problem& p, cudaStream_t s);
+void build_rows_ev(Problem& p, cudaStream_t s, bool tiles = true);
 void build_rows_fv(Problem& p, cudaStream_t s);
 void mesh_patches(Mesh& m, cudaStream_t s);
 void mesh_set_owned(Mesh& m, const uint8_t* owned_d, cudaStream_t s);
@@ -245,6 +251,8 @@ void jit_load(Term& t, const void* image);
 void jit_unload(Term& t);
 void jit_patch_load(Problem& p, const void* image);
 void jit_patch_unload(Problem& p);
+void jit_rows_load(Problem& p, const void* image);
+void jit_rows_unload(Problem& p);
 
 
 // elem_kernels.cu (element-parallel, atomic accumulation)
@@ -252,7 +260,10 @@ enum Mode { MODE_ENERGY = 0, MODE_GRAD = 1, MODE_HESS = 2, MODE_HVP = 3 };
 // launch the problem's traced patch kernel for a mode (args: the filled
 // patch::PatchArgs, passed as void* to keep this header light)
 void jit_patch_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t np, int nvp_max,
-                      int blocks_max, size_t smem, cudaStream_t s);
+                      int blocks_max, size_t smem, cudaStream_t s, int64_t grid = -1);
+// launch the problem's traced row kernel (args: a filled rows::EvArgs)
+void jit_rows_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t grid, int block, size_t smem,
+                     cudaStream_t s);
 
 struct LaunchCtx {
   const double* x;
@@ -276,6 +287,9 @@ int64_t elem_partials_needed(const Term& t);
 int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 // edge_kernels.cu (two-point edge fast path of the patch-owner assembly)
 int64_t launch_patch_ev(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
+// ... with the problem's traced row module (returns the energy partials written)
+int64_t launch_rows_jit(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
+bool rows_jit_supported(const Problem& p);
 // face_kernels.cu (face row kernel)
 int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t partial_offset);
 // timing hooks around the main kernel (no-ops unless p.timing)

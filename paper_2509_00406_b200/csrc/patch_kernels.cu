@@ -141,8 +141,18 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
   if (p.ev_fast) return launch_patch_ev(p, mode, c, partial_offset);
   int64_t n_fast = 0;
   // face row kernels: Dirichlet in every mode; sphere for gradient / HVP
-  const bool fast = p.fv_fast && (p.terms[0].dev.type != MG_TERM_SPHERE || mode == MODE_GRAD || mode == MODE_HVP);
+  bool fast = p.fv_fast && (p.terms[0].dev.type != MG_TERM_SPHERE || mode == MODE_GRAD || mode == MODE_HVP);
   if (fast) n_fast = launch_patch_fv(p, mode, c, partial_offset);
+  // traced terms with radial edge callbacks: the generated row kernel
+  if (p.ev_jit && p.patch_module) {
+    n_fast = launch_rows_jit(p, mode, c, partial_offset);
+    fast = true;
+  }
+  // the exact re-run writes one partial per patch; without it the partials
+  // past the fast kernel's must read as zero
+  if (fast && mode != MODE_HVP && m.patches.num > n_fast)
+    MG_CUDA(cudaMemsetAsync(c.partials + partial_offset + n_fast, 0, sizeof(double) * (m.patches.num - n_fast),
+                            c.stream));
   PatchArgs a;
   a.R = m.patches.R;
   a.nterms = (int)p.terms.size();
@@ -187,10 +197,18 @@ int64_t launch_patch(const Problem& p, Mode mode, const LaunchCtx& c, int64_t pa
     for (int i = 0; i < a.nterms; ++i) a.terms[i] = p.terms[i].dev;
     const size_t sm = smem_bytes(p.n, mode, a.R, nvp, nb);
     if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "patch does not fit in shared memory");
-    timing_begin(p, c.stream);
-    jit_patch_launch(p, mode, c.psd, &a, np, nvp, nb, sm, c.stream);
-    timing_end(p, c.stream);
-    return mode == MODE_HVP ? 0 : np;
+    if (!fast) timing_begin(p, c.stream);
+    int64_t grid = np;
+    if (a.redo) {  // exact re-run: a small persistent grid that exits unless the flag is raised
+      int dev = 0, sms = 148;
+      MG_CUDA(cudaGetDevice(&dev));
+      MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      grid = np < (int64_t)sms * 4 ? np : (int64_t)sms * 4;
+    }
+    jit_patch_launch(p, mode, c.psd, &a, np, nvp, nb, sm, c.stream, grid);
+    if (!fast) timing_end(p, c.stream);
+    if (mode == MODE_HVP) return 0;
+    return np > n_fast ? np : n_fast;
   }
   unsigned used = 0;
   for (int i = 0; i < a.nterms; ++i) {

@@ -822,7 +822,7 @@ void build_tiles_ev(Problem& p, cudaStream_t s) {
   p.tiles_ready = fits;
 }
 
-void build_rows_ev(Problem& p, cudaStream_t s) {
+void build_rows_ev(Problem& p, cudaStream_t s, bool tiles) {
   Mesh& m = *p.mesh;
   PatchSet& ps = m.patches;
   const int64_t V = m.V, Vr = m.Vr, E = m.E;
@@ -885,7 +885,7 @@ void build_rows_ev(Problem& p, cudaStream_t s) {
   }
   MG_CUDA(cudaStreamSynchronize(s));
   p.recomputed_elements = 0;
-  build_tiles_ev(p, s);
+  if (tiles) build_tiles_ev(p, s);
   p.ev_fast = true;
   p.layout_ready = true;
 }
@@ -970,6 +970,7 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
   const int64_t V = m.V, Vr = m.Vr, np = ps.num;  // Vr: rows in patch order
   const int R = ps.R;
   p.layout_ready = false;
+  p.ev_jit = false;
   if (V == 0 || np == 0) return;
   p.ev_fast = false;
   {
@@ -1179,6 +1180,11 @@ void build_patch_layout(Problem& p, cudaStream_t s) {
     bool fv = (t0 == MG_TERM_SYM_DIRICHLET || t0 == MG_TERM_SPHERE) && p.n == 2 && m.F < (int64_t(1) << 30) &&
               m.F > 0;
     if (fv) build_rows_fv(p, s);
+  }
+  if (p.patch_module && rows_jit_supported(p)) {  // traced radial edge terms: the row layout too
+    build_rows_ev(p, s, false);
+    p.ev_fast = false;
+    p.ev_jit = true;
   }
   p.layout_ready = true;
 }

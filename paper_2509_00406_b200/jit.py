@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import re
 import subprocess
 from pathlib import Path
 
@@ -41,15 +42,17 @@ class _Graph:
     def __init__(self, num_elements):
         self.M = num_elements
         self.lines = []
+        self.ops = []  # (name, kind, operand expressions) per line, for structure analysis
         self.attrs = []  # (M,) float64 arrays
         self._attr_ids = {}
         self._pins = []  # keep operand objects alive so their ids stay unique
         self.count = 0
 
-    def new(self, expr):
+    def new(self, expr, kind="?", args=()):
         name = f"t{self.count}"
         self.count += 1
         self.lines.append(f"auto {name} = {expr};")
+        self.ops.append((name, kind, tuple(args)))
         return Sym(self, name)
 
     def operand(self, v):
@@ -99,38 +102,38 @@ class Sym:
         self.g = g
         self.name = name
 
-    def _bin(self, other, fmt, reflect=False):
+    def _bin(self, other, fmt, kind, reflect=False):
         a, b = self.g.operand(self), self.g.operand(other)
         if reflect:
             a, b = b, a
-        return self.g.new(fmt.format(a=a, b=b))
+        return self.g.new(fmt.format(a=a, b=b), kind, (a, b))
 
     def __add__(self, o):
-        return self._bin(o, "{a} + {b}")
+        return self._bin(o, "{a} + {b}", "add")
 
     def __radd__(self, o):
-        return self._bin(o, "{a} + {b}", reflect=True)
+        return self._bin(o, "{a} + {b}", "add", reflect=True)
 
     def __sub__(self, o):
-        return self._bin(o, "{a} - {b}")
+        return self._bin(o, "{a} - {b}", "sub")
 
     def __rsub__(self, o):
-        return self._bin(o, "{a} - {b}", reflect=True)
+        return self._bin(o, "{a} - {b}", "sub", reflect=True)
 
     def __mul__(self, o):
-        return self._bin(o, "{a} * {b}")
+        return self._bin(o, "{a} * {b}", "mul")
 
     def __rmul__(self, o):
-        return self._bin(o, "{a} * {b}", reflect=True)
+        return self._bin(o, "{a} * {b}", "mul", reflect=True)
 
     def __truediv__(self, o):
-        return self._bin(o, "{a} / {b}")
+        return self._bin(o, "{a} / {b}", "div")
 
     def __rtruediv__(self, o):
-        return self._bin(o, "{a} / {b}", reflect=True)
+        return self._bin(o, "{a} / {b}", "div", reflect=True)
 
     def __neg__(self):
-        return self.g.new(f"-{self.name}")
+        return self.g.new(f"-{self.name}", "neg", (self.name,))
 
     def __pos__(self):
         return self
@@ -140,32 +143,32 @@ class Sym:
             raise TypeError("only integer exponents are supported")  # active.py:225-227
         if p == 1:
             return self
-        return self.g.new(f"mg::powi({self.name}, {int(p)})")
+        return self.g.new(f"mg::powi({self.name}, {int(p)})", "powi", (self.name,))
 
     def __abs__(self):
-        return self.g.new(f"mg::abs_({self.name})")
+        return self.g.new(f"mg::abs_({self.name})", "abs", (self.name,))
 
     # elementary-function hooks (paper_2509_00406_b200.active dispatch)
     def _mg_sqrt(self):
-        return self.g.new(f"sqrt({self.name})")
+        return self.g.new(f"sqrt({self.name})", "sqrt", (self.name,))
 
     def _mg_log(self):
-        return self.g.new(f"log({self.name})")
+        return self.g.new(f"log({self.name})", "log", (self.name,))
 
     def _mg_exp(self):
-        return self.g.new(f"exp({self.name})")
+        return self.g.new(f"exp({self.name})", "exp", (self.name,))
 
     def _mg_sin(self):
-        return self.g.new(f"sin({self.name})")
+        return self.g.new(f"sin({self.name})", "sin", (self.name,))
 
     def _mg_cos(self):
-        return self.g.new(f"cos({self.name})")
+        return self.g.new(f"cos({self.name})", "cos", (self.name,))
 
     def _mg_abs(self):
         return self.__abs__()
 
     def _mg_positive_guard(self):
-        return self.g.new(f"positive_guard({self.name})")
+        return self.g.new(f"positive_guard({self.name})", "guard", (self.name,))
 
     def __bool__(self):
         raise TypeError("traced callbacks cannot branch on input values")
@@ -196,9 +199,10 @@ class _Vars:
 class TracedTerm:
     """Result of tracing: C++ body, attribute streams, shape."""
 
-    def __init__(self, op: str, P: int, n: int, body: list, ret: str, attrs: list):
+    def __init__(self, op: str, P: int, n: int, body: list, ret: str, attrs: list, ops: list | None = None):
         self.op, self.P, self.n = op, P, n
         self.body, self.ret, self.attrs = body, ret, attrs
+        self.ops = ops or []
 
     def functor(self, name: str = "Traced") -> str:
         """The recorded SSA as a C++ functor over the engine's duals."""
@@ -266,6 +270,165 @@ MG_PATCH_JIT_INSTANTIATE(Policy, {n})
 """
 
 
+_XIN = re.compile(r"^X\[(\d+)\]\[(\d+)\]$")
+_ATTR = re.compile(r"A\[(\d+)\]\[e\]")
+
+
+def radial_form(tt: TracedTerm):
+    """Prove that an EV callback depends on its vertex positions only through
+    r = |x_0 - x_1|^2, from the recorded operations: every use of an input
+    is a component difference d_c = x_0[c] - x_1[c] (either orientation),
+    those are only squared (d_c * d_c, equal signs) and the squares only
+    summed until one symbol r holds each component's square exactly once
+    (ActiveVec.norm2 / dot, active.py); every later operation reaches the
+    inputs only through r. Returns (r name, [phi lines]) — the operations
+    after r, in order, with r bound to the input R — or None.
+    (The reference's K = 2n duals of such a term give gradient 2 phi' d and
+    Hessian blocks +-(2 phi' I + 4 phi'' d d^T): jit_rows.cuh.)"""
+    if tt.op != "EV" or tt.P != 2 or not tt.ops or len(tt.ops) != len(tt.body):
+        return None
+    n = tt.n
+    full = tuple(range(n))
+    xdep, dsym, sq, post = set(), {}, {}, set()
+    r_name = None
+    for name, kind, args in tt.ops:
+        xin = [_XIN.match(o) for o in args]
+        dep = [o for o, m in zip(args, xin) if m or o in xdep]
+        if not dep:
+            continue
+        xdep.add(name)
+        if any(xin):
+            if kind != "sub" or len(args) != 2 or not all(xin):
+                return None
+            (q0, c0), (q1, c1) = [(int(m.group(1)), int(m.group(2))) for m in xin]
+            if c0 != c1 or {q0, q1} != {0, 1}:
+                return None
+            dsym[name] = (c0, 1 if q0 == 0 else -1)
+            continue
+        if kind == "mul" and len(args) == 2 and args[0] in dsym and args[1] in dsym:
+            (ca, sa), (cb, sb) = dsym[args[0]], dsym[args[1]]
+            if ca != cb or sa != sb:
+                return None
+            sq[name] = (ca,)
+            continue
+        if kind == "add" and len(args) == 2 and args[0] in sq and args[1] in sq:
+            comps = tuple(sorted(sq[args[0]] + sq[args[1]]))
+            if len(set(comps)) != len(comps):
+                return None
+            sq[name] = comps
+            continue
+        for o in dep:  # beyond the quadratic form: inputs only through r
+            if o in post:
+                continue
+            if sq.get(o) == full and (r_name is None or r_name == o):
+                r_name = o
+                continue
+            return None
+        post.add(name)
+    ret = tt.ret
+    if r_name is None:
+        if sq.get(ret) != full:  # e.g. the energy |d|^2 itself
+            return None
+        r_name = ret
+    elif ret not in post and ret != r_name:
+        return None
+    lines = [f"auto {r_name} = R;"] + [ln for (nm, _, _), ln in zip(tt.ops, tt.body) if nm in post]
+    return r_name, lines
+
+
+def _preloaded(text: str) -> str:
+    """Attribute-stream reads A[k][e] -> av[k] (values loaded ahead, jit_rows.cuh)."""
+    return _ATTR.sub(r"av[\1]", text)
+
+
+def rows_source(terms: list, n: int) -> str | None:
+    """One module for a problem's traced terms on the edge row kernel
+    (csrc/jit_rows.cuh), or None unless every term is a V term or an EV term
+    radial_form proves radial (and at least one is EV). Attribute streams of
+    all terms, in term order, are EvArgs::js; each term's are preloaded into
+    av (V terms: per row; EV terms: per incidence, with the gathers)."""
+    if not terms or any(t.op not in ("V", "EV") for t in terms) or not any(t.op == "EV" for t in terms):
+        return None
+    funcs, vcalls, ecalls, vloads, eloads = [], [], [], [], []
+    js = nv = ne = 0
+    for i, t in enumerate(terms):
+        k = len(t.attrs)
+        ret = _preloaded(t.ret)
+        if t.op == "V":
+            body = "\n      ".join(_preloaded(ln) for ln in t.body)
+            funcs.append(f"""struct V{i} {{
+  template <int N, class S>
+  MG_DI auto operator()(const double* av, const mg::Vec<S, N>* X) const {{
+      using namespace mg;
+      (void)av;
+      {body}
+      return {ret};
+  }}
+}};""")
+            vloads += [f"p.v[{nv + j}] = a.js[{js + j}][g];" for j in range(k)]
+            vcalls.append(f"mg::rows::jit_vterm<N, MODE, PSD>(V{i}{{}}, p.v + {nv}, fr, xs, us, a.floor, eacc, vec, dg);")
+            nv += k
+        else:
+            rf = radial_form(t)
+            if rf is None:
+                return None
+            body = "\n      ".join(_preloaded(ln) for ln in rf[1])
+            funcs.append(f"""struct E{i} {{
+  template <class S>
+  MG_DI auto operator()(const double* av, const S& R) const {{
+      using namespace mg;
+      (void)av;
+      {body}
+      return {ret};
+  }}
+}};""")
+            eloads += [f"p.v[{ne + j}] = a.js[{js + j}][e];" for j in range(k)]
+            ecalls.append(f"mg::rows::jit_radial<MODE, NEEDV>(E{i}{{}}, p.v + {ne}, rr, one);")
+            ne += k
+        js += k
+    if js > 24:  # rows::MAX_JS
+        return None
+    j = "\n    "
+    return f"""// generated by paper_2509_00406_b200/jit.py — a problem's traced terms on the edge row kernel
+#include "jit_rows.cuh"
+
+namespace {{
+{chr(10).join(funcs)}
+
+struct Pol {{
+  static constexpr bool kXFreeHvp = false;
+  template <int N, int MODE>
+  MG_DI static mg::rows::JPre<{nv}> vload(const mg::rows::EvArgs& a, int g) {{
+    mg::rows::JPre<{nv}> p;
+    (void)a; (void)g;
+    {j.join(vloads)}
+    return p;
+  }}
+  template <int N, int MODE, bool PSD>
+  MG_DI static void vterms(const mg::rows::EvArgs& a, int g, bool fr, const mg::rows::JPre<{nv}>& p, const double* xs,
+                           const double* us, double& eacc, double* vec, double* dg) {{
+    (void)a; (void)g; (void)fr; (void)p; (void)xs; (void)us; (void)eacc; (void)vec; (void)dg;
+    {j.join(vcalls)}
+  }}
+  template <int MODE>
+  MG_DI static mg::rows::JPre<{ne}> eload(const mg::rows::EvArgs& a, uint32_t e) {{
+    mg::rows::JPre<{ne}> p;
+    (void)a; (void)e;
+    {j.join(eloads)}
+    return p;
+  }}
+  template <int MODE, bool NEEDV, class F>
+  MG_DI static void eterms(const mg::rows::EvArgs& a, const mg::rows::JPre<{ne}>& p, double rr, uint32_t e, F&& one) {{
+    (void)a; (void)e;
+    {j.join(ecalls)}
+  }}
+}};
+}}  // namespace
+
+MG_ROWS_JIT_INSTANTIATE(Pol, {n})
+"""
+
+
 def trace_callback(fn, op: str, n: int, num_elements: int, sel=None, index=None) -> TracedTerm:
     """Run `fn(handle, nbrs, x)` once on symbolic inputs (ref problem.py:440-452).
     sel: (M, P) vertex ids of the elements (EV / FV / VV), so that a vertex
@@ -296,8 +459,8 @@ def trace_callback(fn, op: str, n: int, num_elements: int, sel=None, index=None)
     if isinstance(out, Sym):
         ret = out.name
     else:
-        ret = g.operand(out) if np.ndim(out) == 0 or np.size(out) == 1 else g.new(g.operand(out)).name
-    return TracedTerm(op, P, n, g.lines, ret, g.attrs)
+        ret = g.operand(out) if np.ndim(out) == 0 or np.size(out) == 1 else g.new(g.operand(out), "copy").name
+    return TracedTerm(op, P, n, g.lines, ret, g.attrs, g.ops)
 
 
 _NVCC_FLAGS = ["-cubin", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "--expt-relaxed-constexpr"]
@@ -331,6 +494,12 @@ def compile_term(tt: TracedTerm) -> bytes:
 def compile_patch(terms: list, n: int) -> bytes:
     """The patch-path module of a problem's traced terms (patch_source)."""
     return compile_source(patch_source(terms, n))
+
+
+def compile_rows(terms: list, n: int) -> bytes | None:
+    """The row-kernel module of a problem's traced terms (rows_source), or None."""
+    src = rows_source(terms, n)
+    return None if src is None else compile_source(src)
 
 
 def compile_source(src: str) -> bytes:

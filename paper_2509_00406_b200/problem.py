@@ -234,6 +234,7 @@ class Problem:
         self._pattern_ready = False
         self._patch_checked = False
         self.patch_module = False  # traced terms run through a generated patch module
+        self.row_module = False  # ... and, radial edge terms, through a generated row module
         self.stats = {
             "eval_terms_calls": 0, "eval_terms_ms": 0.0,
             "energy_only_calls": 0, "energy_only_ms": 0.0,
@@ -255,7 +256,7 @@ class Problem:
         a builtin term from `paper_2509_00406_b200.terms`."""
         if SOURCE_KIND[op] is not kind:
             raise ValueError(f"{op.name} iterates over {SOURCE_KIND[op].value} elements, not {kind.value}")
-        self._patch_checked = self.patch_module = False  # the library drops a generated patch module on add
+        self._patch_checked = self.patch_module = self.row_module = False  # the library drops a generated patch module on add
         if op not in _TERM_OPS:
             raise ValueError(f"{op.name} does not resolve to vertex variables; terms support FV, EV, VV, V")
         if not isinstance(fn, BuiltinTerm):
@@ -277,7 +278,7 @@ class Problem:
         rec.tid = tid.value
         self._terms.append(rec)
         self._pattern_ready = False
-        self._patch_checked = self.patch_module = False
+        self._patch_checked = self.patch_module = self.row_module = False
         return len(self._terms) - 1
 
     def _num_elements(self, op: Op) -> int:
@@ -310,7 +311,7 @@ class Problem:
         rec.tid = tid.value
         self._terms.append(rec)
         self._pattern_ready = False
-        self._patch_checked = self.patch_module = False
+        self._patch_checked = self.patch_module = self.row_module = False
         return len(self._terms) - 1
 
     def _one_rings(self):
@@ -401,6 +402,14 @@ class Problem:
         buf = ctypes.create_string_buffer(image, len(image))
         _lib.check(self._lib.mg_problem_set_patch_module(self._h, buf))
         self.patch_module = True
+        # every EV callback radial (proved on the trace), the rest V terms: the
+        # edge row kernel, with the patch module as its exact re-run
+        if os.environ.get("MG_JIT_ROWS", "1") != "0":
+            rimage = jit.compile_rows([r.traced for r in recs], self.n)
+            if rimage is not None:
+                rbuf = ctypes.create_string_buffer(rimage, len(rimage))
+                _lib.check(self._lib.mg_problem_set_row_module(self._h, rbuf))
+                self.row_module = True
 
     def _sync_attrs(self):
         if self.live_host_attrs:

@@ -27,14 +27,20 @@ def traced_problem(d):
     return p
 
 
-@pytest.mark.parametrize("path", ["element", "patch"])
+@pytest.mark.parametrize("path", ["element", "patch", "rows"])
 @pytest.mark.parametrize("name", CASES)
 def test_traced_callbacks_match_reference(name, path, monkeypatch):
-    """Both engine paths for traced terms: element-parallel kernels (one
-    module per term, fixed-order gather) and the problem's generated patch
-    module (jit_patch.cuh; forced here at golden sizes by MG_JIT_PATCH_MIN=0)."""
-    monkeypatch.setenv("MG_JIT_PATCH_MIN", "0" if path == "patch" else str(1 << 62))
+    """The three engine paths for traced terms: element-parallel kernels (one
+    module per term, fixed-order gather), the problem's generated patch
+    module (jit_patch.cuh) and, when the tracer proves every edge callback
+    radial, the generated edge row module (jit_rows.cuh, the patch module as
+    its exact re-run); the last two forced here at golden sizes by
+    MG_JIT_PATCH_MIN=0."""
+    monkeypatch.setenv("MG_JIT_PATCH_MIN", "0" if path != "element" else str(1 << 62))
+    monkeypatch.setenv("MG_JIT_ROWS", "1" if path == "rows" else "0")
     d = load(name)
+    if path == "rows" and not {op for op, _ in build_terms(d)} <= {"V", "EV"}:
+        pytest.skip("face terms: no edge row module")
     p = traced_problem(d)
     assert all(r.traced is not None for r in p._terms)
     if p.with_hessian:
@@ -43,7 +49,9 @@ def test_traced_callbacks_match_reference(name, path, monkeypatch):
         assert np.array_equal(h.col_indices, d["col_indices"])
     else:
         p.eval_terms()
-    assert p.patch_module == (path == "patch")
+    assert p.patch_module == (path != "element")
+    if path == "rows":
+        assert p.row_module, "the tracer should prove these edge callbacks radial"
     for s in states(d):
         x = d[f"s{s}_x"]
         p.x = x

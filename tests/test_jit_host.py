@@ -88,3 +88,51 @@ def test_vv_trace_uses_center_and_ring_slots():
     assert tt.attrs and all(np.array_equal(a, w[ids]) for a in tt.attrs)
     with pytest.raises(ValueError, match="neighbourhoods"):
         jit.trace_callback(ring, "VV", 3, 2, None)
+
+
+def _ev(fn, n=3, M=4):
+    return jit.trace_callback(fn, "EV", n, M, sel=np.zeros((M, 2), np.int64))
+
+
+def test_radial_form_proves_spring_and_edge_length():
+    """radial_form finds r = |x_0 - x_1|^2 in the trace and returns the
+    operations after it (the row module's phi(r))."""
+    rf = jit.radial_form(_ev(spring(np.linspace(1.0, 2.0, 4), 0.5)))
+    assert rf is not None
+    r, lines = rf
+    assert lines[0] == f"auto {r} = R;" and not any("X[" in ln for ln in lines)
+    rf = jit.radial_form(_ev(lambda e, v, x: (x[v[1]] - x[v[0]]).norm2(), n=2))  # the energy is r itself
+    assert rf is not None and len(rf[1]) == 1
+    rf = jit.radial_form(_ev(lambda e, v, x: sqrt((x[v[0]] - x[v[1]]).dot(x[v[0]] - x[v[1]])) * 2.0))
+    assert rf is not None  # dot(d, d) of two equal differences, then sqrt
+
+
+@pytest.mark.parametrize("fn", [
+    lambda e, v, x: (x[v[0]] - x[v[1]])[0] * (x[v[0]] - x[v[1]])[0],        # one component only
+    lambda e, v, x: (x[v[0]] - x[v[1]]).norm2() + x[v[0]][0],                # a direct use of x
+    lambda e, v, x: (x[v[0]] - x[v[1]]).dot(x[v[1]] - x[v[0]]),              # -|d|^2: mixed signs
+    lambda e, v, x: (x[v[0]] - x[v[1]]).norm2() * (x[v[0]] - x[v[1]])[1],    # d beyond the norm
+    lambda e, v, x: (x[v[0]] - x[v[1]]).norm2() + (x[v[0]] - x[v[1]]).norm2(),  # two r symbols
+    lambda e, v, x: (x[v[0]] + x[v[1]]).norm2(),                              # not a difference
+])
+def test_radial_form_rejects_non_radial(fn):
+    assert jit.radial_form(_ev(fn)) is None
+
+
+def test_rows_source_needs_every_edge_term_radial():
+    rad = _ev(spring(np.linspace(1.0, 2.0, 4), 0.5))
+    lin = _ev(lambda e, v, x: (x[v[0]] - x[v[1]])[0] * 1.0)
+    vt = jit.trace_callback(lambda h, nb, x: 0.5 * x[h].norm2(), "V", 3, 5)
+    src = jit.rows_source([vt, rad], 3)
+    assert src is not None and "MG_ROWS_JIT_INSTANTIATE(Pol, 3)" in src and "A[" not in src
+    assert jit.rows_source([vt, rad, lin], 3) is None
+    assert jit.rows_source([vt], 3) is None  # no edge term: nothing for the edge row kernel
+
+
+def test_generated_row_module_compiles():
+    import shutil
+    if shutil.which("nvcc") is None:
+        pytest.skip("nvcc not available")
+    rad = _ev(spring(np.linspace(1.0, 2.0, 4), 0.5))
+    vt = jit.trace_callback(lambda h, nb, x: 0.5 * x[h].norm2(), "V", 3, 5)
+    assert len(jit.compile_rows([vt, rad], 3)) > 1000
