@@ -102,6 +102,8 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
         )
     lib = ctypes.CDLL(str(p))
     for name, res, args in SIGNATURES:
+        if path is not None and os.environ.get("MG_LIB") and not hasattr(lib, name):
+            continue  # an A/B build of an older revision (tools/ab_*.sh) may lack newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -396,6 +396,7 @@ MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const dou
 template <int EVT>
 struct BuiltinRows {
   static constexpr bool kXFreeHvp = EVT == MG_TERM_EDGE_LENGTH;
+  static constexpr bool kVertexOnly = EVT == MG_TERM_EDGE_LENGTH;
   template <int N, int MODE>
   MG_DI static VPreload<N> vload(const EvArgs& a, int g) { return vterms_load<N, MODE>(a, g); }
   template <int N, int MODE, bool PSD>
@@ -875,6 +876,20 @@ bool persistent_enabled() {
   return on;
 }
 
+// grid of a gradient / HVP row kernel: one row block per CTA, or with
+// EV_FLAT_PERSIST a persistent grid of resident CTAs
+template <class K>
+int64_t flat_grid(K kern, int64_t V, int block) {
+  const int64_t nb = (V + block - 1) / block;
+  if (!EV_FLAT_PERSIST) return nb;
+  int dev = 0, sms = 148, per_sm = 1;
+  MG_CUDA(cudaGetDevice(&dev));
+  MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, 0));
+  const int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  return g < nb ? g : nb;
+}
+
 template <int N, int MODE, bool PSD, int EVT>
 void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
@@ -910,7 +925,7 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
       timing_end(p, st);
     } else {
       constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
-      fast<<<(unsigned)((a.V + FB - 1) / FB), FB, sm, st>>>(a);
+      fast<<<(unsigned)flat_grid(fast, a.V, FB), FB, sm, st>>>(a);
       MG_LAUNCH_CHECK();
       timing_end(p, st);
     }
@@ -919,8 +934,8 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
     // threads walk their rows with the next row's level-1 streams in flight)
     constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
     const int64_t nfb = (a.V + FB - 1) / FB;
-    int64_t grid = nfb;
-    if (persistent_enabled()) {
+    int64_t grid = MODE == MODE_HESS ? nfb : flat_grid(fast, a.V, FB);
+    if (MODE == MODE_HESS && persistent_enabled()) {
       int dev = 0, sms = 148, per_sm = 1;
       MG_CUDA(cudaGetDevice(&dev));
       MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -979,6 +994,7 @@ void fill_ev_args(const Problem& p, const LaunchCtx& c, int64_t partial_offset, 
   a.pfix = p.pfix.p;
   a.rmeta = p.rmeta.p;
   a.ell = p.ell.p;
+  a.ell32 = p.ell32_ok ? p.ell32.p : nullptr;
   a.rinc_off = p.rinc_off.p;
   a.rrec = p.rrec.p;
   a.prow_ro = p.prow_ro.p;
@@ -1057,10 +1073,9 @@ int64_t launch_rows_jit(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.np_total = np;
   const size_t sm = mode == MODE_HESS ? (size_t)p.max_patch_hdoubles * 8 + 16 : 0;
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
-  constexpr int B = EV_ROW_BLOCK;
-  static_assert(FastCfg<MODE_HESS, false>::BLOCK == B && FastCfg<MODE_HVP, false>::BLOCK == B &&
-                FastCfg<MODE_HVP, true>::BLOCK == B && FastCfg<MODE_GRAD, false>::BLOCK == B,
-                "row module launches assume one block size");
+  const int B = mode == MODE_HESS ? FastCfg<MODE_HESS, false>::BLOCK
+                : mode == MODE_GRAD ? FastCfg<MODE_GRAD, false>::BLOCK
+                : c.psd ? FastCfg<MODE_HVP, true>::BLOCK : FastCfg<MODE_HVP, false>::BLOCK;
   timing_begin(p, c.stream);
   jit_rows_launch(p, mode, c.psd, &a, (m.Vr + B - 1) / B, B, sm, c.stream);
   timing_end(p, c.stream);

@@ -5,6 +5,8 @@
 //
 //   static constexpr bool kXFreeHvp;   // EV Hessian independent of x (the
 //                                      // unclamped HVP reads directions only)
+//   static constexpr bool kVertexOnly; // no per-edge attribute: the gradient /
+//                                      // HVP kernels may read 32-bit records
 //   template <int N, int MODE> static auto vload(const EvArgs&, int g);
 //       V-term attribute loads, issued before the incidence gathers
 //   template <int N, int MODE, bool PSD> static void vterms(a, g, fr, pre, xs, us, eacc, vec, dg);
@@ -31,6 +33,8 @@ struct EvArgs {
   const uint8_t* pfix;       // (V) pinned flag of each row
   const uint32_t* rmeta;     // (V) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
   const uint64_t* ell;       // (EV_ELL_K, V) first incidences, slot-major
+  const uint32_t* ell32;     // (EV_ELL_K, V) vertex-only 32-bit records for the gradient / HVP kernels
+                             // when no EV term reads a per-edge attribute (patch_setup.cu k_ell32), or null
   const int32_t* rinc_off;   // (V+1)
   const uint64_t* rrec;      // lo: edge | slot << 31, hi: other | pinned(other) << 31
   const int64_t* prow_ro;
@@ -119,6 +123,11 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
 #ifndef EV_FLAT_BLOCK
 #define EV_FLAT_BLOCK 64
 #endif
+// 1: gradient / HVP kernels walk row blocks grid-stride too, with the next
+// row's level-1 streams in flight (A/B knob)
+#ifndef EV_FLAT_PERSIST
+#define EV_FLAT_PERSIST 0
+#endif
 // MAXI: incidences in flight; BLOCK: threads per CTA (the Hessian kernel's CTA
 // is its row-buffer group, EV_ROW_BLOCK); MINB: CTAs per SM to fit
 template <int MODE, bool PSD> struct FastCfg {
@@ -126,6 +135,9 @@ template <int MODE, bool PSD> struct FastCfg {
 };
 #ifndef EV_HVP_MAXI
 #define EV_HVP_MAXI 4
+#endif
+#ifndef EV_XFREE_MAXI
+#define EV_XFREE_MAXI 6  // incidences in flight of the x-free HVP (directions only): 0.313 -> 0.278 ms at 4 -> 6 (smoothing, icosphere(10))
 #endif
 #ifndef EV_HVP_THREADS
 #define EV_HVP_THREADS 512  // measured: 0.269 ms vs 0.288 at 640 (row-kernel spring HVP, 2048^2)
@@ -151,11 +163,11 @@ template <int MODE, bool PSD, bool XFREE_HVP> struct FastMinb {
 template <int N, int MODE, bool PSD, class Pol>
 MG_DI void rows_fast_body(const EvArgs& a) {
   constexpr int T = TriN<N>::value, NN = N * N;
-  constexpr int MAXI = FastCfg<MODE, PSD>::MAXI;
   constexpr int PTB = FastCfg<MODE, PSD>::BLOCK;
   // e.g. the edge length's Hessian 2 [[I,-I],[-I,I]] does not depend on x
   // (apps/smooth.py:27-28): its unclamped HVP reads only the direction
   constexpr bool XFREE = MODE == MODE_HVP && !PSD && Pol::kXFreeHvp;
+  constexpr int MAXI = XFREE ? EV_XFREE_MAXI : FastCfg<MODE, PSD>::MAXI;
   extern __shared__ __align__(16) double hbuf[];
   // Row blocks are walked grid-stride (a persistent grid for the Hessian, one
   // block per CTA otherwise); the level-1 streams of the thread's next row are
@@ -168,7 +180,9 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     uint64_t rc[EV_ELL_K];
   };
   // level 1: static per-row streams, all indexed by the row alone
-  // (coalesced): vertex, meta word, row start / buffer offset, ELL records
+  // (coalesced): vertex, meta word, row start / buffer offset, ELL records.
+  // The gradient / HVP kernels read 32-bit vertex-only records when no term
+  // needs the edge id (half the bytes) and expand them to the 64-bit form here.
   auto load_l1 = [&](int64_t r, L1& l) {
     if (r >= a.V) return;
     l.g = a.order ? a.order[r] : (int)r;  // null: identity row order
@@ -176,17 +190,29 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     if constexpr (MODE == MODE_HESS) {
       l.ro = a.prow_ro[r];
       l.ho = a.hoff[r];
-    }
 #pragma unroll
-    for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
+      for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
+    } else if (Pol::kVertexOnly && a.ell32) {  // vertex-only records (no per-edge attribute is read)
+#pragma unroll
+      for (int j = 0; j < EV_ELL_K; ++j) {
+        const uint32_t q = a.ell32[(int64_t)j * a.V + r];
+        const uint32_t o = q & 0x7fffffffu;
+        const uint32_t lo = (uint32_t)(o < (uint32_t)l.g) << 31;  // edge id unused; first vertex: o > g
+        l.rc[j] = (uint64_t)lo | ((uint64_t)q << 32);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
+    }
   };
   const int64_t nblk = (a.V + PTB - 1) / PTB;
   bool finite = true;
   L1 cur, nxt;
-  if constexpr (MODE == MODE_HESS) load_l1((int64_t)blockIdx.x * PTB + threadIdx.x, cur);
+  constexpr bool PERSIST = MODE == MODE_HESS || EV_FLAT_PERSIST;
+  if constexpr (PERSIST) load_l1((int64_t)blockIdx.x * PTB + threadIdx.x, cur);
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
   const int64_t row = blk * PTB + threadIdx.x;
-  if constexpr (MODE == MODE_HESS) {
+  if constexpr (PERSIST) {
     if (blk + gridDim.x < nblk) load_l1(row + (int64_t)gridDim.x * PTB, nxt);
   } else {
     load_l1(row, cur);
@@ -298,11 +324,19 @@ MG_DI void rows_fast_body(const EvArgs& a) {
         for (int i = 0; i < N; ++i) vec[i] += gam * d[i];
       }
       if constexpr (MODE == MODE_HVP) {  // y_row = M (u_row - u_other) + dl (u_row + u_other)
-        double dw = 0.0;
+        if constexpr (XFREE) {  // M = ci I (the axial coefficient is exactly zero)
 #pragma unroll
-        for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo_[c]);
+          for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo_[i]);
+        } else {
+          double dw = 0.0;
 #pragma unroll
-        for (int i = 0; i < N; ++i) vec[i] += ci_s * (us[i] - uo_[i]) + cd_s * d[i] * dw + dl * (us[i] + uo_[i]);
+          for (int c = 0; c < N; ++c) dw += d[c] * (us[c] - uo_[c]);
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            if constexpr (PSD) vec[i] += ci_s * (us[i] - uo_[i]) + cd_s * d[i] * dw + dl * (us[i] + uo_[i]);
+            else vec[i] += ci_s * (us[i] - uo_[i]) + cd_s * d[i] * dw;  // dl is zero without a clamp
+          }
+        }
       }
       if constexpr (MODE == MODE_HESS) {
         // t = cd d d^T (6 unique products) feeds both the diagonal sum and the
@@ -376,7 +410,7 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
     if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
   }
-  if constexpr (MODE == MODE_HESS) cur = nxt;
+  if constexpr (PERSIST) cur = nxt;
   else break;  // one row block per CTA outside the Hessian
   }
   if (!finite) *a.redo = 1;

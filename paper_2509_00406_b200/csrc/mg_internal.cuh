@@ -185,6 +185,8 @@ struct Problem {
   DBuf<uint8_t> pfix;          // (Vr) pinned flag of each row
   DBuf<uint32_t> rmeta;        // (Vr) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
   DBuf<uint64_t> ell;          // (EV_ELL_K, Vr) first incidences of each row, slot-major
+  DBuf<uint32_t> ell32;        // (EV_ELL_K, Vr) vertex-only 32-bit records (k_ell32): gradient / HVP edge rows
+  bool ell32_ok = false;       // built (no EV term reads a per-edge attribute)
   DBuf<uint64_t> ellv;         // face rows: (EV_ELL_K, Vr) the incidence's other two corners (s+1 | s+2 << 32)
   DBuf<int64_t> prow_ro;       // (Vr) row start
   DBuf<int32_t> prow_len;      // (Vr) row length (blocks)

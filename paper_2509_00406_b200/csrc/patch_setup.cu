@@ -411,6 +411,22 @@ __global__ void k_ell(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr,
   for (int k = 0; k < K; ++k) ell[(int64_t)k * Vr + i] = k < c ? rrec[k0 + k] : 0ull;
 }
 
+// Vertex-only 32-bit copies of the ELL incidence records (other |
+// pinned(other) << 31) for the gradient / HVP row kernels of problems whose EV
+// terms read no per-edge attribute (edge_rows.cuh; half the record bytes).
+// Unused slots hold the row's own vertex (a valid address, never used). The
+// first-vertex flag is other > vertex (canonical edges). Measured: +2% on the
+// smoothing HVP / gradient; an edge-id delta variant for the spring was 2%
+// slower (the decode sits on the gathers' dependency chain) and was dropped.
+__global__ void k_ell32(const int32_t* rinc_off, const uint64_t* rrec, const int32_t* order, int64_t Vr, int K,
+                        uint32_t* ell32) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Vr) return;
+  const int k0 = rinc_off[i], c = rinc_off[i + 1] - k0;
+  const int64_t g = order ? order[i] : i;
+  for (int k = 0; k < K; ++k) ell32[(int64_t)k * Vr + i] = k < c ? (uint32_t)(rrec[k0 + k] >> 32) : (uint32_t)g;
+}
+
 // face rows: the other two corners (s+1, s+2 mod 3) of each ELL face incidence,
 // so the row kernels skip the faces[] lookup (one dependent level less)
 __global__ void k_ellv(const int32_t* rinc_off, const uint64_t* rrec, const int32_t* faces, int64_t Vr, int K,
@@ -876,6 +892,21 @@ void build_rows_ev(Problem& p, cudaStream_t s, bool tiles) {
     k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
   }
   MG_LAUNCH_CHECK();
+  // vertex-only records for the gradient / HVP kernels when no edge term reads
+  // a per-edge attribute (MG_ELL32=0: 64-bit records, A/B runs)
+  {
+    bool vo = true;
+    for (auto& t : p.terms)
+      if (t.dev.op == MG_OP_EV) vo &= t.jit ? t.jit_attrs.empty() : t.dev.type == MG_TERM_EDGE_LENGTH;
+    const char* env = getenv("MG_ELL32");
+    p.ell32_ok = vo && Vr > 0 && !(env && env[0] == '0');
+    p.ell32.alloc(p.ell32_ok ? (int64_t)EV_ELL_K * Vr : 1);
+    const bool ident = m.row_order_used == MG_ROW_IDENTITY && !m.owned.p;
+    if (p.ell32_ok)
+      k_ell32<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, ident ? nullptr : ps.order.p, Vr, EV_ELL_K,
+                                           p.ell32.p);
+    MG_LAUNCH_CHECK();
+  }
   MG_CUDA(cudaStreamSynchronize(s));
   p.redo.alloc(1);
   MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
