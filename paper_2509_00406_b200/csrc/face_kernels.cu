@@ -61,6 +61,14 @@ struct FvArgs {
   double* fpsd6;             // faces with a pinned corner: the clamped masked 6x6, packed (F, 21)
   const uint8_t* fixed;      // (nv) pinned vertices, or null
   int64_t nf;                // faces of the (shard) mesh
+  // CTA face lists (k_cta_dirichlet): per 64-row block its distinct incident
+  // faces (face | corner-0-row-in-block << 31), and per incidence the face's
+  // slot in its block's list (ELL slot-major for the first KF, then CSR)
+  const int32_t* cf_off;     // (blocks + 1)
+  const int4* cf_face;       // {face | own0 << 31, corner 0, 1, 2}
+  const uint16_t* eslot;     // (KF, V)
+  const uint16_t* rslot;     // (incidences) parallel to rrec
+  int cf_max;                // max faces of one block (shared-memory records)
 };
 
 MG_DI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -145,6 +153,52 @@ MG_DI bool dirichlet_closed(const double* J, double area, double& val, double* g
   return D > 0.0 && isfinite(chk);
 }
 
+// The reduced PSD clamp of one face (see the header): M = (I (x) L_W)^T H_J
+// (I (x) L_W), then P_f(M) in place — Cholesky test, else the certified
+// rank-one update from the twist direction, else round-robin Jacobi.
+// Non-finite faces (fin false) are left unclamped (the caller raises redo).
+MG_DI void face_psd_reduce(const double* J, double R0, double R1, double R2, double R3, const double* h,
+                           double floor_, bool fin, double* M) {
+  const double Wa0 = -(R0 + R2), Wa1 = -(R1 + R3);
+  // Q_W rows (corners): (1/sqrt2, 1/sqrt6), (-1/sqrt2, 1/sqrt6), (0, -2/sqrt6); L_W = W Q_W
+  const double Lw00 = (Wa0 - R0) * INV_SQRT2, Lw01 = (Wa0 + R0 - 2.0 * R2) * INV_SQRT6;
+  const double Lw10 = (Wa1 - R1) * INV_SQRT2, Lw11 = (Wa1 + R1 - 2.0 * R3) * INV_SQRT6;
+  const double Lw[2][2] = {{Lw00, Lw01}, {Lw10, Lw11}};
+#pragma unroll
+  for (int I = 0; I < 4; ++I)
+#pragma unroll
+    for (int Jx = 0; Jx <= I; ++Jx) {
+      const int c = I >> 1, aa = I & 1, c2 = Jx >> 1, bb = Jx & 1;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
+      M[tri(I, Jx)] = acc;
+    }
+  // non-finite faces: the row kernel takes the exact path
+  if (fin && !shifted_pd<4>(M, floor_)) {
+    // only the twist mode of the isotropic energy can be negative: start the
+    // eigen-iteration from J's twist direction [[q, -p], [p, q]] (p = tr-like,
+    // q = skew part of J) mapped through the reduced basis (M = C^T H_J C,
+    // C = I (x) L_W: v0 = C^-1 u_T)
+    const double p = J[0] + J[3], q = J[1] - J[2];
+    const double uT[4] = {q, -p, p, q};
+    const double dl = Lw00 * Lw11 - Lw01 * Lw10;
+    double v0[4];
+    if (dl != 0.0) {
+      const double idl = 1.0 / dl;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // solve sum_a Lw[k][a] y_a = uT[2c+k]
+        const double u0 = uT[2 * c], u1 = uT[2 * c + 1];
+        v0[2 * c] = (Lw11 * u0 - Lw01 * u1) * idl;
+        v0[2 * c + 1] = (-Lw10 * u0 + Lw00 * u1) * idl;
+      }
+    }
+    if (dl == 0.0 || !psd_rank1_update<4>(M, floor_, v0)) jacobi_project_rr<4>(M, floor_);
+  }
+}
+
 // Per-face PSD clamp of the reduced 4x4 matrix M = (I (x) L_W)^T H_J (I (x) L_W)
 // (see the header), once per face: the three owner rows of a face then read
 // P_f(M) instead of each recomputing the eigen-decomposition.
@@ -172,47 +226,35 @@ __global__ void __launch_bounds__(128) k_face_psd(const __grid_constant__ FvArgs
   double v, g[4], h[10];
   const bool fin = dirichlet_closed<true>(J, area, v, g, h);
   double M[10];
-  const double Wa0 = -(R0 + R2), Wa1 = -(R1 + R3);
-  // Q_W rows (corners): (1/sqrt2, 1/sqrt6), (-1/sqrt2, 1/sqrt6), (0, -2/sqrt6); L_W = W Q_W
-  const double Lw00 = (Wa0 - R0) * INV_SQRT2, Lw01 = (Wa0 + R0 - 2.0 * R2) * INV_SQRT6;
-  const double Lw10 = (Wa1 - R1) * INV_SQRT2, Lw11 = (Wa1 + R1 - 2.0 * R3) * INV_SQRT6;
-  const double Lw[2][2] = {{Lw00, Lw01}, {Lw10, Lw11}};
-#pragma unroll
-  for (int I = 0; I < 4; ++I)
-#pragma unroll
-    for (int Jx = 0; Jx <= I; ++Jx) {
-      const int c = I >> 1, aa = I & 1, c2 = Jx >> 1, bb = Jx & 1;
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2) acc += Lw[k][aa] * h[tri(2 * c + k, 2 * c2 + k2)] * Lw[k2][bb];
-      M[tri(I, Jx)] = acc;
-    }
-  // non-finite faces: the row kernel takes the exact path
-  if (fin && !shifted_pd<4>(M, a.floor)) {
-    // only the twist mode of the isotropic energy can be negative: start the
-    // eigen-iteration from J's twist direction [[q, -p], [p, q]] (p = tr-like,
-    // q = skew part of J) mapped through the reduced basis (M = C^T H_J C,
-    // C = I (x) L_W: v0 = C^-1 u_T)
-    const double p = J[0] + J[3], q = J[1] - J[2];
-    const double uT[4] = {q, -p, p, q};
-    const double dl = Lw00 * Lw11 - Lw01 * Lw10;
-    double v0[4];
-    if (dl != 0.0) {
-      const double idl = 1.0 / dl;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {  // solve sum_a Lw[k][a] y_a = uT[2c+k]
-        const double u0 = uT[2 * c], u1 = uT[2 * c + 1];
-        v0[2 * c] = (Lw11 * u0 - Lw01 * u1) * idl;
-        v0[2 * c + 1] = (-Lw10 * u0 + Lw00 * u1) * idl;
-      }
-    }
-    if (dl == 0.0 || !psd_rank1_update<4>(M, a.floor, v0)) jacobi_project_rr<4>(M, a.floor);
-  }
+  face_psd_reduce(J, R0, R1, R2, R3, h, a.floor, fin, M);
   double2* out = reinterpret_cast<double2*>(a.fpsd + f * 10);
 #pragma unroll
   for (int k = 0; k < 5; ++k) out[k] = make_double2(M[2 * k], M[2 * k + 1]);
+}
+
+// Faces with a pinned corner under a clamp: the masked 6x6 (pinned corners'
+// rows / columns zero), clamped in full, packed (rows 2q + c).
+MG_DI void face_psd6(double R0, double R1, double R2, double R3, const double* h, const bool* pq, double floor_,
+                     bool fin, double* H6) {
+  const double W[3][2] = {{-(R0 + R2), -(R1 + R3)}, {R0, R1}, {R2, R3}};
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int q2 = 0; q2 <= q; ++q2)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const int R = 2 * q + c, C = 2 * q2 + c2;
+          if (C > R) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int k2 = 0; k2 < 2; ++k2) acc += W[q][k] * h[tri(2 * c + k, 2 * c2 + k2)] * W[q2][k2];
+          H6[tri(R, C)] = (pq[q] || pq[q2]) ? 0.0 : acc;
+        }
+  if (fin) project_if_needed<6>(H6, floor_);  // non-finite faces: the row kernel takes the exact path
 }
 
 // Faces with a pinned corner under a clamp (launched only when the problem
@@ -246,26 +288,8 @@ __global__ void __launch_bounds__(128) k_face_psd_pinned(const __grid_constant__
   double v, g[4], h[10];
   const bool fin = dirichlet_closed<true>(J, area, v, g, h);
   const bool pq[3] = {p0, p1, p2};
-  const double W[3][2] = {{-(R0 + R2), -(R1 + R3)}, {R0, R1}, {R2, R3}};
   double H6[21];
-#pragma unroll
-  for (int q = 0; q < 3; ++q)
-#pragma unroll
-    for (int q2 = 0; q2 <= q; ++q2)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2) {
-          const int R = 2 * q + c, C = 2 * q2 + c2;
-          if (C > R) continue;
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int k2 = 0; k2 < 2; ++k2) acc += W[q][k] * h[tri(2 * c + k, 2 * c2 + k2)] * W[q2][k2];
-          H6[tri(R, C)] = (pq[q] || pq[q2]) ? 0.0 : acc;
-        }
-  if (fin) project_if_needed<6>(H6, a.floor);  // non-finite faces: the row kernel takes the exact path
+  face_psd6(R0, R1, R2, R3, h, pq, a.floor, fin, H6);
 #pragma unroll
   for (int k = 0; k < 21; ++k) a.fpsd6[f * 21 + k] = H6[k];
 }
@@ -675,6 +699,383 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
     if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
+  }
+  if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// CTA face-list variant (default): each face is evaluated ONCE per 64-row
+// block instead of once per owner row. Phase A: the block's threads walk its
+// distinct incident faces (setup: cf_off / cf_face; Morton rows put ~177
+// faces behind 64 rows, against 384 row incidences) and write per corner q
+// what its row needs into a shared-memory record: the gradient (HVP: H u)
+// part, and for the Hessian the diagonal block (3 unique entries) and the
+// off-diagonal block (q, q+1 mod 3) (its transpose is block (q+1, q), so the
+// two come out bitwise transposed). The PSD clamp runs here too, once per
+// face, in registers (no P_f(M) round trip through HBM). Phase B: one thread
+// per row sums its incidences' records in the same fixed incidence order as
+// the per-row kernel, builds its row in the shared-memory row buffer and
+// streams it out with one bulk copy. The energy counts each face in the block
+// that owns its first corner's row.
+template <int MODE> struct CfRec { static constexpr int S = MODE == MODE_HESS ? 27 : 6; };
+
+// one face's inputs (phase A loads them for two faces before computing)
+struct CfIn {
+  double X[3][2], U[3][2], R[4], area;
+  bool pq[3];
+};
+template <int MODE, bool PSD>
+MG_DI void cf_load(const FvArgs& a, const int4& fe, CfIn& d) {
+  const int64_t f = (uint32_t)fe.x & 0x7fffffffu;
+  const int v[3] = {fe.y, fe.z, fe.w};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) d.pq[q] = (MODE == MODE_HVP || PSD) && a.fixed && a.fixed[v[q]];
+  // (caller buffers: 8-byte alignment only, scalar loads)
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    d.X[q][0] = a.x[(int64_t)v[q] * 2];
+    d.X[q][1] = a.x[(int64_t)v[q] * 2 + 1];
+    if constexpr (MODE == MODE_HVP) {
+      d.U[q][0] = a.w[(int64_t)v[q] * 2];
+      d.U[q][1] = a.w[(int64_t)v[q] * 2 + 1];
+    }
+  }
+  const double* Rp = a.t.a[0] + 4 * f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) d.R[k] = Rp[k];
+  d.area = a.t.a[1][f];
+}
+
+template <int MODE, bool PSD, bool PIN>
+MG_DI void cf_face(const FvArgs& a, const CfIn& d, double* out, double& val, bool& ok) {
+  double X[3][2], U[3][2];
+  bool pq[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    pq[q] = d.pq[q];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      X[q][c] = d.X[q][c];
+      U[q][c] = (MODE == MODE_HVP && !pq[q]) ? d.U[q][c] : 0.0;
+    }
+  }
+  const double R0 = d.R[0], R1 = d.R[1], R2 = d.R[2], R3 = d.R[3];
+  const double area = d.area;
+  double J[4];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double d1 = X[1][c] - X[0][c], d2 = X[2][c] - X[0][c];
+    J[2 * c] = d1 * R0 + d2 * R2;
+    J[2 * c + 1] = d1 * R1 + d2 * R3;
+  }
+  // corner weights on J's columns: J[2c + k] = sum_q W[q][k] X[q][c]
+  const double W[3][2] = {{-(R0 + R2), -(R1 + R3)}, {R0, R1}, {R2, R3}};
+  // Q_W (orthonormal basis of 1-perp) rows: the clamped blocks' weights
+  const double QW[3][2] = {{INV_SQRT2, INV_SQRT6}, {-INV_SQRT2, INV_SQRT6}, {0.0, -2.0 * INV_SQRT6}};
+  const bool pinned_face = PSD && PIN && (pq[0] || pq[1] || pq[2]);
+  val = 0.0;
+  if constexpr (MODE == MODE_GRAD) {
+    double gJ[4];
+    ok &= dirichlet_closed<false>(J, area, val, gJ, nullptr);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) out[2 * q + c] = W[q][0] * gJ[2 * c] + W[q][1] * gJ[2 * c + 1];
+    return;
+  }
+  double gJ[4], h[10];
+  bool fin;
+  if constexpr (MODE == MODE_HESS || PSD) {
+    fin = dirichlet_closed<true>(J, area, val, gJ, h);
+  }
+  // G (4x4, J space) and the corner weights its blocks contract with
+  double G[10], M6[PIN ? 21 : 1];
+  const double(*wt)[2] = W;
+  const double fl3 = PSD ? a.floor * (1.0 / 3.0) : 0.0;
+  if constexpr (PSD) {
+    if (pinned_face) {
+      if constexpr (PIN) {
+        face_psd6(R0, R1, R2, R3, h, pq, a.floor, fin, M6);
+        double chk = 0.0;
+#pragma unroll
+        for (int k = 0; k < 21; ++k) chk += M6[k];
+        fin = fin && isfinite(chk);
+      }
+    } else {
+      face_psd_reduce(J, R0, R1, R2, R3, h, a.floor, fin, G);
+      double chk = 0.0;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) chk += G[k];
+      fin = fin && isfinite(chk);
+    }
+    wt = QW;
+    ok &= fin;
+  } else if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) G[k] = h[k];
+    ok &= fin;
+  }
+  // X(u, v, c, c2) = sum_{k,k2} u[k] G[(c,k),(c2,k2)] v[k2]
+  auto Xf = [&](const double* u, const double* w2, int c, int c2) {
+    return u[0] * (G[tri(2 * c, 2 * c2)] * w2[0] + G[tri(2 * c, 2 * c2 + 1)] * w2[1]) +
+           u[1] * (G[tri(2 * c + 1, 2 * c2)] * w2[0] + G[tri(2 * c + 1, 2 * c2 + 1)] * w2[1]);
+  };
+  if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) out[2 * q + c] = W[q][0] * gJ[2 * c] + W[q][1] * gJ[2 * c + 1];
+      const int q1 = q == 2 ? 0 : q + 1;
+      double* dq = out + 6 + 3 * q;
+      double* oq = out + 15 + 4 * q;
+      if (PIN && pinned_face) {
+        dq[0] = M6[tri(2 * q, 2 * q)];
+        dq[1] = M6[tri(2 * q, 2 * q + 1)];
+        dq[2] = M6[tri(2 * q + 1, 2 * q + 1)];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) oq[2 * c + c2] = M6[tri(2 * q + c, 2 * q1 + c2)];
+      } else {
+        // the reference's symmetrisation on the diagonal block
+        dq[0] = Xf(wt[q], wt[q], 0, 0) + fl3;
+        dq[1] = 0.5 * (Xf(wt[q], wt[q], 0, 1) + Xf(wt[q], wt[q], 1, 0));
+        dq[2] = Xf(wt[q], wt[q], 1, 1) + fl3;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) oq[2 * c + c2] = Xf(wt[q], wt[q1], c, c2) + (c == c2 ? fl3 : 0.0);
+      }
+    }
+  } else {  // HVP: y_q = block row q . u
+    if (PIN && pinned_face) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          double y = 0.0;
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) y += M6[tri(2 * q + c, 2 * t + c2)] * U[t][c2];
+          out[2 * q + c] = y;
+        }
+      return;
+    }
+    double dv[4], gv[4];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) dv[2 * c + k] = wt[0][k] * U[0][c] + wt[1][k] * U[1][c] + wt[2][k] * U[2][c];
+    if constexpr (PSD) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc += G[tri(i, j)] * dv[j];
+        gv[i] = acc;
+      }
+    } else {
+      ok &= dirichlet_hv_closed(J, dv, area, gv);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double y = wt[q][0] * gv[2 * c] + wt[q][1] * gv[2 * c + 1];
+        if constexpr (PSD) y += fl3 * (U[0][c] + U[1][c] + U[2][c]);
+        out[2 * q + c] = y;
+      }
+  }
+}
+
+// threads per CTA (64 rows): the Hessian's larger records allow fewer CTAs
+// per SM, so its CTAs bring two threads per row to phase A
+template <int MODE, bool PSD> struct CfCfg {
+  static constexpr int NT = MODE == MODE_HESS ? 128 : 64;
+  static constexpr int MINB = MODE == MODE_HESS ? 3 : 6;
+};
+template <int MODE, bool PSD, bool PIN>
+__global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB))
+    k_cta_dirichlet(const __grid_constant__ FvArgs a) {
+  constexpr int NT = CfCfg<MODE, PSD>::NT;
+  constexpr int S = CfRec<MODE>::S, NN = 4;
+  extern __shared__ __align__(16) double smem[];
+  double* rec = smem;
+  double* hbuf = smem + (((size_t)a.cf_max * S + 1) & ~(size_t)1);  // 16-byte aligned: the row buffers' phases
+  const int64_t blk = blockIdx.x;
+  const int64_t row = blk * PT + threadIdx.x;
+  // phase B's row streams first: their loads overlap phase A
+  int g = 0;
+  uint32_t meta = 0;
+  int64_t ro = 0;
+  int ho = 0;
+  uint64_t rc[KF];
+  int sl[KF];
+  const bool has_row = threadIdx.x < PT && row < a.V;
+  if (has_row) {
+    g = a.order ? a.order[row] : (int)row;
+    meta = a.rmeta[row];
+    if constexpr (MODE == MODE_HESS) {
+      ro = a.prow_ro[row];
+      ho = a.hoff[row];
+    }
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      rc[j] = a.ell[(int64_t)j * a.V + row];
+      sl[j] = a.eslot[(int64_t)j * a.V + row];
+    }
+  }
+  // phase A: the block's faces, once each
+  const int i0 = a.cf_off[blk], nfc = a.cf_off[blk + 1] - i0;
+  double eacc = 0.0;
+  bool ok = true;
+  // two faces' loads in flight (one under a clamp: register pressure)
+  constexpr int NB = PSD ? 1 : 2;
+  for (int i = threadIdx.x; i < nfc; i += NB * NT) {
+    int4 fe[NB];
+    CfIn d[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int ib = i + b * NT;
+      fe[b] = a.cf_face[i0 + (ib < nfc ? ib : i)];
+      cf_load<MODE, PSD>(a, fe[b], d[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int ib = i + b * NT;
+      if (ib < nfc) {
+        double val;
+        cf_face<MODE, PSD, PIN>(a, d[b], rec + (size_t)ib * S, val, ok);
+        if (MODE != MODE_HVP && ((uint32_t)fe[b].x >> 31)) eacc += val;
+      }
+    }
+  }
+  __syncthreads();
+  // phase B: rows sum their incidences' records in incidence order
+  if (has_row) {
+    const bool fr = !((meta >> 8) & 1);
+    const int dp = (int)(meta >> 16) & 0xff;
+    const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
+    const bool fan = (meta >> 9) & 1;
+    double* hrow = hbuf + ho;
+    int nblk = 0;
+    if constexpr (MODE == MODE_HESS) {
+      nblk = (int)((meta >> 24) & 0xff);
+      if (!fan)
+        for (int k = 0; k < nblk * NN; ++k) hrow[k] = 0.0;
+    }
+    double vec[2] = {0.0, 0.0}, dg[3] = {0.0, 0.0, 0.0};
+    double carry[4] = {0.0, 0.0, 0.0, 0.0}, first[4] = {0.0, 0.0, 0.0, 0.0};
+    int first_pos = 255, last_pos2 = 255;
+    auto incidence = [&](uint64_t r64, int slot, int jidx) {
+      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
+      const int s = (int)(lo >> 30);
+      const double* r = rec + (size_t)slot * S;
+      vec[0] += r[2 * s];
+      vec[1] += r[2 * s + 1];
+      if constexpr (MODE == MODE_HESS) {
+        const int pos1 = (int)(hi & 0xff), pos2 = (int)((hi >> 8) & 0xff);
+        const int s2 = s == 0 ? 2 : s - 1;
+        const double* dq = r + 6 + 3 * s;
+        dg[0] += dq[0];
+        dg[1] += dq[1];
+        dg[2] += dq[2];
+        const double* o1 = r + 15 + 4 * s;   // block (s, s+1)
+        const double* o2 = r + 15 + 4 * s2;  // block (s-1, s): block (s, s-1) is its transpose
+        const double b1[4] = {o1[0], o1[1], o1[2], o1[3]};
+        const double b2[4] = {o2[0], o2[2], o2[1], o2[3]};
+        if (fan) {
+          if (jidx == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) first[k] = b1[k];
+            first_pos = pos1;
+          } else if (pos1 != 255) {
+            double* dst = hrow + pos1 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = carry[k] + b1[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) carry[k] = b2[k];
+          last_pos2 = pos2;
+        } else {
+          if (pos1 != 255) {
+            double* dst = hrow + pos1 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] += b1[k];
+          }
+          if (pos2 != 255) {
+            double* dst = hrow + pos2 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] += b2[k];
+          }
+        }
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < KF; ++j)
+      if (j < cnt) incidence(rc[j], sl[j], j);
+    for (int k = KF; k < cnt; ++k) {
+      const int64_t q = a.rinc_off[row] + k;
+      incidence(a.rrec[q], a.rslot[q], k);
+    }
+    if constexpr (MODE == MODE_HESS) {
+      if (fan && cnt > 0) {  // close the fan: the first block meets the last carry, or both stand alone
+        if (last_pos2 == first_pos) {
+          if (first_pos != 255) {
+            double* dst = hrow + first_pos * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = carry[k] + first[k];
+          }
+        } else {
+          if (first_pos != 255) {
+            double* dst = hrow + first_pos * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = first[k];
+          }
+          if (last_pos2 != 255) {
+            double* dst = hrow + last_pos2 * NN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[k] = carry[k];
+          }
+        }
+      }
+    }
+    double* vout = MODE == MODE_HVP ? a.y : a.grad;
+    vout[(int64_t)g * 2] = fr ? vec[0] : 0.0;
+    vout[(int64_t)g * 2 + 1] = fr ? vec[1] : 0.0;
+    if constexpr (MODE == MODE_HESS) {
+      if (fr && dp != 255) {
+        double* dst = hrow + dp * NN;
+        dst[0] = dg[0];
+        dst[1] = dg[1];
+        dst[2] = dg[1];
+        dst[3] = dg[2];
+      }
+      if (nblk > 0) {
+        fence_proxy_async_smem();
+        row_store_bulk(a.hess + ro * NN, hrow, nblk * NN);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  }
+  if (!ok) *a.redo = 1;
+  if constexpr (MODE != MODE_HVP) {
+    // the block's face energies (spread over all its threads by phase A) in
+    // fixed order into its first warp's partial; its other row warp's slot is zero
+    __shared__ double wsum[NT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = eacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = wsum[0];
+#pragma unroll
+      for (int w = 1; w < NT / 32; ++w) t += wsum[w];
+      a.partials[(blk * PT) >> 5] = t;
+    } else if (threadIdx.x == 32 && blk * PT + 32 < a.V) {
+      a.partials[(blk * PT + 32) >> 5] = 0.0;
+    }
   }
   if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -1138,12 +1539,45 @@ void launch_sphere(const Problem& p, const FvArgs& a, cudaStream_t st) {
   timing_end(p, st);
 }
 
+// MG_FV_CTA=0: the per-row kernel (each face evaluated by each owner row)
+// with the per-face PSD pre-pass (A/B runs)
+bool fv_cta_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MG_FV_CTA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// shared memory of the CTA face-list kernel (face records, then the row buffers)
+size_t cta_smem(int mode, int cf_max, int hd_max) {
+  const size_t S = mode == MODE_HESS ? CfRec<MODE_HESS>::S : CfRec<MODE_GRAD>::S;
+  return (((size_t)cf_max * S + 1) & ~(size_t)1) * 8 + (mode == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0);
+}
+// the unclamped Hessian keeps the per-row kernel (measured 2.05 vs 2.98 ms at
+// icosphere(10): the 27-double face records cap residency at 3 CTAs/SM)
+bool fv_use_cta(const Problem& p, int mode, bool psd) {
+  const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
+  return (mode != MODE_HESS || psd) && p.cf_max > 0 && cta_smem(mode, p.cf_max, hd) <= 227 * 1024 &&
+         fv_cta_enabled();
+}
+
 template <int MODE, bool PSD>
 void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
   const int64_t nb = (a.V + PT - 1) / PT;
   if (!nb) return;
+  const size_t smc = cta_smem(MODE, a.cf_max, hd_max);
+  if (fv_use_cta(p, MODE, PSD)) {
+    auto kc = (PSD && a.fixed) ? k_cta_dirichlet<MODE, PSD, true> : k_cta_dirichlet<MODE, PSD, false>;
+    MG_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
+    timing_begin(p, st);
+    kc<<<(unsigned)nb, CfCfg<MODE, PSD>::NT, smc, st>>>(a);
+    MG_LAUNCH_CHECK();
+    timing_end(p, st);
+    return;
+  }
   auto kern = (PSD && a.fpsd6) ? k_rows_dirichlet<MODE, PSD, true> : k_rows_dirichlet<MODE, PSD, false>;
   if (sm) MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   timing_begin(p, st);
@@ -1188,7 +1622,12 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.fpsd = nullptr;
   a.fpsd6 = nullptr;
   a.fixed = p.any_fixed ? p.fixed.p : nullptr;
-  if (c.psd && mode != MODE_GRAD && a.t.type != MG_TERM_SPHERE) {
+  a.cf_off = p.cf_off.p;
+  a.cf_face = p.cf_face.p;
+  a.eslot = p.eslot.p;
+  a.rslot = p.rslot.p;
+  a.cf_max = p.cf_max;
+  if (c.psd && mode != MODE_GRAD && a.t.type != MG_TERM_SPHERE && !fv_use_cta(p, mode, true)) {
     if (p.fpsd.n < 10 * m.F) p.fpsd.alloc(10 * m.F > 0 ? 10 * m.F : 2);
     a.fpsd = p.fpsd.p;
     if (p.any_fixed) {

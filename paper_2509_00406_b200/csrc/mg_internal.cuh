@@ -188,6 +188,13 @@ struct Problem {
   DBuf<uint32_t> ell32;        // (EV_ELL_K, Vr) vertex-only 32-bit records (k_ell32): gradient / HVP edge rows
   bool ell32_ok = false;       // built (no EV term reads a per-edge attribute)
   DBuf<uint64_t> ellv;         // face rows: (EV_ELL_K, Vr) the incidence's other two corners (s+1 | s+2 << 32)
+  // face rows, CTA face lists (k_cta_dirichlet): per EV_ROW_BLOCK rows its
+  // distinct faces (face | corner 0 in block << 31); per incidence its slot
+  DBuf<int32_t> cf_off;        // (blocks + 1)
+  DBuf<int4> cf_face;          // {face | corner 0 in block << 31, corners}
+  DBuf<uint16_t> eslot;        // (EV_ELL_K, Vr)
+  DBuf<uint16_t> rslot;        // (incidences), parallel to rrec
+  int cf_max = 0;              // max faces of one block; 0: lists not built
   DBuf<int64_t> prow_ro;       // (Vr) row start
   DBuf<int32_t> prow_len;      // (Vr) row length (blocks)
   DBuf<uint8_t> prow_dp;       // (Vr) diagonal block position (255: none)

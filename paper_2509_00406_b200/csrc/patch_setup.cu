@@ -447,6 +447,54 @@ __global__ void k_ellv(const int32_t* rinc_off, const uint64_t* rrec, const int3
   }
 }
 
+// CTA face lists of the face row kernel (k_cta_dirichlet): key (block << 32 |
+// face) for every face corner whose row is owned (block = row / RB)
+__global__ void k_cf_keys(const int32_t* faces, int64_t F, const int32_t* rank, int64_t Vr, int RB,
+                          uint64_t* keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 3 * F) return;
+  const int64_t row = rank[faces[i]];
+  keys[i] = row < Vr ? ((uint64_t)(row / RB) << 32) | (uint64_t)(i / 3) : ~0ull;
+}
+
+// {face | (its corner 0's row is in the block) << 31, corners} (one 16-byte
+// coalesced load per face in the kernel: no dependent faces[] gather)
+__global__ void k_cf_faces(const uint64_t* keys, int64_t n, const int32_t* faces, const int32_t* rank, int64_t Vr,
+                           int RB, int4* cf) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t blk = (int64_t)(keys[i] >> 32);
+  const uint32_t f = (uint32_t)keys[i];
+  const int v0 = faces[3 * (int64_t)f], v1 = faces[3 * (int64_t)f + 1], v2 = faces[3 * (int64_t)f + 2];
+  const int64_t r0 = rank[v0];
+  const bool own0 = r0 < Vr && r0 / RB == blk;
+  cf[i] = make_int4((int)(f | ((uint32_t)own0 << 31)), v0, v1, v2);
+}
+
+// per incidence: its face's slot in the row's block list (binary search, the
+// list is sorted by face); ELL copy of the first K slot-major
+__global__ void k_cf_slots(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr, int RB, int K,
+                           const int32_t* cf_off, const int4* cf, uint16_t* rslot, uint16_t* eslot, int* bad) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= Vr) return;
+  const int64_t blk = r / RB;
+  const int b0 = cf_off[blk], b1 = cf_off[blk + 1];
+  const int k0 = rinc_off[r], c = rinc_off[r + 1] - k0;
+  for (int k = 0; k < c; ++k) {
+    const uint32_t f = (uint32_t)rrec[k0 + k] & 0x3fffffffu;
+    int lo = b0, hi = b1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (((uint32_t)cf[mid].x & 0x7fffffffu) < f) lo = mid + 1; else hi = mid;
+    }
+    if (lo >= b1 || ((uint32_t)cf[lo].x & 0x7fffffffu) != f || lo - b0 > 0xffff) *bad = 1;
+    const uint16_t sl = (uint16_t)(lo - b0);
+    rslot[k0 + k] = sl;
+    if (k < K) eslot[(int64_t)k * Vr + r] = sl;
+  }
+  for (int k = c; k < K; ++k) eslot[(int64_t)k * Vr + r] = 0;
+}
+
 // Face rows: order each row's incidences around its vertex (face j's second
 // other corner is face j+1's first: consistently oriented manifold fans, open
 // or closed, at most 16 faces) and flag the row (meta bit 9); other rows keep
@@ -984,6 +1032,43 @@ void build_rows_fv(Problem& p, cudaStream_t s) {
     k_ellv<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, EV_ELL_K, p.ellv.p);
   }
   MG_LAUNCH_CHECK();
+  // CTA face lists (k_cta_dirichlet): each block's distinct faces, per
+  // incidence the face's slot in its block list
+  p.cf_max = 0;
+  if (Vr && m.F) {
+    const int64_t F = m.F;
+    uint64_t* keys = nullptr;
+    MG_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * 3 * F, s));
+    k_cf_keys<<<grid_for(3 * F), TPB, 0, s>>>(m.faces.p, F, ps.rank.p, Vr, RB, keys);
+    MG_LAUNCH_CHECK();
+    int64_t n = sort_unique(keys, 3 * F, 64, s);
+    if (n > 0) {
+      uint64_t last = 0;
+      MG_CUDA(cudaMemcpyAsync(&last, keys + n - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      if (last == ~0ull) --n;
+    }
+    p.cf_off.alloc(nb + 1);
+    p.cf_face.alloc(n > 0 ? n : 1);
+    k_lower_bounds<<<grid_for(nb + 1), TPB, 0, s>>>(keys, n, nb, p.cf_off.p);
+    if (n) k_cf_faces<<<grid_for(n), TPB, 0, s>>>(keys, n, m.faces.p, ps.rank.p, Vr, RB, p.cf_face.p);
+    MG_LAUNCH_CHECK();
+    cudaFreeAsync(keys, s);
+    int32_t ninc = 0;
+    MG_CUDA(cudaMemcpyAsync(&ninc, p.rinc_off.p + Vr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    p.rslot.alloc(ninc > 0 ? ninc : 1);
+    p.eslot.alloc((int64_t)EV_ELL_K * Vr);
+    MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+    k_cf_slots<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, RB, EV_ELL_K, p.cf_off.p, p.cf_face.p,
+                                           p.rslot.p, p.eslot.p, mx.p);
+    MG_LAUNCH_CHECK();
+    const bool bad = to_host_int(mx.p, s) != 0;
+    MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+    k_max_diff<<<grid_for(nb), TPB, 0, s>>>(p.cf_off.p, nb, mx.p);
+    MG_LAUNCH_CHECK();
+    p.cf_max = bad ? 0 : to_host_int(mx.p, s);
+  }
   MG_CUDA(cudaStreamSynchronize(s));
   p.redo.alloc(1);
   MG_CUDA(cudaMemsetAsync(p.redo.p, 0, sizeof(int), s));
