@@ -718,6 +718,12 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
 // streams it out with one bulk copy. The energy counts each face in the block
 // that owns its first corner's row.
 template <int MODE> struct CfRec { static constexpr int S = MODE == MODE_HESS ? 27 : 6; };
+#ifndef CF_DIRECT
+#define CF_DIRECT 1
+#endif
+#ifndef CF_HESS_MINB
+#define CF_HESS_MINB 4
+#endif
 
 // one face's inputs (phase A loads them for two faces before computing)
 struct CfIn {
@@ -893,7 +899,7 @@ MG_DI void cf_face(const FvArgs& a, const CfIn& d, double* out, double& val, boo
 // per SM, so its CTAs bring two threads per row to phase A
 template <int MODE, bool PSD> struct CfCfg {
   static constexpr int NT = MODE == MODE_HESS ? 128 : 64;
-  static constexpr int MINB = MODE == MODE_HESS ? 3 : 6;
+  static constexpr int MINB = MODE == MODE_HESS ? CF_HESS_MINB : 6;
 };
 template <int MODE, bool PSD, bool PIN>
 __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB))
@@ -903,6 +909,7 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB)
   extern __shared__ __align__(16) double smem[];
   double* rec = smem;
   double* hbuf = smem + (((size_t)a.cf_max * S + 1) & ~(size_t)1);  // 16-byte aligned: the row buffers' phases
+  (void)hbuf;
   const int64_t blk = blockIdx.x;
   const int64_t row = blk * PT + threadIdx.x;
   // phase B's row streams first: their loads overlap phase A
@@ -958,7 +965,10 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB)
     const int dp = (int)(meta >> 16) & 0xff;
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
     const bool fan = (meta >> 9) & 1;
-    double* hrow = hbuf + ho;
+    // CF_DIRECT: blocks go straight to the output row (each 32-byte block is
+    // one sector; fan rows write every block once), no row buffer in shared
+    // memory; other rows are cleared, then accumulated in place
+    double* hrow = CF_DIRECT ? a.hess + ro * NN : hbuf + ho;
     int nblk = 0;
     if constexpr (MODE == MODE_HESS) {
       nblk = (int)((meta >> 24) & 0xff);
@@ -1052,7 +1062,7 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB)
         dst[2] = dg[1];
         dst[3] = dg[2];
       }
-      if (nblk > 0) {
+      if (!CF_DIRECT && nblk > 0) {
         fence_proxy_async_smem();
         row_store_bulk(a.hess + ro * NN, hrow, nblk * NN);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -1077,7 +1087,7 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB)
       a.partials[(blk * PT + 32) >> 5] = 0.0;
     }
   }
-  if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if constexpr (MODE == MODE_HESS && !CF_DIRECT) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1549,16 +1559,20 @@ bool fv_cta_enabled() {
   return on;
 }
 
+// CF_HESS_CTA 0: the unclamped Hessian keeps the per-row kernel (icosphere(10):
+// per-row 2.05 ms, CTA lists 2.53 with direct block stores / 2.80 with the row
+// buffers; under the clamp the CTA lists win, 3.32 vs 3.87 ms)
+#ifndef CF_HESS_CTA
+#define CF_HESS_CTA 0
+#endif
 // shared memory of the CTA face-list kernel (face records, then the row buffers)
 size_t cta_smem(int mode, int cf_max, int hd_max) {
   const size_t S = mode == MODE_HESS ? CfRec<MODE_HESS>::S : CfRec<MODE_GRAD>::S;
-  return (((size_t)cf_max * S + 1) & ~(size_t)1) * 8 + (mode == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0);
+  return (((size_t)cf_max * S + 1) & ~(size_t)1) * 8 + (mode == MODE_HESS && !CF_DIRECT ? (size_t)hd_max * 8 + 16 : 0);
 }
-// the unclamped Hessian keeps the per-row kernel (measured 2.05 vs 2.98 ms at
-// icosphere(10): the 27-double face records cap residency at 3 CTAs/SM)
 bool fv_use_cta(const Problem& p, int mode, bool psd) {
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
-  return (mode != MODE_HESS || psd) && p.cf_max > 0 && cta_smem(mode, p.cf_max, hd) <= 227 * 1024 &&
+  return (mode != MODE_HESS || psd || CF_HESS_CTA) && p.cf_max > 0 && cta_smem(mode, p.cf_max, hd) <= 227 * 1024 &&
          fv_cta_enabled();
 }
 
