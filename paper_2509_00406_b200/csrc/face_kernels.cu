@@ -1537,6 +1537,10 @@ __global__ void __launch_bounds__(PT) k_rows_face_gather(const __grid_constant__
   a.y[(int64_t)g * 2 + 1] = fr ? y1 : 0.0;
 }
 
+// (a CTA face-list variant of the sphere kernels, each face once per 64-row
+// block like k_cta_dirichlet, measured slower at icosphere(10): gradient
+// 1.23 vs 1.105 ms, HVP 2.07 vs 1.54 — the per-incidence work is light once
+// the retraction is per vertex, so the records' round trip does not pay)
 template <int MODE>
 void launch_sphere(const Problem& p, const FvArgs& a, cudaStream_t st) {
   const int64_t nb = (a.V + PT - 1) / PT;
