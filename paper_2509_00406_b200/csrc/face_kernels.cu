@@ -724,6 +724,12 @@ template <int MODE> struct CfRec { static constexpr int S = MODE == MODE_HESS ? 
 #ifndef CF_HESS_MINB
 #define CF_HESS_MINB 4
 #endif
+#ifndef CF_FLAT_MINB
+#define CF_FLAT_MINB 8
+#endif
+#ifndef CF_NB
+#define CF_NB 3  // faces per thread with their loads in flight together (unclamped; HVP 0.866 -> 0.848 ms with MINB 8)
+#endif
 
 // one face's inputs (phase A loads them for two faces before computing)
 struct CfIn {
@@ -897,12 +903,15 @@ MG_DI void cf_face(const FvArgs& a, const CfIn& d, double* out, double& val, boo
 
 // threads per CTA (64 rows): the Hessian's larger records allow fewer CTAs
 // per SM, so its CTAs bring two threads per row to phase A
-template <int MODE, bool PSD> struct CfCfg {
+// (problems with pinned vertices under a clamp compile the masked 6x6 clamp
+// in: fewer CTAs per SM, more registers)
+template <int MODE, bool PSD, bool PIN = false> struct CfCfg {
   static constexpr int NT = MODE == MODE_HESS ? 128 : 64;
-  static constexpr int MINB = MODE == MODE_HESS ? CF_HESS_MINB : 6;
+  static constexpr int MINB = (PSD && PIN) ? (MODE == MODE_HESS ? 2 : 4)
+                                           : (MODE == MODE_HESS ? CF_HESS_MINB : CF_FLAT_MINB);
 };
 template <int MODE, bool PSD, bool PIN>
-__global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB))
+__global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::MINB))
     k_cta_dirichlet(const __grid_constant__ FvArgs a) {
   constexpr int NT = CfCfg<MODE, PSD>::NT;
   constexpr int S = CfRec<MODE>::S, NN = 4;
@@ -938,7 +947,7 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD>::MINB)
   double eacc = 0.0;
   bool ok = true;
   // two faces' loads in flight (one under a clamp: register pressure)
-  constexpr int NB = PSD ? 1 : 2;
+  constexpr int NB = PSD ? 1 : CF_NB;
   for (int i = threadIdx.x; i < nfc; i += NB * NT) {
     int4 fe[NB];
     CfIn d[NB];
