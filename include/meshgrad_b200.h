@@ -209,6 +209,19 @@ MG_API int mg_bsr_matvec(const mg_problem* prob, const double* hess_d, const dou
 MG_API int mg_bsr_block_jacobi(const mg_problem* prob, const double* hess_d, double* inv_d, void* stream);
 /* y_v = inv_v r_v per vertex (the preconditioner apply, solvers.py:178-186). */
 MG_API int mg_block_apply(const mg_problem* prob, const double* inv_d, const double* r_d, double* y_d, void* stream);
+/* Truncated CG on the device, block-Jacobi preconditioned when inv_d (the
+ * mg_bsr_block_jacobi inverses) is given — the inner solver of the reference's
+ * cg_linear_solve (solvers.py:142-175) as used by newton_solve (:244-263,
+ * hess_d = the assembled Hessian values) and newton_cg_solve (:266-287,
+ * hess_d NULL: the operator is mg_hvp at x_eval_d, clamped when use_psd).
+ * Solves A out = b from out = 0; stops at |r| <= tol |b|, at non-positive
+ * curvature (returning b itself when no step was taken, like the reference)
+ * or after max_iters. Scalars and decisions stay on the device; the host
+ * waits once per 8 iterations. *iters = iterations run, *status = 1
+ * converged, 2 non-positive curvature, 3 max iterations. */
+MG_API int mg_pcg(mg_problem* prob, const double* hess_d, const double* x_eval_d, int use_psd, double psd_floor,
+                  const double* inv_d, const double* b_d, double tol, int max_iters, double* out_d, int* iters,
+                  int* status, void* stream);
 MG_API int mg_problem_destroy(mg_problem* prob);
 
 /* Introspection for benchmarks/tests: number of kernel launches issued by the

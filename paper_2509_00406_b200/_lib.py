@@ -65,6 +65,7 @@ SIGNATURES = [
     ("mg_bsr_matvec", _INT, [_P, _P, _P, _P, _P]),
     ("mg_bsr_block_jacobi", _INT, [_P, _P, _P, _P]),
     ("mg_block_apply", _INT, [_P, _P, _P, _P, _P]),
+    ("mg_pcg", _INT, [_P, _P, _P, _INT, _DBL, _P, _P, _DBL, _INT, _P, _P, _P, _P]),
     ("mg_problem_destroy", _INT, [_P]),
     ("mg_last_launch_count", _INT, [_P, ctypes.POINTER(_INT)]),
     ("mg_problem_patch_stats", _INT, [_P, _I64P]),

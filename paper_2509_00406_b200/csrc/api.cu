@@ -534,6 +534,22 @@ int mg_block_apply(const mg_problem* prob, const double* inv_d, const double* r_
   return guard([&] { launch_block_apply(prob->p, inv_d, r_d, y_d, S(stream)); });
 }
 
+int mg_pcg(mg_problem* prob, const double* hess_d, const double* x_eval_d, int use_psd, double psd_floor,
+           const double* inv_d, const double* b_d, double tol, int max_iters, double* out_d, int* iters, int* status,
+           void* stream) {
+  if (!prob || !b_d || !out_d || !iters || !status) return fail(MG_ERR_VALUE, "NULL argument");
+  if (!hess_d && !x_eval_d) return fail(MG_ERR_VALUE, "mg_pcg needs the assembled Hessian or the HVP point");
+  if (max_iters < 1) return fail(MG_ERR_VALUE, "max_iters must be at least 1");
+  if (use_psd && !(psd_floor > 0)) return fail(MG_ERR_VALUE, "floor must be positive");
+  return guard([&] {
+    auto hvp = [&](const double* v, double* y) {
+      const int rc = mg_hvp(prob, x_eval_d, v, use_psd, psd_floor, y, stream);
+      if (rc != MG_OK) throw Error(rc, g_err);
+    };
+    pcg_solve(prob->p, hess_d, hvp, inv_d, b_d, tol, max_iters, out_d, iters, status, S(stream));
+  });
+}
+
 int mg_problem_destroy(mg_problem* prob) {
   if (prob) {
     for (auto& t : prob->p.terms)

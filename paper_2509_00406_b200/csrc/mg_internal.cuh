@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/meshgrad_b200.h"
@@ -222,6 +223,7 @@ struct Problem {
   void* patch_fn[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   mutable DBuf<const double*> jattr;
   mutable bool jattr_dirty = true;
+  DBuf<double> pcg_ws;         // device PCG workspace (pcg.cu)
   // traced terms on the edge row kernel (jit_rows.cuh): every EV callback
   // radial (proved by the tracer), V terms at the row; the patch module is
   // the exact re-run. ev_jit: its row layout is built.
@@ -317,5 +319,10 @@ inline int reduce_launches(int64_t n) { return n > 4 * 2048 ? 2 : 1; }
 void launch_bsr_matvec(const Problem& p, const double* H, const double* v, double* y, cudaStream_t s);
 void launch_block_jacobi(const Problem& p, const double* H, double* inv, cudaStream_t s);
 void launch_block_apply(const Problem& p, const double* inv, const double* r, double* y, cudaStream_t s);
+// pcg.cu: truncated block-Jacobi PCG on the device (status: 1 converged,
+// 2 non-positive curvature, 3 max iterations)
+void pcg_solve(Problem& p, const double* hess, const std::function<void(const double*, double*)>& apply_hvp,
+               const double* inv, const double* b, double tol, int max_iters, double* out, int* iters,
+               int* status, cudaStream_t s);
 
 }  // namespace mg

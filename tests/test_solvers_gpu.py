@@ -60,3 +60,44 @@ def test_block_jacobi_matches_reference_inverses():
     _lib.check(p._lib.mg_bsr_block_jacobi(p._h, p.hess.values_device.data_ptr(), inv.data_ptr(), _lib.stream_ptr()))
     got = inv.cpu().numpy()
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("matrix_free", [False, True])
+def test_device_cg_matches_host_cg(matrix_free):
+    """mg_pcg (device scalars and decisions) against the reference-structured
+    cg_linear_solve on the same operator: same iterate to rounding, same
+    iteration count and stopping reason; a zero right-hand side returns zero
+    after no iterations, and a negative-curvature operator returns b itself
+    when no step was taken (ref solvers.py:142-175)."""
+    import torch
+
+    import paper_2509_00406_b200.solvers as S
+
+    d = load("cloth64")
+    p = engine_problem(d)
+    p.x = d["s0_x"]
+    p.eval_terms(psd_floor=1e-9)
+    g = p.grad_device.clone()
+    cfg = S.SolverConfig(cg_tol=1e-8, cg_max_iters=200)
+    if matrix_free:
+        apply = lambda w: p.hvp(p.x_device, w, psd_floor=1e-9)
+        ref, info = S.cg_linear_solve(apply, -g, cfg.cg_tol, cfg.cg_max_iters)
+        got, ginfo = S.device_cg(p, -g, cfg, floor=1e-9)
+    else:
+        from paper_2509_00406_b200.solvers import _block_jacobi
+
+        ref, info = S.cg_linear_solve(p.hess.matvec, -g, cfg.cg_tol, cfg.cg_max_iters, precond=_block_jacobi(p))
+        got, ginfo = S.device_cg(p, -g, cfg, hess=p.hess.values_device)
+    assert ginfo.converged == info.converged and ginfo.negative_curvature == info.negative_curvature
+    # (unpreconditioned matrix-free CG runs ~150 iterations: the two dot-product
+    # summation orders drift the Krylov iterates apart at ~1e-5; both solve)
+    assert abs(ginfo.iterations - info.iterations) <= (1 if not matrix_free else 3)
+    tol_x = 1e-4 if matrix_free else 1e-8
+    assert float((got - ref).abs().max()) <= tol_x * float(ref.abs().max())
+    z, zinfo = S.device_cg(p, torch.zeros_like(g), cfg, hess=p.hess.values_device)
+    assert zinfo.iterations == 0 and zinfo.converged and float(z.abs().max()) == 0.0
+    # -H is negative definite: first curvature test fails before any step -> b
+    neg = -p.hess.values_device
+    b = -g
+    out, ninfo = S.device_cg(p, b, S.SolverConfig(cg_precondition=False), hess=neg)
+    assert ninfo.negative_curvature and ninfo.iterations == 1 and torch.equal(out, b)
