@@ -671,7 +671,42 @@ def run_extras(p, v, V, E, nnzb, steps, peak, peak_kind):
                                      cloth_hvp_bytes(V, E), kernel_label(p, "hvp_psd"), peak, peak_kind, k),
         "cloth_energy_only": call_record(p, lambda: p.eval_energy_only(xd), te, "term_elements",
                                          cloth_energy_bytes(V, E), "k_elem energy (3 launches)", peak, peak_kind, k),
+        "cloth_newton_cg": run_pcg(p, nnzb, V),
     }
+
+
+def run_pcg(p, nnzb, V, iters=40):
+    """The Newton direction solve on the headline Hessian (newton_solve's inner
+    CG, block-Jacobi PCG, a fixed 40 iterations: tol 0): the device PCG
+    (mg_pcg, scalars on the GPU) against the reference-structured
+    cg_linear_solve on the same device operators (3 host syncs per
+    iteration); per-iteration wall time on the host clock (syncs included),
+    and the SpMV's HBM fraction (72 nnzb + 48 V bytes per iteration)."""
+    import torch
+
+    import paper_2509_00406_b200.solvers as S
+
+    p.eval_terms(psd_floor=FLOOR)
+    b = -p.grad_device.clone()
+    cfg = S.SolverConfig(cg_tol=0.0, cg_max_iters=iters)
+    out = {}
+    for name, fn in (("device_pcg", lambda: S.device_cg(p, b, cfg, hess=p.hess.values_device)),
+                     ("host_cg", lambda: S.cg_linear_solve(p.hess.matvec, b, 0.0, iters,
+                                                           precond=S._block_jacobi(p)))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            _, info = fn()
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t0) * 1e3 / 3
+        out[name] = {"ms_per_solve": ms, "iterations": info.iterations, "ms_per_iteration": ms / info.iterations}
+    spmv_bytes = 72 * nnzb + 48 * V
+    it_ms = out["device_pcg"]["ms_per_iteration"]
+    out["device_pcg"]["spmv_bytes_per_iteration"] = spmv_bytes
+    out["device_pcg"]["hbm_frac_spmv_bytes"] = spmv_bytes / (it_ms * 1e-3) / 1e9 / peaks()[0]
+    out["speedup"] = out["host_cg"]["ms_per_solve"] / out["device_pcg"]["ms_per_solve"]
+    return out
 
 
 def run_traced(n, steps, peak, peak_kind):
@@ -779,11 +814,11 @@ def run_configs(peak, peak_kind, sub=10):
     out[pre + "_grad_hess"] = call_record(p, lambda: p.eval_terms(sync=False), F, "faces", b_hess,
                                           "k_rows_dirichlet<HESS>", peak, peak_kind, extra=ex)
     out[pre + "_grad_hess_psd"] = call_record(p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), F, "faces",
-                                              b_hess, "k_face_psd + k_rows_dirichlet<HESS,psd>", peak, peak_kind)
+                                              b_hess, "k_cta_dirichlet<HESS,psd>", peak, peak_kind)
     out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces", b_hvp,
-                                    "k_rows_dirichlet<HVP>", peak, peak_kind)
+                                    "k_cta_dirichlet<HVP>", peak, peak_kind)
     out[pre + "_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), F, "faces", b_hvp,
-                                        "k_face_psd + k_rows_dirichlet<HVP,psd>", peak, peak_kind)
+                                        "k_cta_dirichlet<HVP,psd>", peak, peak_kind)
     del p, vd, y, mesh
     gc_cuda()
     # config 4: sphere manifold HVP (and its gradient), smoothing HVP (and gradient)

@@ -23,6 +23,10 @@ def label_of(kernel):
     if m:
         mode, psd, _ = m.groups()
         return f"k_rows_dirichlet<{MODES[mode]}{',psd' if psd == '1' else ''}>"
+    m = re.search(r"k_cta_dirichlet<(\d), (\d), (\d)>", kernel)
+    if m:
+        mode, psd, _ = m.groups()
+        return f"k_cta_dirichlet<{MODES[mode]}{',psd' if psd == '1' else ''}>"
     m = re.search(r"k_rows_sphere<(\d)>", kernel)
     if m:
         return f"k_rows_sphere<{MODES[m.group(1)]}>"
