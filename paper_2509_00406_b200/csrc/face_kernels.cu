@@ -66,8 +66,8 @@ struct FvArgs {
   // slot in its block's list (ELL slot-major for the first KF, then CSR)
   const int32_t* cf_off;     // (blocks + 1)
   const int4* cf_face;       // {face | own0 << 31, corner 0, 1, 2}
-  const uint16_t* eslot;     // (KF, V)
-  const uint16_t* rslot;     // (incidences) parallel to rrec
+  const uint16_t* eslot;     // (KF, V) slot | corner << 14
+  const uint16_t* rslot;     // (incidences) parallel to rrec, same packing
   int cf_max;                // max faces of one block (shared-memory records)
 };
 
@@ -938,7 +938,9 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
     }
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
-      rc[j] = a.ell[(int64_t)j * a.V + row];
+      // the gradient / HVP rows need only the slot and the corner (packed in
+      // eslot); the Hessian rows also the records' block positions
+      rc[j] = MODE == MODE_HESS ? a.ell[(int64_t)j * a.V + row] : 0;
       sl[j] = a.eslot[(int64_t)j * a.V + row];
     }
   }
@@ -987,9 +989,9 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
     double vec[2] = {0.0, 0.0}, dg[3] = {0.0, 0.0, 0.0};
     double carry[4] = {0.0, 0.0, 0.0, 0.0}, first[4] = {0.0, 0.0, 0.0, 0.0};
     int first_pos = 255, last_pos2 = 255;
-    auto incidence = [&](uint64_t r64, int slot, int jidx) {
-      const uint32_t lo = (uint32_t)r64, hi = (uint32_t)(r64 >> 32);
-      const int s = (int)(lo >> 30);
+    auto incidence = [&](uint64_t r64, int sp, int jidx) {
+      const uint32_t hi = (uint32_t)(r64 >> 32);
+      const int s = sp >> 14, slot = sp & 0x3fff;
       const double* r = rec + (size_t)slot * S;
       vec[0] += r[2 * s];
       vec[1] += r[2 * s + 1];

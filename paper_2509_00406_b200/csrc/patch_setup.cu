@@ -472,7 +472,7 @@ __global__ void k_cf_faces(const uint64_t* keys, int64_t n, const int32_t* faces
 }
 
 // per incidence: its face's slot in the row's block list (binary search, the
-// list is sorted by face); ELL copy of the first K slot-major
+// list is sorted by face) | the row's corner << 14; ELL copy of the first K slot-major
 __global__ void k_cf_slots(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr, int RB, int K,
                            const int32_t* cf_off, const int4* cf, uint16_t* rslot, uint16_t* eslot, int* bad) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -487,8 +487,9 @@ __global__ void k_cf_slots(const int32_t* rinc_off, const uint64_t* rrec, int64_
       const int mid = (lo + hi) >> 1;
       if (((uint32_t)cf[mid].x & 0x7fffffffu) < f) lo = mid + 1; else hi = mid;
     }
-    if (lo >= b1 || ((uint32_t)cf[lo].x & 0x7fffffffu) != f || lo - b0 > 0xffff) *bad = 1;
-    const uint16_t sl = (uint16_t)(lo - b0);
+    if (lo >= b1 || ((uint32_t)cf[lo].x & 0x7fffffffu) != f || lo - b0 >= (1 << 14)) *bad = 1;
+    // slot | the row's corner in the face << 14 (all the gradient / HVP rows need)
+    const uint16_t sl = (uint16_t)((lo - b0) | (((uint32_t)rrec[k0 + k] >> 30) << 14));
     rslot[k0 + k] = sl;
     if (k < K) eslot[(int64_t)k * Vr + r] = sl;
   }
