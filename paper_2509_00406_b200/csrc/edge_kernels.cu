@@ -881,7 +881,7 @@ bool persistent_enabled() {
 template <class K>
 int64_t flat_grid(K kern, int64_t V, int block) {
   const int64_t nb = (V + block - 1) / block;
-  if (!EV_FLAT_PERSIST) return nb;
+  if (!EV_FLAT_PERSIST && !EV_STAGED) return nb;
   int dev = 0, sms = 148, per_sm = 1;
   MG_CUDA(cudaGetDevice(&dev));
   MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -990,11 +990,13 @@ void fill_ev_args(const Problem& p, const LaunchCtx& c, int64_t partial_offset, 
   std::memset(&a, 0, sizeof(a));
   a.nterms = (int)p.terms.size();
   a.V = m.Vr;
-  a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr : m.patches.order.p;
+  a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr
+            : (p.order_pad.n >= m.Vr && p.order_pad.p ? p.order_pad.p : m.patches.order.p);
   a.pfix = p.pfix.p;
   a.rmeta = p.rmeta.p;
   a.ell = p.ell.p;
   a.ell32 = p.ell32_ok ? p.ell32.p : nullptr;
+  a.es = p.ell_stride ? p.ell_stride : m.Vr;
   a.rinc_off = p.rinc_off.p;
   a.rrec = p.rrec.p;
   a.prow_ro = p.prow_ro.p;
@@ -1076,8 +1078,17 @@ int64_t launch_rows_jit(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   const int B = mode == MODE_HESS ? FastCfg<MODE_HESS, false>::BLOCK
                 : mode == MODE_GRAD ? FastCfg<MODE_GRAD, false>::BLOCK
                 : c.psd ? FastCfg<MODE_HVP, true>::BLOCK : FastCfg<MODE_HVP, false>::BLOCK;
+  int64_t grid = (m.Vr + B - 1) / B;
+  if (EV_STAGED && mode != MODE_HESS) {  // persistent CTAs (their residency: the kernels' launch bounds)
+    int dev = 0, sms = 148;
+    MG_CUDA(cudaGetDevice(&dev));
+    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t per_sm = mode == MODE_GRAD ? FastMinb<MODE_GRAD, false, false>::v
+                           : c.psd ? FastMinb<MODE_HVP, true, false>::v : FastMinb<MODE_HVP, false, false>::v;
+    if ((int64_t)sms * per_sm < grid) grid = (int64_t)sms * per_sm;
+  }
   timing_begin(p, c.stream);
-  jit_rows_launch(p, mode, c.psd, &a, (m.Vr + B - 1) / B, B, sm, c.stream);
+  jit_rows_launch(p, mode, c.psd, &a, grid, B, sm, c.stream);
   timing_end(p, c.stream);
   return np;
 }

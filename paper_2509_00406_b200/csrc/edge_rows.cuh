@@ -33,6 +33,7 @@ struct EvArgs {
   const uint8_t* pfix;       // (V) pinned flag of each row
   const uint32_t* rmeta;     // (V) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
   const uint64_t* ell;       // (EV_ELL_K, V) first incidences, slot-major
+  int64_t es;                // slot stride of ell / ell32 (V padded to whole row blocks; rmeta / order padded too)
   const uint32_t* ell32;     // (EV_ELL_K, V) vertex-only 32-bit records for the gradient / HVP kernels
                              // when no EV term reads a per-edge attribute (patch_setup.cu k_ell32), or null
   const int32_t* rinc_off;   // (V+1)
@@ -113,6 +114,31 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
   cd = r > 0.0 ? (md - mt) * rcp_fast(r) : 0.0;
 }
 
+// mbarrier + bulk (TMA) copy helpers: one thread arms a stage's barrier with
+// the byte count and issues the copies; the copies complete the transaction
+MG_DI uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+MG_DI void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+MG_DI void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+MG_DI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+MG_DI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+MG_DI void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n"
+               ".reg .pred P1;\n"
+               "LAB_WAIT:\n"
+               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               "@P1 bra DONE;\n"
+               "bra LAB_WAIT;\n"
+               "DONE:\n"
+               "}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 // incidences per row held in registers (the rest are streamed) and the
 // occupancy target: the Hessian kernel is bounded by its shared-memory row
 // buffers anyway; the smem-free HVP / gradient kernels trade prefetch depth
@@ -127,6 +153,15 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
 // row's level-1 streams in flight (A/B knob)
 #ifndef EV_FLAT_PERSIST
 #define EV_FLAT_PERSIST 0
+#endif
+// gradient / HVP kernels: persistent CTAs whose row blocks' level-1 streams
+// (ELL records, meta words, row order) arrive by bulk (TMA) copies EV_STAGES
+// blocks ahead into a shared-memory ring (0: per-thread loads)
+#ifndef EV_STAGED
+#define EV_STAGED 1
+#endif
+#ifndef EV_STAGES
+#define EV_STAGES 2  // cloth HVP 0.190 -> 0.173 ms at 2 or 3 (2240^2); smoothing HVP 0.281 -> 0.271 at 2, 0.295 at 3
 #endif
 // MAXI: incidences in flight; BLOCK: threads per CTA (the Hessian kernel's CTA
 // is its row-buffer group, EV_ROW_BLOCK); MINB: CTAs per SM to fit
@@ -191,28 +226,84 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       l.ro = a.prow_ro[r];
       l.ho = a.hoff[r];
 #pragma unroll
-      for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
-    } else if (Pol::kVertexOnly && a.ell32) {  // vertex-only records (no per-edge attribute is read)
+      for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.es + r];
+    } else if (Pol::kVertexOnly) {  // vertex-only records (no per-edge attribute is read)
 #pragma unroll
       for (int j = 0; j < EV_ELL_K; ++j) {
-        const uint32_t q = a.ell32[(int64_t)j * a.V + r];
+        const uint32_t q = a.ell32[(int64_t)j * a.es + r];
         const uint32_t o = q & 0x7fffffffu;
         const uint32_t lo = (uint32_t)(o < (uint32_t)l.g) << 31;  // edge id unused; first vertex: o > g
         l.rc[j] = (uint64_t)lo | ((uint64_t)q << 32);
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.V + r];
+      for (int j = 0; j < EV_ELL_K; ++j) l.rc[j] = a.ell[(int64_t)j * a.es + r];
     }
   };
   const int64_t nblk = (a.V + PTB - 1) / PTB;
   bool finite = true;
   L1 cur, nxt;
-  constexpr bool PERSIST = MODE == MODE_HESS || EV_FLAT_PERSIST;
+  constexpr bool STAGED = MODE != MODE_HESS && EV_STAGED;
+  constexpr bool PERSIST = MODE == MODE_HESS || (EV_FLAT_PERSIST && !STAGED);
   if constexpr (PERSIST) load_l1((int64_t)blockIdx.x * PTB + threadIdx.x, cur);
-  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  // staged level 1 (see EV_STAGED): ring of EV_STAGES stages, each one row
+  // block's slot-major ELL slices, meta words and row order
+  // (vertex-only problems always carry the 32-bit records: patch_setup.cu)
+  constexpr bool vo = Pol::kVertexOnly;
+  constexpr int ST_ELL = EV_ELL_K * PTB * (vo ? 4 : 8), ST_BYTES = ST_ELL + 2 * PTB * 4;
+  __shared__ __align__(128) unsigned char stg[STAGED ? EV_STAGES : 1][STAGED ? ST_BYTES : 16];
+  __shared__ __align__(8) uint64_t sbar[EV_STAGES];
+  auto stage_issue = [&](int st, int64_t b) {  // one thread
+    constexpr uint32_t esz = vo ? 4u : 8u;
+    mbar_expect_tx(&sbar[st], EV_ELL_K * PTB * esz + PTB * 4 + (a.order ? PTB * 4 : 0));
+#pragma unroll
+    for (int j = 0; j < EV_ELL_K; ++j) {
+      const void* src = vo ? (const void*)(a.ell32 + (int64_t)j * a.es + b * PTB)
+                           : (const void*)(a.ell + (int64_t)j * a.es + b * PTB);
+      bulk_g2s(stg[st] + j * PTB * esz, src, PTB * esz, &sbar[st]);
+    }
+    bulk_g2s(stg[st] + ST_ELL, a.rmeta + b * PTB, PTB * 4, &sbar[st]);
+    if (a.order) bulk_g2s(stg[st] + ST_ELL + PTB * 4, a.order + b * PTB, PTB * 4, &sbar[st]);
+  };
+  if constexpr (STAGED) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < EV_STAGES; ++st) mbar_init(&sbar[st], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int st = 0; st < EV_STAGES; ++st) {
+        const int64_t b = blockIdx.x + (int64_t)st * gridDim.x;
+        if (b < nblk) stage_issue(st, b);
+      }
+  }
+  int it = 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
   const int64_t row = blk * PTB + threadIdx.x;
-  if constexpr (PERSIST) {
+  if constexpr (STAGED) {
+    const int st = it % EV_STAGES;
+    mbar_wait(&sbar[st], (uint32_t)(it / EV_STAGES) & 1u);
+    const unsigned char* sp = stg[st];
+    cur.g = a.order ? reinterpret_cast<const int32_t*>(sp + ST_ELL + PTB * 4)[threadIdx.x] : (int)row;
+    cur.meta = reinterpret_cast<const uint32_t*>(sp + ST_ELL)[threadIdx.x];
+#pragma unroll
+    for (int j = 0; j < EV_ELL_K; ++j) {
+      if (vo) {
+        const uint32_t q = reinterpret_cast<const uint32_t*>(sp)[j * PTB + threadIdx.x];
+        const uint32_t lo = (uint32_t)((q & 0x7fffffffu) < (uint32_t)cur.g) << 31;
+        cur.rc[j] = (uint64_t)lo | ((uint64_t)q << 32);
+      } else {
+        cur.rc[j] = reinterpret_cast<const uint64_t*>(sp)[j * PTB + threadIdx.x];
+      }
+    }
+    __syncthreads();  // every thread has read the stage: refill it
+    if (threadIdx.x == 0 && blk + (int64_t)EV_STAGES * gridDim.x < nblk) {
+      // the threads' generic-proxy reads of the stage before the bulk copy's
+      // async-proxy writes into it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      stage_issue(st, blk + (int64_t)EV_STAGES * gridDim.x);
+    }
+  } else if constexpr (PERSIST) {
     if (blk + gridDim.x < nblk) load_l1(row + (int64_t)gridDim.x * PTB, nxt);
   } else {
     load_l1(row, cur);
@@ -411,7 +502,7 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
   }
   if constexpr (PERSIST) cur = nxt;
-  else break;  // one row block per CTA outside the Hessian
+  else if constexpr (!STAGED) break;  // one row block per CTA (unstaged gradient / HVP)
   }
   if (!finite) *a.redo = 1;
   if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

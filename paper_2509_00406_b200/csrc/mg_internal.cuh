@@ -187,6 +187,8 @@ struct Problem {
   DBuf<uint32_t> rmeta;        // (Vr) incidence count (sat. 255) | pinned << 8 | diagonal position << 16
   DBuf<uint64_t> ell;          // (EV_ELL_K, Vr) first incidences of each row, slot-major
   DBuf<uint32_t> ell32;        // (EV_ELL_K, Vr) vertex-only 32-bit records (k_ell32): gradient / HVP edge rows
+  int64_t ell_stride = 0;      // edge rows: slot stride of ell / ell32 (Vr padded to whole row blocks)
+  DBuf<int32_t> order_pad;     // edge rows: the row order padded to whole row blocks (staged kernels)
   bool ell32_ok = false;       // built (no EV term reads a per-edge attribute)
   DBuf<uint64_t> ellv;         // face rows: (EV_ELL_K, Vr) the incidence's other two corners (s+1 | s+2 << 32)
   // face rows, CTA face lists (k_cta_dirichlet): per EV_ROW_BLOCK rows its

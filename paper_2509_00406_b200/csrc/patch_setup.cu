@@ -404,11 +404,13 @@ __global__ void k_row_meta(const int32_t* rinc_off, const uint8_t* pfix, const u
 
 // ELL copy of the first K incidences of every row, slot-major (slot k of row i
 // at k * Vr + i: consecutive rows read consecutive words)
-__global__ void k_ell(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr, int K, uint64_t* ell) {
+__global__ void k_ell(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr, int K, uint64_t* ell,
+                      int64_t stride = 0) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Vr) return;
+  if (!stride) stride = Vr;
   const int k0 = rinc_off[i], c = rinc_off[i + 1] - k0;
-  for (int k = 0; k < K; ++k) ell[(int64_t)k * Vr + i] = k < c ? rrec[k0 + k] : 0ull;
+  for (int k = 0; k < K; ++k) ell[(int64_t)k * stride + i] = k < c ? rrec[k0 + k] : 0ull;
 }
 
 // Vertex-only 32-bit copies of the ELL incidence records (other |
@@ -419,12 +421,12 @@ __global__ void k_ell(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr,
 // smoothing HVP / gradient; an edge-id delta variant for the spring was 2%
 // slower (the decode sits on the gathers' dependency chain) and was dropped.
 __global__ void k_ell32(const int32_t* rinc_off, const uint64_t* rrec, const int32_t* order, int64_t Vr, int K,
-                        uint32_t* ell32) {
+                        uint32_t* ell32, int64_t stride) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Vr) return;
   const int k0 = rinc_off[i], c = rinc_off[i + 1] - k0;
   const int64_t g = order ? order[i] : i;
-  for (int k = 0; k < K; ++k) ell32[(int64_t)k * Vr + i] = k < c ? (uint32_t)(rrec[k0 + k] >> 32) : (uint32_t)g;
+  for (int k = 0; k < K; ++k) ell32[(int64_t)k * stride + i] = k < c ? (uint32_t)(rrec[k0 + k] >> 32) : (uint32_t)g;
 }
 
 // face rows: the other two corners (s+1, s+2 mod 3) of each ELL face incidence,
@@ -934,26 +936,44 @@ void build_rows_ev(Problem& p, cudaStream_t s, bool tiles) {
     MG_LAUNCH_CHECK();
     p.max_patch_hdoubles = to_host_int(mx.p, s);
   }
-  p.rmeta.alloc(Vr > 0 ? Vr : 1);
-  p.ell.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
+  // the edge rows' per-row streams padded to whole row blocks (slot stride
+  // Vp = a multiple of EV_ROW_BLOCK): every block's slice of every stream is
+  // one aligned bulk (TMA) copy for the staged gradient / HVP kernels
+  const int64_t Vp = (Vr + RB - 1) / RB * RB;
+  p.ell_stride = Vp;
+  p.rmeta.alloc(Vp > 0 ? Vp : 1);
+  p.ell.alloc(Vp > 0 ? (int64_t)EV_ELL_K * Vp : 1);
+  if (Vp) {
+    MG_CUDA(cudaMemsetAsync(p.rmeta.p, 0, sizeof(uint32_t) * Vp, s));
+    MG_CUDA(cudaMemsetAsync(p.ell.p, 0, sizeof(uint64_t) * EV_ELL_K * Vp, s));
+  }
   if (Vr) {
     k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, p.prow_len.p, Vr, p.rmeta.p);
-    k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
+    k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p, Vp);
   }
   MG_LAUNCH_CHECK();
+  {
+    const bool ident = m.row_order_used == MG_ROW_IDENTITY && !m.owned.p;
+    p.order_pad.alloc(!ident && Vp > 0 ? Vp : 1);
+    if (!ident && Vp) {
+      MG_CUDA(cudaMemsetAsync(p.order_pad.p, 0, sizeof(int32_t) * Vp, s));
+      MG_CUDA(cudaMemcpyAsync(p.order_pad.p, ps.order.p, sizeof(int32_t) * Vr, cudaMemcpyDeviceToDevice, s));
+    }
+  }
   // vertex-only records for the gradient / HVP kernels when no edge term reads
-  // a per-edge attribute (MG_ELL32=0: 64-bit records, A/B runs)
+  // a per-edge attribute (the kernels of such problems read only these)
   {
     bool vo = true;
     for (auto& t : p.terms)
       if (t.dev.op == MG_OP_EV) vo &= t.jit ? t.jit_attrs.empty() : t.dev.type == MG_TERM_EDGE_LENGTH;
-    const char* env = getenv("MG_ELL32");
-    p.ell32_ok = vo && Vr > 0 && !(env && env[0] == '0');
-    p.ell32.alloc(p.ell32_ok ? (int64_t)EV_ELL_K * Vr : 1);
+    p.ell32_ok = vo && Vr > 0;
+    p.ell32.alloc(p.ell32_ok ? (int64_t)EV_ELL_K * Vp : 1);
     const bool ident = m.row_order_used == MG_ROW_IDENTITY && !m.owned.p;
-    if (p.ell32_ok)
+    if (p.ell32_ok) {
+      MG_CUDA(cudaMemsetAsync(p.ell32.p, 0, sizeof(uint32_t) * EV_ELL_K * Vp, s));
       k_ell32<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, ident ? nullptr : ps.order.p, Vr, EV_ELL_K,
-                                           p.ell32.p);
+                                           p.ell32.p, Vp);
+    }
     MG_LAUNCH_CHECK();
   }
   MG_CUDA(cudaStreamSynchronize(s));

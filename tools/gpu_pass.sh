@@ -1,4 +1,5 @@
-tag=r2a
+# One GPU-box pass: GPU test suite, smoke(), default bench line. usage (under gpurun): bash tools/gpu_pass.sh <tag>
+tag=${1:-pass}
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/smi_${tag}.txt 2>&1
 timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_${tag}.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_${tag}.log
