@@ -935,7 +935,7 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
     constexpr int FB = FastCfg<MODE, PSD>::BLOCK;
     const int64_t nfb = (a.V + FB - 1) / FB;
     int64_t grid = MODE == MODE_HESS ? nfb : flat_grid(fast, a.V, FB);
-    if (MODE == MODE_HESS && persistent_enabled()) {
+    if (MODE == MODE_HESS && (persistent_enabled() || EV_STAGED_HESS)) {
       int dev = 0, sms = 148, per_sm = 1;
       MG_CUDA(cudaGetDevice(&dev));
       MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -160,6 +160,12 @@ MG_DI void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifndef EV_STAGED
 #define EV_STAGED 1
 #endif
+#ifndef EV_STAGED_HESS
+#define EV_STAGED_HESS 1  // headline 0.617 -> 0.543 ms (cloth 2048^2 grad+H(psd)), plain 0.553 -> 0.485
+#endif
+#ifndef EV_STAGES_HESS
+#define EV_STAGES_HESS 2
+#endif
 #ifndef EV_STAGES
 #define EV_STAGES 2  // cloth HVP 0.190 -> 0.173 ms at 2 or 3 (2240^2); smoothing HVP 0.281 -> 0.271 at 2, 0.295 at 3
 #endif
@@ -243,36 +249,45 @@ MG_DI void rows_fast_body(const EvArgs& a) {
   const int64_t nblk = (a.V + PTB - 1) / PTB;
   bool finite = true;
   L1 cur, nxt;
-  constexpr bool STAGED = MODE != MODE_HESS && EV_STAGED;
-  constexpr bool PERSIST = MODE == MODE_HESS || (EV_FLAT_PERSIST && !STAGED);
+  constexpr bool STAGED = MODE != MODE_HESS ? EV_STAGED : EV_STAGED_HESS;
+  constexpr bool PERSIST = !STAGED && (MODE == MODE_HESS || EV_FLAT_PERSIST);
+  constexpr bool HS = MODE == MODE_HESS;  // the Hessian's stages also carry row starts and row-buffer offsets
   if constexpr (PERSIST) load_l1((int64_t)blockIdx.x * PTB + threadIdx.x, cur);
   // staged level 1 (see EV_STAGED): ring of EV_STAGES stages, each one row
   // block's slot-major ELL slices, meta words and row order
   // (vertex-only problems always carry the 32-bit records: patch_setup.cu)
   constexpr bool vo = Pol::kVertexOnly;
-  constexpr int ST_ELL = EV_ELL_K * PTB * (vo ? 4 : 8), ST_BYTES = ST_ELL + 2 * PTB * 4;
-  __shared__ __align__(128) unsigned char stg[STAGED ? EV_STAGES : 1][STAGED ? ST_BYTES : 16];
-  __shared__ __align__(8) uint64_t sbar[EV_STAGES];
+  constexpr int ST_ELL = EV_ELL_K * PTB * ((vo && !HS) ? 4 : 8);
+  constexpr int ST_RO = ST_ELL + 2 * PTB * 4, ST_HO = ST_RO + PTB * 8;
+  constexpr int ST_BYTES = HS ? ST_HO + PTB * 4 : ST_RO;
+  constexpr int NST = HS ? EV_STAGES_HESS : EV_STAGES;
+  __shared__ __align__(128) unsigned char stg[STAGED ? NST : 1][STAGED ? ST_BYTES : 16];
+  __shared__ __align__(8) uint64_t sbar[NST];
   auto stage_issue = [&](int st, int64_t b) {  // one thread
-    constexpr uint32_t esz = vo ? 4u : 8u;
-    mbar_expect_tx(&sbar[st], EV_ELL_K * PTB * esz + PTB * 4 + (a.order ? PTB * 4 : 0));
+    constexpr bool v32 = vo && !HS;
+    constexpr uint32_t esz = v32 ? 4u : 8u;
+    mbar_expect_tx(&sbar[st], EV_ELL_K * PTB * esz + PTB * 4 + (a.order ? PTB * 4 : 0) + (HS ? PTB * 12 : 0));
 #pragma unroll
     for (int j = 0; j < EV_ELL_K; ++j) {
-      const void* src = vo ? (const void*)(a.ell32 + (int64_t)j * a.es + b * PTB)
-                           : (const void*)(a.ell + (int64_t)j * a.es + b * PTB);
+      const void* src = v32 ? (const void*)(a.ell32 + (int64_t)j * a.es + b * PTB)
+                            : (const void*)(a.ell + (int64_t)j * a.es + b * PTB);
       bulk_g2s(stg[st] + j * PTB * esz, src, PTB * esz, &sbar[st]);
     }
     bulk_g2s(stg[st] + ST_ELL, a.rmeta + b * PTB, PTB * 4, &sbar[st]);
     if (a.order) bulk_g2s(stg[st] + ST_ELL + PTB * 4, a.order + b * PTB, PTB * 4, &sbar[st]);
+    if constexpr (HS) {
+      bulk_g2s(stg[st] + ST_RO, a.prow_ro + b * PTB, PTB * 8, &sbar[st]);
+      bulk_g2s(stg[st] + ST_HO, a.hoff + b * PTB, PTB * 4, &sbar[st]);
+    }
   };
   if constexpr (STAGED) {
     if (threadIdx.x == 0) {
-      for (int st = 0; st < EV_STAGES; ++st) mbar_init(&sbar[st], 1);
+      for (int st = 0; st < NST; ++st) mbar_init(&sbar[st], 1);
       mbar_fence_init();
     }
     __syncthreads();
     if (threadIdx.x == 0)
-      for (int st = 0; st < EV_STAGES; ++st) {
+      for (int st = 0; st < NST; ++st) {
         const int64_t b = blockIdx.x + (int64_t)st * gridDim.x;
         if (b < nblk) stage_issue(st, b);
       }
@@ -281,14 +296,18 @@ MG_DI void rows_fast_body(const EvArgs& a) {
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
   const int64_t row = blk * PTB + threadIdx.x;
   if constexpr (STAGED) {
-    const int st = it % EV_STAGES;
-    mbar_wait(&sbar[st], (uint32_t)(it / EV_STAGES) & 1u);
+    const int st = it % NST;
+    mbar_wait(&sbar[st], (uint32_t)(it / NST) & 1u);
     const unsigned char* sp = stg[st];
     cur.g = a.order ? reinterpret_cast<const int32_t*>(sp + ST_ELL + PTB * 4)[threadIdx.x] : (int)row;
     cur.meta = reinterpret_cast<const uint32_t*>(sp + ST_ELL)[threadIdx.x];
+    if constexpr (HS) {
+      cur.ro = reinterpret_cast<const int64_t*>(sp + ST_RO)[threadIdx.x];
+      cur.ho = reinterpret_cast<const int32_t*>(sp + ST_HO)[threadIdx.x];
+    }
 #pragma unroll
     for (int j = 0; j < EV_ELL_K; ++j) {
-      if (vo) {
+      if (vo && !HS) {
         const uint32_t q = reinterpret_cast<const uint32_t*>(sp)[j * PTB + threadIdx.x];
         const uint32_t lo = (uint32_t)((q & 0x7fffffffu) < (uint32_t)cur.g) << 31;
         cur.rc[j] = (uint64_t)lo | ((uint64_t)q << 32);
@@ -297,11 +316,11 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       }
     }
     __syncthreads();  // every thread has read the stage: refill it
-    if (threadIdx.x == 0 && blk + (int64_t)EV_STAGES * gridDim.x < nblk) {
+    if (threadIdx.x == 0 && blk + (int64_t)NST * gridDim.x < nblk) {
       // the threads' generic-proxy reads of the stage before the bulk copy's
       // async-proxy writes into it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      stage_issue(st, blk + (int64_t)EV_STAGES * gridDim.x);
+      stage_issue(st, blk + (int64_t)NST * gridDim.x);
     }
   } else if constexpr (PERSIST) {
     if (blk + gridDim.x < nblk) load_l1(row + (int64_t)gridDim.x * PTB, nxt);

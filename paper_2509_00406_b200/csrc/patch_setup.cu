@@ -923,13 +923,16 @@ void build_rows_ev(Problem& p, cudaStream_t s, bool tiles) {
   if (p.with_hessian && p.pattern_ready) {
     p.diag_pos.alloc(V > 0 ? V : 1);
     if (V) k_diag_pos<<<grid_for(V), TPB, 0, s>>>(p.row_offsets.p, p.col32.p, V, p.diag_pos.p);
-    p.prow_ro.alloc(Vr > 0 ? Vr : 1);
+    const int64_t Vpad = (Vr + RB - 1) / RB * RB;  // whole row blocks (staged kernels' bulk copies)
+    p.prow_ro.alloc(Vpad > 0 ? Vpad : 1);
+    if (Vpad) MG_CUDA(cudaMemsetAsync(p.prow_ro.p, 0, sizeof(int64_t) * Vpad, s));
     p.prow_len.alloc(Vr > 0 ? Vr : 1);
     p.prow_dp.alloc(Vr > 0 ? Vr : 1);
     if (Vr) k_patch_rows<<<grid_for(Vr), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, p.diag_pos.p, Vr, p.prow_ro.p,
                                                      p.prow_len.p, p.prow_dp.p);
     MG_LAUNCH_CHECK();
-    p.hoff.alloc(Vr > 0 ? Vr : 1);
+    p.hoff.alloc(Vpad > 0 ? Vpad : 1);
+    if (Vpad) MG_CUDA(cudaMemsetAsync(p.hoff.p, 0, sizeof(int32_t) * Vpad, s));
     MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
     if (nb) k_row_smem_offsets<<<grid_for(nb), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, Vr, RB, nb, p.n * p.n,
                                                            p.hoff.p, mx.p);
