@@ -25,6 +25,7 @@
 #include "elem_eval.cuh"
 #include "mg_internal.cuh"
 #include "psd.cuh"
+#include "stage.cuh"
 
 namespace mg {
 
@@ -41,6 +42,7 @@ struct FvArgs {
   const uint32_t* rmeta;     // incidence count (sat. 255) | pinned << 8 | diagonal position << 16
   const uint64_t* ell;       // (KF, V) slot-major incidence records
   const uint64_t* ellv;      // (KF, V) the incidence's other two corners (s+1, s+2)
+  int64_t es;                // slot stride of ell / ellv (V padded to whole row blocks)
   const int32_t* rinc_off;   // (V+1) CSR of all incidences
   const uint64_t* rrec;
   const int64_t* prow_ro;
@@ -320,6 +322,9 @@ MG_DI bool dirichlet_hv_closed(const double* J, const double* V, double area, do
 #ifndef FV_MINB
 #define FV_MINB 6
 #endif
+#ifndef FV_STAGES
+#define FV_STAGES 2  // staged level-1 ring of the per-row face kernels
+#endif
 // CTAs per SM to fit: the clamped Hessian path carries the per-face P_f(M)
 // of two incidences in flight and gets more registers
 template <int MODE, bool PSD> struct FvMinb {
@@ -329,24 +334,67 @@ template <int MODE, bool PSD, bool PIN = false>
 __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(const __grid_constant__ FvArgs a) {
   constexpr int N = 2, NN = 4;
   extern __shared__ __align__(16) double hbuf[];
-  const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
-  double eacc = 0.0;
   bool ok = true;
-  if (row < a.V) {
-    const int g = a.order ? a.order[row] : (int)row;
-    const uint32_t meta = a.rmeta[row];
-    int64_t ro = 0;
-    int ho = 0;
-    if constexpr (MODE == MODE_HESS) {
-      ro = a.prow_ro[row];
-      ho = a.hoff[row];
-    }
-    uint64_t rc[KF], ov[KF];
+  // Persistent CTAs walk row blocks grid-stride; each block's level-1 streams
+  // (ELL records and other-corner records, meta words, row order, row starts,
+  // row-buffer offsets) arrive by TMA FV_STAGES blocks ahead (stage.cuh)
+  constexpr bool HS = MODE == MODE_HESS;
+  constexpr int S_RC = 0, S_OV = KF * PT * 8, S_ME = 2 * KF * PT * 8, S_OR = S_ME + PT * 4, S_RO = S_OR + PT * 4,
+                S_HO = S_RO + PT * 8, S_BYTES = HS ? S_HO + PT * 4 : S_RO;
+  __shared__ __align__(128) unsigned char stg[FV_STAGES][S_BYTES];
+  __shared__ __align__(8) uint64_t sbar[FV_STAGES];
+  const int64_t nblocks = (a.V + PT - 1) / PT;
+  auto stage_issue = [&](int st, int64_t b) {  // one thread
+    mbar_expect_tx(&sbar[st], 2 * KF * PT * 8 + PT * 4 + (a.order ? PT * 4 : 0) + (HS ? PT * 12 : 0));
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
-      rc[j] = a.ell[(int64_t)j * a.V + row];
-      ov[j] = a.ellv[(int64_t)j * a.V + row];
+      bulk_g2s(stg[st] + S_RC + j * PT * 8, a.ell + (int64_t)j * a.es + b * PT, PT * 8, &sbar[st]);
+      bulk_g2s(stg[st] + S_OV + j * PT * 8, a.ellv + (int64_t)j * a.es + b * PT, PT * 8, &sbar[st]);
     }
+    bulk_g2s(stg[st] + S_ME, a.rmeta + b * PT, PT * 4, &sbar[st]);
+    if (a.order) bulk_g2s(stg[st] + S_OR, a.order + b * PT, PT * 4, &sbar[st]);
+    if constexpr (HS) {
+      bulk_g2s(stg[st] + S_RO, a.prow_ro + b * PT, PT * 8, &sbar[st]);
+      bulk_g2s(stg[st] + S_HO, a.hoff + b * PT, PT * 4, &sbar[st]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < FV_STAGES; ++st) mbar_init(&sbar[st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int st = 0; st < FV_STAGES; ++st)
+      if (blockIdx.x + (int64_t)st * gridDim.x < nblocks) stage_issue(st, blockIdx.x + (int64_t)st * gridDim.x);
+  int it = 0;
+  for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x, ++it) {
+  const int64_t row = blk * PT + threadIdx.x;
+  double eacc = 0.0;
+  const int stn = it % FV_STAGES;
+  mbar_wait(&sbar[stn], (uint32_t)(it / FV_STAGES) & 1u);
+  const unsigned char* sp = stg[stn];
+  const int g = a.order ? reinterpret_cast<const int32_t*>(sp + S_OR)[threadIdx.x] : (int)row;
+  const uint32_t meta = reinterpret_cast<const uint32_t*>(sp + S_ME)[threadIdx.x];
+  int64_t ro = 0;
+  int ho = 0;
+  if constexpr (HS) {
+    ro = reinterpret_cast<const int64_t*>(sp + S_RO)[threadIdx.x];
+    ho = reinterpret_cast<const int32_t*>(sp + S_HO)[threadIdx.x];
+  }
+  uint64_t rc[KF], ov[KF];
+#pragma unroll
+  for (int j = 0; j < KF; ++j) {
+    rc[j] = reinterpret_cast<const uint64_t*>(sp + S_RC)[j * PT + threadIdx.x];
+    ov[j] = reinterpret_cast<const uint64_t*>(sp + S_OV)[j * PT + threadIdx.x];
+  }
+  __syncthreads();  // every thread has read the stage: refill it
+  if (threadIdx.x == 0 && blk + (int64_t)FV_STAGES * gridDim.x < nblocks) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    stage_issue(stn, blk + (int64_t)FV_STAGES * gridDim.x);
+  }
+  // the previous block's bulk row stores must have read the row buffers
+  if constexpr (HS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if (row < a.V) {
     const bool fr = !((meta >> 8) & 1);
     const int dp = (int)(meta >> 16) & 0xff;
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
@@ -694,12 +742,13 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
       }
     }
   }
-  if (!ok) *a.redo = 1;
   if constexpr (MODE != MODE_HVP) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
     if ((threadIdx.x & 31) == 0) a.partials[row >> 5] = eacc;
   }
+  }  // row blocks
+  if (!ok) *a.redo = 1;
   if constexpr (MODE == MODE_HESS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
@@ -940,7 +989,7 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
     for (int j = 0; j < KF; ++j) {
       // the gradient / HVP rows need only the slot and the corner (packed in
       // eslot); the Hessian rows also the records' block positions
-      rc[j] = MODE == MODE_HESS ? a.ell[(int64_t)j * a.V + row] : 0;
+      rc[j] = MODE == MODE_HESS ? a.ell[(int64_t)j * a.es + row] : 0;
       sl[j] = a.eslot[(int64_t)j * a.V + row];
     }
   }
@@ -1198,7 +1247,7 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
     const uint32_t meta = a.rmeta[row];
     uint64_t rc[KF];
 #pragma unroll
-    for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+    for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.es + row];
     const bool fr = !((meta >> 8) & 1);
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
     const bool barrier = a.t.c[0] != 0.0, stretch = a.t.c[1] != 0.0;
@@ -1304,7 +1353,7 @@ __global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvAr
     const int ne = cnt < KF ? cnt : KF;
     uint64_t ov[KF];
 #pragma unroll
-    for (int j = 0; j < KF; ++j) ov[j] = a.ellv[(int64_t)j * a.V + row];
+    for (int j = 0; j < KF; ++j) ov[j] = a.ellv[(int64_t)j * a.es + row];
     // corners streamed one incidence ahead of the compute
     Other cur;
     if (ne > 0) cur = load_other((int)(uint32_t)ov[0], (int)(ov[0] >> 32));
@@ -1524,7 +1573,7 @@ __global__ void __launch_bounds__(PT) k_rows_face_gather(const __grid_constant__
   const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
   uint64_t rc[KF];
 #pragma unroll
-  for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.V + row];
+  for (int j = 0; j < KF; ++j) rc[j] = a.ell[(int64_t)j * a.es + row];
   double2 yv[KF];
 #pragma unroll
   for (int j = 0; j < KF; ++j) {
@@ -1609,6 +1658,15 @@ void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
   }
   auto kern = (PSD && a.fpsd6) ? k_rows_dirichlet<MODE, PSD, true> : k_rows_dirichlet<MODE, PSD, false>;
   if (sm) MG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  // persistent CTAs (the staged level-1 ring): as many as are resident
+  int64_t grid = nb;
+  {
+    int dev = 0, sms = 148, per_sm = 1;
+    MG_CUDA(cudaGetDevice(&dev));
+    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, sm));
+    if ((int64_t)sms * (per_sm > 0 ? per_sm : 1) < grid) grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  }
   timing_begin(p, st);
   if constexpr (PSD) {
     if (a.nf) k_face_psd<<<(unsigned)((a.nf + 127) / 128), 128, 0, st>>>(a);
@@ -1616,7 +1674,7 @@ void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
     if (a.nf && a.fpsd6) k_face_psd_pinned<<<(unsigned)((a.nf + 127) / 128), 128, 0, st>>>(a);
     MG_LAUNCH_CHECK();
   }
-  kern<<<(unsigned)nb, PT, sm, st>>>(a);
+  kern<<<(unsigned)grid, PT, sm, st>>>(a);
   MG_LAUNCH_CHECK();
   timing_end(p, st);
 }
@@ -1627,7 +1685,8 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   const Mesh& m = *p.mesh;
   FvArgs a;
   a.V = m.Vr;
-  a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr : m.patches.order.p;
+  a.order = (m.row_order_used == MG_ROW_IDENTITY && !m.owned.p) ? nullptr
+            : (p.order_pad.n >= m.Vr && p.order_pad.p ? p.order_pad.p : m.patches.order.p);
   a.rmeta = p.rmeta.p;
   a.ell = p.ell.p;
   a.rinc_off = p.rinc_off.p;
@@ -1636,6 +1695,7 @@ int64_t launch_patch_fv(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   a.hoff = p.hoff.p;
   a.faces = m.faces.p;
   a.ellv = p.ellv.p;
+  a.es = p.ell_stride ? p.ell_stride : m.Vr;
   a.x = c.x;
   a.w = c.w;
   a.grad = c.grad;

@@ -432,7 +432,7 @@ __global__ void k_ell32(const int32_t* rinc_off, const uint64_t* rrec, const int
 // face rows: the other two corners (s+1, s+2 mod 3) of each ELL face incidence,
 // so the row kernels skip the faces[] lookup (one dependent level less)
 __global__ void k_ellv(const int32_t* rinc_off, const uint64_t* rrec, const int32_t* faces, int64_t Vr, int K,
-                       uint64_t* ellv) {
+                       uint64_t* ellv, int64_t stride) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Vr) return;
   const int k0 = rinc_off[i], c = rinc_off[i + 1] - k0;
@@ -445,7 +445,7 @@ __global__ void k_ellv(const int32_t* rinc_off, const uint64_t* rrec, const int3
       const uint32_t o1 = (uint32_t)faces[3 * f + (s + 1) % 3], o2 = (uint32_t)faces[3 * f + (s + 2) % 3];
       v = (uint64_t)o1 | ((uint64_t)o2 << 32);
     }
-    ellv[(int64_t)k * Vr + i] = v;
+    ellv[(int64_t)k * stride + i] = v;
   }
 }
 
@@ -1032,28 +1032,47 @@ void build_rows_fv(Problem& p, cudaStream_t s) {
   if (p.with_hessian && p.pattern_ready) {
     p.diag_pos.alloc(V > 0 ? V : 1);
     if (V) k_diag_pos<<<grid_for(V), TPB, 0, s>>>(p.row_offsets.p, p.col32.p, V, p.diag_pos.p);
-    p.prow_ro.alloc(Vr > 0 ? Vr : 1);
+    const int64_t Vpad = (Vr + RB - 1) / RB * RB;  // whole row blocks (staged kernels' bulk copies)
+    p.prow_ro.alloc(Vpad > 0 ? Vpad : 1);
+    if (Vpad) MG_CUDA(cudaMemsetAsync(p.prow_ro.p, 0, sizeof(int64_t) * Vpad, s));
     p.prow_len.alloc(Vr > 0 ? Vr : 1);
     p.prow_dp.alloc(Vr > 0 ? Vr : 1);
     if (Vr) k_patch_rows<<<grid_for(Vr), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, p.diag_pos.p, Vr, p.prow_ro.p,
                                                      p.prow_len.p, p.prow_dp.p);
     MG_LAUNCH_CHECK();
-    p.hoff.alloc(Vr > 0 ? Vr : 1);
+    p.hoff.alloc(Vpad > 0 ? Vpad : 1);
+    if (Vpad) MG_CUDA(cudaMemsetAsync(p.hoff.p, 0, sizeof(int32_t) * Vpad, s));
     MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
     if (nb) k_row_smem_offsets<<<grid_for(nb), TPB, 0, s>>>(ps.order.p, p.row_offsets.p, Vr, RB, nb, p.n * p.n,
                                                            p.hoff.p, mx.p);
     MG_LAUNCH_CHECK();
     p.max_patch_hdoubles = to_host_int(mx.p, s);
   }
-  p.rmeta.alloc(Vr > 0 ? Vr : 1);
-  p.ell.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
-  p.ellv.alloc(Vr > 0 ? (int64_t)EV_ELL_K * Vr : 1);
+  // per-row streams padded to whole row blocks (the staged kernels' bulk copies)
+  const int64_t Vp = (Vr + RB - 1) / RB * RB;
+  p.ell_stride = Vp;
+  p.rmeta.alloc(Vp > 0 ? Vp : 1);
+  p.ell.alloc(Vp > 0 ? (int64_t)EV_ELL_K * Vp : 1);
+  p.ellv.alloc(Vp > 0 ? (int64_t)EV_ELL_K * Vp : 1);
+  if (Vp) {
+    MG_CUDA(cudaMemsetAsync(p.rmeta.p, 0, sizeof(uint32_t) * Vp, s));
+    MG_CUDA(cudaMemsetAsync(p.ell.p, 0, sizeof(uint64_t) * EV_ELL_K * Vp, s));
+    MG_CUDA(cudaMemsetAsync(p.ellv.p, 0, sizeof(uint64_t) * EV_ELL_K * Vp, s));
+  }
+  {
+    const bool ident = m.row_order_used == MG_ROW_IDENTITY && !m.owned.p;
+    p.order_pad.alloc(!ident && Vp > 0 ? Vp : 1);
+    if (!ident && Vp) {
+      MG_CUDA(cudaMemsetAsync(p.order_pad.p, 0, sizeof(int32_t) * Vp, s));
+      MG_CUDA(cudaMemcpyAsync(p.order_pad.p, ps.order.p, sizeof(int32_t) * Vr, cudaMemcpyDeviceToDevice, s));
+    }
+  }
   if (Vr) {
     k_row_meta<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.pfix.p, p.prow_dp.p, p.prow_len.p, Vr, p.rmeta.p);
     if (p.with_hessian && p.pattern_ready)
       k_fan_order<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, p.rmeta.p);
-    k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p);
-    k_ellv<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, EV_ELL_K, p.ellv.p);
+    k_ell<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, EV_ELL_K, p.ell.p, Vp);
+    k_ellv<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, m.faces.p, Vr, EV_ELL_K, p.ellv.p, Vp);
   }
   MG_LAUNCH_CHECK();
   // CTA face lists (k_cta_dirichlet): each block's distinct faces, per
