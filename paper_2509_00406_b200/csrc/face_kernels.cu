@@ -767,8 +767,11 @@ __global__ void __launch_bounds__(PT, FvMinb<MODE, PSD>::v) k_rows_dirichlet(con
 // streams it out with one bulk copy. The energy counts each face in the block
 // that owns its first corner's row.
 template <int MODE> struct CfRec { static constexpr int S = MODE == MODE_HESS ? 27 : 6; };
-#ifndef CF_DIRECT
-#define CF_DIRECT 1
+#ifndef CF_STAGES
+#define CF_STAGES 2  // staged row blocks (face lists + row streams) in flight per CTA
+#endif
+#ifndef CF_PERSIST_HESS
+#define CF_PERSIST_HESS 0
 #endif
 #ifndef CF_HESS_MINB
 #define CF_HESS_MINB 4
@@ -959,45 +962,109 @@ template <int MODE, bool PSD, bool PIN = false> struct CfCfg {
   static constexpr int MINB = (PSD && PIN) ? (MODE == MODE_HESS ? 2 : 4)
                                            : (MODE == MODE_HESS ? CF_HESS_MINB : CF_FLAT_MINB);
 };
+// shared-memory stage of one row block (k_cta_dirichlet): its face-list
+// entries, the rows' slot ids (slot | corner << 14), meta words, row order,
+// and for the Hessian the incidence records, row starts and row count
+template <int MODE> struct CfStage {
+  static constexpr int SL = 0, ME = KF * PT * 2, OR = ME + PT * 4, RC = OR + PT * 4,
+                       RO = RC + (MODE == MODE_HESS ? KF * PT * 8 : 0), CF = RO + (MODE == MODE_HESS ? PT * 8 : 0);
+  __host__ __device__ static size_t bytes(int cf_max) { return (size_t)CF + (size_t)cf_max * 16; }
+};
+
 template <int MODE, bool PSD, bool PIN>
 __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::MINB))
     k_cta_dirichlet(const __grid_constant__ FvArgs a) {
   constexpr int NT = CfCfg<MODE, PSD>::NT;
   constexpr int S = CfRec<MODE>::S, NN = 4;
-  extern __shared__ __align__(16) double smem[];
-  double* rec = smem;
-  double* hbuf = smem + (((size_t)a.cf_max * S + 1) & ~(size_t)1);  // 16-byte aligned: the row buffers' phases
-  (void)hbuf;
-  const int64_t blk = blockIdx.x;
+  using STG = CfStage<MODE>;
+  // the clamped Hessian reads its streams with plain loads, one row block per
+  // CTA (staged: 3.4-3.6 ms vs 3.12 at icosphere(10); its 27-double records
+  // already bound residency)
+  constexpr bool STAGED = MODE != MODE_HESS;
+  constexpr int NSTG = STAGED ? CF_STAGES : 1;
+  // persistent CTAs walk row blocks grid-stride; a block's stage (face list,
+  // row streams) arrives by TMA NSTG blocks ahead, so phase A starts
+  // with its gathers instead of a DRAM round trip for the list
+  extern __shared__ __align__(128) unsigned char cf_smem[];
+  const size_t sbytes = (STG::bytes(a.cf_max) + 127) & ~(size_t)127;
+  double* rec = reinterpret_cast<double*>(cf_smem + (STAGED ? NSTG * sbytes : 0));
+  __shared__ __align__(8) uint64_t sbar[NSTG];
+  __shared__ int snf[NSTG];
+  __shared__ double wsum[NT / 32];
+  const int64_t nblocks = (a.V + PT - 1) / PT;
+  auto stage_issue = [&](int st, int64_t b) {  // one thread
+    unsigned char* sp = cf_smem + st * sbytes;
+    const int i0 = a.cf_off[b], nf = a.cf_off[b + 1] - i0;
+    snf[st] = nf;
+    uint32_t bytes = KF * PT * 2 + PT * 4 + (a.order ? PT * 4 : 0) + (uint32_t)nf * 16;
+    if constexpr (MODE == MODE_HESS) bytes += KF * PT * 8 + PT * 8;
+    mbar_expect_tx(&sbar[st], bytes);
+#pragma unroll
+    for (int j = 0; j < KF; ++j) bulk_g2s(sp + STG::SL + j * PT * 2, a.eslot + (int64_t)j * a.es + b * PT, PT * 2, &sbar[st]);
+    bulk_g2s(sp + STG::ME, a.rmeta + b * PT, PT * 4, &sbar[st]);
+    if (a.order) bulk_g2s(sp + STG::OR, a.order + b * PT, PT * 4, &sbar[st]);
+    if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+      for (int j = 0; j < KF; ++j) bulk_g2s(sp + STG::RC + j * PT * 8, a.ell + (int64_t)j * a.es + b * PT, PT * 8, &sbar[st]);
+      bulk_g2s(sp + STG::RO, a.prow_ro + b * PT, PT * 8, &sbar[st]);
+    }
+    if (nf) bulk_g2s(sp + STG::CF, a.cf_face + i0, (uint32_t)nf * 16, &sbar[st]);
+  };
+  if constexpr (STAGED) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < NSTG; ++st) mbar_init(&sbar[st], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int st = 0; st < NSTG; ++st)
+        if (blockIdx.x + (int64_t)st * gridDim.x < nblocks) stage_issue(st, blockIdx.x + (int64_t)st * gridDim.x);
+  }
+  bool ok = true;
+  int it = 0;
+  for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x, ++it) {
   const int64_t row = blk * PT + threadIdx.x;
-  // phase B's row streams first: their loads overlap phase A
+  const int stn = it % NSTG;
+  const unsigned char* sp = cf_smem + stn * sbytes;
+  int nfc;
+  const int4* cfl;
+  if constexpr (STAGED) {
+    mbar_wait(&sbar[stn], (uint32_t)(it / NSTG) & 1u);
+    nfc = snf[stn];
+    cfl = reinterpret_cast<const int4*>(sp + STG::CF);
+  } else {
+    const int i0 = a.cf_off[blk];
+    nfc = a.cf_off[blk + 1] - i0;
+    cfl = a.cf_face + i0;
+  }
+  // phase B's row streams, from the stage into registers
   int g = 0;
   uint32_t meta = 0;
   int64_t ro = 0;
-  int ho = 0;
   uint64_t rc[KF];
   int sl[KF];
   const bool has_row = threadIdx.x < PT && row < a.V;
-  if (has_row) {
-    g = a.order ? a.order[row] : (int)row;
-    meta = a.rmeta[row];
-    if constexpr (MODE == MODE_HESS) {
-      ro = a.prow_ro[row];
-      ho = a.hoff[row];
-    }
+  if (has_row && STAGED) {
+    g = a.order ? reinterpret_cast<const int32_t*>(sp + STG::OR)[threadIdx.x] : (int)row;
+    meta = reinterpret_cast<const uint32_t*>(sp + STG::ME)[threadIdx.x];
 #pragma unroll
     for (int j = 0; j < KF; ++j) {
-      // the gradient / HVP rows need only the slot and the corner (packed in
-      // eslot); the Hessian rows also the records' block positions
+      rc[j] = 0;
+      sl[j] = reinterpret_cast<const uint16_t*>(sp + STG::SL)[j * PT + threadIdx.x];
+    }
+  } else if (has_row) {  // plain loads (their latency overlaps phase A)
+    g = a.order ? a.order[row] : (int)row;
+    meta = a.rmeta[row];
+    if constexpr (MODE == MODE_HESS) ro = a.prow_ro[row];
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
       rc[j] = MODE == MODE_HESS ? a.ell[(int64_t)j * a.es + row] : 0;
-      sl[j] = a.eslot[(int64_t)j * a.V + row];
+      sl[j] = a.eslot[(int64_t)j * a.es + row];
     }
   }
   // phase A: the block's faces, once each
-  const int i0 = a.cf_off[blk], nfc = a.cf_off[blk + 1] - i0;
   double eacc = 0.0;
-  bool ok = true;
-  // two faces' loads in flight (one under a clamp: register pressure)
+  // two / three faces' loads in flight (one under a clamp: register pressure)
   constexpr int NB = PSD ? 1 : CF_NB;
   for (int i = threadIdx.x; i < nfc; i += NB * NT) {
     int4 fe[NB];
@@ -1005,7 +1072,7 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int ib = i + b * NT;
-      fe[b] = a.cf_face[i0 + (ib < nfc ? ib : i)];
+      fe[b] = cfl[ib < nfc ? ib : i];
       cf_load<MODE, PSD>(a, fe[b], d[b]);
     }
 #pragma unroll
@@ -1018,29 +1085,31 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
       }
     }
   }
-  __syncthreads();
-  // phase B: rows sum their incidences' records in incidence order
+  __syncthreads();  // records complete; the stage is read: refill it
+  if (STAGED && threadIdx.x == 0 && blk + (int64_t)NSTG * gridDim.x < nblocks) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    stage_issue(stn, blk + (int64_t)NSTG * gridDim.x);
+  }
+  // phase B: rows sum their incidences' records in incidence order; Hessian
+  // blocks go straight to the output row (each 32-byte block is one sector;
+  // fan rows write every block once; other rows are cleared, then accumulated)
   if (has_row) {
     const bool fr = !((meta >> 8) & 1);
     const int dp = (int)(meta >> 16) & 0xff;
     const int cnt = (meta & 0xff) < 255 ? (int)(meta & 0xff) : a.rinc_off[row + 1] - a.rinc_off[row];
     const bool fan = (meta >> 9) & 1;
-    // CF_DIRECT: blocks go straight to the output row (each 32-byte block is
-    // one sector; fan rows write every block once), no row buffer in shared
-    // memory; other rows are cleared, then accumulated in place
-    double* hrow = CF_DIRECT ? a.hess + ro * NN : hbuf + ho;
-    int nblk = 0;
+    double* hrow = MODE == MODE_HESS ? a.hess + ro * NN : nullptr;
     if constexpr (MODE == MODE_HESS) {
-      nblk = (int)((meta >> 24) & 0xff);
+      const int nblk = (int)((meta >> 24) & 0xff);
       if (!fan)
         for (int k = 0; k < nblk * NN; ++k) hrow[k] = 0.0;
     }
     double vec[2] = {0.0, 0.0}, dg[3] = {0.0, 0.0, 0.0};
     double carry[4] = {0.0, 0.0, 0.0, 0.0}, first[4] = {0.0, 0.0, 0.0, 0.0};
     int first_pos = 255, last_pos2 = 255;
-    auto incidence = [&](uint64_t r64, int sp, int jidx) {
+    auto incidence = [&](uint64_t r64, int spk, int jidx) {
       const uint32_t hi = (uint32_t)(r64 >> 32);
-      const int s = sp >> 14, slot = sp & 0x3fff;
+      const int s = spk >> 14, slot = spk & 0x3fff;
       const double* r = rec + (size_t)slot * S;
       vec[0] += r[2 * s];
       vec[1] += r[2 * s + 1];
@@ -1122,18 +1191,11 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
         dst[2] = dg[1];
         dst[3] = dg[2];
       }
-      if (!CF_DIRECT && nblk > 0) {
-        fence_proxy_async_smem();
-        row_store_bulk(a.hess + ro * NN, hrow, nblk * NN);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
     }
   }
-  if (!ok) *a.redo = 1;
   if constexpr (MODE != MODE_HVP) {
     // the block's face energies (spread over all its threads by phase A) in
     // fixed order into its first warp's partial; its other row warp's slot is zero
-    __shared__ double wsum[NT / 32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(0xffffffffu, eacc, o);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = eacc;
@@ -1147,7 +1209,9 @@ __global__ void __launch_bounds__(CfCfg<MODE, PSD>::NT, (CfCfg<MODE, PSD, PIN>::
       a.partials[(blk * PT + 32) >> 5] = 0.0;
     }
   }
-  if constexpr (MODE == MODE_HESS && !CF_DIRECT) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncthreads();  // phase B has read the records (and thread 0 the sums) before the next block's phase A
+  }  // row blocks
+  if (!ok) *a.redo = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1629,10 +1693,12 @@ bool fv_cta_enabled() {
 #ifndef CF_HESS_CTA
 #define CF_HESS_CTA 0
 #endif
-// shared memory of the CTA face-list kernel (face records, then the row buffers)
-size_t cta_smem(int mode, int cf_max, int hd_max) {
+// shared memory of the CTA face-list kernel: CF_STAGES stages, then the face records
+size_t cta_smem(int mode, int cf_max, int) {
   const size_t S = mode == MODE_HESS ? CfRec<MODE_HESS>::S : CfRec<MODE_GRAD>::S;
-  return (((size_t)cf_max * S + 1) & ~(size_t)1) * 8 + (mode == MODE_HESS && !CF_DIRECT ? (size_t)hd_max * 8 + 16 : 0);
+  const size_t sb = mode == MODE_HESS ? CfStage<MODE_HESS>::bytes(cf_max) : CfStage<MODE_GRAD>::bytes(cf_max);
+  return (mode == MODE_HESS ? 1 : CF_STAGES) * ((sb + 127) & ~(size_t)127) * (mode == MODE_HESS ? 0 : 1) +
+         (size_t)cf_max * S * 8;
 }
 bool fv_use_cta(const Problem& p, int mode, bool psd) {
   const int hd = mode == MODE_HESS ? p.max_patch_hdoubles : 0;
@@ -1650,8 +1716,16 @@ void launch_fv(const Problem& p, const FvArgs& a, int hd_max, cudaStream_t st) {
   if (fv_use_cta(p, MODE, PSD)) {
     auto kc = (PSD && a.fixed) ? k_cta_dirichlet<MODE, PSD, true> : k_cta_dirichlet<MODE, PSD, false>;
     MG_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc));
+    int64_t grid = nb;  // persistent CTAs: as many as are resident (the clamped Hessian: one block per CTA,
+    if (MODE != MODE_HESS || CF_PERSIST_HESS) {  // measured 3.12 vs 3.42 ms persistent at icosphere(10))
+      int dev = 0, sms = 148, per_sm = 1;
+      MG_CUDA(cudaGetDevice(&dev));
+      MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, CfCfg<MODE, PSD>::NT, smc));
+      if ((int64_t)sms * (per_sm > 0 ? per_sm : 1) < grid) grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    }
     timing_begin(p, st);
-    kc<<<(unsigned)nb, CfCfg<MODE, PSD>::NT, smc, st>>>(a);
+    kc<<<(unsigned)grid, CfCfg<MODE, PSD>::NT, smc, st>>>(a);
     MG_LAUNCH_CHECK();
     timing_end(p, st);
     return;

@@ -476,7 +476,8 @@ __global__ void k_cf_faces(const uint64_t* keys, int64_t n, const int32_t* faces
 // per incidence: its face's slot in the row's block list (binary search, the
 // list is sorted by face) | the row's corner << 14; ELL copy of the first K slot-major
 __global__ void k_cf_slots(const int32_t* rinc_off, const uint64_t* rrec, int64_t Vr, int RB, int K,
-                           const int32_t* cf_off, const int4* cf, uint16_t* rslot, uint16_t* eslot, int* bad) {
+                           const int32_t* cf_off, const int4* cf, uint16_t* rslot, uint16_t* eslot, int* bad,
+                           int64_t stride) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= Vr) return;
   const int64_t blk = r / RB;
@@ -493,9 +494,9 @@ __global__ void k_cf_slots(const int32_t* rinc_off, const uint64_t* rrec, int64_
     // slot | the row's corner in the face << 14 (all the gradient / HVP rows need)
     const uint16_t sl = (uint16_t)((lo - b0) | (((uint32_t)rrec[k0 + k] >> 30) << 14));
     rslot[k0 + k] = sl;
-    if (k < K) eslot[(int64_t)k * Vr + r] = sl;
+    if (k < K) eslot[(int64_t)k * stride + r] = sl;
   }
-  for (int k = c; k < K; ++k) eslot[(int64_t)k * Vr + r] = 0;
+  for (int k = c; k < K; ++k) eslot[(int64_t)k * stride + r] = 0;
 }
 
 // Face rows: order each row's incidences around its vertex (face j's second
@@ -1101,10 +1102,11 @@ void build_rows_fv(Problem& p, cudaStream_t s) {
     MG_CUDA(cudaMemcpyAsync(&ninc, p.rinc_off.p + Vr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
     p.rslot.alloc(ninc > 0 ? ninc : 1);
-    p.eslot.alloc((int64_t)EV_ELL_K * Vr);
+    p.eslot.alloc((int64_t)EV_ELL_K * Vp);
+    MG_CUDA(cudaMemsetAsync(p.eslot.p, 0, sizeof(uint16_t) * EV_ELL_K * Vp, s));
     MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
     k_cf_slots<<<grid_for(Vr), TPB, 0, s>>>(p.rinc_off.p, p.rrec.p, Vr, RB, EV_ELL_K, p.cf_off.p, p.cf_face.p,
-                                           p.rslot.p, p.eslot.p, mx.p);
+                                           p.rslot.p, p.eslot.p, mx.p, Vp);
     MG_LAUNCH_CHECK();
     const bool bad = to_host_int(mx.p, s) != 0;
     MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
