@@ -22,6 +22,8 @@ namespace {
 constexpr int VB = 256;           // threads per vector block
 constexpr int VG = 4 * 148;       // vector blocks (fixed: the reduction order does not depend on the device)
 constexpr int CHECK_EVERY = 8;    // iterations between host checks of the status word
+// (an 8-lanes-per-row SpMV with coalesced block reads measured 2x slower than
+// one thread per row: 1.65 vs 0.80 ms per iteration on the 2048^2 cloth)
 enum { RUN = 0, CONVERGED = 1, NEGATIVE = 2, MAXITER = 3 };
 
 struct PcgState {
