@@ -250,11 +250,15 @@ def ncu_kernel(label):
         return {}
 
 
-def roofline_obj(label, kernel_ms, nbytes, hbm_peak, hbm_src, note=None):
+def roofline_obj(label, kernel_ms, nbytes, hbm_peak, hbm_src, note=None, workload="grid2048"):
     """Roofline object of one launch: the HBM fraction of the algorithmic
     bytes always; the FP64 fraction of the ncu-executed flops when the
-    capture has them; `bound` = the unit ncu shows busier."""
+    capture has them; `bound` = the unit ncu shows busier. ncu facts (DRAM
+    traffic, executed flops) are per launch of the captured workload, so they
+    are used only for that workload."""
     nk = ncu_kernel(label)
+    if nk.get("workload", "grid2048") != workload:
+        nk = {}
     achieved = nbytes / (kernel_ms * 1e-3) / 1e9
     r = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
          "traffic": nk.get("traffic"), "peak_source": hbm_src, "kernel": label,
@@ -543,7 +547,8 @@ def run_engine(args):
     label = kernel_label(p, "psd")
     if world == 1:
         roofline = roofline_obj(label, kms, cloth_bytes(V, E, nnzb_local), peak, peak_kind,
-                                "24V x + 24V target + 8V masses + 8E rest lengths + 8E edge ids + 24V grad + 72 nnzb H")
+                                "24V x + 24V target + 8V masses + 8E rest lengths + 8E edge ids + 24V grad + 72 nnzb H",
+                                workload=f"grid{n}")
         roofline["kernel_share_of_step"] = kms / ms
     else:
         roofline = {"bound": "hbm", "kernel": label, "kernel_ms": kms, "note": "per-rank shard; see the N=1 line"}
@@ -643,11 +648,12 @@ def gc_cuda():
     torch.cuda.empty_cache()
 
 
-def call_record(p, fn, units, unit, nbytes, label, peak, peak_kind, steps=10, extra=None):
+def call_record(p, fn, units, unit, nbytes, label, peak, peak_kind, steps=10, extra=None, workload="grid2048"):
     ms, kms = time_with_kernel(p, fn, steps, 3)
     t = kms if kms else ms
     r = {"ms": ms, "kernel_ms": kms, unit + "_per_s": units / (ms * 1e-3), "algorithmic_bytes": nbytes,
-         "hbm_frac": nbytes / (t * 1e-3) / 1e9 / peak, "roofline": roofline_obj(label, t, nbytes, peak, peak_kind)}
+         "hbm_frac": nbytes / (t * 1e-3) / 1e9 / peak,
+         "roofline": roofline_obj(label, t, nbytes, peak, peak_kind, workload=workload)}
     if extra:
         r.update(extra)
     return r
@@ -664,13 +670,13 @@ def run_extras(p, v, V, E, nnzb, steps, peak, peak_kind):
     te = 2 * V + E
     return {
         "cloth_grad_hess": call_record(p, lambda: p.eval_terms(sync=False), te, "term_elements",
-                                       cloth_bytes(V, E, nnzb), kernel_label(p, "plain"), peak, peak_kind, k),
+                                       cloth_bytes(V, E, nnzb), kernel_label(p, "plain"), peak, peak_kind, k, workload="grid2048"),
         "cloth_hvp": call_record(p, lambda: p.hvp(xd, vd, out=y), te, "term_elements", cloth_hvp_bytes(V, E),
-                                 kernel_label(p, "hvp"), peak, peak_kind, k),
+                                 kernel_label(p, "hvp"), peak, peak_kind, k, workload="grid2048"),
         "cloth_hvp_psd": call_record(p, lambda: p.hvp(xd, vd, psd_floor=FLOOR, out=y), te, "term_elements",
-                                     cloth_hvp_bytes(V, E), kernel_label(p, "hvp_psd"), peak, peak_kind, k),
+                                     cloth_hvp_bytes(V, E), kernel_label(p, "hvp_psd"), peak, peak_kind, k, workload="grid2048"),
         "cloth_energy_only": call_record(p, lambda: p.eval_energy_only(xd), te, "term_elements",
-                                         cloth_energy_bytes(V, E), "k_elem energy (3 launches)", peak, peak_kind, k),
+                                         cloth_energy_bytes(V, E), "k_elem energy (3 launches)", peak, peak_kind, k, workload="grid2048"),
         "cloth_newton_cg": run_pcg(p, nnzb, V),
     }
 
@@ -786,15 +792,15 @@ def run_configs(peak, peak_kind, sub=10):
     ex = {"V": V, "E": E, "F": 2 * (n - 1) ** 2, "setup_s": st}
     out["cloth2240_grad_hess_psd"] = call_record(
         p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), 2 * V + E, "term_elements",
-        cloth_bytes(V, E, p.hess.nnz_blocks), kernel_label(p, "psd"), peak, peak_kind, extra=ex)
+        cloth_bytes(V, E, p.hess.nnz_blocks), kernel_label(p, "psd"), peak, peak_kind, extra=ex, workload="grid2240")
     out["cloth2240_grad_hess"] = call_record(
         p, lambda: p.eval_terms(sync=False), 2 * V + E, "term_elements", cloth_bytes(V, E, p.hess.nnz_blocks),
-        kernel_label(p, "plain"), peak, peak_kind)
+        kernel_label(p, "plain"), peak, peak_kind, workload="grid2240")
     out["cloth2240_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), 2 * V + E, "term_elements",
-                                       cloth_hvp_bytes(V, E), kernel_label(p, "hvp"), peak, peak_kind)
+                                       cloth_hvp_bytes(V, E), kernel_label(p, "hvp"), peak, peak_kind, workload="grid2240")
     out["cloth2240_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), 2 * V + E,
                                            "term_elements", cloth_hvp_bytes(V, E), kernel_label(p, "hvp_psd"), peak,
-                                           peak_kind)
+                                           peak_kind, workload="grid2240")
     del p, vd, y
     gc_cuda()
     # config 3: symmetric Dirichlet on the punctured icosphere (stereographic UV, all det J > 0)
@@ -815,13 +821,13 @@ def run_configs(peak, peak_kind, sub=10):
           "bytes_note": "16V uv + 12F faces + 32F rest_inv + 8F areas + 16V grad + 32 nnzb H (HVP: + 16V v, y for grad/H)"}
     pre = f"dirichlet_ico{sub}"
     out[pre + "_grad_hess"] = call_record(p, lambda: p.eval_terms(sync=False), F, "faces", b_hess,
-                                          "k_rows_dirichlet<HESS>", peak, peak_kind, extra=ex)
+                                          "k_rows_dirichlet<HESS>", peak, peak_kind, extra=ex, workload=f"ico{sub}")
     out[pre + "_grad_hess_psd"] = call_record(p, lambda: p.eval_terms(psd_floor=FLOOR, sync=False), F, "faces",
-                                              b_hess, "k_cta_dirichlet<HESS,psd>", peak, peak_kind)
+                                              b_hess, "k_cta_dirichlet<HESS,psd>", peak, peak_kind, workload=f"ico{sub}")
     out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces", b_hvp,
-                                    "k_cta_dirichlet<HVP>", peak, peak_kind)
+                                    "k_cta_dirichlet<HVP>", peak, peak_kind, workload=f"ico{sub}")
     out[pre + "_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), F, "faces", b_hvp,
-                                        "k_cta_dirichlet<HVP,psd>", peak, peak_kind)
+                                        "k_cta_dirichlet<HVP,psd>", peak, peak_kind, workload=f"ico{sub}")
     del p, vd, y, mesh
     gc_cuda()
     # config 4: sphere manifold HVP (and its gradient), smoothing HVP (and gradient)
@@ -841,11 +847,11 @@ def run_configs(peak, peak_kind, sub=10):
     ex = {"V": V, "F": F, "setup_s": st, "bytes_note": "16V x + 72V base/b1/b2 + 12F faces + 16V out (HVP: + 16V v)"}
     pre = f"sphere_ico{sub}"
     out[pre + "_grad"] = call_record(p, lambda: p.eval_terms(sync=False), F, "faces", b_grad,
-                                     "k_rows_sphere<GRAD>", peak, peak_kind, extra=ex)
+                                     "k_rows_sphere<GRAD>", peak, peak_kind, extra=ex, workload=f"ico{sub}")
     out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), F, "faces", b_hvp,
-                                    "k_rows_sphere<HVP>", peak, peak_kind)
+                                    "k_rows_sphere<HVP>", peak, peak_kind, workload=f"ico{sub}")
     out[pre + "_hvp_psd"] = call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), F, "faces", b_hvp,
-                                        "k_sphere_face_hvp_psd", peak, peak_kind)
+                                        "k_sphere_face_hvp_psd", peak, peak_kind, workload=f"ico{sub}")
     del p, vd, y
     gc_cuda()
     p = edge_length_problem(mesh)
@@ -856,10 +862,10 @@ def run_configs(peak, peak_kind, sub=10):
     pre = f"smooth_ico{sub}"
     out[pre + "_grad"] = call_record(p, lambda: p.eval_terms(sync=False), E, "edges", 24 * V + 8 * E + 24 * V,
                                      "k_rows_fast<3,GRAD,EDGE_LENGTH>", peak, peak_kind,
-                                     extra={"bytes_note": "24V x + 8E edge ids + 24V grad"})
+                                     extra={"bytes_note": "24V x + 8E edge ids + 24V grad"}, workload=f"ico{sub}")
     out[pre + "_hvp"] = call_record(p, lambda: p.hvp(p.x_device, vd, out=y), E, "edges", 24 * V + 8 * E + 24 * V,
                                     "k_rows_fast<3,HVP,EDGE_LENGTH>", peak, peak_kind,
-                                    extra={"bytes_note": "24V v + 8E edge ids + 24V y (the Hessian is constant)"})
+                                    extra={"bytes_note": "24V v + 8E edge ids + 24V y (the Hessian is constant)"}, workload=f"ico{sub}")
     del p, vd, y, mesh
     gc_cuda()
     return out
@@ -915,12 +921,12 @@ def run_config5(peak, peak_kind, n=7072):
     out = {
         "cloth7072_grad": call_record(p, lambda: p.eval_terms(sync=False), te, "term_elements",
                                       cloth_energy_bytes(V, E) + 24 * V, "k_rows_fast<3,GRAD,SPRING>", peak,
-                                      peak_kind, extra=ex),
+                                      peak_kind, extra=ex, workload="grid7072"),
         "cloth7072_hvp": call_record(p, lambda: p.hvp(p.x_device, vd, out=y), te, "term_elements",
-                                     cloth_hvp_bytes(V, E), "k_rows_fast<3,HVP,SPRING>", peak, peak_kind),
+                                     cloth_hvp_bytes(V, E), "k_rows_fast<3,HVP,SPRING>", peak, peak_kind, workload="grid7072"),
         "cloth7072_hvp_psd": call_record(p, lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), te,
                                          "term_elements", cloth_hvp_bytes(V, E), "k_rows_fast<3,HVP,psd,SPRING>",
-                                         peak, peak_kind),
+                                         peak, peak_kind, workload="grid7072"),
     }
     del p, vd, y, x, target, masses, l2, mesh
     gc_cuda()

@@ -48,7 +48,12 @@ def parse(path):
         ms = num(r"gpu__time_duration.sum: ([\d.,]+) ms")
         dur_us = ms * 1e3 if ms is not None else None
     tag = re.search(r"== (\S+) \((.*)\)", txt)
+    cmd = tag.group(2) if tag else ""
+    g = re.search(r"--grid (\d+)", cmd)
+    sub = re.search(r"--sub (\d+)", cmd)
+    workload = f"grid{g.group(1)}" if g else (f"ico{sub.group(1)}" if sub else "grid2048")
     return label_of(kern), {
+        "workload": workload,
         "traffic": int(round((rd + wr) * 1e9)), "dram_read": int(round(rd * 1e9)), "dram_write": int(round(wr * 1e9)),
         "fp64_flops": flops, "dram_pct": num(r"DRAM Throughput: ([\d.]+) %"),
         "fp64_pipe_pct": num(r"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active: ([\d.]+) %"),
