@@ -1078,17 +1078,10 @@ int64_t launch_rows_jit(const Problem& p, Mode mode, const LaunchCtx& c, int64_t
   const int B = mode == MODE_HESS ? FastCfg<MODE_HESS, false>::BLOCK
                 : mode == MODE_GRAD ? FastCfg<MODE_GRAD, false>::BLOCK
                 : c.psd ? FastCfg<MODE_HVP, true>::BLOCK : FastCfg<MODE_HVP, false>::BLOCK;
-  int64_t grid = (m.Vr + B - 1) / B;
-  if (EV_STAGED && mode != MODE_HESS) {  // persistent CTAs (their residency: the kernels' launch bounds)
-    int dev = 0, sms = 148;
-    MG_CUDA(cudaGetDevice(&dev));
-    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int64_t per_sm = mode == MODE_GRAD ? FastMinb<MODE_GRAD, false, false>::v
-                           : c.psd ? FastMinb<MODE_HVP, true, false>::v : FastMinb<MODE_HVP, false, false>::v;
-    if ((int64_t)sms * per_sm < grid) grid = (int64_t)sms * per_sm;
-  }
+  const int64_t grid = (m.Vr + B - 1) / B;
+  const bool persistent = mode == MODE_HESS ? EV_STAGED_HESS : EV_STAGED;
   timing_begin(p, c.stream);
-  jit_rows_launch(p, mode, c.psd, &a, grid, B, sm, c.stream);
+  jit_rows_launch(p, mode, c.psd, &a, grid, B, sm, c.stream, persistent);
   timing_end(p, c.stream);
   return np;
 }

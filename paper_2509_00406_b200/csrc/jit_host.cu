@@ -20,6 +20,7 @@ typedef int (*PFN_launch)(void*, unsigned, unsigned, unsigned, unsigned, unsigne
 typedef int (*PFN_unload)(void*);
 typedef int (*PFN_errstr)(int, const char**);
 typedef int (*PFN_setattr)(void*, int, int);
+typedef int (*PFN_occ)(int*, void*, int, size_t);
 
 struct Driver {
   PFN_load load = nullptr;
@@ -28,6 +29,7 @@ struct Driver {
   PFN_unload unload = nullptr;
   PFN_errstr errstr = nullptr;
   PFN_setattr setattr = nullptr;
+  PFN_occ occupancy = nullptr;
 };
 
 Driver& driver() {
@@ -44,6 +46,7 @@ Driver& driver() {
       d.unload = (PFN_unload)dlsym(h, "cuModuleUnload");
       d.errstr = (PFN_errstr)dlsym(h, "cuGetErrorString");
       d.setattr = (PFN_setattr)dlsym(h, "cuFuncSetAttribute");
+      d.occupancy = (PFN_occ)dlsym(h, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     }
   }
   if (!d.load || !d.getfn || !d.launch) throw Error(MG_ERR_CUDA, "CUDA driver API (libcuda) unavailable");
@@ -156,13 +159,20 @@ void jit_rows_unload(Problem& p) {
 }
 
 void jit_rows_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t grid, int block, size_t smem,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool persistent) {
   Driver& d = driver();
   if (mode != MODE_GRAD && mode != MODE_HESS && mode != MODE_HVP)
     throw Error(MG_ERR_UNSUPPORTED, "traced row kernels assemble grad / Hessian / HVP only");
   const int k = mode == MODE_GRAD ? 0 : mode == MODE_HESS ? (psd ? 2 : 1) : (psd ? 4 : 3);
   if (d.setattr) drv_check(d.setattr(p.row_fn[k], 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */,
                                      (int)smem), "cuFuncSetAttribute");
+  if (persistent && d.occupancy) {  // the staged kernels walk row blocks grid-stride: as many CTAs as are resident
+    int per_sm = 0, dev = 0, sms = 148;
+    drv_check(d.occupancy(&per_sm, p.row_fn[k], block, smem), "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    MG_CUDA(cudaGetDevice(&dev));
+    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (per_sm > 0 && (int64_t)sms * per_sm < grid) grid = (int64_t)sms * per_sm;
+  }
   void* params[1] = {args};
   if (grid > 0)
     drv_check(d.launch(p.row_fn[k], (unsigned)grid, 1, 1, (unsigned)block, 1, 1, (unsigned)smem, s, params, nullptr),

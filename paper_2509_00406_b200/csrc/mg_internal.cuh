@@ -276,7 +276,7 @@ void jit_patch_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t
                       int blocks_max, size_t smem, cudaStream_t s, int64_t grid = -1);
 // launch the problem's traced row kernel (args: a filled rows::EvArgs)
 void jit_rows_launch(const Problem& p, Mode mode, bool psd, void* args, int64_t grid, int block, size_t smem,
-                     cudaStream_t s);
+                     cudaStream_t s, bool persistent);
 
 struct LaunchCtx {
   const double* x;
