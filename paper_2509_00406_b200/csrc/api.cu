@@ -467,9 +467,16 @@ int mg_energy(mg_problem* prob, const double* x_d, double* energy_d, void* strea
     LaunchCtx c{x_d, nullptr, nullptr, nullptr, nullptr, nullptr, p.partials.p, false, 0.0, s};
     int64_t np = 0;
     int launches = 0;
-    for (auto& t : p.terms) {
-      np += launch_elem(p, t, MODE_ENERGY, c, np);
-      ++launches;
+    if (p.ev_fast && p.layout_ready) {
+      // builtin radial terms: the edge row kernel's probe mode (each edge at its
+      // first vertex, every value in the reference's own operations)
+      np = launch_patch_ev(p, MODE_ENERGY, c, 0);
+      launches = 1;
+    } else {
+      for (auto& t : p.terms) {
+        np += launch_elem(p, t, MODE_ENERGY, c, np);
+        ++launches;
+      }
     }
     reduce_partials(p.partials.p, np, energy_d, s);
     p.last_launches = launches + reduce_launches(np);

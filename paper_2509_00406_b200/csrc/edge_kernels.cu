@@ -393,10 +393,72 @@ MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const dou
 // the V terms with early attribute loads, and the radial closed forms of the
 // EV terms; EVT fixes the single EV term's type at compile time (0: any mix,
 // dispatched per incidence).
+// The energy probe (MODE_ENERGY): every element value in the reference's own
+// operations and order, unfused (numpy float64: ActiveVec.norm2 / dot left to
+// right, division as a * (1 / b), active.py:180-211, 383-400), so each value
+// — NaN / Inf included — is bitwise the reference's; only the sum's order differs.
+MG_DI double ref_norm2(const double* d, int n) {
+  double t = __dmul_rn(d[0], d[0]);
+  for (int c = 1; c < n; ++c) t = __dadd_rn(t, __dmul_rn(d[c], d[c]));
+  return t;
+}
+
 template <int EVT>
 struct BuiltinRows {
   static constexpr bool kXFreeHvp = EVT == MG_TERM_EDGE_LENGTH;
   static constexpr bool kVertexOnly = EVT == MG_TERM_EDGE_LENGTH;
+  // energy of one edge at its first vertex (d = x_first - x_second, as the
+  // reference's x[verts[0]] - x[verts[1]]): spring (apps/cloth.py:106-110,
+  // coef * l2 * (s * s), s = |d|^2 / l2 - 1), edge length (apps/smooth.py:27-28)
+  template <int N>
+  MG_DI static double evalue(const EvArgs& a, double av, const double* d, uint32_t e) {
+    if constexpr (EVT == MG_TERM_SPRING) {
+      const double c = a.terms[a.ev_idx[0]].c[0];
+      const double s = __dsub_rn(__dmul_rn(ref_norm2(d, N), __ddiv_rn(1.0, av)), 1.0);
+      return __dmul_rn(__dmul_rn(c, av), __dmul_rn(s, s));
+    } else if constexpr (EVT == MG_TERM_EDGE_LENGTH) {
+      return ref_norm2(d, N);
+    } else {
+      double v = 0.0;
+      for (int j = 0; j < a.nev; ++j) {
+        const TermDev& t = a.terms[a.ev_idx[j]];
+        double x;
+        if (t.type == MG_TERM_SPRING) {
+          const double l2 = (j == 0 && a.ev_a0) ? av : t.a[0][e];
+          const double s = __dsub_rn(__dmul_rn(ref_norm2(d, N), __ddiv_rn(1.0, l2)), 1.0);
+          x = __dmul_rn(__dmul_rn(t.c[0], l2), __dmul_rn(s, s));
+        } else {
+          x = ref_norm2(d, N);
+        }
+        v = j == 0 ? x : __dadd_rn(v, x);
+      }
+      return v;
+    }
+  }
+  // energies of the row's V terms: inertia 0.5 m |x - t|^2 (apps/cloth.py:102-104),
+  // gravity (-h2) (m x.g) (:112-113)
+  template <int N>
+  MG_DI static double venergy(const EvArgs& a, int g, const VPreload<N>& v, const double* xs) {
+    double eacc = 0.0;
+    for (int j = 0; j < a.nvt; ++j) {
+      const TermDev& t = a.terms[a.vt_idx[j]];
+      const double m = j < VPRE ? v.m[j] : t.a[0][g];
+      double val;
+      if (t.type == MG_TERM_INERTIA) {
+        double d[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) d[c] = __dsub_rn(xs[c], j < VPRE ? v.tg[j][c] : t.a[1][(int64_t)g * N + c]);
+        val = __dmul_rn(__dmul_rn(0.5, m), ref_norm2(d, N));
+      } else {
+        double dot = __dmul_rn(xs[0], t.c[1]);
+#pragma unroll
+        for (int c = 1; c < N; ++c) dot = __dadd_rn(dot, __dmul_rn(xs[c], t.c[1 + c]));
+        val = __dmul_rn(-t.c[0], __dmul_rn(m, dot));
+      }
+      eacc += val;
+    }
+    return eacc;
+  }
   template <int N, int MODE>
   MG_DI static VPreload<N> vload(const EvArgs& a, int g) { return vterms_load<N, MODE>(a, g); }
   template <int N, int MODE, bool PSD>
@@ -897,7 +959,9 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
   const int64_t nb = (a.V + PT - 1) / PT;
   if (!nb) return;
   auto fast = k_rows_fast<N, MODE, PSD, EVT>;
-  auto exact = k_rows_ev<N, MODE, PSD, true>;
+  // (the energy probe's values are the reference's own operations: no exact re-run)
+  constexpr int XMODE = MODE == MODE_ENERGY ? MODE_GRAD : MODE;
+  auto exact = k_rows_ev<N, XMODE, PSD, true>;
   if (sm) {
     MG_CUDA(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     MG_CUDA(cudaFuncSetAttribute(exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -947,6 +1011,7 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
     MG_LAUNCH_CHECK();
     timing_end(p, st);
   }
+  if constexpr (MODE == MODE_ENERGY) return;
   // exact re-run only when a lane was non-finite (reads the flag and exits otherwise)
   int dev = 0, sms = 148;
   MG_CUDA(cudaGetDevice(&dev));
@@ -967,6 +1032,7 @@ void launch_rows(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st)
 template <int N>
 void launch_rows_mode(const Problem& p, const EvArgs& a, int hd, Mode mode, bool psd, cudaStream_t st) {
   switch (mode) {
+    case MODE_ENERGY: launch_rows<N, MODE_ENERGY, false>(p, a, hd, st); break;
     case MODE_GRAD: launch_rows<N, MODE_GRAD, false>(p, a, hd, st); break;
     case MODE_HESS:
       if (psd) launch_rows<N, MODE_HESS, true>(p, a, hd, st);
@@ -976,7 +1042,7 @@ void launch_rows_mode(const Problem& p, const EvArgs& a, int hd, Mode mode, bool
       if (psd) launch_rows<N, MODE_HVP, true>(p, a, hd, st);
       else launch_rows<N, MODE_HVP, false>(p, a, hd, st);
       break;
-    default: throw Error(MG_ERR_UNSUPPORTED, "edge row kernel assembles grad / Hessian / HVP only");
+    default: throw Error(MG_ERR_UNSUPPORTED, "edge row kernel evaluates energy / grad / Hessian / HVP only");
   }
 }
 

@@ -168,6 +168,9 @@ template <> struct FastCfg<MODE_HVP, true> {
 template <> struct FastCfg<MODE_GRAD, false> {
   static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
 };
+template <> struct FastCfg<MODE_ENERGY, false> {  // the energy probe: first-vertex edges only
+  static constexpr int MAXI = 6, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
+};
 // the x-free HVP holds only directions: full occupancy (64 registers)
 template <int MODE, bool PSD, bool XFREE_HVP> struct FastMinb {
   static constexpr int v = (MODE == MODE_HVP && !PSD && XFREE_HVP) ? 1024 / EV_FLAT_BLOCK : FastCfg<MODE, PSD>::MINB;
@@ -337,9 +340,11 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       const uint32_t hi = (uint32_t)(rc[j] >> 32);
       const int64_t o = hi & 0x7fffffffu;
       const bool fo = !(hi >> 31);
+      // the energy probe evaluates an edge at its first vertex only
+      const bool need = MODE != MODE_ENERGY || !((uint32_t)rc[j] >> 31);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        xo[j][c] = !XFREE ? a.x[o * N + c] : 0.0;
+        xo[j][c] = (!XFREE && need) ? a.x[o * N + c] : 0.0;
         if constexpr (MODE == MODE_HVP) {
           const double wv = a.w[o * N + c];
           uo[j][c] = fo ? wv : 0.0;
@@ -347,7 +352,7 @@ MG_DI void rows_fast_body(const EvArgs& a) {
           uo[j][c] = 0.0;
         }
       }
-      ep[j] = Pol::template eload<MODE>(a, (uint32_t)rc[j] & 0x7fffffffu);
+      if (need) ep[j] = Pol::template eload<MODE>(a, (uint32_t)rc[j] & 0x7fffffffu);
     };
 #pragma unroll
     for (int j = 0; j < MAXI; ++j) issue(j);
@@ -364,7 +369,8 @@ MG_DI void rows_fast_body(const EvArgs& a) {
 #pragma unroll
     for (int i = 0; i < T; ++i) dg[i] = 0.0;
     // V terms (their attribute loads overlapped the level-3 loads)
-    Pol::template vterms<N, MODE, PSD>(a, g, fr, vpre, xs, us, eacc, vec, dg);
+    if constexpr (MODE == MODE_ENERGY) eacc += Pol::template venergy<N>(a, g, vpre, xs);
+    else Pol::template vterms<N, MODE, PSD>(a, g, fr, vpre, xs, us, eacc, vec, dg);
     double* hrow = hbuf + ho;
     int pos = 0;
     // one incidence: contributions to this row
@@ -373,6 +379,15 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       const uint32_t e = lo & 0x7fffffffu;
       const bool first = (lo >> 31) == 0;  // the row is the edge's first vertex
       const bool fo = !(hi >> 31);
+      if constexpr (MODE == MODE_ENERGY) {
+        if (first) {
+          double d[N];
+#pragma unroll
+          for (int c = 0; c < N; ++c) d[c] = __dsub_rn(xs[c], xo_[c]);
+          eacc += Pol::template evalue<N>(a, av, d, e);
+        }
+        return;
+      }
       double d[N], rr = 0.0;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
@@ -472,8 +487,10 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       incidence(r64, x1, u1, av);
     }
     double* vout = MODE == MODE_HVP ? a.y : a.grad;
+    if constexpr (MODE != MODE_ENERGY) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+      for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+    }
     if constexpr (MODE == MODE_HESS) {
       if (fr && dp != 255) {
         double* dst = hrow + dp * NN;
