@@ -400,6 +400,73 @@ class CpuCloth:
         return statistics.median(rates), rates
 
 
+def cpu_config_rates(sub=8, stride=16, steps=3):
+    """CPU oracle port rates of BASELINE configs 3 and 4 (all host threads,
+    atomic accumulation, the reference CLI default): per call, the elements
+    per second of a fixed-stride 1/stride chunk sample, median of `steps`
+    after one warm-up. The oracle runs the reference's numpy path chunk by
+    chunk (4096 elements), so its per-element rate does not depend on the
+    mesh size; its setup (pattern, layout) on icosphere(10) would take
+    minutes, so the sample mesh is icosphere(`sub`)."""
+    from oracle import OracleProblem
+    from oracle.engine import default_workers
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import initial_sphere, rest_geometry, tangent_bases
+    from paper_2509_00406_b200.mesh import _host_edges
+    from paper_2509_00406_b200.terms import EdgeLength, SphereBarrierStretch, SymDirichlet
+
+    workers = default_workers()
+    rng = np.random.default_rng(1)
+    out = {}
+
+    def rate(op, name, fn):
+        sizes = [sl.stop - sl.start for _, _, _, sl in op._tasks()]
+        rates = []
+        for k in range(steps + 1):
+            op.task_slice = slice(k % stride, None, stride)
+            units = sum(sizes[k % stride::stride])
+            t0 = time.perf_counter()
+            fn()
+            dt = time.perf_counter() - t0
+            if k:
+                rates.append(units / dt)
+        op.task_slice = None
+        return statistics.median(rates)
+
+    pos, faces, uv = mg.punctured_icosphere_arrays(sub)
+    mesh = mg.Mesh(pos, faces)
+    ri, ar = rest_geometry(mesh)
+    op = OracleProblem(len(pos), faces, _host_edges(faces, None, len(pos)), 2,
+                       [("FV", SymDirichlet(np.ascontiguousarray(ri).reshape(-1, 4), ar))], with_hessian=True,
+                       workers=workers, accumulation="atomic")
+    x, v = uv.ravel(), rng.normal(size=2 * len(pos))
+    out["dirichlet"] = {"grad_hess": rate(op, "eval_terms", lambda: op.eval_terms(x)),
+                        "hvp": rate(op, "hvp", lambda: op.hvp(x, v)), "unit": "faces/s"}
+    del op
+    pos, faces = mg.icosphere_arrays(sub)
+    mesh = mg.Mesh(pos, faces)
+    edges = _host_edges(faces, None, len(pos))
+    base = initial_sphere(mesh)
+    b1, b2 = tangent_bases(base)
+    op = OracleProblem(len(pos), faces, edges, 2, [("FV", SphereBarrierStretch(base, b1, b2, True, True))],
+                       with_hessian=False, workers=workers, accumulation="atomic")
+    x, v = 1e-5 * rng.normal(size=2 * len(pos)), rng.normal(size=2 * len(pos))
+    out["sphere"] = {"grad": rate(op, "eval_terms", lambda: op.eval_terms(x)),
+                     "hvp": rate(op, "hvp", lambda: op.hvp(x, v)), "unit": "faces/s"}
+    del op
+    op = OracleProblem(len(pos), faces, edges, 3, [("EV", EdgeLength())], with_hessian=False, workers=workers,
+                       accumulation="atomic")
+    x, v = pos.ravel(), rng.normal(size=3 * len(pos))
+    out["smoothing"] = {"grad": rate(op, "eval_terms", lambda: op.eval_terms(x)),
+                        "hvp": rate(op, "hvp", lambda: op.hvp(x, v)), "unit": "edges/s"}
+    out.update({"cores": workers, "kind": "port", "sample": (
+        f"icosphere({sub}) meshes (the per-element rate of the chunked numpy path is size-independent; setup on "
+        f"icosphere(10) takes minutes), every {stride}th 4096-element chunk, median of {steps} after 1 warm-up, "
+        f"atomic, {workers} threads"), "host": cpu_info()})
+    return out
+
+
 def cpu_baseline_line(n, stride=64, steps=3):
     """cpu_baseline of the engine arm: the oracle port on the same problem, all
     host threads, a 1/stride chunk sample of eval_terms(psd_floor) per step."""
@@ -607,6 +674,8 @@ def run_engine(args):
         del p
         gc_cuda()
         extras.update(run_configs(peak, peak_kind, args.sub))
+        if not args.no_cpu:
+            extras["configs_cpu_baseline"] = cpu_config_rates()
         if not args.no_config5:
             extras.update(run_config5(peak, peak_kind, args.grid5))
     if world > 1 and not args.no_config5:
