@@ -670,6 +670,7 @@ def run_engine(args):
         for k, r in run_traced(n, max(5, steps // 2), peak, peak_kind).items():
             r["vs_builtin_newton_step"] = r["newton_step_ms"] / ms
             extras[k] = r
+        extras.update(run_fp32(n, max(5, steps // 2), peak, peak_kind))
     if not args.no_configs and world == 1:
         del p
         gc_cuda()
@@ -748,6 +749,47 @@ def run_extras(p, v, V, E, nnzb, steps, peak, peak_kind):
                                          cloth_energy_bytes(V, E), "k_elem energy (3 launches)", peak, peak_kind, k, workload="grid2048"),
         "cloth_newton_cg": run_pcg(p, nnzb, V),
     }
+
+
+def run_fp32(n, steps, peak, peak_kind):
+    """The headline problem with fp32 storage (Problem(dtype=torch.float32)):
+    x, target, masses, rest lengths, gradient, Hessian values and HVP vectors
+    in fp32, the edge row kernels computing in fp64; algorithmic bytes halve
+    except the int32 edge ids (12V x + 12V target + 4V masses + 4E l2 + 8E ids
+    + 12V grad + 36 nnzb)."""
+    import torch
+
+    import paper_2509_00406_b200 as mg
+    from paper_2509_00406_b200.apps import ClothConfig, cloth_problem, default_pins, lumped_masses
+
+    pos, faces, target, x, v = cloth_inputs(n)
+    mesh = mg.Mesh(pos, faces)
+    cfg = ClothConfig(grid_n=n, spacing=1.0 / (n - 1))
+    p = cloth_problem(cfg, mesh, torch.from_numpy(target).cuda(),
+                      masses=torch.from_numpy(lumped_masses(mesh, cfg.mass_density)).cuda(), pinned=default_pins(n),
+                      dtype=torch.float32, live_host_attrs=False)
+    p.precompute_sparsity()
+    p.x = x
+    V, E = cloth_sizes(n)
+    nnzb = p.hess.nnz_blocks
+    b_h = 12 * V + 12 * V + 4 * V + 4 * E + 8 * E + 12 * V + 36 * nnzb
+    b_v = 12 * V + 12 * V + 4 * V + 4 * E + 8 * E + 12 * V
+    vd = torch.from_numpy(v).cuda().to(torch.float32)
+    y = torch.empty_like(vd)
+    te = 2 * V + E
+    out = {}
+    for name, fn, nb in (("grad_hess_psd", lambda: p.eval_terms(psd_floor=FLOOR, sync=False), b_h),
+                         ("grad_hess", lambda: p.eval_terms(sync=False), b_h),
+                         ("hvp", lambda: p.hvp(p.x_device, vd, out=y), b_v),
+                         ("hvp_psd", lambda: p.hvp(p.x_device, vd, psd_floor=FLOOR, out=y), b_v)):
+        ms, kms = time_with_kernel(p, fn, steps, 3)
+        t = kms if kms else ms
+        out["cloth_fp32_" + name] = {"ms": ms, "kernel_ms": kms, "term_elements_per_s": te / (ms * 1e-3),
+                                     "algorithmic_bytes": nb, "hbm_frac": nb / (t * 1e-3) / 1e9 / peak,
+                                     "storage": "fp32 (fp64 arithmetic)", "parity": "tests/test_fp32_gpu.py: 1e-5"}
+    del p, vd, y, mesh
+    gc_cuda()
+    return out
 
 
 def run_pcg(p, nnzb, V, iters=40):

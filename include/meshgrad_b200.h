@@ -175,6 +175,15 @@ MG_API int mg_problem_set_patch_module(mg_problem* prob, const void* image);
  * one-variable second-order dual; results agree with the full-dual path to
  * rounding. NULL drops it; adding a term drops it. */
 MG_API int mg_problem_set_row_module(mg_problem* prob, const void* image);
+/* Storage precision of x, the HVP direction, the gradient, the Hessian values,
+ * the HVP result and the builtin terms' attribute arrays: 64 (default, the
+ * reference's float64) or 32 (half the bytes; every kernel computes in fp64
+ * and rounds on store). fp32 storage runs on the edge row kernels only —
+ * deterministic problems whose terms are builtin vertex and radial edge terms
+ * (cloth, smoothing) — for mg_eval, mg_hvp and mg_energy (energy in fp64);
+ * other calls and problems return MG_ERR_UNSUPPORTED. Non-finite values keep
+ * the closed forms' propagation (no exact re-run). Set before the first call. */
+MG_API int mg_problem_set_storage(mg_problem* prob, int bits);
 MG_API int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d);
 /* Rebind one attribute pointer of a registered term (closure arrays that the
  * reference rewrites in place between calls, apps/cloth.py:128, sphere.py:121-127). */

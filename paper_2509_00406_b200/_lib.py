@@ -55,6 +55,7 @@ SIGNATURES = [
                                             ctypes.POINTER(_INT)]),
     ("mg_problem_set_patch_module", _INT, [_P, _P]),
     ("mg_problem_set_row_module", _INT, [_P, _P]),
+    ("mg_problem_set_storage", _INT, [_P, _INT]),
     ("mg_problem_set_jit_attr", _INT, [_P, _INT, _INT, _P]),
     ("mg_problem_set_attr", _INT, [_P, _INT, _INT, _P]),
     ("mg_precompute_sparsity", _INT, [_P, _I64P, _P]),

@@ -89,16 +89,18 @@ def rest_lengths2(mesh: Mesh) -> np.ndarray:
 
 
 def cloth_problem(cfg: ClothConfig, mesh: Mesh, target, masses=None, pinned=None,
-                  accumulation: str = "deterministic") -> Problem:
+                  accumulation: str = "deterministic", dtype=None, live_host_attrs: bool = True) -> Problem:
     """Inertia + spring + gravity, registered V, EV, V (cloth.py:115-117).
     `target` (V,3) is the inertial target x_n + h v_n: pass a CUDA tensor to
-    update it in place between calls, or a numpy array (re-read each call)."""
+    update it in place between calls, or a numpy array (re-read each call).
+    dtype=torch.float32: fp32 storage (Problem)."""
     h2 = cfg.h * cfg.h
     if masses is None:
         masses = lumped_masses(mesh, cfg.mass_density)
     if pinned is None:
         pinned = cfg.pinned if cfg.pinned is not None else ()
-    p = Problem(mesh, 3, with_hessian=True, fixed_vertices=tuple(pinned), accumulation=accumulation)
+    p = Problem(mesh, 3, with_hessian=True, fixed_vertices=tuple(pinned), accumulation=accumulation, dtype=dtype,
+                live_host_attrs=live_host_attrs)
     p.add_term(Element.VERTEX, Op.V, Inertia(masses, target))
     import torch  # rest lengths are derived here, not a caller closure: device-resident, never re-uploaded
 

@@ -84,6 +84,13 @@ void ensure_partials(Problem& p, int64_t need) {
   }
 }
 
+// fp32 storage runs on the edge row kernels only
+void require_storage(const Problem& p) {
+  if (p.store32 && !(p.ev_fast && p.layout_ready && p.deterministic))
+    throw Error(MG_ERR_UNSUPPORTED, "float32 storage runs on the edge row kernels: deterministic problems with "
+                                    "builtin vertex and radial edge terms only");
+}
+
 int64_t partials_needed(const Problem& p) {
   int64_t need = 1;
   for (auto& t : p.terms) need += elem_partials_needed(t);
@@ -365,6 +372,13 @@ int mg_problem_set_row_module(mg_problem* prob, const void* image) {
   });
 }
 
+int mg_problem_set_storage(mg_problem* prob, int bits) {
+  if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  if (bits != 32 && bits != 64) return fail(MG_ERR_VALUE, "storage is 32 or 64 bits");
+  prob->p.store32 = bits == 32;
+  return MG_OK;
+}
+
 int mg_problem_set_jit_attr(mg_problem* prob, int term_id, int slot, const double* attr_d) {
   if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
   if (term_id < 0 || term_id >= (int)prob->p.terms.size() || !prob->p.terms[term_id].jit)
@@ -419,6 +433,7 @@ int mg_eval(mg_problem* prob, const double* x_d, int use_psd, double psd_floor, 
   return guard([&] {
     cudaStream_t s = S(stream);
     ensure_ready(p, s);
+    require_storage(p);
     ensure_partials(p, partials_needed(p));
     LaunchCtx c{x_d, nullptr, p.any_fixed ? p.fixed.p : nullptr, grad_d, hess_d, nullptr,
                 p.partials.p, use_psd != 0, psd_floor, s};
@@ -463,6 +478,10 @@ int mg_energy(mg_problem* prob, const double* x_d, double* energy_d, void* strea
   if (p.terms.empty()) return fail(MG_ERR_VALUE, "no energy terms registered");
   return guard([&] {
     cudaStream_t s = S(stream);
+    if (p.store32) {
+      ensure_ready(p, s);
+      require_storage(p);
+    }
     ensure_partials(p, partials_needed(p));
     LaunchCtx c{x_d, nullptr, nullptr, nullptr, nullptr, nullptr, p.partials.p, false, 0.0, s};
     int64_t np = 0;
@@ -493,6 +512,7 @@ int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, 
   return guard([&] {
     cudaStream_t s = S(stream);
     if (p.deterministic) ensure_ready(p, s);
+    require_storage(p);
     ensure_partials(p, partials_needed(p));
     LaunchCtx c{x_d, v_d, p.any_fixed ? p.fixed.p : nullptr, nullptr, nullptr, y_d,
                 p.partials.p, use_psd != 0, psd_floor, s};
@@ -526,6 +546,7 @@ int mg_hvp(mg_problem* prob, const double* x_d, const double* v_d, int use_psd, 
 
 int mg_bsr_matvec(const mg_problem* prob, const double* hess_d, const double* v_d, double* y_d, void* stream) {
   if (!prob) return fail(MG_ERR_VALUE, "problem is NULL");
+  if (prob->p.store32) return fail(MG_ERR_UNSUPPORTED, "the BSR kernels are fp64 (float32 storage: eval / hvp / energy)");
   if (!prob->p.pattern_ready) return fail(MG_ERR_STATE, "sparsity pattern not computed");
   return guard([&] { launch_bsr_matvec(prob->p, hess_d, v_d, y_d, S(stream)); });
 }

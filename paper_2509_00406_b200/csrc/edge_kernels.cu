@@ -318,7 +318,7 @@ template <int N>
 struct VPreload {
   double m[VPRE], tg[VPRE][N];
 };
-template <int N, int MODE>
+template <int N, int MODE, class ST = double>
 MG_DI VPreload<N> vterms_load(const EvArgs& a, int g) {
   VPreload<N> v;
 #pragma unroll
@@ -328,10 +328,10 @@ MG_DI VPreload<N> vterms_load(const EvArgs& a, int g) {
     for (int c = 0; c < N; ++c) v.tg[j][c] = 0.0;
     if (j < a.nvt) {
       const TermDev& t = a.terms[a.vt_idx[j]];
-      v.m[j] = t.a[0][g];
+      v.m[j] = ldv<ST>(t.a[0], g);
       if (MODE != MODE_HVP && t.type == MG_TERM_INERTIA) {
 #pragma unroll
-        for (int c = 0; c < N; ++c) v.tg[j][c] = t.a[1][(int64_t)g * N + c];
+        for (int c = 0; c < N; ++c) v.tg[j][c] = ldv<ST>(t.a[1], (int64_t)g * N + c);
       }
     }
   }
@@ -373,7 +373,7 @@ MG_DI void vterm_one(const EvArgs& a, const TermDev& t, double m, const double* 
     for (int c = 0; c < N; ++c) vec[c] += hd * us[c];
   }
 }
-template <int N, int MODE, bool PSD>
+template <int N, int MODE, bool PSD, class ST = double>
 MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const double* xs, const double* us,
                          double& eacc, double* vec, double* dg) {
 #pragma unroll
@@ -384,8 +384,8 @@ MG_DI void vterms_closed(const EvArgs& a, int g, const VPreload<N>& v, const dou
     double tg[N];
 #pragma unroll
     for (int c = 0; c < N; ++c)
-      tg[c] = (MODE != MODE_HVP && t.type == MG_TERM_INERTIA) ? t.a[1][(int64_t)g * N + c] : 0.0;
-    vterm_one<N, MODE, PSD>(a, t, t.a[0][g], tg, xs, us, eacc, vec, dg);
+      tg[c] = (MODE != MODE_HVP && t.type == MG_TERM_INERTIA) ? ldv<ST>(t.a[1], (int64_t)g * N + c) : 0.0;
+    vterm_one<N, MODE, PSD>(a, t, ldv<ST>(t.a[0], g), tg, xs, us, eacc, vec, dg);
   }
 }
 
@@ -403,10 +403,11 @@ MG_DI double ref_norm2(const double* d, int n) {
   return t;
 }
 
-template <int EVT>
+template <int EVT, class ST = double>
 struct BuiltinRows {
   static constexpr bool kXFreeHvp = EVT == MG_TERM_EDGE_LENGTH;
   static constexpr bool kVertexOnly = EVT == MG_TERM_EDGE_LENGTH;
+  using Store = ST;
   // energy of one edge at its first vertex (d = x_first - x_second, as the
   // reference's x[verts[0]] - x[verts[1]]): spring (apps/cloth.py:106-110,
   // coef * l2 * (s * s), s = |d|^2 / l2 - 1), edge length (apps/smooth.py:27-28)
@@ -424,7 +425,7 @@ struct BuiltinRows {
         const TermDev& t = a.terms[a.ev_idx[j]];
         double x;
         if (t.type == MG_TERM_SPRING) {
-          const double l2 = (j == 0 && a.ev_a0) ? av : t.a[0][e];
+          const double l2 = (j == 0 && a.ev_a0) ? av : ldv<ST>(t.a[0], e);
           const double s = __dsub_rn(__dmul_rn(ref_norm2(d, N), __ddiv_rn(1.0, l2)), 1.0);
           x = __dmul_rn(__dmul_rn(t.c[0], l2), __dmul_rn(s, s));
         } else {
@@ -442,12 +443,12 @@ struct BuiltinRows {
     double eacc = 0.0;
     for (int j = 0; j < a.nvt; ++j) {
       const TermDev& t = a.terms[a.vt_idx[j]];
-      const double m = j < VPRE ? v.m[j] : t.a[0][g];
+      const double m = j < VPRE ? v.m[j] : ldv<ST>(t.a[0], g);
       double val;
       if (t.type == MG_TERM_INERTIA) {
         double d[N];
 #pragma unroll
-        for (int c = 0; c < N; ++c) d[c] = __dsub_rn(xs[c], j < VPRE ? v.tg[j][c] : t.a[1][(int64_t)g * N + c]);
+        for (int c = 0; c < N; ++c) d[c] = __dsub_rn(xs[c], j < VPRE ? v.tg[j][c] : ldv<ST>(t.a[1], (int64_t)g * N + c));
         val = __dmul_rn(__dmul_rn(0.5, m), ref_norm2(d, N));
       } else {
         double dot = __dmul_rn(xs[0], t.c[1]);
@@ -460,14 +461,14 @@ struct BuiltinRows {
     return eacc;
   }
   template <int N, int MODE>
-  MG_DI static VPreload<N> vload(const EvArgs& a, int g) { return vterms_load<N, MODE>(a, g); }
+  MG_DI static VPreload<N> vload(const EvArgs& a, int g) { return vterms_load<N, MODE, ST>(a, g); }
   template <int N, int MODE, bool PSD>
   MG_DI static void vterms(const EvArgs& a, int g, bool, const VPreload<N>& v, const double* xs, const double* us,
                            double& eacc, double* vec, double* dg) {
-    vterms_closed<N, MODE, PSD>(a, g, v, xs, us, eacc, vec, dg);
+    vterms_closed<N, MODE, PSD, ST>(a, g, v, xs, us, eacc, vec, dg);
   }
   template <int MODE>
-  MG_DI static double eload(const EvArgs& a, uint32_t e) { return a.ev_a0 ? a.ev_a0[e] : 0.0; }
+  MG_DI static double eload(const EvArgs& a, uint32_t e) { return a.ev_a0 ? ldv<ST>(a.ev_a0, e) : 0.0; }
   template <int MODE, bool NEEDV, class F>
   MG_DI static void eterms(const EvArgs& a, double av, double rr, uint32_t e, F&& one) {
     if constexpr (EVT != 0) {
@@ -477,7 +478,7 @@ struct BuiltinRows {
     } else {
       for (int j = 0; j < a.nev; ++j) {
         const TermDev& t = a.terms[a.ev_idx[j]];
-        const double at = (j == 0 && a.ev_a0) ? av : (t.type == MG_TERM_SPRING ? t.a[0][e] : 0.0);
+        const double at = (j == 0 && a.ev_a0) ? av : (t.type == MG_TERM_SPRING ? ldv<ST>(t.a[0], e) : 0.0);
         double pv, p1, p2;
         const bool ok = radial_any(t, at, rr, pv, p1, p2);
         one(ok, pv, p1, p2);
@@ -486,11 +487,11 @@ struct BuiltinRows {
   }
 };
 
-template <int N, int MODE, bool PSD, int EVT>
+template <int N, int MODE, bool PSD, int EVT, class ST = double>
 __global__ void __launch_bounds__(FastCfg<MODE, PSD>::BLOCK,
                                   (FastMinb<MODE, PSD, BuiltinRows<EVT>::kXFreeHvp>::v))
     k_rows_fast(const __grid_constant__ EvArgs a) {
-  rows_fast_body<N, MODE, PSD, BuiltinRows<EVT>>(a);
+  rows_fast_body<N, MODE, PSD, BuiltinRows<EVT, ST>>(a);
 }
 
 // Staged tile kernel, persistent and software-pipelined. Dispatched for the
@@ -952,13 +953,14 @@ int64_t flat_grid(K kern, int64_t V, int block) {
   return g < nb ? g : nb;
 }
 
-template <int N, int MODE, bool PSD, int EVT>
+template <int N, int MODE, bool PSD, int EVT, class ST>
 void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
+  constexpr bool F32 = sizeof(ST) == 4;  // fp32 storage: no row buffers, no fp64-only variants
   const size_t sm = MODE == MODE_HESS ? (size_t)hd_max * 8 + 16 : 0;
   if (sm > 227 * 1024) throw Error(MG_ERR_UNSUPPORTED, "row block does not fit in shared memory");
   const int64_t nb = (a.V + PT - 1) / PT;
   if (!nb) return;
-  auto fast = k_rows_fast<N, MODE, PSD, EVT>;
+  auto fast = k_rows_fast<N, MODE, PSD, EVT, ST>;
   // (the energy probe's values are the reference's own operations: no exact re-run)
   constexpr int XMODE = MODE == MODE_ENERGY ? MODE_GRAD : MODE;
   auto exact = k_rows_ev<N, XMODE, PSD, true>;
@@ -968,7 +970,7 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
   }
   timing_begin(p, st);
   if constexpr (MODE == MODE_HVP && !PSD && EVT != MG_TERM_EDGE_LENGTH) {
-    if (p.tiles_ready && tiles_enabled()) {
+    if (!F32 && p.tiles_ready && tiles_enabled()) {
       constexpr int SW = (MODE == MODE_HVP && PSD) ? 2 * N : N;
       constexpr bool XF = MODE == MODE_HVP && !PSD && EVT == MG_TERM_EDGE_LENGTH;
       constexpr int XW = (XF ? 0 : N) + (MODE == MODE_HVP ? N : 0);
@@ -1011,7 +1013,9 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
     MG_LAUNCH_CHECK();
     timing_end(p, st);
   }
-  if constexpr (MODE == MODE_ENERGY) return;
+  // fp32 storage: the closed forms' own NaN / Inf propagation (the exact K = n
+  // dual re-run is fp64)
+  if constexpr (MODE == MODE_ENERGY || F32) return;
   // exact re-run only when a lane was non-finite (reads the flag and exits otherwise)
   int dev = 0, sms = 148;
   MG_CUDA(cudaGetDevice(&dev));
@@ -1024,9 +1028,15 @@ void launch_rows_t(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t s
 template <int N, int MODE, bool PSD>
 void launch_rows(const Problem& p, const EvArgs& a, int hd_max, cudaStream_t st) {
   const int t0 = a.nev == 1 ? a.terms[a.ev_idx[0]].type : 0;
-  if (t0 == MG_TERM_SPRING) launch_rows_t<N, MODE, PSD, MG_TERM_SPRING>(p, a, hd_max, st);
-  else if (t0 == MG_TERM_EDGE_LENGTH) launch_rows_t<N, MODE, PSD, MG_TERM_EDGE_LENGTH>(p, a, hd_max, st);
-  else launch_rows_t<N, MODE, PSD, 0>(p, a, hd_max, st);
+  if (p.store32) {
+    if (t0 == MG_TERM_SPRING) launch_rows_t<N, MODE, PSD, MG_TERM_SPRING, float>(p, a, hd_max, st);
+    else if (t0 == MG_TERM_EDGE_LENGTH) launch_rows_t<N, MODE, PSD, MG_TERM_EDGE_LENGTH, float>(p, a, hd_max, st);
+    else launch_rows_t<N, MODE, PSD, 0, float>(p, a, hd_max, st);
+    return;
+  }
+  if (t0 == MG_TERM_SPRING) launch_rows_t<N, MODE, PSD, MG_TERM_SPRING, double>(p, a, hd_max, st);
+  else if (t0 == MG_TERM_EDGE_LENGTH) launch_rows_t<N, MODE, PSD, MG_TERM_EDGE_LENGTH, double>(p, a, hd_max, st);
+  else launch_rows_t<N, MODE, PSD, 0, double>(p, a, hd_max, st);
 }
 
 template <int N>

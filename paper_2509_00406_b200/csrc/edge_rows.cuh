@@ -16,6 +16,7 @@
 //   template <int MODE, bool NEEDV, class EP, class F> static void eterms(a, ep, rr, e, one);
 //       phi, phi', phi'' of every radial EV term at r = |d|^2, handed to
 //       one(ok, phi, phi', phi'')
+//   using Store = double | float;      // storage of x, w, outputs, attributes
 #pragma once
 #include "mg_internal.cuh"
 #include "stage.cuh"
@@ -91,6 +92,23 @@ MG_DI void row_store_bulk(double* dst, const double* src, int n) {
   }
 }
 
+// the same for floats (fp32 storage): 4-byte head until dst is 16-byte
+// aligned, one bulk copy of the aligned middle, 4-byte tail
+MG_DI void row_store_bulk_f(float* dst, const float* src, int n) {
+  int k0 = 0;
+  while (k0 < n && (reinterpret_cast<uintptr_t>(dst + k0) & 15)) {
+    dst[k0] = src[k0];
+    ++k0;
+  }
+  int m = (n - k0) & ~3;
+  for (int k = k0 + m; k < n; ++k) dst[k] = src[k];
+  if (m > 0) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src + k0);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(dst + k0), "r"(sa), "r"((uint32_t)m * 4u) : "memory");
+  }
+}
+
 // 1/x to full fp64 precision without the IEEE division sequence: hardware
 // reciprocal estimate + two Newton steps (non-finite / zero inputs give
 // non-finite results, which send the call to the exact kernel)
@@ -102,6 +120,12 @@ MG_DI double rcp_fast(double x) {
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
+
+// Storage of the per-vertex / per-element streams: fp64 (the reference's), or
+// fp32 (Problem(dtype=float32): half the bytes; arithmetic stays fp64). The
+// EvArgs pointers are typed double and reinterpreted by the storage type.
+template <class T> MG_DI double ldv(const double* p, int64_t i) { return (double)reinterpret_cast<const T*>(p)[i]; }
+template <class T> MG_DI void stv(double* p, int64_t i, double v) { reinterpret_cast<T*>(p)[i] = (T)v; }
 
 // Closed-form clamp of a radial block c_i I + c_d d d^T (r = |d|^2): the
 // transverse eigenvalue is c_i, the axial one c_i + c_d r. Already above the
@@ -183,6 +207,8 @@ template <int MODE, bool PSD, bool XFREE_HVP> struct FastMinb {
 template <int N, int MODE, bool PSD, class Pol>
 MG_DI void rows_fast_body(const EvArgs& a) {
   constexpr int T = TriN<N>::value, NN = N * N;
+  using ST = typename Pol::Store;
+  constexpr bool F32 = sizeof(ST) == 4;  // fp32 storage
   constexpr int PTB = FastCfg<MODE, PSD>::BLOCK;
   // e.g. the edge length's Hessian 2 [[I,-I],[-I,I]] does not depend on x
   // (apps/smooth.py:27-28): its unclamped HVP reads only the direction
@@ -324,8 +350,8 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     double xs[N], us[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
-      xs[c] = a.x[(int64_t)g * N + c];
-      if constexpr (MODE == MODE_HVP) us[c] = a.w[(int64_t)g * N + c];
+      xs[c] = ldv<ST>(a.x, (int64_t)g * N + c);
+      if constexpr (MODE == MODE_HVP) us[c] = ldv<ST>(a.w, (int64_t)g * N + c);
       else us[c] = 0.0;
     }
     const auto vpre = Pol::template vload<N, MODE>(a, g);
@@ -344,9 +370,9 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       const bool need = MODE != MODE_ENERGY || !((uint32_t)rc[j] >> 31);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        xo[j][c] = (!XFREE && need) ? a.x[o * N + c] : 0.0;
+        xo[j][c] = (!XFREE && need) ? ldv<ST>(a.x, o * N + c) : 0.0;
         if constexpr (MODE == MODE_HVP) {
-          const double wv = a.w[o * N + c];
+          const double wv = ldv<ST>(a.w, o * N + c);
           uo[j][c] = fo ? wv : 0.0;
         } else {
           uo[j][c] = 0.0;
@@ -372,6 +398,10 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     if constexpr (MODE == MODE_ENERGY) eacc += Pol::template venergy<N>(a, g, vpre, xs);
     else Pol::template vterms<N, MODE, PSD>(a, g, fr, vpre, xs, us, eacc, vec, dg);
     double* hrow = hbuf + ho;
+    // fp32 storage: the row built as floats in the row's (double-sized) slot of
+    // the buffer, shifted so its 16-byte phase matches the destination's
+    ST* grow = reinterpret_cast<ST*>(hbuf) + 2 * ho + (int)(((uint64_t)ro * NN - 2 * (uint64_t)ho) & 3u);
+    (void)grow;
     int pos = 0;
     // one incidence: contributions to this row
     auto incidence = [&](uint64_t r64, const double* xo_, const double* uo_, const EP& av) {
@@ -460,9 +490,15 @@ MG_DI void rows_fast_body(const EvArgs& a) {
           for (int i = 0; i < N; ++i)
 #pragma unroll
             for (int c = 0; c < N; ++c) blk[i * N + c] = -t[tri(i, c)] + (i == c ? dl - ci_s : 0.0);
-          double* dst = hrow + pos * NN;
+          if constexpr (F32) {
+            ST* dst = grow + pos * NN;
 #pragma unroll
-          for (int k = 0; k < NN; ++k) dst[k] = blk[k];
+            for (int k = 0; k < NN; ++k) dst[k] = (ST)blk[k];
+          } else {
+            double* dst = hrow + pos * NN;
+#pragma unroll
+            for (int k = 0; k < NN; ++k) dst[k] = blk[k];
+          }
           ++pos;
         }
       }
@@ -479,8 +515,8 @@ MG_DI void rows_fast_body(const EvArgs& a) {
       double x1[N], u1[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        x1[c] = a.x[o * N + c];
-        if constexpr (MODE == MODE_HVP) u1[c] = fo ? a.w[o * N + c] : 0.0;
+        x1[c] = ldv<ST>(a.x, o * N + c);
+        if constexpr (MODE == MODE_HVP) u1[c] = fo ? ldv<ST>(a.w, o * N + c) : 0.0;
         else u1[c] = 0.0;
       }
       const EP av = Pol::template eload<MODE>(a, (uint32_t)r64 & 0x7fffffffu);
@@ -489,21 +525,32 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     double* vout = MODE == MODE_HVP ? a.y : a.grad;
     if constexpr (MODE != MODE_ENERGY) {
 #pragma unroll
-      for (int i = 0; i < N; ++i) vout[(int64_t)g * N + i] = fr ? vec[i] : 0.0;
+      for (int i = 0; i < N; ++i) stv<ST>(vout, (int64_t)g * N + i, fr ? vec[i] : 0.0);
     }
     if constexpr (MODE == MODE_HESS) {
       if (fr && dp != 255) {
-        double* dst = hrow + dp * NN;
+        if constexpr (F32) {
+          ST* dst = grow + dp * NN;
 #pragma unroll
-        for (int i = 0; i < N; ++i)
+          for (int i = 0; i < N; ++i)
 #pragma unroll
-          for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
+            for (int c = 0; c < N; ++c) dst[i * N + c] = (ST)dg[tri(i, c)];
+        } else {
+          double* dst = hrow + dp * NN;
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int c = 0; c < N; ++c) dst[i * N + c] = dg[tri(i, c)];
+        }
       }
       // blocks written: off-diagonals, plus the diagonal if the walk never passed it
       const int len = (fr && dp != 255) ? (pos > dp + 1 ? pos : dp + 1) : pos;
       if (len > 0) {
         fence_proxy_async_smem();
-        row_store_bulk(a.hess + ro * NN, hrow, len * NN);
+        if constexpr (F32)
+          row_store_bulk_f(reinterpret_cast<float*>(a.hess) + ro * NN, reinterpret_cast<const float*>(grow), len * NN);
+        else
+          row_store_bulk(a.hess + ro * NN, hrow, len * NN);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }

@@ -232,6 +232,9 @@ struct Problem {
   void* row_module = nullptr;
   void* row_fn[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   bool ev_jit = false;
+  // fp32 storage of x, w, gradient, Hessian values, HVP and the builtin terms'
+  // attributes (mg_problem_set_storage): the edge row kernels only
+  bool store32 = false;
 };
 
 // element vertex ids of an op (nullptr for V: the element is the vertex)

@@ -398,6 +398,7 @@ namespace {{
 struct Pol {{
   static constexpr bool kXFreeHvp = false;
   static constexpr bool kVertexOnly = {"true" if ne == 0 else "false"};
+  using Store = double;
   template <int N, int MODE>
   MG_DI static mg::rows::JPre<{nv}> vload(const mg::rows::EvArgs& a, int g) {{
     mg::rows::JPre<{nv}> p;

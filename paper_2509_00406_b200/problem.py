@@ -195,7 +195,7 @@ class Problem:
     def __init__(self, mesh: Mesh, var_dim: int, with_hessian: bool = True,
                  fixed_vertices=(), accumulation: str = "deterministic",
                  workers: int = 1, valence_cap: int = DEFAULT_VALENCE_CAP,
-                 chunk_elements: int = 4096, live_host_attrs: bool = True):
+                 chunk_elements: int = 4096, live_host_attrs: bool = True, dtype=None):
         if var_dim < 1:
             raise ValueError("var_dim must be at least 1")
         if accumulation not in ("deterministic", "atomic"):
@@ -204,6 +204,16 @@ class Problem:
             accumulation = "deterministic"
         torch = _torch()
         self._lib = _lib.require_cuda()
+        # storage precision (the reference computes in float64, active.py:333):
+        # float32 halves every stream's bytes; the kernels still compute in fp64
+        # (mg_problem_set_storage). Edge row kernels only: builtin vertex and
+        # radial edge terms, deterministic accumulation; eval_terms / hvp /
+        # eval_energy_only (the solvers' BSR kernels stay fp64).
+        self.dtype = torch.float64 if dtype is None else dtype
+        if self.dtype not in (torch.float64, torch.float32):
+            raise ValueError("dtype must be torch.float64 or torch.float32")
+        if self.dtype == torch.float32 and accumulation != "deterministic":
+            raise ValueError("float32 storage needs deterministic accumulation")
         self.mesh = mesh
         self.n = var_dim
         self.with_hessian = with_hessian
@@ -225,8 +235,10 @@ class Problem:
                                                self._fixed_device.data_ptr() if nv else None,
                                                int(accumulation == "deterministic"), ctypes.byref(h)))
         self._h = h
-        self.x_device = torch.zeros(self._num_dofs, dtype=torch.float64, device=self._dev)
-        self.grad_device = torch.zeros(self._num_dofs, dtype=torch.float64, device=self._dev)
+        if self.dtype == torch.float32:
+            _lib.check(self._lib.mg_problem_set_storage(h, 32))
+        self.x_device = torch.zeros(self._num_dofs, dtype=self.dtype, device=self._dev)
+        self.grad_device = torch.zeros(self._num_dofs, dtype=self.dtype, device=self._dev)
         self._energy_device = torch.full((1,), float("nan"), dtype=torch.float64, device=self._dev)
         self.hess: BlockSparseMatrix | None = None
         self.energy: float = float("nan")
@@ -267,6 +279,11 @@ class Problem:
         torch = _torch()
         rec = _TermRecord(fn, kind, op)
         for a in fn.attrs():
+            if self.dtype == torch.float32:  # fp32 copies (a CUDA tensor is snapshotted: refresh_attrs updates)
+                rec.host_attrs.append(a)
+                rec.dev_attrs.append(_as_device(a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a,
+                                                torch, self._dev).to(torch.float32))
+                continue
             rec.host_attrs.append(None if isinstance(a, torch.Tensor) else a)
             rec.dev_attrs.append(_as_device(a, torch, self._dev))
         params = fn.params(self.n)
@@ -288,6 +305,11 @@ class Problem:
         return {Op.V: None, Op.EV: self.mesh.edges, Op.FV: self.mesh.faces}[op]
 
     def _add_traced_term(self, kind: Element, op: Op, fn) -> int:
+        if self.dtype != _torch().float64:
+            raise NotImplementedError("float32 storage supports the builtin terms only")
+        return self._add_traced_term64(kind, op, fn)
+
+    def _add_traced_term64(self, kind: Element, op: Op, fn) -> int:
         """A general callback (ref problem.py:8-14, 301-310): traced once on
         symbolic inputs, compiled to an sm_100a module, launched by the engine
         (jit.py). Closure arrays indexed by `handle.index` become per-element
@@ -457,6 +479,9 @@ class Problem:
                 continue
             for slot, host in enumerate(rec.host_attrs):
                 if host is not None:
+                    if isinstance(host, _torch().Tensor):  # float32 storage: a snapshotted CUDA tensor
+                        rec.dev_attrs[slot].view(-1).copy_(host.reshape(-1))
+                        continue
                     src = np.ascontiguousarray(np.asarray(host, dtype=np.float64)).reshape(-1)
                     rec.dev_attrs[slot].view(-1).copy_(_torch().from_numpy(src), non_blocking=False)
 
@@ -493,7 +518,7 @@ class Problem:
     def x(self, value) -> None:
         torch = _torch()
         if isinstance(value, torch.Tensor):
-            src = value.detach().to(device=self._dev, dtype=torch.float64).reshape(-1)
+            src = value.detach().to(device=self._dev, dtype=self.dtype).reshape(-1)
         else:
             src = torch.from_numpy(np.ascontiguousarray(np.asarray(value, dtype=np.float64)).reshape(-1))
         if src.numel() != self._num_dofs:
@@ -517,7 +542,7 @@ class Problem:
         ci = torch.empty(max(1, nnzb.value), dtype=torch.int64, device=self._dev)
         _lib.check(self._lib.mg_copy_pattern(self._h, ro.data_ptr(), ci.data_ptr(), _lib.stream_ptr()))
         n = self.n
-        values = torch.zeros((nnzb.value, n, n), dtype=torch.float64, device=self._dev)
+        values = torch.zeros((nnzb.value, n, n), dtype=self.dtype, device=self._dev)
         self.hess = BlockSparseMatrix(n, nv, ro.cpu().numpy(), ci[: nnzb.value].cpu().numpy(), values, self)
         self.hess.row_offsets_device = ro
         self.hess.col_indices_device = ci[: nnzb.value]
@@ -572,11 +597,11 @@ class Problem:
         if isinstance(v, torch.Tensor):
             if v.numel() != self._num_dofs:
                 raise ValueError(msg.format(self._num_dofs))
-            return v.detach().to(device=self._dev, dtype=torch.float64).contiguous().reshape(-1)
+            return v.detach().to(device=self._dev, dtype=self.dtype).contiguous().reshape(-1)
         a = np.asarray(v, dtype=np.float64)
         if a.shape != (self._num_dofs,):
             raise ValueError(msg.format(self._num_dofs))
-        return torch.from_numpy(np.ascontiguousarray(a)).to(self._dev)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self._dev).to(self.dtype)
 
     def hvp(self, x, v, psd_floor: float | None = None, out=None):
         """Matrix-free Hessian-vector product (ref problem.py:578-617).
@@ -591,11 +616,11 @@ class Problem:
         xd = self._vec_in(x, msg)
         vd = self._vec_in(v, msg)
         self._sync_attrs()
-        if out is not None and not (isinstance(out, torch.Tensor) and out.dtype == torch.float64
+        if out is not None and not (isinstance(out, torch.Tensor) and out.dtype == self.dtype
                                     and out.device == vd.device and out.is_contiguous()
                                     and out.numel() == self._num_dofs):
-            raise ValueError(f"out must be a contiguous float64 CUDA tensor of {self._num_dofs} entries")
-        y = out if out is not None else torch.empty(self._num_dofs, dtype=torch.float64, device=self._dev)
+            raise ValueError(f"out must be a contiguous {self.dtype} CUDA tensor of {self._num_dofs} entries")
+        y = out if out is not None else torch.empty(self._num_dofs, dtype=self.dtype, device=self._dev)
         _lib.check(self._lib.mg_hvp(self._h, xd.data_ptr(), vd.data_ptr(), int(psd_floor is not None),
                                     float(psd_floor or 0.0), y.data_ptr(), _lib.stream_ptr()))
         res = y.cpu().numpy() if host else y
