@@ -15,10 +15,11 @@ EVT = {"2": "SPRING", "4": "EDGE_LENGTH", "0": "ANY"}
 
 
 def label_of(kernel):
-    m = re.search(r"k_rows_fast<(\d), (\d), (\d), (\d)>", kernel)
+    m = re.search(r"k_rows_fast<(\d), (\d), (\d), (\d)(?:, (double|float))?>", kernel)
     if m:
-        n, mode, psd, evt = m.groups()
-        return f"k_rows_fast<{n},{MODES[mode]}{',psd' if psd == '1' else ''},{EVT[evt]}>"
+        n, mode, psd, evt, st = m.groups()
+        return (f"k_rows_fast<{n},{MODES[mode]}{',psd' if psd == '1' else ''},{EVT[evt]}"
+                f"{',fp32' if st == 'float' else ''}>")
     m = re.search(r"k_rows_dirichlet<(\d), (\d), (\d)>", kernel)
     if m:
         mode, psd, _ = m.groups()
