@@ -464,7 +464,7 @@ struct BuiltinRows {
   MG_DI static VPreload<N> vload(const EvArgs& a, int g) { return vterms_load<N, MODE, ST>(a, g); }
   template <int N, int MODE, bool PSD>
   MG_DI static void vterms(const EvArgs& a, int g, bool, const VPreload<N>& v, const double* xs, const double* us,
-                           double& eacc, double* vec, double* dg) {
+                           double& eacc, double* vec, double* dg, bool&) {
     vterms_closed<N, MODE, PSD, ST>(a, g, v, xs, us, eacc, vec, dg);
   }
   template <int MODE>

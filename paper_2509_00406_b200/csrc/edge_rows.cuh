@@ -9,8 +9,9 @@
 //                                      // HVP kernels may read 32-bit records
 //   template <int N, int MODE> static auto vload(const EvArgs&, int g);
 //       V-term attribute loads, issued before the incidence gathers
-//   template <int N, int MODE, bool PSD> static void vterms(a, g, fr, pre, xs, us, eacc, vec, dg);
+//   template <int N, int MODE, bool PSD> static void vterms(a, g, fr, pre, xs, us, eacc, vec, dg, finite);
 //       the row's V terms: energy, gradient / H u into vec, Hessian into dg
+//       (closed forms that can miss the reference's NaN placement clear finite)
 //   template <int MODE> static auto eload(const EvArgs&, uint32_t e);
 //       per-edge attribute loads of one incidence (issued with the gathers)
 //   template <int MODE, bool NEEDV, class EP, class F> static void eterms(a, ep, rr, e, one);
@@ -396,7 +397,7 @@ MG_DI void rows_fast_body(const EvArgs& a) {
     for (int i = 0; i < T; ++i) dg[i] = 0.0;
     // V terms (their attribute loads overlapped the level-3 loads)
     if constexpr (MODE == MODE_ENERGY) eacc += Pol::template venergy<N>(a, g, vpre, xs);
-    else Pol::template vterms<N, MODE, PSD>(a, g, fr, vpre, xs, us, eacc, vec, dg);
+    else Pol::template vterms<N, MODE, PSD>(a, g, fr, vpre, xs, us, eacc, vec, dg, finite);
     double* hrow = hbuf + ho;
     // fp32 storage: the row built as floats in the row's (double-sized) slot of
     // the buffer, shifted so its 16-byte phase matches the destination's

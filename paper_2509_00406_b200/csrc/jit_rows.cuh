@@ -66,6 +66,59 @@ template <class R> MG_DI double jr_d2(const R& r) {
 }
 MG_DI double jr_d2(double) { return 0.0; }
 
+// one traced V term the tracer proved radial in d = x - t (t an attribute
+// or constant vector; jit.py radial_vform): E = phi(|d|^2) on a one-variable
+// second-order dual, gradient 2 phi' d, Hessian A = 2 phi' I + 4 phi'' d d^T
+// (clamped in closed form under a PSD floor). A non-finite value clears
+// `finite` (the patch module's exact re-run then places NaN like the reference).
+template <int N, int MODE, bool PSD, class PHI>
+MG_DI void jit_vradial(const PHI& phi, const double* av, const double* d, const double* us, double floor,
+                       double& eacc, double* vec, double* dg, bool& finite) {
+  double rr = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c) rr = d[c] * d[c] + rr;
+  double pv, p1, p2;
+  if constexpr (MODE == MODE_GRAD || MODE == MODE_ENERGY) {
+    Dg<1> R;
+    R.v = rr;
+    R.g[0] = 1.0;
+    const auto r = phi(av, R);
+    pv = jr_value(r);
+    p1 = jr_d1(r);
+    p2 = 0.0;
+  } else {
+    Dh<1, true> R;
+    R.v = rr;
+    R.g[0] = 1.0;
+    const auto r = phi(av, R);
+    pv = jr_value(r);
+    p1 = jr_d1(r);
+    p2 = jr_d2(r);
+  }
+  finite &= isfinite(pv + p1 + p2);
+  eacc += pv;
+  if constexpr (MODE == MODE_GRAD || MODE == MODE_HESS) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) vec[c] += 2.0 * p1 * d[c];
+  }
+  if constexpr (MODE == MODE_HESS || MODE == MODE_HVP) {
+    double ci = 2.0 * p1, cd = 4.0 * p2;
+    if constexpr (PSD) radial_clamp_fast(ci, cd, rr, floor);
+    if constexpr (MODE == MODE_HESS) {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c <= i; ++c) dg[tri(i, c)] += cd * d[i] * d[c] + (i == c ? ci : 0.0);
+    } else {
+      double du = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) du += d[c] * us[c];
+#pragma unroll
+      for (int i = 0; i < N; ++i) vec[i] += ci * us[i] + cd * d[i] * du;
+    }
+  }
+}
+
 // phi, phi', phi'' of one traced radial EV term at r (gradient mode: a
 // first-order dual, phi'' = 0)
 template <int MODE, bool NEEDV, class PHI, class F>

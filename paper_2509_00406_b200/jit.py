@@ -274,36 +274,30 @@ _XIN = re.compile(r"^X\[(\d+)\]\[(\d+)\]$")
 _ATTR = re.compile(r"A\[(\d+)\]\[e\]")
 
 
-def radial_form(tt: TracedTerm):
-    """Prove that an EV callback depends on its vertex positions only through
-    r = |x_0 - x_1|^2, from the recorded operations: every use of an input
-    is a component difference d_c = x_0[c] - x_1[c] (either orientation),
-    those are only squared (d_c * d_c, equal signs) and the squares only
-    summed until one symbol r holds each component's square exactly once
-    (ActiveVec.norm2 / dot, active.py); every later operation reaches the
-    inputs only through r. Returns (r name, [phi lines]) — the operations
-    after r, in order, with r bound to the input R — or None.
-    (The reference's K = 2n duals of such a term give gradient 2 phi' d and
-    Hessian blocks +-(2 phi' I + 4 phi'' d d^T): jit_rows.cuh.)"""
-    if tt.op != "EV" or tt.P != 2 or not tt.ops or len(tt.ops) != len(tt.body):
-        return None
+def _radial(tt: TracedTerm, dsym_of):
+    """Shared proof of radial structure (radial_form / radial_vform).
+    dsym_of(kind, args) -> (component, sign, C++ expression of d_c) for an
+    operation that forms a difference component, None for one that uses the
+    inputs otherwise (then the term is not radial), or False when the
+    operation does not read an input directly."""
     n = tt.n
     full = tuple(range(n))
     xdep, dsym, sq, post = set(), {}, {}, set()
+    dexpr = {}
     r_name = None
     for name, kind, args in tt.ops:
-        xin = [_XIN.match(o) for o in args]
-        dep = [o for o, m in zip(args, xin) if m or o in xdep]
+        direct = any(_XIN.match(o) for o in args)
+        dep = [o for o in args if _XIN.match(o) or o in xdep]
         if not dep:
             continue
         xdep.add(name)
-        if any(xin):
-            if kind != "sub" or len(args) != 2 or not all(xin):
+        if direct:
+            got = dsym_of(kind, args)
+            if not got:
                 return None
-            (q0, c0), (q1, c1) = [(int(m.group(1)), int(m.group(2))) for m in xin]
-            if c0 != c1 or {q0, q1} != {0, 1}:
-                return None
-            dsym[name] = (c0, 1 if q0 == 0 else -1)
+            c, sign, expr = got
+            dsym[name] = (c, sign)
+            dexpr.setdefault(c, expr)
             continue
         if kind == "mul" and len(args) == 2 and args[0] in dsym and args[1] in dsym:
             (ca, sa), (cb, sb) = dsym[args[0]], dsym[args[1]]
@@ -333,7 +327,61 @@ def radial_form(tt: TracedTerm):
     elif ret not in post and ret != r_name:
         return None
     lines = [f"auto {r_name} = R;"] + [ln for (nm, _, _), ln in zip(tt.ops, tt.body) if nm in post]
-    return r_name, lines
+    return r_name, lines, [dexpr[c] for c in full] if set(dexpr) == set(full) else None
+
+
+def radial_form(tt: TracedTerm):
+    """Prove that an EV callback depends on its vertex positions only through
+    r = |x_0 - x_1|^2, from the recorded operations: every use of an input
+    is a component difference d_c = x_0[c] - x_1[c] (either orientation),
+    those are only squared (d_c * d_c, equal signs) and the squares only
+    summed until one symbol r holds each component's square exactly once
+    (ActiveVec.norm2 / dot, active.py); every later operation reaches the
+    inputs only through r. Returns (r name, [phi lines]) — the operations
+    after r, in order, with r bound to the input R — or None.
+    (The reference's K = 2n duals of such a term give gradient 2 phi' d and
+    Hessian blocks +-(2 phi' I + 4 phi'' d d^T): jit_rows.cuh.)"""
+    if tt.op != "EV" or tt.P != 2 or not tt.ops or len(tt.ops) != len(tt.body):
+        return None
+
+    def dsym_of(kind, args):
+        xin = [_XIN.match(o) for o in args]
+        if kind != "sub" or len(args) != 2 or not all(xin):
+            return None
+        (q0, c0), (q1, c1) = [(int(m.group(1)), int(m.group(2))) for m in xin]
+        if c0 != c1 or {q0, q1} != {0, 1}:
+            return None
+        return c0, 1 if q0 == 0 else -1, ""
+
+    rf = _radial(tt, dsym_of)
+    return None if rf is None else (rf[0], rf[1])
+
+
+def radial_vform(tt: TracedTerm):
+    """The same proof for a V callback: the inputs enter only as differences
+    d_c = x[c] - t_c with t_c an attribute stream or a constant (either
+    orientation; inertia 0.5 m |x - t|^2, apps/cloth.py:102-104), squared and
+    summed into r. Returns (r name, [phi lines], [C++ d_c over x[], av[]]) or
+    None."""
+    if tt.op != "V" or not tt.ops or len(tt.ops) != len(tt.body):
+        return None
+
+    def dsym_of(kind, args):
+        if kind != "sub" or len(args) != 2:
+            return None
+        xin = [_XIN.match(o) for o in args]
+        if all(xin) or not any(xin):
+            return None
+        k = 0 if xin[0] else 1
+        c = int(xin[k].group(2))
+        other = _preloaded(args[1 - k])
+        expr = f"x[{c}] - {other}" if k == 0 else f"{other} - x[{c}]"
+        return c, 1 if k == 0 else -1, expr
+
+    rf = _radial(tt, dsym_of)
+    if rf is None or rf[2] is None:
+        return None
+    return rf
 
 
 def _preloaded(text: str) -> str:
@@ -354,7 +402,29 @@ def rows_source(terms: list, n: int) -> str | None:
     for i, t in enumerate(terms):
         k = len(t.attrs)
         ret = _preloaded(t.ret)
-        if t.op == "V":
+        rv = radial_vform(t) if t.op == "V" else None
+        if rv is not None:
+            body = "\n      ".join(_preloaded(ln) for ln in rv[1])
+            dlines = "\n    ".join(f"d[{c}] = {e};" for c, e in enumerate(rv[2]))
+            funcs.append(f"""struct V{i} {{
+  template <class S>
+  MG_DI auto operator()(const double* av, const S& R) const {{
+      using namespace mg;
+      (void)av;
+      {body}
+      return {ret};
+  }}
+  MG_DI static void dvec(const double* av, const double* x, double* d) {{
+    (void)av;
+    {dlines}
+  }}
+}};""")
+            vloads += [f"p.v[{nv + j}] = a.js[{js + j}][g];" for j in range(k)]
+            vcalls.append(f"{{ double d[N]; V{i}::dvec(p.v + {nv}, xs, d); "
+                          f"mg::rows::jit_vradial<N, MODE, PSD>(V{i}{{}}, p.v + {nv}, d, us, a.floor, eacc, vec, dg, "
+                          f"finite); }}")
+            nv += k
+        elif t.op == "V":
             body = "\n      ".join(_preloaded(ln) for ln in t.body)
             funcs.append(f"""struct V{i} {{
   template <int N, class S>
@@ -408,8 +478,8 @@ struct Pol {{
   }}
   template <int N, int MODE, bool PSD>
   MG_DI static void vterms(const mg::rows::EvArgs& a, int g, bool fr, const mg::rows::JPre<{nv}>& p, const double* xs,
-                           const double* us, double& eacc, double* vec, double* dg) {{
-    (void)a; (void)g; (void)fr; (void)p; (void)xs; (void)us; (void)eacc; (void)vec; (void)dg;
+                           const double* us, double& eacc, double* vec, double* dg, bool& finite) {{
+    (void)a; (void)g; (void)fr; (void)p; (void)xs; (void)us; (void)eacc; (void)vec; (void)dg; (void)finite;
     {j.join(vcalls)}
   }}
   template <int MODE>
