@@ -52,6 +52,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import resource
 import statistics
 import subprocess
 import sys
@@ -163,7 +164,8 @@ def build_engine_cloth(n, accumulation, patch=64):
 
 def build_engine_cloth_shard(n, world, rank, accumulation):
     """Rank `rank`'s shard of the weak-scaling cloth: a 2048 x (2048 world) grid."""
-    import paper_2509_00406_b200 as mg
+    import torch
+
     from paper_2509_00406_b200.distributed import DistributedProblem
     from paper_2509_00406_b200.terms import Gravity, Inertia, Spring
 
@@ -171,18 +173,30 @@ def build_engine_cloth_shard(n, world, rank, accumulation):
     sp = 1.0 / (n - 1)
     pos, faces = grid_rect_arrays(n, ny, sp)
     target, x, v = cloth_state(pos, n)
-    areas = 0.5 * np.linalg.norm(np.cross(pos[faces[:, 1]] - pos[faces[:, 0]], pos[faces[:, 2]] - pos[faces[:, 0]]), axis=1)
-    masses = np.bincount(faces.ravel(), weights=np.repeat(areas / 3.0, 3), minlength=len(pos))
-    edges = mg.mesh._host_edges(faces, None, len(pos))
-    d = pos[edges[:, 1]] - pos[edges[:, 0]]
+    # lumped masses and rest lengths built on the rank's device (every rank
+    # holds the whole grid's inputs; a host build is O(mesh) numpy per rank),
+    # and passed as device attributes as on the N = 1 path (numpy attributes
+    # are re-read on every call, the reference's live-closure semantics)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    pos_d, f_d = dev(pos), dev(faces)
+    cr = torch.linalg.cross(pos_d[f_d[:, 1]] - pos_d[f_d[:, 0]], pos_d[f_d[:, 2]] - pos_d[f_d[:, 0]])
+    area3 = (0.5 * torch.linalg.vector_norm(cr, dim=1) / 3.0).repeat_interleave(3)
+    masses_d = torch.zeros(len(pos), dtype=torch.float64, device="cuda").index_add_(0, f_d.reshape(-1), area3)
+    sides = torch.cat([f_d[:, [0, 1]], f_d[:, [1, 2]], f_d[:, [2, 0]]])
+    keys = torch.unique(sides.min(dim=1).values * len(pos) + sides.max(dim=1).values)  # the engine's edge order
+    dd = pos_d[keys % len(pos)] - pos_d[keys // len(pos)]
+    l2 = (dd * dd).sum(dim=1)
+    n_edges = keys.numel()
+    del cr, area3, sides, keys, dd, pos_d, f_d
     h = 0.01
-    terms = [("V", Inertia(masses, target)), ("EV", Spring(np.einsum("ij,ij->i", d, d), 0.5 * 1e4 * h * h)),
-             ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
+    terms = [("V", Inertia(masses_d, dev(target))), ("EV", Spring(l2, 0.5 * 1e4 * h * h)),
+             ("V", Gravity(masses_d, np.array([0.0, -9.8, 0.0]), h * h))]
     pins = (n * (ny - 1), n * ny - 1)
-    dp = DistributedProblem(pos, faces, 3, terms, fixed_vertices=pins, accumulation=accumulation)
+    # id-range partition: horizontal 2048-row stripes of the row-major grid
+    dp = DistributedProblem(pos, faces, 3, terms, fixed_vertices=pins, accumulation=accumulation, partition="range")
     dp.set_x_global(x)
     dp.problem.precompute_sparsity()
-    return dp, len(pos), len(edges)
+    return dp, len(pos), n_edges
 
 
 class Clocks:
@@ -553,8 +567,11 @@ def run_engine(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MG_BENCH_DIST=1: the sharded path (NCCL, halo exchange, energy all_reduce)
+    # even at one rank, so a one-GPU box runs the N > 1 code end to end
+    sharded = world > 1 or os.environ.get("MG_BENCH_DIST") == "1"
     dist = None
-    if world > 1:
+    if sharded:
         import torch.distributed as tdist
 
         # MG_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo (a functional run
@@ -572,7 +589,7 @@ def run_engine(args):
 
     n = args.grid
     t_setup = time.perf_counter()
-    if world == 1:
+    if not sharded:
         V, E = cloth_sizes(n)
         p, x, v = build_engine_cloth(n, args.accumulation, args.patch)
         dp = None
@@ -612,7 +629,7 @@ def run_engine(args):
     value = units / (ms * 1e-3)
     peak, peak_kind = peaks()
     label = kernel_label(p, "psd")
-    if world == 1:
+    if not sharded:
         roofline = roofline_obj(label, kms, cloth_bytes(V, E, nnzb_local), peak, peak_kind,
                                 "24V x + 24V target + 8V masses + 8E rest lengths + 8E edge ids + 24V grad + 72 nnzb H",
                                 workload=f"grid{n}")
@@ -622,7 +639,7 @@ def run_engine(args):
 
     # e2e through the public API with host buffers
     extras = {}
-    if world == 1:
+    if not sharded:
         x_host = torch.from_numpy(x).pin_memory()
         g_host = torch.empty(p.num_dofs, dtype=torch.float64).pin_memory()
         e_host = torch.empty(1, dtype=torch.float64).pin_memory()
@@ -657,7 +674,7 @@ def run_engine(args):
     e2e = {"value": units / (ms_e2e * 1e-3), "unit": "term-elements/s",
            "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": d2h,
            "ms_per_step": ms_e2e, "path": path}
-    if world == 1:
+    if not sharded:
         ms_dev_h, _ = time_device(lambda: e2e_step(False), max(3, steps // 2), 2, dist)
         extras["cloth_e2e_h_on_device"] = {
             "ms": ms_dev_h, "term_elements_per_s": units / (ms_dev_h * 1e-3),
@@ -665,13 +682,13 @@ def run_engine(args):
             "path": "as e2e, but the Hessian stays on the device"}
         del h_host
 
-    if not args.no_extras and world == 1:
+    if not args.no_extras and not sharded:
         extras.update(run_extras(p, v, V, E, nnzb_local, steps, peak, peak_kind))
         for k, r in run_traced(n, max(5, steps // 2), peak, peak_kind).items():
             r["vs_builtin_newton_step"] = r["newton_step_ms"] / ms
             extras[k] = r
         extras.update(run_fp32(n, max(5, steps // 2), peak, peak_kind))
-    if not args.no_configs and world == 1:
+    if not args.no_configs and not sharded:
         del p
         gc_cuda()
         extras.update(run_configs(peak, peak_kind, args.sub))
@@ -679,12 +696,12 @@ def run_engine(args):
             extras["configs_cpu_baseline"] = cpu_config_rates()
         if not args.no_config5:
             extras.update(run_config5(peak, peak_kind, args.grid5))
-    if world > 1 and not args.no_config5:
+    if sharded and not args.no_config5:
         del p, dp
         gc_cuda()
         extras.update(run_config5_dist(world, rank, dist, args.grid5))
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not sharded and not args.no_cpu:
         cpu = cpu_baseline_line(n)
     if rank == 0:
         cfg = headline_config(n, world, args.accumulation)
@@ -1080,11 +1097,15 @@ def run_config5_dist(world, rank, dist, n=7072, steps=10):
     h = 0.01
     terms = [("V", Inertia(masses, target)), ("EV", Spring(l2, 0.5 * 1e4 * h * h)),
              ("V", Gravity(masses, np.array([0.0, -9.8, 0.0]), h * h))]
-    dp = DistributedProblem(pos, faces, 3, terms, fixed_vertices=default_pins(n), with_hessian=False, overlap=True)
+    # id-range partition: horizontal stripes of the row-major grid (two ribbon
+    # rows per cut); owned rows are contiguous slices, so the direction is
+    # written straight into the shard's buffer and the result read as a view
+    dp = DistributedProblem(pos, faces, 3, terms, fixed_vertices=default_pins(n), with_hessian=False, overlap=True,
+                            partition="range")
     dp.set_x_global(x.cpu().numpy())
     own = torch.as_tensor(dp.plan.owned_global, device="cuda")
-    v_own = v.view(-1, 3).index_select(0, own).contiguous()
-    y_own = torch.empty_like(v_own)
+    v_own = dp.v_owned_buffer()
+    v_own.copy_(v.view(-1, 3).index_select(0, own))
     del pos_d, x, v, target, masses, l2
     gc_cuda()
     st = time.perf_counter() - t0
@@ -1092,10 +1113,11 @@ def run_config5_dist(world, rank, dist, n=7072, steps=10):
     te = 2 * V + E
     out = {"setup_s": st, "owned_rows": len(dp.plan.owned_global), "interior_rows": dp.interior_rows,
            "boundary_rows": dp.boundary_rows, "halo_bytes_per_exchange": dp.halo.bytes_per_call,
-           "scaling": "strong (one 7072^2 mesh over all ranks)"}
+           "scaling": f"strong (one {n}^2 mesh over all ranks)", "partition": "global id ranges (grid stripes)",
+           "host_max_rss_gb": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20}
     ms, _ = time_device(lambda: dp.eval_terms(sync=False), steps, 3, dist)
     out["grad"] = {"ms": ms, "term_elements_per_s": te / (ms * 1e-3)}
-    ms, _ = time_device(lambda: dp.hvp_owned(v_own, out=y_own), steps, 3, dist)
+    ms, _ = time_device(lambda: dp.hvp_owned(v_own), steps, 3, dist)
     out["hvp"] = {"ms": ms, "term_elements_per_s": te / (ms * 1e-3)}
     del dp
     gc_cuda()

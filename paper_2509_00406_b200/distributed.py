@@ -72,6 +72,15 @@ def morton_owner(positions, world: int) -> np.ndarray:
     return _morton_owner_t(torch.from_numpy(np.asarray(positions, dtype=np.float64)), world).numpy()
 
 
+def range_owner(nv: int, world: int) -> np.ndarray:
+    """Rank owning each vertex when the ranks own balanced contiguous global
+    id ranges. For meshes numbered coherently in space (generate_grid's
+    row-major grid: horizontal stripes, two ribbon rows per cut) the owned rows
+    are then one contiguous slice of every shard-local array (local ids
+    increase with global ids), so owned-row inputs and results are views."""
+    return (np.arange(nv, dtype=np.int64) * world // max(nv, 1)).astype(np.int32)
+
+
 def _edge_keys(faces, nv):
     import torch
 
@@ -280,23 +289,31 @@ class DistributedProblem:
 
     def __init__(self, positions, faces, var_dim: int, terms, fixed_vertices=(), edges=None,
                  with_hessian: bool = True, accumulation: str = "deterministic", group=None, plan=None,
-                 patch_vertices: int = 128, overlap: bool = False):
+                 patch_vertices: int = 128, overlap: bool = False, partition: str = "morton"):
         """overlap (gradient-mode problems, deterministic accumulation): the
         owned rows are split into interior rows (no ribbon vertex in any
         incident element) and boundary rows, assembled by two engine problems
         on the same shard and sharing x / gradient / HVP buffers; the interior
         kernel runs while the ribbon exchange is in flight, the boundary
-        kernel after it lands."""
+        kernel after it lands.
+
+        partition: "morton" (default; balanced Morton ranges of the
+        positions, any numbering) or "range" (balanced global id ranges,
+        `range_owner`; owned rows become contiguous views). Ignored when
+        `plan` is given."""
         import torch
         import torch.distributed as dist
 
         from .mesh import Element, Mesh, Op
         from .problem import Problem
 
+        if partition not in ("morton", "range"):
+            raise ValueError(f"partition must be 'morton' or 'range', got {partition!r}")
         if plan is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
             rank = dist.get_rank(group) if dist.is_initialized() else 0
-            plan = ShardPlan(positions, faces, edges, world, rank, device="cuda", group=group)
+            owner = range_owner(len(positions), world) if partition == "range" else None
+            plan = ShardPlan(positions, faces, edges, world, rank, owner=owner, device="cuda", group=group)
         self.plan = plan
         pl = self.plan
         self.n = var_dim
@@ -340,11 +357,17 @@ class DistributedProblem:
         else:
             self.problem = Problem(mesh, var_dim, with_hessian=with_hessian, fixed_vertices=fixed_l,
                                    accumulation=accumulation)
+            self.interior_rows, self.boundary_rows = int(pl.owned.sum()), 0
             for op, t in sterms:
                 self.problem.add_term(kinds[op], getattr(Op, op), t)
             self._boundary = None
         self.halo = HaloExchange(pl, var_dim, torch.device("cuda"), group)
         self._owned_rows = torch.as_tensor(np.flatnonzero(pl.owned), device="cuda")
+        self.num_owned = int(pl.owned.sum())
+        # owned rows contiguous in the local numbering (id-range partitions:
+        # local ids increase with global ids): views instead of gathers
+        o0 = int(np.argmax(pl.owned)) if self.num_owned else 0
+        self._slice = slice(o0, o0 + self.num_owned) if pl.owned[o0:o0 + self.num_owned].all() else None
         self._v_local = None
         self._x_fresh = False  # ribbon rows of x hold their owners' current values
 
@@ -362,7 +385,10 @@ class DistributedProblem:
 
         xl = self.problem.x_device.view(-1, self.n)
         src = torch.as_tensor(x_owned, dtype=torch.float64, device=xl.device).view(-1, self.n)
-        xl.index_copy_(0, self._owned_rows, src)
+        if self._slice is not None:
+            xl[self._slice].copy_(src)
+        else:
+            xl.index_copy_(0, self._owned_rows, src)
         self._x_fresh = False
 
     def _sync_x(self):
@@ -398,17 +424,29 @@ class DistributedProblem:
 
     def grad_owned(self):
         """(owned, n) gradient rows of this rank (device tensor)."""
-        return self.problem.grad_device.view(-1, self.n).index_select(0, self._owned_rows)
+        return self.owned_view(self.problem.grad_device)
+
+    def owned_view(self, local):
+        """(owned, n) rows of a shard-local array: a view when the owned rows
+        are contiguous (id-range partitions), else a gather."""
+        t = local.view(-1, self.n)
+        return t[self._slice] if self._slice is not None else t.index_select(0, self._owned_rows)
 
     def hvp_owned(self, v_owned, psd_floor=None, out=None):
-        """y = H v restricted to owned rows; v given on owned rows (halo-exchanged here)."""
+        """y = H v restricted to owned rows; v given on owned rows (halo-exchanged here).
+        Without `out` the rows are a view of the shard's result buffer when the
+        owned rows are contiguous (overwritten by the next call)."""
         import torch
 
         if self._v_local is None:
             self._v_local = torch.zeros_like(self.problem.x_device)
             self._y_local = torch.empty_like(self.problem.x_device)
         vl = self._v_local.view(-1, self.n)
-        vl.index_copy_(0, self._owned_rows, torch.as_tensor(v_owned, dtype=torch.float64, device=vl.device).view(-1, self.n))
+        src = torch.as_tensor(v_owned, dtype=torch.float64, device=vl.device).view(-1, self.n)
+        if self._slice is None:
+            vl.index_copy_(0, self._owned_rows, src)
+        elif src.data_ptr() != vl[self._slice].data_ptr():  # v_owned_buffer(): written in place
+            vl[self._slice].copy_(src)
         if self._boundary is not None:
             hv = self.halo.start(self._v_local)
             hx = None if self._x_fresh else self.halo.start(self.problem.x_device)
@@ -422,11 +460,24 @@ class DistributedProblem:
             self.halo.exchange(self._v_local)
             self._sync_x()  # x only when its owned rows changed since the last exchange
             y = self.problem.hvp(self.problem.x_device, self._v_local, psd_floor=psd_floor, out=self._y_local)
-        rows = y.view(-1, self.n).index_select(0, self._owned_rows)
+        rows = self.owned_view(y)
         if out is not None:
             out.view(-1, self.n).copy_(rows)
             return out
         return rows
+
+    def v_owned_buffer(self):
+        """The (owned, n) direction rows hvp_owned reads, as a writable view of
+        the shard-local direction (id-range partitions): a caller that writes
+        its direction here and passes this view skips the copy-in."""
+        import torch
+
+        if self._v_local is None:
+            self._v_local = torch.zeros_like(self.problem.x_device)
+            self._y_local = torch.empty_like(self.problem.x_device)
+        if self._slice is None:
+            raise ValueError("owned rows are not contiguous in the shard numbering (use partition='range')")
+        return self._v_local.view(-1, self.n)[self._slice]
 
     def hvp_from_global(self, v_global, psd_floor=None):
         """Owned rows of H v for a full global v (every rank passes the same
@@ -436,7 +487,7 @@ class DistributedProblem:
         vl = torch.as_tensor(np.asarray(v_global, dtype=np.float64).reshape(-1, self.n)[self.plan.verts].ravel(),
                              device="cuda")
         y = self.problem.hvp(self.problem.x_device, vl, psd_floor=psd_floor)
-        return y.view(-1, self.n).index_select(0, self._owned_rows)
+        return self.owned_view(y)
 
     def hess_rows_owned(self):
         """(row_offsets, global col_indices, values) of the owned rows, in owned-row order."""

@@ -158,3 +158,27 @@ def test_partition_balanced_and_contiguous():
             # send/recv lists are mirror images
             for q_, lst in p.send.items():
                 assert np.array_equal(p.verts[lst], plans[q_].verts[plans[q_].recv[p.rank]])
+
+
+def test_range_partition_owned_rows_contiguous():
+    """Id-range partitions of a row-major grid are horizontal stripes: owned
+    rows form one contiguous slice of every shard's numbering (the views the
+    gradient / HVP calls return), and each cut carries one ribbon row per side."""
+    from paper_2509_00406_b200.distributed import ShardPlan, range_owner
+    from paper_2509_00406_b200.mesh import grid_arrays
+
+    n = 32
+    pos, faces = grid_arrays(n, 1.0)
+    for world in (1, 2, 4, 8):
+        owner = range_owner(len(pos), world)
+        counts = np.bincount(owner, minlength=world)
+        assert counts.max() - counts.min() <= 1
+        assert np.all(np.diff(owner) >= 0)
+        plans = [ShardPlan(pos, faces, None, world, r, owner=owner) for r in range(world)]
+        for p in plans:
+            o = np.flatnonzero(p.owned)
+            assert np.array_equal(o, np.arange(o[0], o[0] + len(o)))  # one slice
+            assert np.array_equal(p.verts[o], np.flatnonzero(owner == p.rank))
+            assert len(p.verts) - len(o) <= 2 * n + 2  # a grid row (and a corner) above and below
+            for q_, lst in p.send.items():
+                assert np.array_equal(p.verts[lst], plans[q_].verts[plans[q_].recv[p.rank]])

@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, q, overlap=False):
+def _worker(rank, world, port, name, q, overlap=False, backend="gloo", partition="morton"):
     import os
     import sys
     from pathlib import Path
@@ -36,7 +36,10 @@ def _worker(rank, world, port, name, q, overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2509_00406_b200.distributed import DistributedProblem
 
@@ -45,13 +48,19 @@ def _worker(rank, world, port, name, q, overlap=False):
         faces = d["faces"]
         edges = d["edges"] if not len(faces) else None
         dp = DistributedProblem(d["positions"], faces, n, build_terms(d), fixed_vertices=d["fixed"].tolist(),
-                                edges=edges, with_hessian=bool(d["with_hessian"]) and not overlap, overlap=overlap)
+                                edges=edges, with_hessian=bool(d["with_hessian"]) and not overlap, overlap=overlap,
+                                partition=partition)
         own = dp.plan.owned_global
         x, v = d["s0_x"].reshape(-1, n), d["s0_v0"].reshape(-1, n)
         dp.set_x_owned(x[own])  # ribbon rows of x arrive through the halo exchange
         out = {"rank": rank, "owned": own, "energy": dp.eval_terms()}
         out["grad"] = dp.grad_owned().cpu().numpy()
         out["hvp"] = dp.hvp_owned(v[own]).cpu().numpy()
+        if partition == "range":  # contiguous owned rows: the direction written in place, results as views
+            assert dp.owned_view(dp.problem.x_device).data_ptr() != 0
+            vb = dp.v_owned_buffer()
+            vb.copy_(torch.as_tensor(v[own], device=vb.device))
+            assert np.array_equal(dp.hvp_owned(vb).cpu().numpy(), out["hvp"])
         out["hvp_psd"] = dp.hvp_owned(v[own], psd_floor=FLOOR).cpu().numpy()
         if dp.problem.with_hessian:
             out["hrows"] = dp.hess_rows_owned()
@@ -66,14 +75,35 @@ CASES = [(n, False) for n in ("cloth64", "dirichlet_ico2", "sphere_ico2", "smoot
 CASES += [(n, True) for n in ("cloth64", "sphere_ico2", "smooth_ico2", "mixed_fv_ev_v")]
 
 
+# NCCL: one rank (NCCL refuses two ranks on one device), so the NCCL branches
+# of the exchange (device buffers, async work handles on the communicator's
+# stream) and the energy all_reduce run on this one-GPU box
+NCCL_CASES = [("cloth64", False), ("cloth64", True), ("dirichlet_ico2", False), ("mixed_fv_ev_v", True)]
+
+
 @pytest.mark.parametrize("name,overlap", CASES)
 def test_two_process_shards_match_reference(name, overlap):
-    world = 2
+    _run(name, overlap, 2, "gloo")
+
+
+# id-range partition (owned rows one contiguous slice of the shard numbering)
+@pytest.mark.parametrize("name,overlap", [("cloth64", False), ("cloth64", True), ("smooth_ico2", True),
+                                          ("dirichlet_ico2", False)])
+def test_two_process_range_partition(name, overlap):
+    _run(name, overlap, 2, "gloo", "range")
+
+
+@pytest.mark.parametrize("name,overlap", NCCL_CASES)
+def test_nccl_shard_matches_reference(name, overlap):
+    _run(name, overlap, 1, "nccl")
+
+
+def _run(name, overlap, world, backend, partition="morton"):
     d = load(name)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, overlap)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, overlap, backend, partition)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
