@@ -245,22 +245,28 @@ MG_DI bool shifted_pd(const double* A, double floor) {
   return ok;
 }
 
-// One eigenvalue below the floor, from a start vector v0 with a negative
-// Rayleigh quotient (the caller knows the clamped mode's approximate
-// direction): Rayleigh-quotient iteration for (lambda, v), then
+// One eigenvalue below the floor, from a start vector v0 with a non-positive
+// shifted Rayleigh quotient: the start is refined by Rayleigh-Ritz on
+// span{v0, A v0} (the smaller Ritz pair of the 2 x 2 projection), then
+// Rayleigh-quotient iteration for (lambda, v), and
 // P_f(A) = A + (f - lambda) v v^T. The error of this update is bounded by the
 // eigenvector residual times |f - lambda| / gap <= 1 (the gap to the next
 // eigenvalue is at least f - lambda), so it is as accurate as the full
-// eigendecomposition. Returns false (A untouched) unless the iteration
-// converged below the floor and A + (s - lambda) v v^T - f I is positive
-// definite for a large s, i.e. no other eigenvalue sits below the floor; the
-// caller then falls back to Jacobi.
+// eigendecomposition. The shifted solves are LDL^T without pivoting (A - rho I
+// is nearly semi-definite once rho approaches the lowest eigenvalue; a pivot
+// that vanishes — rho an eigenvalue to working precision — is replaced by
+// 2^-52 |A|_F, so the solve still returns the eigenvector to full precision).
+// Convergence is judged on the true residual |A v - rho v|, so the solver's
+// conditioning never reaches the result. Returns false (A untouched) unless
+// the iteration converged below the floor and A + (s - lambda) v v^T - f I is
+// positive definite for a large s, i.e. no other eigenvalue sits below the
+// floor; the caller then falls back to Jacobi.
 template <int K>
 MG_DI bool psd_rank1_update(double* A, double floor, const double* v0) {
   double v[K], nrm = 0.0, fro2 = 0.0;
 #pragma unroll
   for (int i = 0; i < K; ++i) nrm += v0[i] * v0[i];
-  if (!(nrm > 0.0)) return false;
+  if (!(nrm > 0.0) || !isfinite(nrm)) return false;
   nrm = rsqrt(nrm);
 #pragma unroll
   for (int i = 0; i < K; ++i) v[i] = v0[i] * nrm;
@@ -269,17 +275,54 @@ MG_DI bool psd_rank1_update(double* A, double floor, const double* v0) {
 #pragma unroll
     for (int j = 0; j <= i; ++j) fro2 += (i == j ? 1.0 : 2.0) * A[tri(i, j)] * A[tri(i, j)];
   const double scale = ::sqrt(fro2);
-  double rho = 0.0;
-  bool conv = false;
-  for (int it = 0; it < 8; ++it) {
-    double w[K];
+  const double tiny = 0x1p-52 * scale;
+  auto matvec = [&](const double* x, double* y) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc += A[tri(i, j)] * v[j];
-      w[i] = acc;
+      for (int j = 0; j < K; ++j) acc += A[i >= j ? tri(i, j) : tri(j, i)] * x[j];
+      y[i] = acc;
     }
+  };
+  {  // Rayleigh-Ritz on span{v, A v}
+    double w[K], u[K], au[K], a = 0.0, nu = 0.0;
+    matvec(v, w);
+#pragma unroll
+    for (int i = 0; i < K; ++i) a += v[i] * w[i];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      u[i] = w[i] - a * v[i];
+      nu += u[i] * u[i];
+    }
+    if (nu > 1e-28 * fro2) {
+      const double inu = rsqrt(nu);
+      nu *= inu;
+#pragma unroll
+      for (int i = 0; i < K; ++i) u[i] *= inu;
+      matvec(u, au);
+      double c = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) c += u[i] * au[i];
+      const double h = 0.5 * (a - c);
+      const double mu = 0.5 * (a + c) - ::sqrt(h * h + nu * nu);
+      double n2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        v[i] = nu * v[i] + (mu - a) * u[i];
+        n2 += v[i] * v[i];
+      }
+      if (!(n2 > 0.0)) return false;
+      n2 = rsqrt(n2);
+#pragma unroll
+      for (int i = 0; i < K; ++i) v[i] *= n2;
+    }
+  }
+  double rho = 0.0;
+  bool conv = false;
+  for (int it = 0; it < 8; ++it) {
+    double w[K];
+    matvec(v, w);
     rho = 0.0;
 #pragma unroll
     for (int i = 0; i < K; ++i) rho += v[i] * w[i];
@@ -290,59 +333,43 @@ MG_DI bool psd_rank1_update(double* A, double floor, const double* v0) {
       conv = true;
       break;
     }
-    // solve (A - rho I) y = v: Gaussian elimination with partial pivoting
-    double B[K][K + 1];
+    // (A - rho I) y = v: LDL^T without pivoting
+    double L[TriN<K>::value], D[K], y[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double d = A[tri(j, j)] - rho;
+#pragma unroll
+      for (int k = 0; k < j; ++k) d -= L[tri(j, k)] * L[tri(j, k)] * D[k];
+      if (fabs(d) < tiny) d = d < 0.0 ? -tiny : tiny;
+      D[j] = d;
+      const double id = psd_rcp(d);
+#pragma unroll
+      for (int i = j + 1; i < K; ++i) {
+        double t = A[tri(i, j)];
+#pragma unroll
+        for (int k = 0; k < j; ++k) t -= L[tri(i, k)] * L[tri(j, k)] * D[k];
+        L[tri(i, j)] = t * id;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
+      double t = v[i];
 #pragma unroll
-      for (int j = 0; j < K; ++j) B[i][j] = A[tri(i, j)] - (i == j ? rho : 0.0);
-      B[i][K] = v[i];
+      for (int k = 0; k < i; ++k) t -= L[tri(i, k)] * y[k];
+      y[i] = t;
     }
-    bool sing = false;
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-      int piv = c;
-      double best = fabs(B[c][c]);
-#pragma unroll
-      for (int r = c + 1; r < K; ++r)
-        if (fabs(B[r][c]) > best) {
-          best = fabs(B[r][c]);
-          piv = r;
-        }
-#pragma unroll
-      for (int r = c + 1; r < K; ++r)
-        if (r == piv)
-#pragma unroll
-          for (int j = 0; j <= K; ++j) {
-            const double t = B[c][j];
-            B[c][j] = B[r][j];
-            B[r][j] = t;
-          }
-      if (!(best > 1e-300)) {
-        sing = true;
-        break;
-      }
-      const double ip = psd_rcp(B[c][c]);
-#pragma unroll
-      for (int r = c + 1; r < K; ++r) {
-        const double f = B[r][c] * ip;
-#pragma unroll
-        for (int j = c; j <= K; ++j) B[r][j] -= f * B[c][j];
-      }
-    }
-    if (sing) {  // rho is an eigenvalue to working precision: v is its vector
-      conv = true;
-      break;
-    }
-    double y[K], yn = 0.0;
+    for (int i = 0; i < K; ++i) y[i] *= psd_rcp(D[i]);
 #pragma unroll
     for (int i = K - 1; i >= 0; --i) {
-      double acc = B[i][K];
+      double t = y[i];
 #pragma unroll
-      for (int j = i + 1; j < K; ++j) acc -= B[i][j] * y[j];
-      y[i] = acc * psd_rcp(B[i][i]);
-      yn += y[i] * y[i];
+      for (int k = i + 1; k < K; ++k) t -= L[tri(k, i)] * y[k];
+      y[i] = t;
     }
+    double yn = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) yn += y[i] * y[i];
     if (!(yn > 0.0) || !isfinite(yn)) return false;
     yn = rsqrt(yn);
 #pragma unroll
@@ -365,14 +392,67 @@ MG_DI bool psd_rank1_update(double* A, double floor, const double* v0) {
   return true;
 }
 
+// shifted_pd, and when A - floor*I is not positive definite a direction z of
+// non-positive curvature: at the first failing pivot j, with the leading j x j
+// block M = L L^T and column b above the pivot, z = [-M^{-1} b; 1; 0...] gives
+// z^T (A - floor I) z = the Schur pivot <= 0 (M^{-1} b = L^{-T} l_j, l_j the
+// factor's row j)
+template <int K>
+MG_DI bool shifted_pd_dir(const double* A, double floor, double* z) {
+  double L[TriN<K>::value];
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double d = A[tri(j, j)] - floor;
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= L[tri(j, k)] * L[tri(j, k)];
+    if (fail < 0 && !(d > 0.0)) fail = j;
+    const double r = d > 0.0 ? rsqrt(d) : 0.0;
+    L[tri(j, j)] = d * r;
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double v = A[tri(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= L[tri(i, k)] * L[tri(j, k)];
+      L[tri(i, j)] = v * r;
+    }
+  }
+  if (fail < 0) return true;
+  double y[K];  // L11^T y = l_fail (back substitution over the leading fail x fail block)
+#pragma unroll
+  for (int i = K - 1; i >= 0; --i) {
+    double rhs = 0.0;
+#pragma unroll
+    for (int c = i + 1; c < K; ++c)
+      if (c == fail) rhs = L[tri(c, i)];
+#pragma unroll
+    for (int k = i + 1; k < K; ++k)
+      if (k < fail) rhs -= L[tri(k, i)] * y[k];
+    y[i] = i < fail ? rhs * psd_rcp(L[tri(i, i)]) : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) z[i] = i < fail ? -y[i] : (i == fail ? 1.0 : 0.0);
+  return false;
+}
+
 // project in place unless already above the floor; 2x2 / 3x3 blocks (vertex
-// terms, two-point edge terms) use the non-iterative solver of psd_small.h
+// terms, two-point edge terms) use the non-iterative solver of psd_small.h.
+// 4x4 / 6x6: one eigenvalue below the floor is the common case (e.g. the
+// sphere face Hessian's one strongly negative mode, every face at the
+// benchmark state): Rayleigh-quotient iteration from the Cholesky test's
+// negative-curvature direction and a certified rank-one update; Jacobi when
+// that fails (several eigenvalues below the floor, or no convergence)
 template <int K>
 MG_DI void project_if_needed(double* A, double floor) {
+  if constexpr (K == 4 || K == 6) {
+    double z[K];
+    if (shifted_pd_dir<K>(A, floor, z)) return;
+    if (!psd_rank1_update<K>(A, floor, z)) jacobi_project_rr<K>(A, floor);
+    return;
+  }
   if (shifted_pd<K>(A, floor)) return;
   if constexpr (K == 2) psd_small::project2(A, floor);
   else if constexpr (K == 3) psd_small::project3(A, floor);
-  else if constexpr (K == 4 || K == 6) jacobi_project_rr<K>(A, floor);
   else jacobi_project<K>(A, floor);
 }
 
