@@ -777,7 +777,7 @@ template <int MODE> struct CfRec { static constexpr int S = MODE == MODE_HESS ? 
 #define CF_HESS_MINB 4
 #endif
 #ifndef CF_FLAT_MINB
-#define CF_FLAT_MINB 8
+#define CF_FLAT_MINB 6  // HVP 0.772 -> 0.699 ms at 8 -> 6 (128 registers spilled 56 bytes); 5: 0.695, 4: 0.694
 #endif
 #ifndef CF_NB
 #define CF_NB 3  // faces per thread with their loads in flight together (unclamped; HVP 0.866 -> 0.848 ms with MINB 8)

@@ -1,0 +1,30 @@
+#!/bin/bash
+# ncu --set full of selected kernels (tools/prof_r02.sh's captures, by name).
+# usage (under gpurun): bash tools/prof_some.sh <tag> <name> [<name> ...]
+tag=$1; shift
+mkdir -p gpurun_out
+M=smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum
+cap() {  # name regex skip command...
+  local name=$1 re=$2 skip=$3; shift 3
+  timeout 600 ncu --set full --clock-control none --import-source on --metrics $M -k "regex:$re" -s $skip -c 1 \
+      -o /tmp/prof_$name "$@" > /tmp/ncu_$name.log 2>&1
+  { echo "== $name ($*)"; python tools/ncu_summary.py /tmp/prof_$name.ncu-rep 14; } > gpurun_out/ncu_${tag}_$name.txt 2>&1
+  cp /tmp/prof_$name.ncu-rep gpurun_out/ 2>/dev/null
+}
+P="python tools/prof_configs.py --sub 10 --configs"
+B="python bench.py --profile --no-cpu"
+for n in "$@"; do
+  case $n in
+    cloth_psd) cap cloth_psd '^k_rows_fast$' 0 $B --profile-call psd ;;
+    cloth_hvp_psd) cap cloth_hvp_psd '^k_rows_fast$' 0 $B --profile-call hvp_psd --grid 2240 ;;
+    dir_hess) cap dir_hess '^k_rows_dirichlet$' 1 $P dirichlet ;;
+    dir_hess_psd) cap dir_hess_psd '^k_cta_dirichlet$' 0 $P dirichlet ;;
+    dir_hvp) cap dir_hvp '^k_cta_dirichlet$' 1 $P dirichlet ;;
+    dir_hvp_psd) cap dir_hvp_psd '^k_cta_dirichlet$' 2 $P dirichlet ;;
+    sph_grad) cap sph_grad '^k_rows_sphere$' 1 $P sphere ;;
+    sph_hvp) cap sph_hvp '^k_rows_sphere$' 2 $P sphere ;;
+    sph_hvp_psd) cap sph_hvp_psd '^k_sphere_face_hvp_psd$' 0 $P sphere ;;
+    smooth_hvp) cap smooth_hvp '^k_rows_fast$' 2 $P smooth ;;
+  esac
+done
+grep -h "^== \|Duration\|DRAM Throughput\|fp64 executed\|Registers\|stalls" gpurun_out/ncu_${tag}_*.txt
