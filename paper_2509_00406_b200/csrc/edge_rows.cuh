@@ -165,10 +165,13 @@ MG_DI void radial_clamp_fast(double& ci, double& cd, double r, double f) {
 #define EV_STAGED_HESS 1  // headline 0.617 -> 0.543 ms (cloth 2048^2 grad+H(psd)), plain 0.553 -> 0.485
 #endif
 #ifndef EV_STAGES_HESS
-#define EV_STAGES_HESS 2
+// one stage: the next block's streams are issued as soon as this block's are
+// read, a whole block's compute ahead, and the 4.3 KB saved lets 6 instead of
+// 5 CTAs (32 KB row buffers) share an SM: headline 0.542 -> 0.485 ms
+#define EV_STAGES_HESS 1
 #endif
 #ifndef EV_STAGES
-#define EV_STAGES 2  // cloth HVP 0.190 -> 0.173 ms at 2 or 3 (2240^2); smoothing HVP 0.281 -> 0.271 at 2, 0.295 at 3
+#define EV_STAGES 1  // cloth HVP 0.190 -> 0.173 ms staged (2240^2); smoothing HVP 0.271 at 1 or 2, 0.295 at 3 (1: 1% faster)
 #endif
 // MAXI: incidences in flight; BLOCK: threads per CTA (the Hessian kernel's CTA
 // is its row-buffer group, EV_ROW_BLOCK); MINB: CTAs per SM to fit
