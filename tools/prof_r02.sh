@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 M=smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum
 cap() {  # name regex skip command...
   local name=$1 re=$2 skip=$3; shift 3
-  timeout 600 ncu --set full --clock-control none --import-source on --metrics $M -k "regex:$re" -s $skip -c 1 \
+  timeout 600 ncu -f --set full --clock-control none --import-source on --metrics $M -k "regex:$re" -s $skip -c 1 \
       -o /tmp/prof_$name "$@" > /tmp/ncu_$name.log 2>&1
   { echo "== $name ($*)"; python tools/ncu_summary.py /tmp/prof_$name.ncu-rep 14; } > gpurun_out/ncu_${tag}_$name.txt 2>&1
 }

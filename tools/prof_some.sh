@@ -6,17 +6,21 @@ mkdir -p gpurun_out
 M=smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum
 cap() {  # name regex skip command...
   local name=$1 re=$2 skip=$3; shift 3
-  timeout 600 ncu --set full --clock-control none --import-source on --metrics $M -k "regex:$re" -s $skip -c 1 \
+  timeout 600 ncu -f --set full --clock-control none --import-source on --metrics $M -k "regex:$re" -s $skip -c 1 \
       -o /tmp/prof_$name "$@" > /tmp/ncu_$name.log 2>&1
   { echo "== $name ($*)"; python tools/ncu_summary.py /tmp/prof_$name.ncu-rep 14; } > gpurun_out/ncu_${tag}_$name.txt 2>&1
-  cp /tmp/prof_$name.ncu-rep gpurun_out/ 2>/dev/null
 }
 P="python tools/prof_configs.py --sub 10 --configs"
 B="python bench.py --profile --no-cpu"
 for n in "$@"; do
   case $n in
     cloth_psd) cap cloth_psd '^k_rows_fast$' 0 $B --profile-call psd ;;
+    cloth_plain) cap cloth_plain '^k_rows_fast$' 0 $B --profile-call plain ;;
+    cloth_hvp) cap cloth_hvp '^k_rows_fast$' 0 $B --profile-call hvp --grid 2240 ;;
     cloth_hvp_psd) cap cloth_hvp_psd '^k_rows_fast$' 0 $B --profile-call hvp_psd --grid 2240 ;;
+    smooth_grad) cap smooth_grad '^k_rows_fast$' 1 $P smooth ;;
+    launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${tag}.csv \
+                  python bench.py --profile --no-cpu > /dev/null 2>&1 ;;
     dir_hess) cap dir_hess '^k_rows_dirichlet$' 1 $P dirichlet ;;
     dir_hess_psd) cap dir_hess_psd '^k_cta_dirichlet$' 0 $P dirichlet ;;
     dir_hvp) cap dir_hvp '^k_cta_dirichlet$' 1 $P dirichlet ;;
