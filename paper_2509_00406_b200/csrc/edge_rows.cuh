@@ -190,11 +190,17 @@ template <int MODE, bool PSD> struct FastCfg {
 template <> struct FastCfg<MODE_HVP, false> {
   static constexpr int MAXI = EV_HVP_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_THREADS / EV_FLAT_BLOCK;
 };
+#ifndef EV_HVP_PSD_THREADS
+#define EV_HVP_PSD_THREADS 512  // 640: 0.275 vs 0.234 ms (clamped HVP, 2240^2)
+#endif
+#ifndef EV_GRAD_THREADS
+#define EV_GRAD_THREADS 768  // 640 / 1024: 1.53 / 1.84 vs 1.48 ms (config 5 gradient, 7072^2)
+#endif
 template <> struct FastCfg<MODE_HVP, true> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 512 / EV_FLAT_BLOCK;
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_PSD_THREADS / EV_FLAT_BLOCK;
 };
 template <> struct FastCfg<MODE_GRAD, false> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
+  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = EV_GRAD_THREADS / EV_FLAT_BLOCK;
 };
 template <> struct FastCfg<MODE_ENERGY, false> {  // the energy probe: first-vertex edges only
   static constexpr int MAXI = 6, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
