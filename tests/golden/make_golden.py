@@ -171,6 +171,46 @@ def case_cloth_asis():
                 "iterates": np.array(count[0])})
 
 
+def case_cloth64_asis():
+    """Config 1 as-is at its own size: every Newton iterate the unmodified
+    64x64 ClothSim visits in 2 steps. The Hessians are stored as H r for one
+    seeded r (full values would be ~2 MB per iterate); the step states after
+    simulate() check the device driver end to end."""
+    sim = ClothSim(ClothConfig(grid_n=64))
+    rec = {}
+    orig = sim.problem.eval_terms
+    count = [0]
+    r = np.random.default_rng(7).normal(size=sim.problem.num_dofs)
+
+    def spy(psd_floor=None):
+        e = orig(psd_floor=psd_floor)
+        i = count[0]
+        rec[f"s{i}_x"] = sim.problem.x.copy()
+        rec[f"s{i}_target"] = sim._target.copy()
+        rec[f"s{i}_floor"] = np.array(np.nan if psd_floor is None else psd_floor)
+        rec[f"s{i}_energy"] = np.array(e)
+        rec[f"s{i}_grad"] = sim.problem.grad.copy()
+        rec[f"s{i}_hr"] = sim.problem.hess.matvec(r)
+        count[0] += 1
+        return e
+
+    sim.problem.eval_terms = spy
+    x, v, reps = sim.simulate(steps=2)
+    cfg = sim.cfg
+    spec = [
+        {"type": "Inertia", "op": "V", "attrs": {"masses": "a_masses", "target": "a_target"}},
+        {"type": "Spring", "op": "EV", "coef": 0.5 * cfg.k * (cfg.h * cfg.h), "attrs": {"rest_len2": "a_l2"}},
+        {"type": "Gravity", "op": "V", "h2": cfg.h * cfg.h, "gravity": list(cfg.gravity),
+         "attrs": {"masses": "a_masses"}},
+    ]
+    rec["r"] = r
+    rec["final_x"], rec["final_v"] = x, v
+    rec["step_energies"] = np.array([rp.final_energy for rp in reps])
+    save("traj_cloth64_asis", sim.mesh, 3, spec, rec, fixed=sim.pinned,
+         extra={"a_masses": sim.masses, "a_target": sim._target.copy(), "a_l2": sim.rest_len2,
+                "iterates": np.array(count[0])})
+
+
 def case_dirichlet():
     p3, f, uv = punctured_icosphere_arrays(2)
     mesh = mg.Mesh(p3, f)
@@ -302,10 +342,15 @@ def case_mixed():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # named cases only, e.g. cloth64_asis
+        for name in sys.argv[1:]:
+            globals()[f"case_{name}"]()
+        sys.exit(0)
     case_springs()
     case_cloth(8, "cloth8")
     case_cloth(64, "cloth64")
     case_cloth_asis()
+    case_cloth64_asis()
     case_dirichlet()
     case_sphere()
     case_smooth()

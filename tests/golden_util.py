@@ -13,7 +13,7 @@ FLOOR = 1e-9
 
 def cases():
     """Problem fixtures (solver trajectories, solver_*.npz, are separate)."""
-    return sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith(("solver_", "vv_", "drivers")))
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith(("solver_", "vv_", "drivers", "traj_")))
 
 
 def solver_cases():

@@ -28,6 +28,21 @@ def test_cloth_sim_steps(g):
     assert np.max(np.abs(v - g["cloth_v"])) <= 1e-5
 
 
+def test_cloth_sim_config1_asis():
+    """Config 1 as-is: 2 implicit-Euler steps of the 64x64 sheet against the
+    unmodified reference ClothSim (tests/golden/make_golden.py case_cloth64_asis)."""
+    from paper_2509_00406_b200.apps import ClothConfig
+    from paper_2509_00406_b200.drivers import ClothSim
+
+    ref = np.load(GOLDEN / "traj_cloth64_asis.npz")
+    sim = ClothSim(ClothConfig(grid_n=64))
+    x, v, reps = sim.simulate(2)
+    e = np.array([r.final_energy for r in reps])
+    assert np.allclose(e, ref["step_energies"], rtol=1e-8, atol=0)
+    assert np.max(np.abs(x - ref["final_x"])) <= 1e-7
+    assert np.max(np.abs(v - ref["final_v"])) <= 1e-5
+
+
 def test_tutte_and_parameterize(g):
     import paper_2509_00406_b200 as mg
     from paper_2509_00406_b200.drivers import ParamConfig, parameterize, tutte_embedding

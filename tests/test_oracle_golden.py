@@ -72,3 +72,28 @@ def test_threaded_deterministic_bitwise():
     r4 = oracle_problem(d, workers=4).eval_terms(d["s0_x"])
     assert r1[0] == r4[0]
     assert np.array_equal(r1[1], r4[1]) and np.array_equal(r1[2], r4[2])
+
+
+def bsr_matvec(row_offsets, col_indices, values, r, n=3):
+    """y = H r for a block-CSR matrix (host, test helper)."""
+    vals = np.asarray(values).reshape(-1, n, n)
+    rows = np.repeat(np.arange(len(row_offsets) - 1), np.diff(row_offsets))
+    prod = np.einsum("kij,kj->ki", vals, r.reshape(-1, n)[col_indices])
+    y = np.zeros((len(row_offsets) - 1, n))
+    np.add.at(y, rows, prod)
+    return y.ravel()
+
+
+@pytest.mark.parametrize("s", [0, 3, 7])
+def test_oracle_cloth64_asis_trajectory(s):
+    """Config 1 as-is at 64x64: Newton iterates of the unmodified ClothSim
+    (first, middle and last of its 8 evaluations over 2 steps)."""
+    d = load("traj_cloth64_asis")
+    assert int(d["iterates"]) == 8
+    d["a_target"] = d[f"s{s}_target"]
+    op = oracle_problem(d)
+    floor = float(d[f"s{s}_floor"])
+    e, g, h = op.eval_terms(d[f"s{s}_x"], psd_floor=None if np.isnan(floor) else floor)
+    assert rel_scalar(e, d[f"s{s}_energy"]) <= TOL
+    assert rel(g, d[f"s{s}_grad"]) <= 1e-11
+    assert rel(bsr_matvec(op.row_offsets, op.col_indices, h, d["r"]), d[f"s{s}_hr"]) <= 1e-11

@@ -101,6 +101,30 @@ def test_cloth_asis_trajectory(mode):
         assert rel(p.hess.values, d[f"s{s}_hess"]) <= TOL
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_cloth64_asis_trajectory(mode):
+    """Config 1 as-is at its own size (64x64): every Newton iterate of the
+    unmodified 2-step ClothSim, the Hessian checked as H r (fixture stores H r)."""
+    import torch
+
+    d = load("traj_cloth64_asis")
+    target = torch.from_numpy(d["s0_target"].copy()).cuda()
+    d["a_target"] = d["s0_target"]
+    p = engine_problem(d, mode)
+    p.set_term_attr(0, "target", target)
+    for s in range(int(d["iterates"])):
+        target.copy_(torch.from_numpy(d[f"s{s}_target"]))
+        p.x = d[f"s{s}_x"]
+        floor = float(d[f"s{s}_floor"])
+        e = p.eval_terms(psd_floor=None if np.isnan(floor) else floor)
+        assert rel_scalar(e, d[f"s{s}_energy"]) <= TOL
+        d["a_target"] = d[f"s{s}_target"]
+        scale = max(np.max(np.abs(g)) for g in per_term_grads(d, d[f"s{s}_x"]))
+        got, ref = p.grad, d[f"s{s}_grad"]
+        assert np.max(np.abs(got - ref)) <= TOL * max(scale, np.max(np.abs(ref)))
+        assert rel(p.hess.matvec(d["r"]), d[f"s{s}_hr"]) <= TOL
+
+
 @pytest.mark.parametrize("name", ["cloth64", "dirichlet_ico2", "sphere_ico2", "smooth_ico2"])
 def test_deterministic_is_bitwise_reproducible(name):
     d = load(name)
