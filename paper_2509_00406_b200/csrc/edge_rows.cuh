@@ -194,13 +194,19 @@ template <> struct FastCfg<MODE_HVP, false> {
 #define EV_HVP_PSD_THREADS 512  // 640: 0.275 vs 0.234 ms (clamped HVP, 2240^2)
 #endif
 #ifndef EV_GRAD_THREADS
-#define EV_GRAD_THREADS 768  // 640 / 1024: 1.53 / 1.84 vs 1.48 ms (config 5 gradient, 7072^2)
+#define EV_GRAD_THREADS 640  // with 6 incidences in flight; 768 with 4: config-5 gradient 1.453 vs 1.483 ms, smoothing gradient 0.280 vs 0.301 (6 at 512: 1.565; 5 at 640 / 768: 1.463 / 1.660)
+#endif
+#ifndef EV_HVP_PSD_MAXI
+#define EV_HVP_PSD_MAXI 4  // 6: clamped cloth HVP 0.241 vs 0.234 ms (2240^2), 0.274 at 384 threads
+#endif
+#ifndef EV_GRAD_MAXI
+#define EV_GRAD_MAXI 6  // the gradient rows' incidences in flight (EV_GRAD_THREADS)
 #endif
 template <> struct FastCfg<MODE_HVP, true> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_PSD_THREADS / EV_FLAT_BLOCK;
+  static constexpr int MAXI = EV_HVP_PSD_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_HVP_PSD_THREADS / EV_FLAT_BLOCK;
 };
 template <> struct FastCfg<MODE_GRAD, false> {
-  static constexpr int MAXI = 4, BLOCK = EV_FLAT_BLOCK, MINB = EV_GRAD_THREADS / EV_FLAT_BLOCK;
+  static constexpr int MAXI = EV_GRAD_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_GRAD_THREADS / EV_FLAT_BLOCK;
 };
 template <> struct FastCfg<MODE_ENERGY, false> {  // the energy probe: first-vertex edges only
   static constexpr int MAXI = 6, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
