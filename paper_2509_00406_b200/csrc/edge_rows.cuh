@@ -179,7 +179,7 @@ template <int MODE, bool PSD> struct FastCfg {
   static constexpr int MAXI = EV_ELL_K, BLOCK = EV_ROW_BLOCK, MINB = EV_HESS_MINB;
 };
 #ifndef EV_HVP_MAXI
-#define EV_HVP_MAXI 4
+#define EV_HVP_MAXI 4  // 5 / 6: config-5 HVP 1.726 / 1.868 vs 1.676 ms (6 at 640 threads: 2.83)
 #endif
 #ifndef EV_XFREE_MAXI
 #define EV_XFREE_MAXI 6  // incidences in flight of the x-free HVP (directions only): 0.313 -> 0.278 ms at 4 -> 6 (smoothing, icosphere(10))

@@ -1302,7 +1302,10 @@ __global__ void k_sphere_retract(const __grid_constant__ FvArgs a, const uint8_t
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(PT) k_rows_sphere(const __grid_constant__ FvArgs a) {
+#ifndef SPH_MINB
+#define SPH_MINB 1  // 118 registers, 8 CTAs/SM; 9 / 10 / 12 CTAs (spills): HVP 1.686 / 1.686 / 1.931 vs 1.542 ms at icosphere(10)
+#endif
+__global__ void __launch_bounds__(PT, SPH_MINB) k_rows_sphere(const __grid_constant__ FvArgs a) {
   const int64_t row = (int64_t)blockIdx.x * PT + threadIdx.x;
   double eacc = 0.0;
   bool ok = true;
