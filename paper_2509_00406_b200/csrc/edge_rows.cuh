@@ -208,8 +208,11 @@ template <> struct FastCfg<MODE_HVP, true> {
 template <> struct FastCfg<MODE_GRAD, false> {
   static constexpr int MAXI = EV_GRAD_MAXI, BLOCK = EV_FLAT_BLOCK, MINB = EV_GRAD_THREADS / EV_FLAT_BLOCK;
 };
+#ifndef EV_ENERGY_THREADS
+#define EV_ENERGY_THREADS 768  // 512 / 640 / 1024: 0.146 / 0.128 / 0.160 vs 0.129 ms (cloth 2048^2 energy probe)
+#endif
 template <> struct FastCfg<MODE_ENERGY, false> {  // the energy probe: first-vertex edges only
-  static constexpr int MAXI = 6, BLOCK = EV_FLAT_BLOCK, MINB = 768 / EV_FLAT_BLOCK;
+  static constexpr int MAXI = 6, BLOCK = EV_FLAT_BLOCK, MINB = EV_ENERGY_THREADS / EV_FLAT_BLOCK;
 };
 // the x-free HVP holds only directions: full occupancy (64 registers; 1280 /
 // 1536 threads per SM measured 0.510 / 0.639 ms vs 0.274, smoothing HVP)
